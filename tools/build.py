@@ -1,0 +1,98 @@
+"""Build every native library of the repo in-tree.
+
+- gen/libasrgen_host.so     gcc     seeded input generator, host build (test/bench infrastructure)
+- gen/libasrgen_dev.so      nvcc    seeded input generator, sm_100a build (test/bench infrastructure)
+- oracle/liborc.so          gcc     fp64 CPU oracle (test infrastructure)
+- paper_2512_11221_b200/libasr.so   nvcc   the product: C-ABI library + sm_100a kernels
+
+Each target is rebuilt only when one of its sources is newer than the .so.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale(out: str, srcs: list[str]) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def _run(cmd: list[str]) -> None:
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError(f"build failed: {cmd[0]} -> exit {r.returncode}")
+
+
+def build_gen_host(force: bool = False) -> str:
+    out = os.path.join(ROOT, "gen", "libasrgen_host.so")
+    srcs = [os.path.join(ROOT, "gen", f) for f in ("asrgen.h", "asrgen_host.c")]
+    if force or _stale(out, srcs):
+        _run(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", out, srcs[1]])
+    return out
+
+
+def build_oracle(force: bool = False) -> str:
+    out = os.path.join(ROOT, "oracle", "liborc.so")
+    srcs = [os.path.join(ROOT, "oracle", f) for f in ("orc.h", "orc.c")]
+    if force or _stale(out, srcs):
+        _run(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
+              "-o", out, srcs[1], "-lm"])
+    return out
+
+
+def build_gen_dev(force: bool = False) -> str:
+    out = os.path.join(ROOT, "gen", "libasrgen_dev.so")
+    srcs = [os.path.join(ROOT, "gen", f) for f in ("asrgen.h", "asrgen_dev.cu")]
+    if force or _stale(out, srcs):
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-o", out, srcs[1]])
+    return out
+
+
+def build_asr(force: bool = False) -> str:
+    pkg = os.path.join(ROOT, "paper_2512_11221_b200")
+    out = os.path.join(pkg, "libasr.so")
+    csrc = os.path.join(pkg, "csrc")
+    cu = sorted(glob.glob(os.path.join(csrc, "*.cu")))
+    cpp = sorted(glob.glob(os.path.join(csrc, "*.cpp")))
+    hdr = sorted(glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h"))
+                 + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    if not (force or _stale(out, cu + cpp + hdr)):
+        return out
+    objdir = os.path.join(ROOT, "build", "asr")
+    os.makedirs(objdir, exist_ok=True)
+    objs = []
+    common = ["-I", os.path.join(ROOT, "include"), "-I", csrc]
+    for s in cu:
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-warn-spills", *common, "-c", s, "-o", o])
+        objs.append(o)
+    for s in cpp:
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
+        _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", *common, "-c", s, "-o", o])
+        objs.append(o)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    return out
+
+
+def build_all(force: bool = False, cuda: bool = True) -> None:
+    build_gen_host(force)
+    build_oracle(force)
+    if cuda:
+        build_gen_dev(force)
+        build_asr(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv, cuda="--no-cuda" not in sys.argv)
+    print("built")
