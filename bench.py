@@ -1,0 +1,360 @@
+"""bench.py — decode throughput of the ASR-KF-EGR per-step KV-management hot path on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl asr|reference]` prints ONE
+JSON line on rank 0.  A "step" = one asr_step over the context's batch: append, entropy + detector
++ recovery, compaction, split-KV attention over the active set with the fused Eq. 2 score,
+combine, decide + tick, and the host-mirror copy — every stage of SURVEY.md §8(a).
+
+Workload (BASELINE.json configs[1]): LLaMA-3-8B shape (32 layers, 32 q / 8 KV heads, d=128,
+vocab 128256), bf16 KV, window K=512, tau=0.5, k=2, batch 1 per GPU, 8K context reached by decoding
+from a 512-token prompt ("grown" state), synthetic LAT inputs (all-cold W0 by default,
+--family w1 for the 30 % hot mix).  Metric: decode tokens/s (unit tok/s, whole job = all ranks).
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching stream
+with a 256 MiB L2 flush between steps (outside the events); barrier + synchronize on both sides;
+the max over ranks of the summed step times.  Multi-GPU: one process per GPU, each rank owns its own
+batch (sequence sharding, no collective on the hot path) -> "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L, HQ, HKV, D, VOCAB = 32, 32, 8, 128, 128256
+TOKEN_KV_BYTES = L * 2 * HKV * D * 2          # one token, all layers, K+V bf16 = 128 KiB
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="asr", choices=["asr", "reference"])
+    ap.add_argument("--context", type=int, default=8192)
+    ap.add_argument("--batch", type=int, default=1, help="sequences per GPU")
+    ap.add_argument("--window", type=int, default=512)
+    ap.add_argument("--family", default="w0", choices=["w0", "w1"])
+    ap.add_argument("--seed", type=int, default=2001)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def gen_params(a, rank: int):
+    import gen
+    return gen.GenParams(seed=a.seed + 7919 * rank, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D,
+                         hot_permille=300 if a.family == "w1" else 0, a_hot=4, vocab=VOCAB)
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the profiling recipe's clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ oracle arm
+
+def oracle_sample(a, seconds_budget: float, steps: int | None = None, warmup: int = 0, layers: int = 2):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the same workload: one sequence at
+    the same context, warm ledger from the policy-only replay (untimed), then full oracle steps over
+    `layers` of the 32 layers.  tokens/s = (layers/32 of a token per step) / time."""
+    import numpy as np
+
+    import gen
+    import oracle
+    g = gen_params(a, 0)
+    g.L = layers
+    P = a.window
+    grow = a.context - P - 1
+    total_steps = (steps if steps is not None else 10_000) + warmup
+    cap = a.context + total_steps + 1
+    cfg = oracle.OrcCfg(L=layers, Hq=HQ, Hkv=HKV, d=D, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB)
+    K, V = gen.kv(g, 0, 0, cap)
+    s = oracle.OracleSeq(cfg, cap, P)
+    below = np.ones(cap, np.uint8)
+    if a.family == "w1":
+        for j in range(cap):
+            below[j] = 0 if gen.is_hot(g, 0, j) else 1
+    for i in range(grow):
+        s.step_policy(below)
+    done, t_total, i = 0, 0.0, grow
+    while True:
+        q = gen.q(g, 0, i)
+        lg = gen.logits(g, 0, i - 1)
+        t0 = time.perf_counter()
+        s.step(q, K, V, lg)
+        dt = time.perf_counter() - t0
+        i += 1
+        if warmup > 0:
+            warmup -= 1
+            continue
+        done += 1
+        t_total += dt
+        if steps is not None and done >= steps:
+            break
+        if steps is None and t_total >= seconds_budget:
+            break
+    frac = layers / L
+    return {"value": done * frac / t_total, "steps": done, "seconds": t_total,
+            "sample": f"1 sequence x {done} decode steps at n~{a.context} over {layers} of {L} layers "
+                      f"(policy-replay warm ledger), fp64 C oracle, tokens scaled by {layers}/{L}"}
+
+
+def run_reference(a, rank: int, world: int):
+    if rank != 0:
+        return
+    r = oracle_sample(a, 0, steps=a.steps, warmup=a.warmup)
+    ms = 1000.0 * r["seconds"] / r["steps"]
+    line = {"impl": "reference", "metric": "decode tokens/s at LLaMA-3-8B shape (8K context, window 512)",
+            "value": r["value"], "unit": "tok/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"llama3-8b-shape ctx{a.context} batch1 window{a.window} {a.family}",
+                       "context": a.context, "batch_per_gpu": 1, "window": a.window, "family": a.family},
+            "cpu_baseline": {"value": r["value"], "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+
+def run_asr(a, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from paper_2512_11221_b200 import Config, Context, KV_BF16
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B = a.batch
+    P = a.window
+    grow = a.context - P - 1                     # steps before the measured region starts
+    W, K = a.warmup, a.steps
+    e2e_steps = 0 if a.no_e2e else K
+    max_ctx = a.context + W + K + e2e_steps + 2
+    g = gen_params(a, rank)
+    cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
+                 kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=1,
+                 device=local_rank)
+    bf = torch.bfloat16
+    pk = torch.empty((B, P, L, HKV, D), dtype=bf, device=dev)
+    pv = torch.empty_like(pk)
+    gen.dev_kv(g, B, 0, P, pk, pv)
+    torch.cuda.synchronize()
+    ctx = Context(cfg, pk, pv, [P] * B)
+    del pk, pv
+    q = torch.empty((B, L, HQ, D), dtype=bf, device=dev)
+    kn = torch.empty((B, L, HKV, D), dtype=bf, device=dev)
+    vn = torch.empty_like(kn)
+    lg = torch.empty((B, VOCAB), dtype=bf, device=dev)
+    o = torch.empty((B, L, HQ, D), dtype=torch.float32, device=dev)
+    ent = torch.empty((B,), dtype=torch.float32, device=dev)
+    pos_dev = torch.full((B,), P, dtype=torch.int32, device=dev)
+
+    def inputs(i, qb, kb, vb, lb):
+        gen.dev_q(g, B, i, qb)
+        gen.dev_kv(g, B, 0, 1, kb, vb, pos0_dev=pos_dev + i)
+        gen.dev_logits(g, B, i - 1, lb)
+
+    t_grow = time.perf_counter()
+    for i in range(grow):
+        inputs(i, q, kn, vn, lg)
+        ctx.step(q, kn, vn, o, logits_prev=lg if i > 0 else None, entropy=ent)
+    torch.cuda.synchronize()
+    t_grow = time.perf_counter() - t_grow
+    ctx.stage_times()  # discard growth-phase events
+    # inputs of the measured steps, resident in HBM before timing
+    n_meas = W + K
+    Q = torch.empty((n_meas, B, L, HQ, D), dtype=bf, device=dev)
+    KN = torch.empty((n_meas, B, L, HKV, D), dtype=bf, device=dev)
+    VN = torch.empty_like(KN)
+    LG = torch.empty((n_meas, B, VOCAB), dtype=bf, device=dev)
+    for t in range(n_meas):
+        inputs(grow + t, Q[t], KN[t], VN[t], LG[t])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream()
+    for t in range(W):
+        flush.zero_()
+        ctx.step(Q[t], KN[t], VN[t], o, logits_prev=LG[t], entropy=ent)
+    torch.cuda.synchronize()
+    ctx.stage_times()
+    attended = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    t_wall = time.perf_counter()
+    for t in range(K):
+        flush.zero_()
+        ev[t][0].record(st)
+        ctx.step(Q[W + t], KN[W + t], VN[W + t], o, logits_prev=LG[W + t], entropy=ent)
+        ev[t][1].record(st)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    total_ms = sum(step_ms)
+    stage_ms, launches = ctx.stage_times()
+    stats = [ctx.stats(b) for b in range(B)]
+    # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
+    # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below
+    att_last = sum(s["attended"] for s in stats)
+    total_t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_t, op=dist.ReduceOp.MAX)
+    total_max = float(total_t.item())
+    # ---- e2e through the C ABI with HOST buffers (copies inside the timed region)
+    e2e = None
+    if e2e_steps:
+        hq = [torch.empty((B, L, HQ, D), dtype=bf).pin_memory() for _ in range(2)]
+        hk = [torch.empty((B, L, HKV, D), dtype=bf).pin_memory() for _ in range(2)]
+        hv = [torch.empty((B, L, HKV, D), dtype=bf).pin_memory() for _ in range(2)]
+        hl = [torch.empty((B, VOCAB), dtype=bf).pin_memory() for _ in range(2)]
+        ho = torch.empty((B, L, HQ, D), dtype=torch.float32).pin_memory()
+        he = torch.empty((B,), dtype=torch.float32).pin_memory()
+        base = grow + n_meas
+        HQs, HKs, HVs, HLs = [], [], [], []
+        for t in range(e2e_steps):
+            inputs(base + t, q, kn, vn, lg)
+            HQs.append(q.cpu().pin_memory()); HKs.append(kn.cpu().pin_memory())
+            HVs.append(vn.cpu().pin_memory()); HLs.append(lg.cpu().pin_memory())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for t in range(e2e_steps):
+            ctx.step(HQs[t], HKs[t], HVs[t], ho, logits_prev=HLs[t], entropy=he)
+        e1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        h2d = B * (L * HQ * D * 2 + 2 * L * HKV * D * 2 + VOCAB * 2)
+        d2h = B * (L * HQ * D * 4 + 4)
+        e2e = {"value": B * e2e_steps * world / (float(e2e_ms.item()) / 1000.0), "unit": "tok/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region"}
+    # ---- roofline of the dominant kernel (attention + fused score), measured live via stage events
+    attn_ms = stage_ms[2]
+    # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);
+    # per (sequence, layer): q (Hq*d*2 B).  |A_i| per step ~ att_last (drifts < 0.5 % over the window).
+    bytes_per_step = L * att_last * (2 * HKV * D * 2 + 8) + B * L * HQ * D * 2
+    achieved = bytes_per_step * K / (attn_ms / 1000.0) / 1e9
+    peak, peak_kind = measured_peak_hbm()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
+            tr = json.load(f)
+            if tr.get("context") == a.context and tr.get("family") == a.family and tr.get("batch") == B:
+                traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    value = B * K * world / (total_max / 1000.0)
+    if rank != 0:
+        return
+    cpu = None
+    if not a.no_cpu_baseline and world == 1:
+        r = oracle_sample(a, a.cpu_seconds)
+        cpu = {"value": r["value"], "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": r["sample"]}
+    line = {
+        "metric": "decode tokens/s at LLaMA-3-8B shape (8K context, window 512)",
+        "value": value, "unit": "tok/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}",
+                   "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": 0.5, "k": 2,
+                   "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": f"sequence-sharded x{world} (no hot-path collective)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "attention+score (split-KV over A_i)",
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "bytes_per_launch": bytes_per_step, "ms_per_launch": attn_ms / K},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "detail": {"attended_per_step": att_last / B, "active_post": stats[0]["active"], "total": stats[0]["total"],
+                   "compression": stats[0]["compression"],
+                   "stage_ms_per_step": {n: v / K for n, v in zip(
+                       ["entropy", "append_recover_compact", "attention_score", "combine", "decide_tick"], stage_ms)},
+                   "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
+                   "wall_s_timed": t_wall, "grow_s": t_grow,
+                   "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_asr(a, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/* include/asr.h — C ABI of the B200-native ASR-KF-EGR per-decode-step KV-management hot path.
+ *
+ * Method: "Adaptive Soft Rolling KV Freeze with Entropy-Guided Recovery", arXiv 2512.11221.
+ * P:n below is line n of the paper text (/root/reference/PAPER.md, section legend in SURVEY.md);
+ * readings of ambiguous passages are listed in DESIGN.md §"Readings" (R-tick, R-W, R-win, ...).
+ *
+ * One context (asr_ctx) owns B sequences.  Each asr_step runs Alg. 1 lines 1-15 for
+ * every sequence and every layer on the GPU, with no host synchronisation:
+ *   (a0) append the previous step's token K/V (Alg. 1 line 16 of the previous step)
+ *   (a6) entropy of logits_prev + spike detector + recovery ladder SR->WR->FR->RR (Sec 3.6)
+ *   (a3) compact the active index list A_i (Alg. 1 "Active KV cache A")
+ *   (a4) decode attention softmax(q K_A^T / sqrt(d)) V_A over A_i only (Eq. 1; line 1)
+ *   (a1) relevance s_j = (1/H) sum_h |q^(h) . k_j^(h)| fused into (a4) (Eq. 2; line 2)
+ *   (a2) threshold s_j < tau outside the window, c_j += 1, d_j = floor(sqrt(c_j)/k), freeze if d_j > 0,
+ *        then tick every frozen timer and restore at d_j <= 0 (Eq. 3; lines 3-15 P:89-101)
+ *   (a5) frozen KV lives in a write-once pinned host mirror (Sec 3.3); see asr_config.
+ * All calls return asr_status.  Thread-compatible: one thread at a time per context.
+ * Errors: argument / configuration errors are detected synchronously and change nothing;
+ * device-side invariant violations latch a flag that surfaces as ASR_E_INVARIANT from the next
+ * asr_step / asr_stats.  asr_last_error() gives a one-line, thread-local message.
+ */
+#ifndef ASR_H
+#define ASR_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct asr_ctx asr_ctx;
+
+typedef enum {
+  ASR_OK = 0,
+  ASR_E_INVALID = 1,   /* bad argument or configuration (nothing was changed) */
+  ASR_E_INVARIANT = 2, /* device-detected ledger invariant violation (latched) */
+  ASR_E_CUDA = 3,      /* CUDA runtime error */
+  ASR_E_OOM = 4,       /* device or pinned-host allocation failed */
+  ASR_E_CAPACITY = 5,  /* a sequence would exceed max_context */
+  ASR_E_STATE = 7      /* call order (e.g. use after destroy) */
+} asr_status;
+
+typedef enum { ASR_KV_BF16 = 0, ASR_KV_F32 = 1 } asr_dtype;
+typedef enum { ASR_TICK_LITERAL = 0 /* R0: Alg. 1 order, default */, ASR_TICK_SKIP_NEW = 1 /* R1 */ } asr_tick;
+typedef enum { ASR_SCORE_RAW = 0 /* Eq. 2 literal, default */, ASR_SCORE_SCALED = 1 /* x 1/sqrt(d) */ } asr_score_mode;
+typedef enum { ASR_SR = 1, ASR_WR = 2, ASR_FR = 3 } asr_level; /* P:80; RR = FR + rewalk flag */
+typedef enum { ASR_MEM_DEVICE = 0, ASR_MEM_HOST = 1 } asr_memory;
+
+typedef struct {
+  /* model shape: Hq % Hkv == 0; query head h reads KV head h / (Hq/Hkv) (GQA, R-gqa);
+   * head_dim in {16, 32, 64, 128, 256} */
+  int32_t n_layers, n_q_heads, n_kv_heads, head_dim;
+  int32_t batch;          /* B sequences in this context */
+  int32_t max_context;    /* tokens per sequence (capacity) */
+  int32_t kv_dtype;       /* asr_dtype of q, k, v (and of the pool) */
+  int32_t window;         /* K >= 1: positions >= n-K are never frozen (R-win) */
+  float tau;              /* threshold, strict s_j < tau */
+  float softness;         /* k > 0 of Eq. 3 */
+  int32_t history_window; /* W: 0 = infinite (R-W, the only value this build accepts) */
+  int32_t pinned_prefix;  /* positions < pinned_prefix are never frozen (R-sink, default 0) */
+  int32_t score_mode;     /* asr_score_mode */
+  int32_t tick_order;     /* asr_tick */
+  int32_t vocab;          /* logits row length for the entropy stage (0 = entropy off) */
+  float entropy_temperature;                  /* T_ent (R-ent), default 1 */
+  int32_t det_enable;     /* spike detector on (R-det) */
+  int32_t det_baseline;   /* previous entropies in the detector window (<= 256), default 64 */
+  int32_t det_cooldown;   /* ladder cooldown (R-ladder), default 16 */
+  int32_t wr_window;      /* N of WR "last N steps", default = window */
+  float det_z;            /* z threshold, default 3 */
+  float det_sigma_floor;  /* sigma floor in nats, default 0.05 */
+  int32_t fr_clear_counts;/* FR also clears detection counts (SPEC reading), default 0 */
+  int32_t host_mirror;    /* 1 = keep the write-once pinned host copy of every token's KV */
+  int32_t profile_stages; /* 1 = record CUDA events around every stage (asr_stage_times) */
+  int32_t device;         /* CUDA device ordinal */
+} asr_config;
+
+/* Fills *cfg with the paper's defaults (K=32, tau=0.5, k=2: P:112) and LLaMA-3-8B shape. */
+void asr_config_defaults(asr_config* cfg);
+
+/* Per-step buffers, owned by the CALLER and valid until the stream passes the step.
+ * memory = ASR_MEM_DEVICE: device pointers.  ASR_MEM_HOST: host pointers (pinned for
+ * asynchrony); the library copies inputs in and o/entropy out on the stream (counted in
+ * asr_stats_t.bytes_h2d / bytes_d2h). */
+typedef struct {
+  const void* q;           /* [B][L][Hq][d]  kv_dtype: the current query Q_i (Eq. 1-2) */
+  const void* k_new;       /* [B][L][Hkv][d] kv_dtype: K of the token appended this step */
+  const void* v_new;       /* [B][L][Hkv][d] kv_dtype */
+  const void* logits_prev; /* [B][vocab] or NULL: the previous step's output logits (Sec 3.6) */
+  int32_t logits_dtype;    /* ASR_KV_BF16 or ASR_KV_F32 */
+  int32_t memory;          /* asr_memory of every pointer in this struct */
+  float* o;                /* out [B][L][Hq][d] fp32 attention output over A_i */
+  float* entropy;          /* out [B] fp32 H(logits_prev), or NULL */
+} asr_step_io;
+
+typedef struct {
+  int64_t step;               /* index i of the last completed step (-1 before the first) */
+  int64_t total;              /* n = tokens held after that step */
+  int64_t attended;           /* |A_i| attended in that step */
+  int64_t active;             /* Active after the tick (Table 1/3 "Active KV" convention) */
+  int64_t frozen;             /* total - active */
+  int64_t frozen_this_step;   /* tokens given d>0 (incl. d=1 ones the same tick restores, R0) */
+  int64_t restored_this_step; /* tick restores + recovery + explicit asr_restore since last step */
+  double compression;         /* 1 - active/total (Tables 1/3) */
+  float entropy;              /* H(logits_prev) in nats */
+  int32_t entropy_valid;
+  int32_t recovery_action;    /* 0 none, 1 SR, 2 WR, 3 FR, 4 RR */
+  int32_t rewalk_requested;   /* RR: the caller should regenerate (needs the model; out of scope) */
+  int64_t bytes_h2d, bytes_d2h; /* host-link bytes moved by the library for this context so far */
+  uint32_t device_error;      /* latched invariant flags (0 = none) */
+} asr_stats_t;
+
+/* Host buffers for a full ledger snapshot of one sequence (any pointer may be NULL). */
+typedef struct {
+  uint8_t* residency;     /* [capacity] 1 Active, 0 Frozen (positions < total) */
+  int32_t* timer;         /* [capacity] d_j */
+  uint32_t* count;        /* [capacity] c_j */
+  int32_t* freeze_step;   /* [capacity] step of the last freeze, -1 never */
+  int32_t* active_list;   /* [capacity] A_i of the last step (sorted positions) */
+  int32_t* active_len;    /* [1] |A_i| */
+  float* scores;          /* [capacity] s_j per attended index of the last step */
+  int32_t capacity;       /* length of the arrays above (>= total) */
+} asr_ledger_view;
+
+/* Create a context: allocates the device KV pool [B][max_context][L][2][Hkv][d], the ledger and
+ * workspaces (and the pinned mirror if host_mirror), then prefills prompt_len[b] tokens of each
+ * sequence as Active with c = d = 0 (no decisions at prefill, R-prefill).
+ *   prompt_k, prompt_v: [B][prompt_stride][L][Hkv][d] kv_dtype in `memory` (NULL if all lengths 0)
+ *   prompt_len: host [B], 0 <= prompt_len[b] <= prompt_stride, prompt_len[b] < max_context
+ * Returns after the prompt copies complete.  *out is NULL on failure. */
+asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* prompt_v,
+                      const int32_t* prompt_len, int32_t prompt_stride, int32_t memory,
+                      void* cuda_stream, asr_ctx** out);
+
+/* One generation step for every sequence (asynchronous on cuda_stream, no host sync).
+ * ASR_E_CAPACITY if any sequence is full (nothing is changed). */
+asr_status asr_step(asr_ctx* ctx, const asr_step_io* io, void* cuda_stream);
+
+/* Explicit recovery at the boundary before the next step: SR restores frozen tokens with
+ * d > 1, WR those frozen in the last wr_window steps, FR all.  seq = -1 applies to all. */
+asr_status asr_restore(asr_ctx* ctx, int32_t seq, int32_t level, void* cuda_stream);
+
+/* Statistics of the last step for one sequence; optional ledger snapshot.  Synchronises the
+ * context's stream.  ASR_E_INVARIANT if a device invariant was violated. */
+asr_status asr_stats(asr_ctx* ctx, int32_t seq, asr_stats_t* out, asr_ledger_view* detail);
+
+/* Read the stored K/V of one token (all layers, [L][Hkv][d] each, kv_dtype) into host buffers,
+ * from the device pool (from_mirror = 0) or the pinned host mirror (1).  Synchronises. */
+asr_status asr_read_kv(asr_ctx* ctx, int32_t seq, int32_t pos, int32_t from_mirror, void* k_out,
+                       void* v_out);
+
+/* Accumulated device time per stage since the last call (needs profile_stages = 1):
+ * ms[0] entropy+detector, [1] append+recovery+compaction, [2] attention+score, [3] combine,
+ * [4] decide+tick; *launches = kernel launches of the library in that period.  Synchronises. */
+asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launches);
+
+/* Synchronise and free everything the context owns. */
+asr_status asr_destroy(asr_ctx* ctx);
+
+const char* asr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASR_H */

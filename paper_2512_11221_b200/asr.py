@@ -1,0 +1,270 @@
+"""Thin ctypes binding of libasr.so (include/asr.h) — argument marshalling only.
+
+Every step of the ASR-KF-EGR hot path runs in the library's sm_100a kernels; this module
+only converts torch tensors / numpy arrays into pointers.  There is no CPU fallback: if
+libasr.so is missing or no CUDA device is present, the calls raise.
+
+The function names are the C ABI's (asr_create, asr_step, asr_restore, asr_stats, asr_read_kv,
+asr_stage_times, asr_destroy); `Context` is a small convenience wrapper over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libasr.so")
+
+ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, ASR_E_STATE = 0, 1, 2, 3, 4, 5, 7
+KV_BF16, KV_F32 = 0, 1
+MEM_DEVICE, MEM_HOST = 0, 1
+SR, WR, FR = 1, 2, 3
+STAGES = ("entropy", "append_recover_compact", "attention_score", "combine", "decide_tick")
+
+
+class AsrError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"asr status {code}: {msg}")
+        self.code = code
+
+
+class asr_config(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("n_q_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("batch", ctypes.c_int32), ("max_context", ctypes.c_int32),
+                ("kv_dtype", ctypes.c_int32), ("window", ctypes.c_int32), ("tau", ctypes.c_float),
+                ("softness", ctypes.c_float), ("history_window", ctypes.c_int32),
+                ("pinned_prefix", ctypes.c_int32), ("score_mode", ctypes.c_int32), ("tick_order", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("entropy_temperature", ctypes.c_float), ("det_enable", ctypes.c_int32),
+                ("det_baseline", ctypes.c_int32), ("det_cooldown", ctypes.c_int32), ("wr_window", ctypes.c_int32),
+                ("det_z", ctypes.c_float), ("det_sigma_floor", ctypes.c_float), ("fr_clear_counts", ctypes.c_int32),
+                ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class asr_step_io(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_void_p), ("k_new", ctypes.c_void_p), ("v_new", ctypes.c_void_p),
+                ("logits_prev", ctypes.c_void_p), ("logits_dtype", ctypes.c_int32), ("memory", ctypes.c_int32),
+                ("o", ctypes.c_void_p), ("entropy", ctypes.c_void_p)]
+
+
+class asr_stats_t(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int64), ("total", ctypes.c_int64), ("attended", ctypes.c_int64),
+                ("active", ctypes.c_int64), ("frozen", ctypes.c_int64), ("frozen_this_step", ctypes.c_int64),
+                ("restored_this_step", ctypes.c_int64), ("compression", ctypes.c_double),
+                ("entropy", ctypes.c_float), ("entropy_valid", ctypes.c_int32),
+                ("recovery_action", ctypes.c_int32), ("rewalk_requested", ctypes.c_int32),
+                ("bytes_h2d", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64), ("device_error", ctypes.c_uint32)]
+
+
+class asr_ledger_view(ctypes.Structure):
+    _fields_ = [("residency", ctypes.c_void_p), ("timer", ctypes.c_void_p), ("count", ctypes.c_void_p),
+                ("freeze_step", ctypes.c_void_p), ("active_list", ctypes.c_void_p),
+                ("active_len", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("capacity", ctypes.c_int32)]
+
+
+EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
+           "asr_stage_times", "asr_destroy", "asr_last_error")
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libasr.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python tools/build.py` (needs nvcc, sm_100a)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32 = ctypes.c_void_p, ctypes.c_int32
+        L.asr_config_defaults.argtypes = [ctypes.POINTER(asr_config)]
+        L.asr_config_defaults.restype = None
+        L.asr_create.argtypes = [ctypes.POINTER(asr_config), vp, vp, vp, i32, i32, vp, ctypes.POINTER(vp)]
+        L.asr_step.argtypes = [vp, ctypes.POINTER(asr_step_io), vp]
+        L.asr_restore.argtypes = [vp, i32, i32, vp]
+        L.asr_stats.argtypes = [vp, i32, ctypes.POINTER(asr_stats_t), ctypes.POINTER(asr_ledger_view)]
+        L.asr_read_kv.argtypes = [vp, i32, i32, i32, vp, vp]
+        L.asr_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(ctypes.c_int64)]
+        L.asr_destroy.argtypes = [vp]
+        for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
+                  "asr_destroy"):
+            getattr(L, f).restype = ctypes.c_int
+        L.asr_last_error.argtypes = []
+        L.asr_last_error.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != ASR_OK:
+        raise AsrError(rc, lib().asr_last_error().decode())
+
+
+@dataclasses.dataclass
+class Config:
+    """Mirror of asr_config; defaults = the paper's K=32, tau=0.5, k=2 at LLaMA-3-8B shape."""
+    n_layers: int = 32
+    n_q_heads: int = 32
+    n_kv_heads: int = 8
+    head_dim: int = 128
+    batch: int = 1
+    max_context: int = 8192
+    kv_dtype: int = KV_BF16
+    window: int = 32
+    tau: float = 0.5
+    softness: float = 2.0
+    history_window: int = 0
+    pinned_prefix: int = 0
+    score_mode: int = 0
+    tick_order: int = 0
+    vocab: int = 128256
+    entropy_temperature: float = 1.0
+    det_enable: int = 1
+    det_baseline: int = 64
+    det_cooldown: int = 16
+    wr_window: int | None = None   # default: window
+    det_z: float = 3.0
+    det_sigma_floor: float = 0.05
+    fr_clear_counts: int = 0
+    host_mirror: int = 1
+    profile_stages: int = 0
+    device: int = 0
+
+    def c(self) -> asr_config:
+        v = dataclasses.asdict(self)
+        if v["wr_window"] is None:
+            v["wr_window"] = self.window
+        return asr_config(**v)
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data
+    assert x.is_contiguous(), "tensors must be contiguous"
+    return x.data_ptr()
+
+
+def _is_host(x) -> bool:
+    return isinstance(x, np.ndarray) or not x.is_cuda
+
+
+def _dtype_code(x) -> int:
+    if isinstance(x, np.ndarray):
+        return KV_BF16 if x.dtype == np.uint16 else KV_F32
+    import torch
+    return KV_BF16 if x.dtype == torch.bfloat16 else KV_F32
+
+
+def _stream(stream) -> int:
+    if stream is not None:
+        return int(stream)
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def asr_create(cfg: Config, prompt_k, prompt_v, prompt_len, stream=None) -> ctypes.c_void_p:
+    """prompt_k/v: [B][P_max][L][Hkv][d] (torch CUDA, torch CPU or numpy); prompt_len: ints [B]."""
+    c = cfg.c()
+    pl = np.ascontiguousarray(np.asarray(prompt_len, np.int32))
+    stride = int(prompt_k.shape[1]) if prompt_k is not None and prompt_k.ndim >= 2 else 0
+    mem = MEM_HOST if prompt_k is None or _is_host(prompt_k) else MEM_DEVICE
+    out = ctypes.c_void_p()
+    _check(lib().asr_create(ctypes.byref(c), _ptr(prompt_k), _ptr(prompt_v), pl.ctypes.data, stride, mem,
+                            _stream(stream), ctypes.byref(out)))
+    return out
+
+
+def asr_step(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None) -> None:
+    io = asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
+                     _dtype_code(logits_prev) if logits_prev is not None else 0,
+                     MEM_HOST if _is_host(q) else MEM_DEVICE, _ptr(o), _ptr(entropy))
+    _check(lib().asr_step(ctx, ctypes.byref(io), _stream(stream)))
+
+
+def asr_restore(ctx, seq: int, level: int, stream=None) -> None:
+    _check(lib().asr_restore(ctx, seq, level, _stream(stream)))
+
+
+def asr_stats(ctx, seq: int, capacity: int = 0, detail: bool = False) -> dict:
+    st = asr_stats_t()
+    view = None
+    arrays = {}
+    if detail:
+        arrays = {"residency": np.zeros(capacity, np.uint8), "timer": np.zeros(capacity, np.int32),
+                  "count": np.zeros(capacity, np.uint32), "freeze_step": np.zeros(capacity, np.int32),
+                  "active_list": np.zeros(capacity, np.int32), "active_len": np.zeros(1, np.int32),
+                  "scores": np.zeros(capacity, np.float32)}
+        view = asr_ledger_view(*(arrays[k].ctypes.data for k in ("residency", "timer", "count", "freeze_step",
+                                                                 "active_list", "active_len", "scores")),
+                               capacity)
+    _check(lib().asr_stats(ctx, seq, ctypes.byref(st), ctypes.byref(view) if view is not None else None))
+    out = {f[0]: getattr(st, f[0]) for f in asr_stats_t._fields_}
+    if detail:
+        n, A = int(st.total), int(arrays["active_len"][0])
+        out["ledger"] = {k: arrays[k][:n] for k in ("residency", "timer", "count", "freeze_step")}
+        out["active_list"] = arrays["active_list"][:A]
+        out["scores"] = arrays["scores"][:A]
+    return out
+
+
+def asr_read_kv(ctx, cfg: Config, seq: int, pos: int, from_mirror: bool = False):
+    dt = np.uint16 if cfg.kv_dtype == KV_BF16 else np.float32
+    k = np.zeros((cfg.n_layers, cfg.n_kv_heads, cfg.head_dim), dt)
+    v = np.zeros_like(k)
+    _check(lib().asr_read_kv(ctx, seq, pos, int(from_mirror), k.ctypes.data, v.ctypes.data))
+    return k, v
+
+
+def asr_stage_times(ctx):
+    ms = (ctypes.c_double * len(STAGES))()
+    n = ctypes.c_int64()
+    _check(lib().asr_stage_times(ctx, ms, len(STAGES), ctypes.byref(n)))
+    return list(ms), int(n.value)
+
+
+def asr_destroy(ctx) -> None:
+    _check(lib().asr_destroy(ctx))
+
+
+class Context:
+    """Convenience owner of one asr_ctx."""
+
+    def __init__(self, cfg: Config, prompt_k, prompt_v, prompt_len, stream=None):
+        self.cfg = cfg
+        self._h = asr_create(cfg, prompt_k, prompt_v, prompt_len, stream)
+
+    def step(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None):
+        asr_step(self._h, q, k_new, v_new, o, logits_prev, entropy, stream)
+
+    def restore(self, seq: int, level: int, stream=None):
+        asr_restore(self._h, seq, level, stream)
+
+    def stats(self, seq: int, detail: bool = False) -> dict:
+        return asr_stats(self._h, seq, self.cfg.max_context, detail)
+
+    def read_kv(self, seq: int, pos: int, from_mirror: bool = False):
+        return asr_read_kv(self._h, self.cfg, seq, pos, from_mirror)
+
+    def stage_times(self):
+        return asr_stage_times(self._h)
+
+    def close(self):
+        if self._h:
+            asr_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

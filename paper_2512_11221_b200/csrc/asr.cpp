@@ -1,0 +1,522 @@
+// paper_2512_11221_b200/csrc/asr.cpp — host side of libasr.so: the C ABI of include/asr.h.
+// Owns the device KV pool, ledger, workspaces, the write-once pinned host mirror and the
+// side stream that fills it; launches one step as a fixed sequence of kernels on the caller's
+// stream with no host synchronisation.
+#include "asr.h"
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <array>
+#include <string>
+#include <vector>
+
+#include "asr_internal.h"
+
+using asr::DevState;
+
+namespace {
+
+thread_local std::string g_err;
+
+asr_status fail(asr_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? ASR_E_OOM : ASR_E_CUDA,                \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+}  // namespace
+
+struct asr_ctx {
+  asr_config cfg{};
+  DevState s{};
+  int num_sms = 0;
+  int attn_grid = 0;
+  size_t kv_elem = 2;
+  size_t tok_bytes = 0;          // one token, all layers, K and V
+  std::vector<int32_t> prompt_len;
+  bool uniform_prompt = true;
+  int64_t step = 0;              // host mirror of the device step counter
+  void* host_mirror = nullptr;   // pinned [B][max_ctx][L][2][Hkv][d]
+  cudaStream_t side = nullptr;   // mirror copies
+  cudaEvent_t ev_append = nullptr, ev_mirror = nullptr;
+  cudaStream_t last_stream = nullptr;
+  // ASR_MEM_HOST staging
+  void* st_q = nullptr;
+  void* st_k = nullptr;
+  void* st_v = nullptr;
+  void* st_logits = nullptr;
+  size_t st_logits_bytes = 0;
+  float* st_o = nullptr;
+  float* st_ent = nullptr;
+  int64_t bytes_h2d = 0, bytes_d2h = 0;
+  int64_t launches = 0;
+  // stage profiling
+  std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_pending;
+  std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_free;
+  std::vector<void*> allocs;
+
+  ~asr_ctx() {
+    for (void* p : allocs) cudaFree(p);
+    if (host_mirror) cudaFreeHost(host_mirror);
+    if (side) cudaStreamDestroy(side);
+    if (ev_append) cudaEventDestroy(ev_append);
+    if (ev_mirror) cudaEventDestroy(ev_mirror);
+    for (auto& a : prof_pending)
+      for (auto e : a) cudaEventDestroy(e);
+    for (auto& a : prof_free)
+      for (auto e : a) cudaEventDestroy(e);
+  }
+
+  template <typename P>
+  cudaError_t alloc(P** p, size_t bytes) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, bytes ? bytes : 16);
+    if (e == cudaSuccess) {
+      allocs.push_back(v);
+      *p = reinterpret_cast<P*>(v);
+    }
+    return e;
+  }
+};
+
+extern "C" {
+
+const char* asr_last_error(void) { return g_err.c_str(); }
+
+void asr_config_defaults(asr_config* c) {
+  memset(c, 0, sizeof(*c));
+  c->n_layers = 32;
+  c->n_q_heads = 32;
+  c->n_kv_heads = 8;
+  c->head_dim = 128;
+  c->batch = 1;
+  c->max_context = 8192;
+  c->kv_dtype = ASR_KV_BF16;
+  c->window = 32;
+  c->tau = 0.5f;
+  c->softness = 2.0f;
+  c->history_window = 0;
+  c->pinned_prefix = 0;
+  c->score_mode = ASR_SCORE_RAW;
+  c->tick_order = ASR_TICK_LITERAL;
+  c->vocab = 128256;
+  c->entropy_temperature = 1.0f;
+  c->det_enable = 1;
+  c->det_baseline = 64;
+  c->det_cooldown = 16;
+  c->wr_window = 32;
+  c->det_z = 3.0f;
+  c->det_sigma_floor = 0.05f;
+  c->fr_clear_counts = 0;
+  c->host_mirror = 1;
+  c->profile_stages = 0;
+  c->device = 0;
+}
+
+static asr_status validate(const asr_config* c) {
+  if (!c) return fail(ASR_E_INVALID, "config is NULL");
+  if (c->n_layers < 1 || c->n_layers > 128) return fail(ASR_E_INVALID, "n_layers out of range [1,128]");
+  if (c->n_kv_heads < 1 || c->n_kv_heads > 32) return fail(ASR_E_INVALID, "n_kv_heads out of range [1,32]");
+  if (c->n_q_heads < 1 || c->n_q_heads % c->n_kv_heads)
+    return fail(ASR_E_INVALID, "n_q_heads must be a positive multiple of n_kv_heads");
+  if (c->n_q_heads / c->n_kv_heads > 8) return fail(ASR_E_INVALID, "at most 8 query heads per KV head");
+  int d = c->head_dim;
+  if (d != 16 && d != 32 && d != 64 && d != 128 && d != 256)
+    return fail(ASR_E_INVALID, "head_dim must be one of 16, 32, 64, 128, 256");
+  if (c->batch < 1 || c->batch > 4096) return fail(ASR_E_INVALID, "batch out of range [1,4096]");
+  if (c->max_context < 2 || c->max_context > (1 << 20)) return fail(ASR_E_INVALID, "max_context out of range");
+  if (c->kv_dtype != ASR_KV_BF16 && c->kv_dtype != ASR_KV_F32) return fail(ASR_E_INVALID, "kv_dtype");
+  if (c->window < 1) return fail(ASR_E_INVALID, "window (K) must be >= 1");
+  if (!(c->softness > 0.f) || !isfinite(c->softness)) return fail(ASR_E_INVALID, "softness k must be > 0");
+  if (!isfinite(c->tau)) return fail(ASR_E_INVALID, "tau must be finite");
+  if (c->history_window != 0)
+    return fail(ASR_E_INVALID, "history_window: only W = 0 (infinite, R-W) is supported");
+  if (c->pinned_prefix < 0) return fail(ASR_E_INVALID, "pinned_prefix < 0");
+  if (c->score_mode != ASR_SCORE_RAW && c->score_mode != ASR_SCORE_SCALED) return fail(ASR_E_INVALID, "score_mode");
+  if (c->tick_order != ASR_TICK_LITERAL && c->tick_order != ASR_TICK_SKIP_NEW) return fail(ASR_E_INVALID, "tick_order");
+  if (c->vocab < 0 || c->vocab >= (1 << 24)) return fail(ASR_E_INVALID, "vocab out of range");
+  if (c->vocab > 0 && !(c->entropy_temperature > 0.f)) return fail(ASR_E_INVALID, "entropy_temperature must be > 0");
+  if (c->det_baseline < 1 || c->det_baseline > asr::kMaxDetBaseline)
+    return fail(ASR_E_INVALID, "det_baseline out of range [1,256]");
+  if (c->det_cooldown < 0 || c->wr_window < 0) return fail(ASR_E_INVALID, "det_cooldown / wr_window < 0");
+  return ASR_OK;
+}
+
+asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* prompt_v,
+                      const int32_t* prompt_len, int32_t prompt_stride, int32_t memory, void* cuda_stream,
+                      asr_ctx** out) {
+  if (!out) return fail(ASR_E_INVALID, "out is NULL");
+  *out = nullptr;
+  asr_status v = validate(cfg);
+  if (v) return v;
+  if (!prompt_len) return fail(ASR_E_INVALID, "prompt_len is NULL");
+  if (memory != ASR_MEM_DEVICE && memory != ASR_MEM_HOST) return fail(ASR_E_INVALID, "memory");
+  int32_t pmax = 0;
+  for (int b = 0; b < cfg->batch; ++b) {
+    if (prompt_len[b] < 0 || prompt_len[b] > prompt_stride || prompt_len[b] >= cfg->max_context)
+      return fail(ASR_E_INVALID, "prompt_len[b] must be in [0, min(prompt_stride, max_context-1)]");
+    pmax = prompt_len[b] > pmax ? prompt_len[b] : pmax;
+  }
+  if (pmax > 0 && (!prompt_k || !prompt_v)) return fail(ASR_E_INVALID, "prompt_k / prompt_v is NULL");
+  CUDA_TRY(cudaSetDevice(cfg->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+
+  asr_ctx* c = new asr_ctx();
+  c->cfg = *cfg;
+  c->prompt_len.assign(prompt_len, prompt_len + cfg->batch);
+  for (int b = 1; b < cfg->batch; ++b) c->uniform_prompt &= prompt_len[b] == prompt_len[0];
+  asr_status rc = [&]() -> asr_status {
+    DevState& s = c->s;
+    s.B = cfg->batch;
+    s.L = cfg->n_layers;
+    s.Hq = cfg->n_q_heads;
+    s.Hkv = cfg->n_kv_heads;
+    s.d = cfg->head_dim;
+    s.max_ctx = cfg->max_context;
+    s.dtype = cfg->kv_dtype;
+    s.window = cfg->window;
+    s.pinned = cfg->pinned_prefix;
+    s.tick_skip_new = cfg->tick_order == ASR_TICK_SKIP_NEW;
+    s.score_scaled = cfg->score_mode == ASR_SCORE_SCALED;
+    s.tau = cfg->tau;
+    s.softness = cfg->softness;
+    s.softness_int = (floorf(cfg->softness) == cfg->softness && cfg->softness <= 65535.f) ? (int)cfg->softness : 0;
+    s.vocab = cfg->vocab;
+    s.ent_temp = cfg->entropy_temperature;
+    s.det_enable = cfg->det_enable;
+    s.det_baseline = cfg->det_baseline;
+    s.det_cooldown = cfg->det_cooldown;
+    s.wr_window = cfg->wr_window;
+    s.fr_clear_counts = cfg->fr_clear_counts;
+    s.det_z = cfg->det_z;
+    s.det_sigma_floor = cfg->det_sigma_floor;
+    CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    // split-KV policy: enough work items to fill the SMs; fp32 KV keeps chunks <= 256 tokens
+    s.chunk_min = 64;
+    long want = (8L * c->num_sms + (long)s.B * s.L - 1) / ((long)s.B * s.L);
+    if (s.dtype == ASR_KV_F32) {
+      long acc = (s.max_ctx + 255) / 256;
+      want = want > acc ? want : acc;
+    }
+    long cap = (s.max_ctx + s.chunk_min - 1) / s.chunk_min;
+    s.max_splits = (int)(want < 1 ? 1 : want > cap ? cap : want);
+    if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
+
+    c->kv_elem = s.dtype == ASR_KV_BF16 ? 2 : 4;
+    c->tok_bytes = (size_t)s.L * 2 * s.Hkv * s.d * c->kv_elem;
+    const size_t BT = (size_t)s.B * s.max_ctx;
+    CUDA_TRY(c->alloc(&s.kv, BT * c->tok_bytes));
+    CUDA_TRY(c->alloc(&s.res, BT));
+    CUDA_TRY(c->alloc(&s.timer, BT * 4));
+    CUDA_TRY(c->alloc(&s.count, BT * 4));
+    CUDA_TRY(c->alloc(&s.fstep, BT * 4));
+    CUDA_TRY(c->alloc(&s.prompt_len, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.step, 4));
+    CUDA_TRY(c->alloc(&s.act_pos, BT * 4));
+    CUDA_TRY(c->alloc(&s.act_len, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.item_start, (size_t)(s.B + 1) * 4));
+    CUDA_TRY(c->alloc(&s.score_part, BT * s.L * 4));
+    CUDA_TRY(c->alloc(&s.score, BT * 4));
+    const size_t max_items = (size_t)s.B * s.L * s.max_splits;
+    CUDA_TRY(c->alloc(&s.part_ml, max_items * s.Hq * 2 * 4));
+    CUDA_TRY(c->alloc(&s.part_acc, max_items * s.Hq * s.d * 4));
+    CUDA_TRY(c->alloc(&s.ent_part, (size_t)s.B * asr::kEntSplits * 3 * 4));
+    CUDA_TRY(c->alloc(&s.ent_ticket, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.hist, (size_t)s.B * s.det_baseline * 8));
+    CUDA_TRY(c->alloc(&s.det, (size_t)s.B * sizeof(asr::DetState)));
+    CUDA_TRY(c->alloc(&s.rec_action, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.stats, (size_t)s.B * sizeof(asr::SeqStats)));
+    CUDA_TRY(c->alloc(&s.err, 4));
+    CUDA_TRY(c->alloc(&s.ticket, 4));
+    // ledger init: prompt tokens Active, c = d = 0 (R-prefill); everything else zero
+    CUDA_TRY(cudaMemsetAsync(s.res, 0, BT, st));
+    CUDA_TRY(cudaMemsetAsync(s.timer, 0, BT * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.count, 0, BT * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.fstep, 0xff, BT * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.step, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.ent_ticket, 0, (size_t)s.B * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.det, 0, (size_t)s.B * sizeof(asr::DetState), st));
+    CUDA_TRY(cudaMemsetAsync(s.rec_action, 0, (size_t)s.B * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.stats, 0, (size_t)s.B * sizeof(asr::SeqStats), st));
+    CUDA_TRY(cudaMemsetAsync(s.err, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.ticket, 0, 4, st));
+    CUDA_TRY(cudaMemcpyAsync(s.prompt_len, prompt_len, (size_t)s.B * 4, cudaMemcpyHostToDevice, st));
+    for (int b = 0; b < s.B; ++b)
+      if (prompt_len[b] > 0) CUDA_TRY(cudaMemsetAsync(s.res + (size_t)b * s.max_ctx, 1, prompt_len[b], st));
+    if (cfg->host_mirror) {
+      cudaError_t e = cudaHostAlloc(&c->host_mirror, BT * c->tok_bytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return fail(ASR_E_OOM, "pinned host mirror allocation failed");
+    }
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_mirror, cudaEventDisableTiming));
+    // prompt KV: [B][stride][L][Hkv][d] K and V -> slots [L][2][Hkv][d]
+    const size_t row = (size_t)s.Hkv * s.d * c->kv_elem;  // K (or V) bytes per token-layer
+    const cudaMemcpyKind kind = memory == ASR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    for (int b = 0; b < s.B; ++b) {
+      if (prompt_len[b] == 0) continue;
+      const size_t rows = (size_t)prompt_len[b] * s.L;
+      const size_t src_off = (size_t)b * prompt_stride * s.L * row;
+      char* dst = (char*)s.kv + (size_t)b * s.max_ctx * c->tok_bytes;
+      CUDA_TRY(cudaMemcpy2DAsync(dst, 2 * row, (const char*)prompt_k + src_off, row, row, rows, kind, st));
+      CUDA_TRY(cudaMemcpy2DAsync(dst + row, 2 * row, (const char*)prompt_v + src_off, row, row, rows, kind, st));
+      if (c->host_mirror) {
+        char* hdst = (char*)c->host_mirror + (size_t)b * s.max_ctx * c->tok_bytes;
+        CUDA_TRY(cudaMemcpyAsync(hdst, dst, (size_t)prompt_len[b] * c->tok_bytes, cudaMemcpyDeviceToHost, st));
+        c->bytes_d2h += (int64_t)prompt_len[b] * c->tok_bytes;
+      }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    c->attn_grid = asr::attention_grid(s, c->num_sms);
+    c->last_stream = st;
+    return ASR_OK;
+  }();
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return ASR_OK;
+}
+
+static asr_status ensure_staging(asr_ctx* c, bool logits, int logits_dtype) {
+  const DevState& s = c->s;
+  if (!c->st_q) {
+    CUDA_TRY(c->alloc(&c->st_q, (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&c->st_k, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&c->st_v, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&c->st_o, (size_t)s.B * s.L * s.Hq * s.d * 4));
+    CUDA_TRY(c->alloc(&c->st_ent, (size_t)s.B * 4));
+  }
+  if (logits) {
+    size_t need = (size_t)s.B * s.vocab * (logits_dtype == ASR_KV_BF16 ? 2 : 4);
+    if (need > c->st_logits_bytes) {
+      CUDA_TRY(c->alloc(&c->st_logits, need));
+      c->st_logits_bytes = need;
+    }
+  }
+  return ASR_OK;
+}
+
+static cudaError_t prof_mark(asr_ctx* c, std::array<cudaEvent_t, asr::kStages + 1>* ev, int k, cudaStream_t st) {
+  if (!ev) return cudaSuccess;
+  return cudaEventRecord((*ev)[k], st);
+}
+
+asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!io || !io->q || !io->k_new || !io->v_new || !io->o) return fail(ASR_E_INVALID, "io has NULL q/k_new/v_new/o");
+  if (io->memory != ASR_MEM_DEVICE && io->memory != ASR_MEM_HOST) return fail(ASR_E_INVALID, "io->memory");
+  const DevState& s = c->s;
+  const bool has_logits = io->logits_prev != nullptr && s.vocab > 0;
+  if (has_logits && io->logits_dtype != ASR_KV_BF16 && io->logits_dtype != ASR_KV_F32)
+    return fail(ASR_E_INVALID, "logits_dtype");
+  for (int b = 0; b < s.B; ++b)
+    if (c->prompt_len[b] + c->step + 1 > s.max_ctx)
+      return fail(ASR_E_CAPACITY, "sequence " + std::to_string(b) + " is at max_context");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  const void* q = io->q;
+  const void* kn = io->k_new;
+  const void* vn = io->v_new;
+  const void* lg = io->logits_prev;
+  float* o = io->o;
+  float* ent = io->entropy;
+  if (io->memory == ASR_MEM_HOST) {
+    asr_status r = ensure_staging(c, has_logits, io->logits_dtype);
+    if (r) return r;
+    const size_t qb = (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem;
+    const size_t kb = (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem;
+    CUDA_TRY(cudaMemcpyAsync(c->st_q, q, qb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(c->st_k, kn, kb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(c->st_v, vn, kb, cudaMemcpyHostToDevice, st));
+    c->bytes_h2d += (int64_t)(qb + 2 * kb);
+    if (has_logits) {
+      const size_t lb = (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
+      CUDA_TRY(cudaMemcpyAsync(c->st_logits, lg, lb, cudaMemcpyHostToDevice, st));
+      c->bytes_h2d += (int64_t)lb;
+      lg = c->st_logits;
+    }
+    q = c->st_q;
+    kn = c->st_k;
+    vn = c->st_v;
+    o = c->st_o;
+    ent = ent ? c->st_ent : nullptr;
+  }
+  std::array<cudaEvent_t, asr::kStages + 1>* ev = nullptr;
+  if (c->cfg.profile_stages) {
+    if (c->prof_free.empty()) {
+      std::array<cudaEvent_t, asr::kStages + 1> a;
+      for (auto& e : a) CUDA_TRY(cudaEventCreate(&e));
+      c->prof_free.push_back(a);
+    }
+    c->prof_pending.push_back(c->prof_free.back());
+    c->prof_free.pop_back();
+    ev = &c->prof_pending.back();
+  }
+  CUDA_TRY(prof_mark(c, ev, 0, st));
+  if (has_logits) {
+    CUDA_TRY(asr::launch_entropy(s, lg, io->logits_dtype, ent, st));
+    c->launches++;
+  }
+  CUDA_TRY(prof_mark(c, ev, 1, st));
+  CUDA_TRY(asr::launch_ledger_pre(s, kn, vn, has_logits ? 1 : 0, st));
+  CUDA_TRY(prof_mark(c, ev, 2, st));
+  CUDA_TRY(asr::launch_attention(s, q, c->attn_grid, st));
+  CUDA_TRY(prof_mark(c, ev, 3, st));
+  CUDA_TRY(asr::launch_combine(s, o, st));
+  CUDA_TRY(prof_mark(c, ev, 4, st));
+  CUDA_TRY(asr::launch_decide(s, st));
+  CUDA_TRY(prof_mark(c, ev, 5, st));
+  c->launches += 4;
+  // (a5) write-once host mirror of the appended token (side stream, overlapped with compute)
+  if (c->host_mirror) {
+    CUDA_TRY(cudaEventRecord(c->ev_append, st));
+    CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_append, 0));
+    const size_t pitch = (size_t)s.max_ctx * c->tok_bytes;
+    if (c->uniform_prompt) {
+      const size_t off = (size_t)(c->prompt_len[0] + c->step) * c->tok_bytes;
+      CUDA_TRY(cudaMemcpy2DAsync((char*)c->host_mirror + off, pitch, (const char*)s.kv + off, pitch,
+                                 c->tok_bytes, s.B, cudaMemcpyDeviceToHost, c->side));
+    } else {
+      for (int b = 0; b < s.B; ++b) {
+        const size_t off = (size_t)b * pitch + (size_t)(c->prompt_len[b] + c->step) * c->tok_bytes;
+        CUDA_TRY(cudaMemcpyAsync((char*)c->host_mirror + off, (const char*)s.kv + off, c->tok_bytes,
+                                 cudaMemcpyDeviceToHost, c->side));
+      }
+    }
+    c->bytes_d2h += (int64_t)s.B * c->tok_bytes;
+  }
+  if (io->memory == ASR_MEM_HOST) {
+    const size_t ob = (size_t)s.B * s.L * s.Hq * s.d * 4;
+    CUDA_TRY(cudaMemcpyAsync(io->o, o, ob, cudaMemcpyDeviceToHost, st));
+    c->bytes_d2h += (int64_t)ob;
+    if (io->entropy && has_logits) {
+      CUDA_TRY(cudaMemcpyAsync(io->entropy, ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, st));
+      c->bytes_d2h += (int64_t)s.B * 4;
+    }
+  }
+  c->step++;
+  c->last_stream = st;
+  return ASR_OK;
+}
+
+asr_status asr_restore(asr_ctx* c, int32_t seq, int32_t level, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (seq < -1 || seq >= c->s.B) return fail(ASR_E_INVALID, "seq out of range");
+  if (level != ASR_SR && level != ASR_WR && level != ASR_FR) return fail(ASR_E_INVALID, "level must be SR, WR or FR");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(asr::launch_restore(c->s, seq, level, (cudaStream_t)cuda_stream));
+  c->launches++;
+  c->last_stream = (cudaStream_t)cuda_stream;
+  return ASR_OK;
+}
+
+asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view* detail) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (seq < 0 || seq >= c->s.B) return fail(ASR_E_INVALID, "seq out of range");
+  if (!out) return fail(ASR_E_INVALID, "out is NULL");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaStreamSynchronize(c->last_stream));
+  CUDA_TRY(cudaStreamSynchronize(c->side));
+  const DevState& s = c->s;
+  asr::SeqStats st;
+  uint32_t err = 0;
+  CUDA_TRY(cudaMemcpy(&st, s.stats + seq, sizeof(st), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&err, s.err, 4, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof(*out));
+  const int64_t n = c->prompt_len[seq] + c->step;
+  out->step = c->step - 1;
+  out->total = n;
+  out->attended = st.attended;
+  out->active = c->step > 0 ? st.active_post : n;
+  out->frozen = n - out->active;
+  out->frozen_this_step = st.frozen_this_step;
+  out->restored_this_step = st.restored_this_step;
+  out->compression = n > 0 ? 1.0 - (double)out->active / (double)n : 0.0;
+  out->entropy = st.entropy;
+  out->entropy_valid = st.entropy_valid;
+  out->recovery_action = st.recovery_action;
+  out->rewalk_requested = st.rewalk_requested;
+  out->bytes_h2d = c->bytes_h2d;
+  out->bytes_d2h = c->bytes_d2h;
+  out->device_error = err;
+  if (detail) {
+    if (detail->capacity < n) return fail(ASR_E_INVALID, "detail->capacity < total");
+    const size_t base = (size_t)seq * s.max_ctx;
+    if (detail->residency) CUDA_TRY(cudaMemcpy(detail->residency, s.res + base, n, cudaMemcpyDeviceToHost));
+    if (detail->timer) CUDA_TRY(cudaMemcpy(detail->timer, s.timer + base, n * 4, cudaMemcpyDeviceToHost));
+    if (detail->count) CUDA_TRY(cudaMemcpy(detail->count, s.count + base, n * 4, cudaMemcpyDeviceToHost));
+    if (detail->freeze_step) CUDA_TRY(cudaMemcpy(detail->freeze_step, s.fstep + base, n * 4, cudaMemcpyDeviceToHost));
+    int32_t A = 0;
+    CUDA_TRY(cudaMemcpy(&A, s.act_len + seq, 4, cudaMemcpyDeviceToHost));
+    if (c->step == 0) A = 0;
+    if (detail->active_len) *detail->active_len = A;
+    if (detail->active_list && A) CUDA_TRY(cudaMemcpy(detail->active_list, s.act_pos + base, (size_t)A * 4, cudaMemcpyDeviceToHost));
+    if (detail->scores && A) CUDA_TRY(cudaMemcpy(detail->scores, s.score + base, (size_t)A * 4, cudaMemcpyDeviceToHost));
+  }
+  if (err) return fail(ASR_E_INVARIANT, "device invariant violation, flags=" + std::to_string(err));
+  return ASR_OK;
+}
+
+asr_status asr_read_kv(asr_ctx* c, int32_t seq, int32_t pos, int32_t from_mirror, void* k_out, void* v_out) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  const DevState& s = c->s;
+  if (seq < 0 || seq >= s.B) return fail(ASR_E_INVALID, "seq out of range");
+  if (pos < 0 || pos >= c->prompt_len[seq] + c->step) return fail(ASR_E_INVALID, "pos not stored");
+  if (from_mirror && !c->host_mirror) return fail(ASR_E_INVALID, "no host mirror");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaStreamSynchronize(c->last_stream));
+  CUDA_TRY(cudaStreamSynchronize(c->side));
+  std::vector<char> tok(c->tok_bytes);
+  const size_t off = ((size_t)seq * s.max_ctx + pos) * c->tok_bytes;
+  if (from_mirror) memcpy(tok.data(), (const char*)c->host_mirror + off, c->tok_bytes);
+  else CUDA_TRY(cudaMemcpy(tok.data(), (const char*)s.kv + off, c->tok_bytes, cudaMemcpyDeviceToHost));
+  const size_t row = (size_t)s.Hkv * s.d * c->kv_elem;
+  for (int l = 0; l < s.L; ++l) {
+    if (k_out) memcpy((char*)k_out + l * row, tok.data() + (2 * l) * row, row);
+    if (v_out) memcpy((char*)v_out + l * row, tok.data() + (2 * l + 1) * row, row);
+  }
+  return ASR_OK;
+}
+
+asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!ms || n < asr::kStages) return fail(ASR_E_INVALID, "ms must hold 5 values");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaStreamSynchronize(c->last_stream));
+  for (int k = 0; k < n; ++k) ms[k] = 0.0;
+  for (auto& a : c->prof_pending) {
+    for (int k = 0; k < asr::kStages; ++k) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, a[k], a[k + 1]));
+      ms[k] += t;
+    }
+    c->prof_free.push_back(a);
+  }
+  c->prof_pending.clear();
+  if (launches) *launches = c->launches;
+  c->launches = 0;
+  return ASR_OK;
+}
+
+asr_status asr_destroy(asr_ctx* c) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  cudaSetDevice(c->cfg.device);
+  cudaStreamSynchronize(c->last_stream);
+  cudaStreamSynchronize(c->side);
+  delete c;
+  return ASR_OK;
+}
+
+}  // extern "C"

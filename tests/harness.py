@@ -1,0 +1,172 @@
+"""Parity harness: drives the CUDA path (through the C ABI) and the fp64 oracle on the same seeded
+inputs, step by step, and compares them element by element.
+
+Bars (BASELINE.json north_star):
+- attended index lists, ledgers (residency, timer, count, freeze step) and per-step counters:
+  bit-exact;
+- Eq. 2 scores: exactly equal on LAT inputs (exact in fp32 in any summation order);
+- attention O: max over (b, l, h) of max_e |o - o*| / max_e |o*|  <= 2e-3 (bf16 KV) / 1e-5 (fp32 KV);
+- entropy: |H - H*| <= 1e-4 nats.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+import gen
+import oracle
+
+TOL_O = {"bf16": 2e-3, "f32": 1e-5}
+TOL_H = 1e-4
+
+
+@dataclasses.dataclass
+class Case:
+    L: int = 1
+    Hq: int = 2
+    Hkv: int = 2
+    d: int = 16
+    B: int = 1
+    prompt: tuple = (32,)
+    steps: int = 32
+    window: int = 16
+    tau: float = 0.5
+    softness: float = 2.0
+    dtype: str = "bf16"
+    seed: int = 1001
+    family: int = gen.LAT
+    hot_permille: int = 0
+    a_hot: int = 4
+    vocab: int = 0
+    spike_first: int = -1
+    spike_period: int = 0
+    spike_count: int = 0
+    needle_pos: int = -1
+    query_first: int = -1
+    query_count: int = 0
+    tick_order: int = 0
+    score_mode: int = 0
+    pinned_prefix: int = 0
+    wr_window: int | None = None
+    host_io: bool = False          # pass host (numpy) buffers through the C ABI
+    restore_at: dict = dataclasses.field(default_factory=dict)  # step -> (seq, level) explicit restore
+    max_context: int = 0
+
+    def gen_params(self) -> gen.GenParams:
+        return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
+                             hot_permille=self.hot_permille, a_hot=self.a_hot, needle_pos=self.needle_pos,
+                             query_first=self.query_first, query_count=self.query_count, vocab=self.vocab,
+                             spike_first=self.spike_first, spike_period=self.spike_period,
+                             spike_count=self.spike_count)
+
+    def capacity(self) -> int:
+        return self.max_context or (max(self.prompt) + self.steps + 1)
+
+
+def orc_cfg(c: Case) -> oracle.OrcCfg:
+    return oracle.OrcCfg(L=c.L, Hq=c.Hq, Hkv=c.Hkv, d=c.d, window=c.window, tau=c.tau, softness=c.softness,
+                         pinned_prefix=c.pinned_prefix, score_scaled=c.score_mode, tick_skip_new=c.tick_order,
+                         vocab=c.vocab, wr_window=c.wr_window)
+
+
+def asr_cfg(c: Case):
+    from paper_2512_11221_b200 import Config, KV_BF16, KV_F32
+    return Config(n_layers=c.L, n_q_heads=c.Hq, n_kv_heads=c.Hkv, head_dim=c.d, batch=c.B,
+                  max_context=c.capacity(), kv_dtype=KV_BF16 if c.dtype == "bf16" else KV_F32,
+                  window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
+                  score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window)
+
+
+def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:
+    """max over rows (b, l, h) of max_e |o - o*| / max_e |o*|."""
+    num = np.abs(o.astype(np.float64) - o_ref).max(-1)
+    den = np.abs(o_ref).max(-1)
+    return float((num / den).max())
+
+
+def run(c: Case, check_o: bool = True) -> dict:
+    """Run c.steps steps on GPU and oracle; assert parity at every step.  Returns a summary."""
+    import torch
+    from paper_2512_11221_b200 import Context
+
+    p = c.gen_params()
+    cap = c.capacity()
+    P = list(c.prompt)
+    assert len(P) == c.B
+    Pmax = max(P)
+    npd = np.uint16 if c.dtype == "bf16" else np.float32
+    tdt = torch.bfloat16 if c.dtype == "bf16" else torch.float32
+    # full K/V per sequence (positions beyond n are unused until appended)
+    KV = [gen.kv(p, b, 0, cap, c.dtype) for b in range(c.B)]
+    pk = np.zeros((c.B, max(Pmax, 1), c.L, c.Hkv, c.d), npd)
+    pv = np.zeros_like(pk)
+    for b in range(c.B):
+        pk[b, :P[b]] = KV[b][0][:P[b]]
+        pv[b, :P[b]] = KV[b][1][:P[b]]
+
+    def to_t(a):
+        t = torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a)
+        t = t.view(torch.bfloat16) if a.dtype == np.uint16 else t
+        return t if c.host_io else t.cuda()
+
+    ctx = Context(asr_cfg(c), to_t(pk), to_t(pv), P)
+    orc = [oracle.OracleSeq(orc_cfg(c), cap, P[b]) for b in range(c.B)]
+    worst_o, worst_h, frozen_total, restored_total = 0.0, 0.0, 0, 0
+    for i in range(c.steps):
+        if i in c.restore_at:
+            seq, level = c.restore_at[i]
+            ctx.restore(seq, level)
+            for b in range(c.B):
+                if seq < 0 or seq == b:
+                    orc[b].restore(level)
+        q = np.stack([gen.q(p, b, i, c.dtype) for b in range(c.B)])
+        kn = np.stack([KV[b][0][P[b] + i] for b in range(c.B)])
+        vn = np.stack([KV[b][1][P[b] + i] for b in range(c.B)])
+        lg = np.stack([gen.logits(p, b, i - 1) for b in range(c.B)]) if (c.vocab and i > 0) else None
+        if c.host_io:
+            o = np.zeros((c.B, c.L, c.Hq, c.d), np.float32)
+            ent = np.zeros(c.B, np.float32)
+            ctx.step(q, kn, vn, o, logits_prev=lg, entropy=ent)
+        else:
+            o_t = torch.zeros((c.B, c.L, c.Hq, c.d), dtype=torch.float32, device="cuda")
+            e_t = torch.zeros(c.B, dtype=torch.float32, device="cuda")
+            ctx.step(to_t(q), to_t(kn), to_t(vn), o_t, logits_prev=None if lg is None else to_t(lg),
+                     entropy=e_t)
+        stats = [ctx.stats(b, detail=True) for b in range(c.B)]
+        if not c.host_io:
+            o = o_t.cpu().numpy()
+            ent = e_t.cpu().numpy()
+        for b in range(c.B):
+            Ob, act, scores, out = orc[b].step(q[b], KV[b][0], KV[b][1], None if lg is None else lg[b])
+            g = stats[b]
+            where = f"step {i} seq {b}"
+            np.testing.assert_array_equal(g["active_list"], act, err_msg=where)
+            assert np.array_equal(g["scores"].astype(np.float64), scores), \
+                f"{where}: scores differ at {np.flatnonzero(g['scores'] != scores)[:5]}"
+            led = orc[b].ledger()
+            for key in ("residency", "timer", "count", "freeze_step"):
+                np.testing.assert_array_equal(g["ledger"][key], led[key], err_msg=f"{where} {key}")
+            assert g["total"] == out["n"] and g["attended"] == out["attended"], where
+            assert g["active"] == out["active_post"] and g["frozen"] == out["frozen_post"], where
+            assert g["frozen_this_step"] == out["frozen_this_step"], where
+            assert g["restored_this_step"] == out["restored_this_step"], (where, g, out)
+            assert g["recovery_action"] == out["recovery_action"], where
+            assert g["rewalk_requested"] == out["rewalk_requested"], where
+            assert g["device_error"] == 0
+            if out["entropy_valid"]:
+                assert g["entropy_valid"] == 1
+                dh = abs(float(g["entropy"]) - out["entropy"])
+                assert dh <= TOL_H, (where, dh)
+                assert abs(float(ent[b]) - out["entropy"]) <= TOL_H
+                worst_h = max(worst_h, dh)
+            if check_o:
+                err = o_rel_err(o[b], Ob)
+                assert err <= TOL_O[c.dtype], (where, err)
+                worst_o = max(worst_o, err)
+            frozen_total += out["frozen_this_step"]
+            restored_total += out["restored_this_step"]
+    summary = {"worst_o": worst_o, "worst_h": worst_h, "frozen": frozen_total, "restored": restored_total,
+               "final": [ctx.stats(b) for b in range(c.B)]}
+    ctx.close()
+    return summary

@@ -1,0 +1,96 @@
+"""CPU checks of the C-ABI boundary (no compute calls: there is no GPU here).
+
+- libasr.so loads and exports every function include/asr.h declares;
+- the ctypes structs match the C layout (sizes and offsets, from a gcc-compiled probe);
+- configuration errors are reported synchronously as ASR_E_INVALID with a message;
+- the oracle and the product path share no code (no cross includes / imports).
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2512_11221_b200 import asr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "asr.h")
+
+
+def declared_functions():
+    txt = open(HDR).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(asr_[a-z_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol():
+    names = declared_functions()
+    assert set(names) == set(asr.EXPORTS), names
+    out = subprocess.run(["nm", "-D", "--defined-only", asr.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (asr_\w+)", out))
+    missing = set(names) - exported
+    assert not missing, missing
+    L = asr.lib()
+    for n in names:
+        assert hasattr(L, n)
+
+
+def test_struct_layout_matches_header(tmp_path):
+    probe = tmp_path / "probe.c"
+    structs = {"asr_config": asr.asr_config, "asr_step_io": asr.asr_step_io, "asr_stats_t": asr.asr_stats_t,
+               "asr_ledger_view": asr.asr_ledger_view}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "asr.h"', "int main(void){"]
+    for s, cls in structs.items():
+        lines.append(f'printf("{s} %zu\\n", sizeof({s}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{s}.{f} %zu\\n", offsetof({s}, {f}));')
+    lines.append("return 0;}")
+    probe.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for s, cls in structs.items():
+        assert int(got[s]) == ctypes.sizeof(cls), s
+        for f, _ in cls._fields_:
+            assert int(got[f"{s}.{f}"]) == getattr(cls, f).offset, (s, f)
+
+
+def test_defaults_are_the_papers():
+    c = asr.asr_config()
+    asr.lib().asr_config_defaults(ctypes.byref(c))
+    assert (c.window, c.tau, c.softness) == (32, 0.5, 2.0)
+    assert (c.n_layers, c.n_q_heads, c.n_kv_heads, c.head_dim, c.vocab) == (32, 32, 8, 128, 128256)
+
+
+@pytest.mark.parametrize("bad", [dict(n_layers=0), dict(n_q_heads=6, n_kv_heads=4), dict(head_dim=48),
+                                 dict(window=0), dict(softness=0.0), dict(history_window=128),
+                                 dict(kv_dtype=7), dict(batch=0), dict(det_baseline=1000)])
+def test_invalid_config_is_rejected_synchronously(bad):
+    cfg = asr.Config(**bad)
+    with pytest.raises(asr.AsrError) as e:
+        asr.asr_create(cfg, None, None, [0] * max(cfg.batch, 1), stream=0)
+    assert e.value.code == asr.ASR_E_INVALID
+    assert asr.lib().asr_last_error()
+
+
+def test_bad_prompt_length_rejected():
+    with pytest.raises(asr.AsrError) as e:
+        asr.asr_create(asr.Config(max_context=16), None, None, [20], stream=0)
+    assert e.value.code == asr.ASR_E_INVALID
+
+
+def test_oracle_and_product_share_no_code():
+    csrc = os.path.join(ROOT, "paper_2512_11221_b200")
+    for dirpath, _, files in os.walk(csrc):
+        for f in files:
+            if f.endswith((".cu", ".cpp", ".h", ".cuh", ".py")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"(?:#include|import|from)\s+[\"<]?(\w+)", txt), f
+                assert "orc.h" not in txt and "asrgen" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".c", ".h", ".py")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            deps = re.findall(r"(?:#include\s+[\"<]([\w./]+)|^\s*(?:import|from)\s+([\w.]+))", txt, flags=re.M)
+            deps = {a or b for a, b in deps}
+            assert not any("asr" in x or "paper_2512" in x or "gen" == x.split(".")[0] for x in deps), (f, deps)

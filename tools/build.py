@@ -54,7 +54,8 @@ def build_gen_dev(force: bool = False) -> str:
     out = os.path.join(ROOT, "gen", "libasrgen_dev.so")
     srcs = [os.path.join(ROOT, "gen", f) for f in ("asrgen.h", "asrgen_dev.cu")]
     if force or _stale(out, srcs):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-Xcompiler", "-fPIC", "-o", out, srcs[1]])
+        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-cudart", "shared", "-Xcompiler", "-fPIC",
+              "-o", out, srcs[1]])
     return out
 
 
@@ -81,7 +82,7 @@ def build_asr(force: bool = False) -> str:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", *common, "-c", s, "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs])
     return out
 
 
