@@ -93,5 +93,7 @@ cudaError_t launch_combine(const DevState& s, float* o, cudaStream_t st);
 cudaError_t launch_decide(const DevState& s, cudaStream_t st);
 cudaError_t launch_restore(const DevState& s, int seq, int level, cudaStream_t st);
 int attention_grid(const DevState& s, int num_sms);
+bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head
+cudaError_t launch_attention_mma(const DevState& s, const void* q, int grid, cudaStream_t st);
 
 }  // namespace asr

@@ -207,12 +207,14 @@ cudaError_t launch_generic(const DevState& s, const void* q, int grid, cudaStrea
 }  // namespace
 
 int attention_grid(const DevState& s, int num_sms) {
+  if (attention_mma_supported(s)) return num_sms;  // persistent: one CTA per SM
   long max_items = (long)s.B * s.L * s.max_splits;
   long g = (long)num_sms * 4;
   return (int)(max_items < g ? max_items : g);
 }
 
 cudaError_t launch_attention(const DevState& s, const void* q, int grid, cudaStream_t st) {
+  if (attention_mma_supported(s)) return launch_attention_mma(s, q, grid, st);
   if (s.dtype == 0) return launch_generic<__nv_bfloat16>(s, q, grid, st);
   return launch_generic<float>(s, q, grid, st);
 }

@@ -1,0 +1,345 @@
+// paper_2512_11221_b200/csrc/kernels_attn_mma.cu — (a4)+(a1) fast path for bf16 KV, head_dim 128,
+// 4 query heads per KV head (LLaMA-3-8B: 32 q / 8 KV heads): split-KV decode attention over the
+// active index list A_i with the Eq. 2 score fused into the QK^T pass.
+//
+//   O_{l,h} = softmax(q_{l,h} K_{A,l,g(h)}^T / sqrt(d)) V_{A,l,g(h)}       Eq. 1, Alg. 1 line 1
+//   part_l(a) = sum_h |q_{l,h} . k_{l,A[a],g(h)}|                           Eq. 2, Alg. 1 line 2
+//
+// Design:
+// - persistent CTAs over the ragged work list (b, l, chunk of A_b), one CTA per SM;
+// - warp specialisation: 1 producer warp gathers the K and V rows of 16 active tokens per stage with
+//   one `cp.async.bulk` (TMA 1-D bulk copy, SASS UBLKCP) per 2 KiB row into a 3-stage shared-memory
+//   ring completed by mbarrier transaction counts; the ring runs across work items, so there is no
+//   pipeline drain between chunks; rows are padded to 2064 B so ldmatrix is bank-conflict free;
+// - 8 consumer warps, one per KV head: S^T = q K^T with `mma.sync.m16n8k16` bf16 -> fp32
+//   (4 query heads on M, tokens on N; exact on the lattice inputs), |S| summed over the 4 heads with
+//   quad shuffles gives the Eq. 2 head sum, fp32 online softmax (exp2), then O += P V with P split
+//   into bf16 hi + lo parts (two MMAs, ~2^-16 relative error instead of bf16's 2^-9);
+// - the producer also finishes the score: after a stage is released it sums the 8 warps' head sums
+//   per token in fixed order and writes one fp32 partial per (b, l, token) — the only extra HBM
+//   traffic of the score (0.1 % of the KV bytes).
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "asr_internal.h"
+
+namespace asr {
+namespace {
+
+constexpr int kD = 128;
+constexpr int kG = 4;                 // query heads per KV head
+constexpr int kHK = 8;                // KV heads (consumer warps)
+constexpr int kTM = 16;               // tokens per stage
+constexpr int kStagesRing = 3;
+constexpr int kRowBytes = kHK * kD * 2;         // 2048: one token-layer K (or V) row, all heads
+constexpr int kRowPad = kRowBytes + 16;         // 2064: ldmatrix conflict-free stride
+constexpr int kStageBytes = kTM * kRowPad;      // K (or V) tile of one stage
+constexpr int kThreads = (kHK + 1) * 32;
+constexpr int kMaxB = 4096;
+
+struct Smem {
+  alignas(128) uint8_t k[kStagesRing][kStageBytes];
+  alignas(128) uint8_t v[kStagesRing][kStageBytes];
+  float sc[kStagesRing][kHK][kTM];      // per-warp head sums |S| of each token
+  alignas(8) uint64_t full[kStagesRing];
+  alignas(8) uint64_t empty[kStagesRing];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D += A(16x16 bf16, row) * B(16x8 bf16, col), fp32 accumulate
+__device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct ItemInfo {
+  int b, l, a0, n;  // sequence, layer, first compact index, tokens
+};
+
+__device__ __forceinline__ ItemInfo decode_item(const DevState& s, const int* start, int item) {
+  int lo = 0, hi = s.B - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  ItemInfo it;
+  it.b = lo;
+  const int A = s.act_len[lo];
+  int chunk, nch;
+  chunking(A, s.max_splits, s.chunk_min, &chunk, &nch);
+  const int r = item - start[lo];
+  it.l = r / nch;
+  const int c = r % nch;
+  it.a0 = c * chunk;
+  it.n = min(A, it.a0 + chunk) - it.a0;
+  return it;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  __shared__ int sh_start[kMaxB + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- prologue: work list (item_start), zeroed ring (masked rows must hold finite values), barriers
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < s.B; ++b) {
+      sh_start[b] = acc;
+      int chunk, nch;
+      chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+      acc += s.L * nch;
+    }
+    sh_start[s.B] = acc;
+    if (blockIdx.x == 0)
+      for (int b = 0; b <= s.B; ++b) s.item_start[b] = sh_start[b];
+    for (int i = 0; i < kStagesRing; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], kHK);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    uint4* z = reinterpret_cast<uint4*>(&sm);
+    const int nz = (int)(offsetof(Smem, sc) / sizeof(uint4));
+    for (int i = threadIdx.x; i < nz; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    // order the generic-proxy zero fill before the async-proxy (bulk copy) writes to the same rows
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const int total = sh_start[s.B];
+  const long row_elems = (long)kHK * kD;  // per token-layer K (or V)
+
+  if (warp == kHK) {
+    // ================================================================== producer warp
+    int g = 0;                       // CTA-local tile counter
+    ItemInfo pend[kStagesRing];      // occupant of each stage (for the score epilogue)
+#pragma unroll
+    for (int i = 0; i < kStagesRing; ++i) pend[i].n = 0;
+    auto epilogue = [&](int stage, const ItemInfo& it) {
+      // it.a0 is the tile's first compact index here, it.n its tokens
+      if (lane < it.n) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < kHK; ++w) t += sm.sc[stage][w][lane];
+        s.score_part[((long)it.b * s.L + it.l) * s.max_ctx + it.a0 + lane] = t;
+      }
+    };
+    for (int item = blockIdx.x; item < total; item += gridDim.x) {
+      const ItemInfo it = decode_item(s, sh_start, item);
+      const int* act = s.act_pos + (long)it.b * s.max_ctx + it.a0;
+      const char* kvb = reinterpret_cast<const char*>(s.kv);
+      for (int t0 = 0; t0 < it.n; t0 += kTM, ++g) {
+        const int stage = g % kStagesRing;
+        const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
+        mbar_wait(&sm.empty[stage], ph ^ 1u);
+        __syncwarp();
+        epilogue(stage, pend[stage]);
+        const int cnt = min(kTM, it.n - t0);
+        ItemInfo tile{it.b, it.l, it.a0 + t0, cnt};
+#pragma unroll
+        for (int i = 0; i < kStagesRing; ++i)
+          if (i == stage) pend[i] = tile;
+        if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * 2u * kRowBytes);
+        __syncwarp();
+        if (lane < cnt) {
+          const long slot = (long)it.b * s.max_ctx + act[t0 + lane];
+          const char* src = kvb + ((slot * s.L + it.l) * 2) * row_elems * 2;
+          bulk_g2s(&sm.k[stage][lane * kRowPad], src, kRowBytes, &sm.full[stage]);
+          bulk_g2s(&sm.v[stage][lane * kRowPad], src + kRowBytes, kRowBytes, &sm.full[stage]);
+        }
+      }
+    }
+    // drain: the last (up to) kStagesRing tiles still owe their score epilogue
+    for (int k = 0; k < kStagesRing; ++k) {
+      const int gg = g + k;  // waiting for the release of tile gg - kStagesRing
+      const int stage = gg % kStagesRing;
+      if (gg - kStagesRing < 0) continue;
+      mbar_wait(&sm.empty[stage], ((uint32_t)(gg / kStagesRing) & 1u) ^ 1u);
+      __syncwarp();
+      epilogue(stage, pend[stage]);
+    }
+    return;
+  }
+
+  // ==================================================================== consumer warps (KV head = warp)
+  const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
+  const int r = lane >> 2, qd = lane & 3;   // fragment row / quad column
+  const uint32_t kbase = smem_u32(&sm.k[0][0]);
+  const uint32_t vbase = smem_u32(&sm.v[0][0]);
+  // ldmatrix lane addresses (bytes within a stage tile, this warp's head)
+  const int mi = lane >> 3, ri = lane & 7;
+  const uint32_t k_lane = (uint32_t)((ri + (mi >> 1) * 8) * kRowPad + warp * kD * 2 + (mi & 1) * 16);
+  const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kRowPad + warp * kD * 2 + (mi >> 1) * 16);
+  int g = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x) {
+    const ItemInfo it = decode_item(s, sh_start, item);
+    // q fragments (rows 0..3 = the 4 query heads of this KV head, rows 4..15 zero)
+    uint32_t qa[8][2];
+    {
+      const __nv_bfloat16* qh = q + (((long)it.b * s.L + it.l) * s.Hq + warp * kG + (r & 3)) * kD;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t lo = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * qd);
+        uint32_t hi = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * qd);
+        qa[ks][0] = r < kG ? lo : 0u;
+        qa[ks][1] = r < kG ? hi : 0u;
+      }
+    }
+    float acc[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t0 = 0; t0 < it.n; t0 += kTM, ++g) {
+      const int stage = g % kStagesRing;
+      const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
+      const int cnt = min(kTM, it.n - t0);
+      mbar_wait(&sm.full[stage], ph);
+      const uint32_t ks_addr = kbase + stage * kStageBytes + k_lane;
+      const uint32_t vs_addr = vbase + stage * kStageBytes + v_lane;
+      // ---- S^T[head][token] = q . k
+      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(ks_addr + ks * 32, b0, b1, b2, b3);
+        mma_bf16(c0, qa[ks][0], 0u, qa[ks][1], 0u, b0, b1);
+        mma_bf16(c1, qa[ks][0], 0u, qa[ks][1], 0u, b2, b3);
+      }
+      // tokens of this thread's columns: n0 = 2qd, n0+1 (tile 0), 8+2qd, 9+2qd (tile 1)
+      const int n0 = 2 * qd;
+      const bool v00 = n0 < cnt, v01 = n0 + 1 < cnt, v10 = n0 + 8 < cnt, v11 = n0 + 9 < cnt;
+      // ---- Eq. 2 head sum: |S| over the 4 valid rows (lanes 0..15) -> lanes 0..3
+      float s00 = fabsf(c0[0]), s01 = fabsf(c0[1]), s10 = fabsf(c1[0]), s11 = fabsf(c1[1]);
+#pragma unroll
+      for (int o = 4; o <= 8; o <<= 1) {
+        s00 += __shfl_xor_sync(0xffffffffu, s00, o);
+        s01 += __shfl_xor_sync(0xffffffffu, s01, o);
+        s10 += __shfl_xor_sync(0xffffffffu, s10, o);
+        s11 += __shfl_xor_sync(0xffffffffu, s11, o);
+      }
+      if (lane < 4) {
+        float* scw = sm.sc[stage][warp];
+        scw[n0] = s00;
+        scw[n0 + 1] = s01;
+        scw[n0 + 8] = s10;
+        scw[n0 + 9] = s11;
+      }
+      // ---- online softmax (row = head r; rows >= 4 are padding and never written out)
+      const float x00 = v00 ? c0[0] * scale : -INFINITY, x01 = v01 ? c0[1] * scale : -INFINITY;
+      const float x10 = v10 ? c1[0] * scale : -INFINITY, x11 = v11 ? c1[1] * scale : -INFINITY;
+      float mt = fmaxf(fmaxf(x00, x01), fmaxf(x10, x11));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 1));
+      mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, 2));
+      const float m_new = fmaxf(m_run, mt);
+      const float corr = exp2f(m_run - m_new);
+      const float p00 = exp2f(x00 - m_new), p01 = exp2f(x01 - m_new);
+      const float p10 = exp2f(x10 - m_new), p11 = exp2f(x11 - m_new);
+      l_run = l_run * corr + (p00 + p01 + p10 + p11);
+      m_run = m_new;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc[i][0] *= corr;
+        acc[i][1] *= corr;
+      }
+      // P = hi + lo (bf16 each)
+      const uint32_t ph0 = pack_bf16(p00, p01), ph1 = pack_bf16(p10, p11);
+      const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&ph0);
+      const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&ph1);
+      const uint32_t pl0 = pack_bf16(p00 - __low2float(h0), p01 - __high2float(h0));
+      const uint32_t pl1 = pack_bf16(p10 - __low2float(h1), p11 - __high2float(h1));
+      // ---- O += P V
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vs_addr + dp * 32, b0, b1, b2, b3);
+        mma_bf16(acc[2 * dp], ph0, 0u, ph1, 0u, b0, b1);
+        mma_bf16(acc[2 * dp], pl0, 0u, pl1, 0u, b0, b1);
+        mma_bf16(acc[2 * dp + 1], ph0, 0u, ph1, 0u, b2, b3);
+        mma_bf16(acc[2 * dp + 1], pl0, 0u, pl1, 0u, b2, b3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    }
+    // ---- partial outputs of this item: rows 0..3 (lanes 0..15)
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if (r < kG) {
+      const long pi = (long)item * s.Hq + warp * kG + r;
+      if (qd == 0) {
+        s.part_ml[pi * 2] = m_run;
+        s.part_ml[pi * 2 + 1] = l_run;
+      }
+      float* dst = s.part_acc + pi * kD + 2 * qd;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) *reinterpret_cast<float2*>(dst + i * 8) = make_float2(acc[i][0], acc[i][1]);
+    }
+  }
+}
+
+}  // namespace
+
+bool attention_mma_supported(const DevState& s) {
+  return s.dtype == 0 && s.d == kD && s.Hkv == kHK && s.Hq == kHK * kG && s.B <= kMaxB;
+}
+
+cudaError_t launch_attention_mma(const DevState& s, const void* q, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(Smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_mma_kernel<<<grid, kThreads, sizeof(Smem), st>>>(s, reinterpret_cast<const __nv_bfloat16*>(q));
+  return cudaGetLastError();
+}
+
+}  // namespace asr
