@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps (for ncu)")
     return ap.parse_args()
 
 
@@ -171,7 +172,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     import torch.distributed as dist
 
     import gen
-    from paper_2512_11221_b200 import Config, Context, KV_BF16
+    from paper_2512_11221_b200 import Config, Context, KV_BF16, STAGES
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -180,10 +181,10 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     grow = a.context - P - 1                     # steps before the measured region starts
     W, K = a.warmup, a.steps
     e2e_steps = 0 if a.no_e2e else K
-    max_ctx = a.context + W + K + e2e_steps + 4
+    max_ctx = a.context + W + 2 * K + e2e_steps + 4
     g = gen_params(a, rank)
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
-                 kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=1,
+                 kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=0,
                  device=local_rank)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, HKV, D), dtype=bf, device=dev)
@@ -212,9 +213,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         ctx.step(q, kn, vn, o, logits_prev=lg if i > 0 else None, entropy=ent)
     torch.cuda.synchronize()
     t_grow = time.perf_counter() - t_grow
-    ctx.stage_times()  # discard growth-phase events
-    # inputs of the measured steps, resident in HBM before timing
-    n_meas = W + K
+    # inputs of the measured steps (warm-up, timed, profiled), resident in HBM before timing
+    n_meas = W + 2 * K
     Q = torch.empty((n_meas, B, L, HQ, D), dtype=bf, device=dev)
     KN = torch.empty((n_meas, B, L, HKV, D), dtype=bf, device=dev)
     VN = torch.empty_like(KN)
@@ -227,12 +227,12 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         flush.zero_()
         ctx.step(Q[t], KN[t], VN[t], o, logits_prev=LG[t], entropy=ent)
     torch.cuda.synchronize()
-    ctx.stage_times()
-    attended = []
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if a.nvtx:
+        torch.cuda.nvtx.range_push("timed")
     t_wall = time.perf_counter()
     for t in range(K):
         flush.zero_()
@@ -241,16 +241,30 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         ev[t][1].record(st)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
+    if a.nvtx:
+        torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     total_ms = sum(step_ms)
-    stage_ms, launches = ctx.stage_times()
     stats = [ctx.stats(b) for b in range(B)]
+    launches_timed = 3 * K   # pre, attention, post per step (one CUDA-graph launch)
+    # ---- the same K-step workload again with stage events (graph event nodes between the kernels, no
+    #      programmatic overlap): per-stage device times and the attention kernel's duration (roofline)
+    ctx.set_profile(True)
+    ctx.stage_times()
+    for t in range(K):
+        flush.zero_()
+        ctx.step(Q[W + K + t], KN[W + K + t], VN[W + K + t], o, logits_prev=LG[W + K + t], entropy=ent)
+    torch.cuda.synchronize()
+    stage_ms, launches = ctx.stage_times()
+    ctx.set_profile(False)
+    stats_p = [ctx.stats(b) for b in range(B)]
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below
     att_last = sum(s["attended"] for s in stats)
+    att_prof = sum(s["attended"] for s in stats_p)
     total_t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(total_t, op=dist.ReduceOp.MAX)
@@ -292,10 +306,10 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region"}
     # ---- roofline of the dominant kernel (attention + fused score), measured live via stage events
-    attn_ms = stage_ms[2]
+    attn_ms = stage_ms[1]
     # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);
     # per (sequence, layer): q (Hq*d*2 B).  |A_i| per step ~ att_last (drifts < 0.5 % over the window).
-    bytes_per_step = L * att_last * (2 * HKV * D * 2 + 8) + B * L * HQ * D * 2
+    bytes_per_step = L * att_prof * (2 * HKV * D * 2 + 8) + B * L * HQ * D * 2
     achieved = bytes_per_step * K / (attn_ms / 1000.0) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = None
@@ -325,15 +339,16 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "attention+score (split-KV over A_i)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "bytes_per_launch": bytes_per_step, "ms_per_launch": attn_ms / K},
+                     "bytes_per_launch": bytes_per_step, "ms_per_launch": attn_ms / K,
+                     "timing": "CUDA event nodes around the kernel in K further steps of the same workload (profiled pass)"},
         "e2e": e2e,
-        "gpu_launches": launches,
+        "gpu_launches": launches_timed,
         "cpu_baseline": cpu,
         "clocks": clk,
         "detail": {"attended_per_step": att_last / B, "active_post": stats[0]["active"], "total": stats[0]["total"],
                    "compression": stats[0]["compression"],
-                   "stage_ms_per_step": {n: v / K for n, v in zip(
-                       ["entropy", "append_recover_compact", "attention_score", "combine", "decide_tick"], stage_ms)},
+                   "stage_ms_per_step_profiled": {n: v / K for n, v in zip(STAGES, stage_ms)},
+                   "profiled_launches": launches,
                    "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
                    "wall_s_timed": t_wall, "grow_s": t_grow,
                    "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES},

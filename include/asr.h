@@ -148,9 +148,15 @@ asr_status asr_read_kv(asr_ctx* ctx, int32_t seq, int32_t pos, int32_t from_mirr
                        void* v_out);
 
 /* Accumulated device time per stage since the last call (needs profile_stages = 1):
- * ms[0] entropy+detector, [1] append+recovery+compaction, [2] attention+score, [3] combine,
- * [4] decide+tick; *launches = kernel launches of the library in that period.  Synchronises. */
+ * ms[0] entropy + detector + ladder + append + recovery + compaction, ms[1] attention + fused
+ * score, ms[2] combine + decide + tick; *launches = kernel launches of the library in that
+ * period.  n >= 3.  Synchronises. */
 asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launches);
+
+/* Switch stage profiling (the events asr_stage_times reads) on or off for the following steps.
+ * While it is on, stages are separated by event nodes, so the kernels of one step do not overlap
+ * (no programmatic dependent launch); off is the production configuration. */
+asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
 
 /* Synchronise and free everything the context owns. */
 asr_status asr_destroy(asr_ctx* ctx);

@@ -22,7 +22,7 @@ ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, A
 KV_BF16, KV_F32 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 SR, WR, FR = 1, 2, 3
-STAGES = ("entropy", "append_recover_compact", "attention_score", "combine", "decide_tick")
+STAGES = ("entropy_append_recover_compact", "attention_score", "combine_decide_tick")
 
 
 class AsrError(RuntimeError):
@@ -65,7 +65,7 @@ class asr_ledger_view(ctypes.Structure):
 
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
-           "asr_stage_times", "asr_destroy", "asr_last_error")
+           "asr_stage_times", "asr_set_profile", "asr_destroy", "asr_last_error")
 
 _lib = None
 
@@ -87,8 +87,9 @@ def lib() -> ctypes.CDLL:
         L.asr_read_kv.argtypes = [vp, i32, i32, i32, vp, vp]
         L.asr_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(ctypes.c_int64)]
         L.asr_destroy.argtypes = [vp]
+        L.asr_set_profile.argtypes = [vp, i32]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
-                  "asr_destroy"):
+                  "asr_set_profile", "asr_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -226,6 +227,10 @@ def asr_stage_times(ctx):
     return list(ms), int(n.value)
 
 
+def asr_set_profile(ctx, on: bool) -> None:
+    _check(lib().asr_set_profile(ctx, int(bool(on))))
+
+
 def asr_destroy(ctx) -> None:
     _check(lib().asr_destroy(ctx))
 
@@ -251,6 +256,9 @@ class Context:
 
     def stage_times(self):
         return asr_stage_times(self._h)
+
+    def set_profile(self, on: bool):
+        asr_set_profile(self._h, on)
 
     def close(self):
         if self._h:

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <array>
@@ -60,12 +61,28 @@ struct asr_ctx {
   float* st_ent = nullptr;
   int64_t bytes_h2d = 0, bytes_d2h = 0;
   int64_t launches = 0;
+  // CUDA graph of one step, per variant (with / without the entropy stage)
+  struct StepGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    bool profiled = false;
+    std::vector<cudaGraphNode_t> knodes;
+    std::vector<asr::KNode> last;
+    std::vector<cudaGraphNode_t> evnodes;
+  };
+  StepGraph graphs[2];
+  bool use_graph = true;
+  bool use_pdl = true;
   // stage profiling
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_pending;
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_free;
   std::vector<void*> allocs;
 
   ~asr_ctx() {
+    for (auto& g : graphs) {
+      if (g.x) cudaGraphExecDestroy(g.x);
+      if (g.g) cudaGraphDestroy(g.g);
+    }
     for (void* p : allocs) cudaFree(p);
     if (host_mirror) cudaFreeHost(host_mirror);
     if (side) cudaStreamDestroy(side);
@@ -182,7 +199,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.Hq = cfg->n_q_heads;
     s.Hkv = cfg->n_kv_heads;
     s.d = cfg->head_dim;
-    s.max_ctx = cfg->max_context;
+    s.max_ctx = (cfg->max_context + 63) & ~63;   // row stride of every per-sequence array (aligned)
     s.dtype = cfg->kv_dtype;
     s.window = cfg->window;
     s.pinned = cfg->pinned_prefix;
@@ -211,6 +228,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     long cap = (s.max_ctx + s.chunk_min - 1) / s.chunk_min;
     s.max_splits = (int)(want < 1 ? 1 : want > cap ? cap : want);
     if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
+    {
+      int db = (s.max_ctx + 2047) / 2048;
+      s.decide_blocks = db < 1 ? 1 : db > 32 ? 32 : db;
+    }
 
     c->kv_elem = s.dtype == ASR_KV_BF16 ? 2 : 4;
     c->tok_bytes = (size_t)s.L * 2 * s.Hkv * s.d * c->kv_elem;
@@ -238,6 +259,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.stats, (size_t)s.B * sizeof(asr::SeqStats)));
     CUDA_TRY(c->alloc(&s.err, 4));
     CUDA_TRY(c->alloc(&s.ticket, 4));
+    CUDA_TRY(c->alloc(&s.pre_ticket, (size_t)s.B * 4));
     // ledger init: prompt tokens Active, c = d = 0 (R-prefill); everything else zero
     CUDA_TRY(cudaMemsetAsync(s.res, 0, BT, st));
     CUDA_TRY(cudaMemsetAsync(s.timer, 0, BT * 4, st));
@@ -250,6 +272,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(cudaMemsetAsync(s.stats, 0, (size_t)s.B * sizeof(asr::SeqStats), st));
     CUDA_TRY(cudaMemsetAsync(s.err, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.ticket, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.pre_ticket, 0, (size_t)s.B * 4, st));
     CUDA_TRY(cudaMemcpyAsync(s.prompt_len, prompt_len, (size_t)s.B * 4, cudaMemcpyHostToDevice, st));
     for (int b = 0; b < s.B; ++b)
       if (prompt_len[b] > 0) CUDA_TRY(cudaMemsetAsync(s.res + (size_t)b * s.max_ctx, 1, prompt_len[b], st));
@@ -278,6 +301,11 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     }
     CUDA_TRY(cudaStreamSynchronize(st));
     c->attn_grid = asr::attention_grid(s, c->num_sms);
+    if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
+    const char* ng = getenv("ASR_NO_GRAPH");
+    c->use_graph = !(ng && ng[0] == '1');
+    const char* np = getenv("ASR_NO_PDL");
+    c->use_pdl = !(np && np[0] == '1');
     c->last_stream = st;
     return ASR_OK;
   }();
@@ -322,7 +350,7 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   if (has_logits && io->logits_dtype != ASR_KV_BF16 && io->logits_dtype != ASR_KV_F32)
     return fail(ASR_E_INVALID, "logits_dtype");
   for (int b = 0; b < s.B; ++b)
-    if (c->prompt_len[b] + c->step + 1 > s.max_ctx)
+    if (c->prompt_len[b] + c->step + 1 > c->cfg.max_context)
       return fail(ASR_E_CAPACITY, "sequence " + std::to_string(b) + " is at max_context");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaSetDevice(c->cfg.device));
@@ -364,21 +392,77 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     c->prof_free.pop_back();
     ev = &c->prof_pending.back();
   }
-  CUDA_TRY(prof_mark(c, ev, 0, st));
-  if (has_logits) {
-    CUDA_TRY(asr::launch_entropy(s, lg, io->logits_dtype, ent, st));
-    c->launches++;
+  // the step as kernel descriptions, one per stage
+  asr::KNode kn_list[asr::kStages];
+  int stage_of[asr::kStages];
+  int nk = 0;
+  asr::node_pre(kn_list[nk], s, has_logits ? lg : nullptr, io->logits_dtype, has_logits ? ent : nullptr, kn, vn);
+  stage_of[nk++] = 0;
+  asr::node_attention(kn_list[nk], s, q, c->attn_grid);
+  stage_of[nk++] = 1;
+  asr::node_post(kn_list[nk], s, o);
+  stage_of[nk++] = 2;
+  if (!c->use_graph) {
+    int k = 0;
+    for (int stg = 0; stg < asr::kStages; ++stg) {
+      CUDA_TRY(prof_mark(c, ev, stg, st));
+      if (k < nk && stage_of[k] == stg) CUDA_TRY(kn_list[k++].launch(st));
+    }
+    CUDA_TRY(prof_mark(c, ev, asr::kStages, st));
+  } else {
+    asr_ctx::StepGraph& G = c->graphs[has_logits ? 1 : 0];
+    const bool prof = ev != nullptr;
+    if (G.x && G.profiled != prof) {
+      cudaGraphExecDestroy(G.x);
+      cudaGraphDestroy(G.g);
+      G = asr_ctx::StepGraph();
+    }
+    if (!G.x) {
+      CUDA_TRY(cudaGraphCreate(&G.g, 0));
+      G.profiled = prof;
+      cudaGraphNode_t prev = nullptr;
+      int k = 0;
+      for (int stg = 0; stg <= asr::kStages; ++stg) {
+        if (prof) {
+          cudaGraphNode_t e;
+          CUDA_TRY(cudaGraphAddEventRecordNode(&e, G.g, prev ? &prev : nullptr, prev ? 1 : 0, (*ev)[stg]));
+          G.evnodes.push_back(e);
+          prev = e;
+        }
+        if (stg < asr::kStages && k < nk && stage_of[k] == stg) {
+          cudaGraphNode_t kn_node;
+          const bool pdl = c->use_pdl && !prof && prev != nullptr;
+          CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
+                                          &kn_list[k].p));
+          if (pdl) {
+            // programmatic edge: the kernel may launch before its upstream completes; it calls
+            // griddepcontrol.wait before reading the upstream's results
+            cudaGraphEdgeData ed{};
+            ed.from_port = cudaGraphKernelNodePortProgrammatic;
+            ed.to_port = 0;
+            ed.type = cudaGraphDependencyTypeProgrammatic;
+            CUDA_TRY(cudaGraphAddDependencies_v2(G.g, &prev, &kn_node, &ed, 1));
+          }
+          G.knodes.push_back(kn_node);
+          G.last.push_back(kn_list[k]);
+          prev = kn_node;
+          ++k;
+        }
+      }
+      CUDA_TRY(cudaGraphInstantiate(&G.x, G.g, 0));
+    } else {
+      for (int k = 0; k < nk; ++k) {
+        if (memcmp(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra)) != 0) {
+          CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.x, G.knodes[k], &kn_list[k].p));
+          memcpy(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra));
+        }
+      }
+      if (prof)
+        for (int e = 0; e <= asr::kStages; ++e) CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.x, G.evnodes[e], (*ev)[e]));
+    }
+    CUDA_TRY(cudaGraphLaunch(G.x, st));
   }
-  CUDA_TRY(prof_mark(c, ev, 1, st));
-  CUDA_TRY(asr::launch_ledger_pre(s, kn, vn, has_logits ? 1 : 0, st));
-  CUDA_TRY(prof_mark(c, ev, 2, st));
-  CUDA_TRY(asr::launch_attention(s, q, c->attn_grid, st));
-  CUDA_TRY(prof_mark(c, ev, 3, st));
-  CUDA_TRY(asr::launch_combine(s, o, st));
-  CUDA_TRY(prof_mark(c, ev, 4, st));
-  CUDA_TRY(asr::launch_decide(s, st));
-  CUDA_TRY(prof_mark(c, ev, 5, st));
-  c->launches += 4;
+  c->launches += nk;
   // (a5) write-once host mirror of the appended token (side stream, overlapped with compute)
   if (c->host_mirror) {
     CUDA_TRY(cudaEventRecord(c->ev_append, st));
@@ -416,7 +500,9 @@ asr_status asr_restore(asr_ctx* c, int32_t seq, int32_t level, void* cuda_stream
   if (seq < -1 || seq >= c->s.B) return fail(ASR_E_INVALID, "seq out of range");
   if (level != ASR_SR && level != ASR_WR && level != ASR_FR) return fail(ASR_E_INVALID, "level must be SR, WR or FR");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
-  CUDA_TRY(asr::launch_restore(c->s, seq, level, (cudaStream_t)cuda_stream));
+  asr::KNode n;
+  asr::node_restore(n, c->s, seq, level);
+  CUDA_TRY(n.launch((cudaStream_t)cuda_stream));
   c->launches++;
   c->last_stream = (cudaStream_t)cuda_stream;
   return ASR_OK;
@@ -439,10 +525,10 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
   out->step = c->step - 1;
   out->total = n;
   out->attended = st.attended;
-  out->active = c->step > 0 ? st.active_post : n;
+  out->active = c->step > 0 ? (int64_t)st.attended - st.frozen_this_step + st.restored_tick : n;
   out->frozen = n - out->active;
   out->frozen_this_step = st.frozen_this_step;
-  out->restored_this_step = st.restored_this_step;
+  out->restored_this_step = (int64_t)st.restored_pre + st.restored_rec + st.restored_tick;
   out->compression = n > 0 ? 1.0 - (double)out->active / (double)n : 0.0;
   out->entropy = st.entropy;
   out->entropy_valid = st.entropy_valid;
@@ -454,7 +540,10 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
   if (detail) {
     if (detail->capacity < n) return fail(ASR_E_INVALID, "detail->capacity < total");
     const size_t base = (size_t)seq * s.max_ctx;
-    if (detail->residency) CUDA_TRY(cudaMemcpy(detail->residency, s.res + base, n, cudaMemcpyDeviceToHost));
+    if (detail->residency) {
+      CUDA_TRY(cudaMemcpy(detail->residency, s.res + base, n, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < n; ++j) detail->residency[j] = asr::res_active(detail->residency[j]) ? 1 : 0;
+    }
     if (detail->timer) CUDA_TRY(cudaMemcpy(detail->timer, s.timer + base, n * 4, cudaMemcpyDeviceToHost));
     if (detail->count) CUDA_TRY(cudaMemcpy(detail->count, s.count + base, n * 4, cudaMemcpyDeviceToHost));
     if (detail->freeze_step) CUDA_TRY(cudaMemcpy(detail->freeze_step, s.fstep + base, n * 4, cudaMemcpyDeviceToHost));
@@ -492,7 +581,7 @@ asr_status asr_read_kv(asr_ctx* c, int32_t seq, int32_t pos, int32_t from_mirror
 
 asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
-  if (!ms || n < asr::kStages) return fail(ASR_E_INVALID, "ms must hold 5 values");
+  if (!ms || n < asr::kStages) return fail(ASR_E_INVALID, "ms must hold 3 values");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   for (int k = 0; k < n; ++k) ms[k] = 0.0;
@@ -507,6 +596,12 @@ asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches)
   c->prof_pending.clear();
   if (launches) *launches = c->launches;
   c->launches = 0;
+  return ASR_OK;
+}
+
+asr_status asr_set_profile(asr_ctx* c, int32_t on) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  c->cfg.profile_stages = on ? 1 : 0;
   return ASR_OK;
 }
 

@@ -3,26 +3,34 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 namespace asr {
 
-constexpr int kStages = 5;          // entropy, ledger_pre, attention, combine, decide
-constexpr int kEntSplits = 32;      // logits row splits for the entropy reduction
+constexpr int kStages = 3;          // pre (entropy+append+recovery+compaction), attention, post (combine+decide)
+constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
 constexpr int kLedgerThreads = 1024;
+constexpr int kDecideThreads = 512;
+
+// Residency byte: 1 = Active; 0 = Frozen; 2 / 3 = Frozen during a step of even / odd index (tag used
+// by the multi-block decide kernel to tell this step's freezes from older ones without ordering).
+__host__ __device__ constexpr bool res_active(uint8_t x) { return x == 1; }
+__host__ __device__ constexpr uint8_t res_tag(int step) { return (uint8_t)(2 + (step & 1)); }
 constexpr int kMaxDetBaseline = 256;
 
 // Per-sequence per-step statistics written by the kernels (read by asr_stats).
 struct SeqStats {
-  int32_t attended;
-  int32_t active_post;
-  int32_t frozen_this_step;
-  int32_t restored_this_step;
+  int32_t attended;           // |A_i|
+  int32_t frozen_this_step;   // d > 0 in the freeze loop
+  int32_t restored_tick;      // restored by the tick (incl. d = 1 freezes under R0)
+  int32_t restored_pre;       // restored at the step boundary by explicit asr_restore calls
+  int32_t restored_rec;       // restored at the step boundary by the entropy-triggered recovery
   int32_t pending_restored;   // explicit asr_restore since the last step
   int32_t recovery_action;
   int32_t rewalk_requested;
   int32_t entropy_valid;
   float entropy;
-  int32_t pad[3];
+  int32_t pad[2];
 };
 
 // Detector / ladder state per sequence (R-det, R-ladder).
@@ -50,6 +58,7 @@ struct DevState {
   int det_enable, det_baseline, det_cooldown, wr_window, fr_clear_counts;
   float det_z, det_sigma_floor;
   int max_splits, chunk_min;
+  int decide_blocks;          // blocks per sequence of the decide kernel
 
   void* kv;                   // pool [B*max_ctx][L][2][Hkv][d]
   uint8_t* res;               // [B][max_ctx] 1 Active / 0 Frozen
@@ -73,7 +82,14 @@ struct DevState {
   SeqStats* stats;            // [B]
   uint32_t* err;              // [1]
   int32_t* ticket;            // [1]
+  int32_t* pre_ticket;        // [B] compaction / recovery meeting point in the pre kernel
 };
+
+// Programmatic dependent launch (PDL): a kernel may let its dependent start early, and a dependent
+// waits for its programmatic upstream before touching the upstream's outputs.  Both are no-ops
+// without a programmatic edge (direct launches, profiled graphs).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, int* chunk, int* nch) {
   int c = (A + max_splits - 1) / max_splits;
@@ -83,17 +99,46 @@ __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, i
   *nch = (A + c - 1) / c;
 }
 
-// Kernel launchers (kernels_*.cu).  Return cudaGetLastError().
-cudaError_t launch_entropy(const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
-                           cudaStream_t st);
-cudaError_t launch_ledger_pre(const DevState& s, const void* k_new, const void* v_new, int has_entropy,
-                              cudaStream_t st);
-cudaError_t launch_attention(const DevState& s, const void* q, int grid, cudaStream_t st);
-cudaError_t launch_combine(const DevState& s, float* o, cudaStream_t st);
-cudaError_t launch_decide(const DevState& s, cudaStream_t st);
-cudaError_t launch_restore(const DevState& s, int seq, int level, cudaStream_t st);
+// One kernel launch described as data, so the same description serves a direct launch
+// (cudaLaunchKernel) and a CUDA-graph kernel node (cudaGraphAddKernelNode /
+// cudaGraphExecKernelNodeSetParams when a caller pointer changes).
+struct KNode {
+  cudaKernelNodeParams p{};
+  DevState s{};
+  uint64_t extra[4] = {0, 0, 0, 0};   // pointer / int arguments after DevState (8-byte slots)
+  void* argv[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  void finalize(const void* func, dim3 grid, dim3 block, unsigned smem) {
+    argv[0] = &s;
+    for (int k = 0; k < 4; ++k) argv[k + 1] = &extra[k];
+    p.func = const_cast<void*>(func);
+    p.gridDim = grid;
+    p.blockDim = block;
+    p.sharedMemBytes = smem;
+    p.kernelParams = argv;
+    p.extra = nullptr;
+  }
+  template <typename P>
+  void set(int k, P v) {
+    extra[k] = 0;
+    static_assert(sizeof(P) <= 8, "arg too large");
+    memcpy(&extra[k], &v, sizeof(P));
+  }
+  cudaError_t launch(cudaStream_t st) const {
+    return cudaLaunchKernel(p.func, p.gridDim, p.blockDim, const_cast<void**>(argv), p.sharedMemBytes, st);
+  }
+};
+
+// Node builders (kernels_*.cu).
+void node_pre(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
+              const void* k_new, const void* v_new);
+void node_attention(KNode& n, const DevState& s, const void* q, int grid);
+void node_post(KNode& n, const DevState& s, float* o);
+void node_restore(KNode& n, const DevState& s, int seq, int level);
 int attention_grid(const DevState& s, int num_sms);
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head
-cudaError_t launch_attention_mma(const DevState& s, const void* q, int grid, cudaStream_t st);
+cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory
+const void* attention_mma_func();
+unsigned attention_mma_smem();
+int attention_mma_threads();
 
 }  // namespace asr

@@ -8,7 +8,8 @@
 // This file holds the generic CUDA-core kernel (any head_dim in {16..256}, bf16 or fp32 KV):
 // one CTA per work item (b, l, chunk of A_b), one warp per KV head, persistent grid-stride over
 // the ragged work list (no host sync: the list is derived on the device from |A_b|).
-// The bf16 / LLaMA-shape fast path lives in kernels_attn_mma.cu.
+// The bf16 / LLaMA-shape fast path lives in kernels_attn_mma.cu; the combine of the split
+// partials runs in post_kernel (kernels_ledger.cu).
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -83,6 +84,8 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
   float* sc = reinterpret_cast<float*>(smem_i + s.B + 1);          // [Hkv][32]
   constexpr int EPL = D >= 32 ? D / 32 : 1;
   constexpr int ACT = D >= 32 ? 32 : D;
+  pdl_wait();
+  pdl_trigger();
   const int total = build_items(s, sh_start);
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = s.Hq / s.Hkv;
@@ -167,41 +170,15 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
   }
 }
 
-// Combine: one CTA per (b, l, h), d threads; fixed chunk order.
-__global__ void combine_kernel(DevState s, float* __restrict__ o) {
-  const int h = blockIdx.x % s.Hq;
-  const int l = (blockIdx.x / s.Hq) % s.L;
-  const int b = blockIdx.x / (s.Hq * s.L);
-  int chunk, nch;
-  chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
-  const long it0 = s.item_start[b] + (long)l * nch;
-  float M = -INFINITY;
-  for (int c = 0; c < nch; ++c) M = fmaxf(M, s.part_ml[((it0 + c) * s.Hq + h) * 2]);
-  float den = 0.f, num = 0.f;
-  const int e = threadIdx.x;
-  for (int c = 0; c < nch; ++c) {
-    const long pi = (it0 + c) * s.Hq + h;
-    const float w = exp2f(s.part_ml[pi * 2] - M);
-    den = fmaf(s.part_ml[pi * 2 + 1], w, den);
-    if (e < s.d) num = fmaf(s.part_acc[pi * s.d + e], w, num);
-  }
-  if (e < s.d) o[(((long)b * s.L + l) * s.Hq + h) * s.d + e] = num / den;
-}
-
 template <typename T>
-cudaError_t launch_generic(const DevState& s, const void* q, int grid, cudaStream_t st) {
-  const int threads = 32 * s.Hkv;
-  const size_t smem = sizeof(int) * (s.B + 1) + sizeof(float) * 32 * s.Hkv;
-  const T* qq = reinterpret_cast<const T*>(q);
-  switch (s.d) {
-    case 16: attn_generic_kernel<T, 16><<<grid, threads, smem, st>>>(s, qq); break;
-    case 32: attn_generic_kernel<T, 32><<<grid, threads, smem, st>>>(s, qq); break;
-    case 64: attn_generic_kernel<T, 64><<<grid, threads, smem, st>>>(s, qq); break;
-    case 128: attn_generic_kernel<T, 128><<<grid, threads, smem, st>>>(s, qq); break;
-    case 256: attn_generic_kernel<T, 256><<<grid, threads, smem, st>>>(s, qq); break;
-    default: return cudaErrorInvalidValue;
+const void* generic_func(int d) {
+  switch (d) {
+    case 16: return (const void*)attn_generic_kernel<T, 16>;
+    case 32: return (const void*)attn_generic_kernel<T, 32>;
+    case 64: return (const void*)attn_generic_kernel<T, 64>;
+    case 128: return (const void*)attn_generic_kernel<T, 128>;
+    default: return (const void*)attn_generic_kernel<T, 256>;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace
@@ -213,16 +190,16 @@ int attention_grid(const DevState& s, int num_sms) {
   return (int)(max_items < g ? max_items : g);
 }
 
-cudaError_t launch_attention(const DevState& s, const void* q, int grid, cudaStream_t st) {
-  if (attention_mma_supported(s)) return launch_attention_mma(s, q, grid, st);
-  if (s.dtype == 0) return launch_generic<__nv_bfloat16>(s, q, grid, st);
-  return launch_generic<float>(s, q, grid, st);
-}
-
-cudaError_t launch_combine(const DevState& s, float* o, cudaStream_t st) {
-  const int threads = s.d < 32 ? 32 : s.d;
-  combine_kernel<<<s.B * s.L * s.Hq, threads, 0, st>>>(s, o);
-  return cudaGetLastError();
+void node_attention(KNode& n, const DevState& s, const void* q, int grid) {
+  n.s = s;
+  n.set(0, q);
+  if (attention_mma_supported(s)) {
+    n.finalize(attention_mma_func(), dim3(grid), dim3(attention_mma_threads()), attention_mma_smem());
+    return;
+  }
+  const unsigned smem = (unsigned)(sizeof(int) * (s.B + 1) + sizeof(float) * 32 * s.Hkv);
+  const void* f = s.dtype == 0 ? generic_func<__nv_bfloat16>(s.d) : generic_func<float>(s.d);
+  n.finalize(f, dim3(grid), dim3(32 * s.Hkv), smem);
 }
 
 }  // namespace asr

@@ -5,16 +5,18 @@
 //   O_{l,h} = softmax(q_{l,h} K_{A,l,g(h)}^T / sqrt(d)) V_{A,l,g(h)}       Eq. 1, Alg. 1 line 1
 //   part_l(a) = sum_h |q_{l,h} . k_{l,A[a],g(h)}|                           Eq. 2, Alg. 1 line 2
 //
-// Design:
+// Design (tools/microbench_gather.cu measured the gather mechanisms on B200):
 // - persistent CTAs over the ragged work list (b, l, chunk of A_b), one CTA per SM;
-// - warp specialisation: 1 producer warp gathers the K and V rows of 16 active tokens per stage with
-//   one `cp.async.bulk` (TMA 1-D bulk copy, SASS UBLKCP) per 2 KiB row into a 3-stage shared-memory
-//   ring completed by mbarrier transaction counts; the ring runs across work items, so there is no
-//   pipeline drain between chunks; rows are padded to 2064 B so ldmatrix is bank-conflict free;
-// - 8 consumer warps, one per KV head: S^T = q K^T with `mma.sync.m16n8k16` bf16 -> fp32
-//   (4 query heads on M, tokens on N; exact on the lattice inputs), |S| summed over the 4 heads with
-//   quad shuffles gives the Eq. 2 head sum, fp32 online softmax (exp2), then O += P V with P split
-//   into bf16 hi + lo parts (two MMAs, ~2^-16 relative error instead of bf16's 2^-9);
+// - warp specialisation: 1 producer warp gathers the 4 KiB K|V row pair of each of 16 active tokens
+//   per stage with ONE `cp.async.bulk` (1-D TMA, SASS UBLKCP) per token into a 3-stage shared-memory
+//   ring completed by mbarrier transaction bytes, and the 8 KiB q of each work item into a 2-slot
+//   q ring; the rings run across work items (no pipeline drain between chunks); the active index
+//   of the next tile is prefetched while the current tile waits for its stage; 4112-byte token rows
+//   keep ldmatrix bank-conflict free;
+// - 8 consumer warps, one per KV head: S^T = q K^T with `mma.sync.m16n8k16` bf16 -> fp32 (4 query
+//   heads on M, tokens on N; exact on the lattice inputs), |S| summed over the 4 heads with quad
+//   shuffles gives the Eq. 2 head sum, fp32 online softmax (exp2), then O += P V with P split into
+//   bf16 hi + lo parts (two MMAs, ~2^-16 relative error instead of bf16's 2^-9);
 // - the producer also finishes the score: after a stage is released it sums the 8 warps' head sums
 //   per token in fixed order and writes one fp32 partial per (b, l, token) — the only extra HBM
 //   traffic of the score (0.1 % of the KV bytes).
@@ -32,17 +34,22 @@ constexpr int kHK = 8;                // KV heads (consumer warps)
 constexpr int kTM = 16;               // tokens per stage
 constexpr int kStagesRing = 3;
 constexpr int kRowBytes = kHK * kD * 2;         // 2048: one token-layer K (or V) row, all heads
-constexpr int kRowPad = kRowBytes + 16;         // 2064: ldmatrix conflict-free stride
-constexpr int kStageBytes = kTM * kRowPad;      // K (or V) tile of one stage
+constexpr int kTokBytes = 2 * kRowBytes;        // 4096: K row then V row (contiguous in the pool)
+constexpr int kTokPad = kTokBytes + 16;         // 4112: ldmatrix conflict-free stride
+constexpr int kStageBytes = kTM * kTokPad;
 constexpr int kThreads = (kHK + 1) * 32;
-constexpr int kMaxB = 4096;
+constexpr int kMaxB = 1024;                     // sequences per context on this path
+constexpr int kQBytes = kHK * kG * kD * 2;      // 8 KiB: q of one (b, l), all heads
 
 struct Smem {
-  alignas(128) uint8_t k[kStagesRing][kStageBytes];
-  alignas(128) uint8_t v[kStagesRing][kStageBytes];
+  alignas(128) uint8_t kv[kStagesRing][kStageBytes];
+  alignas(128) uint8_t q[2][kQBytes];    // q of the current / next work item
   float sc[kStagesRing][kHK][kTM];      // per-warp head sums |S| of each token
+  int start[kMaxB + 1];                 // work list: first item of each sequence
   alignas(8) uint64_t full[kStagesRing];
   alignas(8) uint64_t empty[kStagesRing];
+  alignas(8) uint64_t qfull[2];
+  alignas(8) uint64_t qempty[2];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -122,44 +129,65 @@ __device__ __forceinline__ ItemInfo decode_item(const DevState& s, const int* st
   return it;
 }
 
+// Iterator over this CTA's tiles: items blockIdx.x, blockIdx.x + gridDim.x, ...; 16 tokens a tile.
+struct TileIt {
+  int item, t0;
+  ItemInfo it;
+  __device__ bool valid(int total) const { return item < total; }
+  __device__ void advance(const DevState& s, const int* start, int total) {
+    t0 += kTM;
+    if (t0 >= it.n) {
+      item += gridDim.x;
+      t0 = 0;
+      if (item < total) it = decode_item(s, start, item);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  __shared__ int sh_start[kMaxB + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- prologue: work list (item_start), zeroed ring (masked rows must hold finite values), barriers
+  // ---- prologue independent of the upstream kernel (overlaps it under PDL): barriers and a zeroed
+  //      ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN would poison O)
   if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < s.B; ++b) {
-      sh_start[b] = acc;
-      int chunk, nch;
-      chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
-      acc += s.L * nch;
-    }
-    sh_start[s.B] = acc;
-    if (blockIdx.x == 0)
-      for (int b = 0; b <= s.B; ++b) s.item_start[b] = sh_start[b];
     for (int i = 0; i < kStagesRing; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], kHK);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.qfull[i], 1);
+      mbar_init(&sm.qempty[i], kHK);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   {
-    uint4* z = reinterpret_cast<uint4*>(&sm);
-    const int nz = (int)(offsetof(Smem, sc) / sizeof(uint4));
+    uint4* z = reinterpret_cast<uint4*>(&sm.kv[0][0]);
+    const int nz = (int)(sizeof(sm.kv) / sizeof(uint4));
     for (int i = threadIdx.x; i < nz; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     // order the generic-proxy zero fill before the async-proxy (bulk copy) writes to the same rows
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  pdl_wait();      // A_i, |A_i|, q and the appended K/V come from the pre kernel
+  pdl_trigger();   // the post kernel may be scheduled as CTAs retire
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < s.B; ++b) {
+      sm.start[b] = acc;
+      int chunk, nch;
+      chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+      acc += s.L * nch;
+    }
+    sm.start[s.B] = acc;
+    if (blockIdx.x == 0)
+      for (int b = 0; b <= s.B; ++b) s.item_start[b] = sm.start[b];
+  }
   __syncthreads();
-  const int total = sh_start[s.B];
-  const long row_elems = (long)kHK * kD;  // per token-layer K (or V)
+  const int total = sm.start[s.B];
 
   if (warp == kHK) {
     // ================================================================== producer warp
-    int g = 0;                       // CTA-local tile counter
     ItemInfo pend[kStagesRing];      // occupant of each stage (for the score epilogue)
 #pragma unroll
     for (int i = 0; i < kStagesRing; ++i) pend[i].n = 0;
@@ -172,30 +200,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
         s.score_part[((long)it.b * s.L + it.l) * s.max_ctx + it.a0 + lane] = t;
       }
     };
-    for (int item = blockIdx.x; item < total; item += gridDim.x) {
-      const ItemInfo it = decode_item(s, sh_start, item);
-      const int* act = s.act_pos + (long)it.b * s.max_ctx + it.a0;
-      const char* kvb = reinterpret_cast<const char*>(s.kv);
-      for (int t0 = 0; t0 < it.n; t0 += kTM, ++g) {
-        const int stage = g % kStagesRing;
-        const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
-        mbar_wait(&sm.empty[stage], ph ^ 1u);
-        __syncwarp();
-        epilogue(stage, pend[stage]);
-        const int cnt = min(kTM, it.n - t0);
-        ItemInfo tile{it.b, it.l, it.a0 + t0, cnt};
-#pragma unroll
-        for (int i = 0; i < kStagesRing; ++i)
-          if (i == stage) pend[i] = tile;
-        if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * 2u * kRowBytes);
-        __syncwarp();
-        if (lane < cnt) {
-          const long slot = (long)it.b * s.max_ctx + act[t0 + lane];
-          const char* src = kvb + ((slot * s.L + it.l) * 2) * row_elems * 2;
-          bulk_g2s(&sm.k[stage][lane * kRowPad], src, kRowBytes, &sm.full[stage]);
-          bulk_g2s(&sm.v[stage][lane * kRowPad], src + kRowBytes, kRowBytes, &sm.full[stage]);
+    const char* kvb = reinterpret_cast<const char*>(s.kv);
+    TileIt cur{(int)blockIdx.x, 0, {}};
+    if (cur.valid(total)) cur.it = decode_item(s, sm.start, cur.item);
+    auto load_idx = [&](const TileIt& t) -> int {
+      if (!t.valid(total) || lane >= min(kTM, t.it.n - t.t0)) return 0;
+      return __ldg(s.act_pos + (long)t.it.b * s.max_ctx + t.it.a0 + t.t0 + lane);
+    };
+    int j_cur = load_idx(cur);
+    int g = 0, it_local = -1;
+    while (cur.valid(total)) {
+      TileIt nxt = cur;
+      nxt.advance(s, sm.start, total);
+      const int j_next = load_idx(nxt);   // in flight while this tile waits for its stage
+      const ItemInfo& it = cur.it;
+      if (cur.t0 == 0) {                  // new work item: stage its q (8 KiB) in the q ring
+        ++it_local;
+        const int qs = it_local & 1;
+        mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
+        if (lane == 0) {
+          mbar_expect_tx(&sm.qfull[qs], kQBytes);
+          bulk_g2s(&sm.q[qs][0], q + ((long)it.b * s.L + it.l) * s.Hq * kD, kQBytes, &sm.qfull[qs]);
         }
       }
+      const int stage = g % kStagesRing;
+      const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
+      mbar_wait(&sm.empty[stage], ph ^ 1u);
+      __syncwarp();
+      epilogue(stage, pend[stage]);
+      const int cnt = min(kTM, it.n - cur.t0);
+      ItemInfo tile{it.b, it.l, it.a0 + cur.t0, cnt};
+#pragma unroll
+      for (int i = 0; i < kStagesRing; ++i)
+        if (i == stage) pend[i] = tile;
+      if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
+      __syncwarp();
+      if (lane < cnt) {
+        const long slot = (long)it.b * s.max_ctx + j_cur;
+        bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + it.l) * (long)kTokBytes, kTokBytes,
+                 &sm.full[stage]);
+      }
+      j_cur = j_next;
+      cur = nxt;
+      ++g;
     }
     // drain: the last (up to) kStagesRing tiles still owe their score epilogue
     for (int k = 0; k < kStagesRing; ++k) {
@@ -212,19 +259,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
   // ==================================================================== consumer warps (KV head = warp)
   const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
   const int r = lane >> 2, qd = lane & 3;   // fragment row / quad column
-  const uint32_t kbase = smem_u32(&sm.k[0][0]);
-  const uint32_t vbase = smem_u32(&sm.v[0][0]);
+  const uint32_t kvbase = smem_u32(&sm.kv[0][0]);
   // ldmatrix lane addresses (bytes within a stage tile, this warp's head)
   const int mi = lane >> 3, ri = lane & 7;
-  const uint32_t k_lane = (uint32_t)((ri + (mi >> 1) * 8) * kRowPad + warp * kD * 2 + (mi & 1) * 16);
-  const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kRowPad + warp * kD * 2 + (mi >> 1) * 16);
-  int g = 0;
+  const uint32_t k_lane = (uint32_t)((ri + (mi >> 1) * 8) * kTokPad + warp * kD * 2 + (mi & 1) * 16);
+  const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kTokPad + kRowBytes + warp * kD * 2 + (mi >> 1) * 16);
+  int g = 0, it_local = -1;
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const ItemInfo it = decode_item(s, sh_start, item);
-    // q fragments (rows 0..3 = the 4 query heads of this KV head, rows 4..15 zero)
+    const ItemInfo it = decode_item(s, sm.start, item);
+    // q fragments from the q ring (rows 0..3 = the 4 query heads of this KV head, rows 4..15 zero)
+    ++it_local;
+    const int qs = it_local & 1;
+    mbar_wait(&sm.qfull[qs], (uint32_t)(it_local >> 1) & 1u);
     uint32_t qa[8][2];
     {
-      const __nv_bfloat16* qh = q + (((long)it.b * s.L + it.l) * s.Hq + warp * kG + (r & 3)) * kD;
+      const __nv_bfloat16* qh = reinterpret_cast<const __nv_bfloat16*>(&sm.q[qs][0]) + (warp * kG + (r & 3)) * kD;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t lo = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * qd);
@@ -233,6 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
         qa[ks][1] = r < kG ? hi : 0u;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.qempty[qs]);
     float acc[16][4];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
@@ -242,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
       const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
       const int cnt = min(kTM, it.n - t0);
       mbar_wait(&sm.full[stage], ph);
-      const uint32_t ks_addr = kbase + stage * kStageBytes + k_lane;
-      const uint32_t vs_addr = vbase + stage * kStageBytes + v_lane;
+      const uint32_t ks_addr = kvbase + stage * kStageBytes + k_lane;
+      const uint32_t vs_addr = kvbase + stage * kStageBytes + v_lane;
       // ---- S^T[head][token] = q . k
       float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -289,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
         acc[i][0] *= corr;
         acc[i][1] *= corr;
       }
-      // P = hi + lo (bf16 each)
+      // P = hi + lo (bf16 each): bf16 P alone would break the 2e-3 bar
       const uint32_t ph0 = pack_bf16(p00, p01), ph1 = pack_bf16(p10, p11);
       const __nv_bfloat162 h0 = *reinterpret_cast<const __nv_bfloat162*>(&ph0);
       const __nv_bfloat162 h1 = *reinterpret_cast<const __nv_bfloat162*>(&ph1);
@@ -330,16 +381,11 @@ bool attention_mma_supported(const DevState& s) {
   return s.dtype == 0 && s.d == kD && s.Hkv == kHK && s.Hq == kHK * kG && s.B <= kMaxB;
 }
 
-cudaError_t launch_attention_mma(const DevState& s, const void* q, int grid, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(Smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  attn_mma_kernel<<<grid, kThreads, sizeof(Smem), st>>>(s, reinterpret_cast<const __nv_bfloat16*>(q));
-  return cudaGetLastError();
+cudaError_t attention_mma_prepare() {
+  return cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
 }
+const void* attention_mma_func() { return (const void*)attn_mma_kernel; }
+unsigned attention_mma_smem() { return (unsigned)sizeof(Smem); }
+int attention_mma_threads() { return kThreads; }
 
 }  // namespace asr

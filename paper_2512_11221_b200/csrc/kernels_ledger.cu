@@ -1,9 +1,11 @@
 // paper_2512_11221_b200/csrc/kernels_ledger.cu — the ledger side of one ASR-KF-EGR step (sm_100a):
-//   entropy_kernel     (a6) H(logits_prev), spike detector, recovery ladder   (Sec 3.6)
-//   ledger_pre_kernel  (a0) append + (a6) recovery levels + (a3) compaction of A_i (Alg. 1)
-//   decide_kernel      (a2) Eq. 2 finish, threshold, Eq. 3 schedule, freeze, tick (Alg. 1 lines 3-15)
-//   restore_kernel     explicit SR / WR / FR (asr_restore)
-// All reductions are in a fixed order, so the step is bitwise deterministic.
+//   pre_kernel      (a6) H(logits_prev) + spike detector + recovery ladder (Sec 3.6),
+//                   (a0) append, recovery levels, (a3) compaction of A_i (Alg. 1)
+//   post_kernel     (a4') fixed-order combine of the split-KV partials -> O, and
+//                   (a2) Eq. 2 finish, threshold, Eq. 3 schedule, freeze, tick (Alg. 1 lines 3-15)
+//   restore_kernel  explicit SR / WR / FR (asr_restore)
+// All floating-point reductions are in a fixed order, so the step is bitwise deterministic; the
+// integer counters use atomics (order-independent).
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -11,11 +13,6 @@
 
 namespace asr {
 namespace {
-
-__device__ __forceinline__ float ldf(const void* p, long i, int dtype) {
-  if (dtype == 0) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
-  return reinterpret_cast<const float*>(p)[i];
-}
 
 // Block-wide sum of int (blockDim multiple of 32, <= 1024).  Result valid in every thread.
 __device__ int block_sum_int(int v, int* sh) {
@@ -31,36 +28,81 @@ __device__ int block_sum_int(int v, int* sh) {
 }
 
 // ---------------------------------------------------------------------------------- (a6) entropy
-// Single pass per split: m = max x/T, Z = sum e^{x/T - m}, S = sum e^{x/T - m} (x/T - m);
-// H = ln Z - S/Z.  The last block of a row (atomic ticket) merges the splits in split order,
+// Per split of the row: m = max x/T, Z = sum e^{x/T - m}, S = sum e^{x/T - m} (x/T - m); the
+// last block of a row (atomic ticket) merges the splits in split order:
+//   H = ln Z - S / Z,  with (m, Z, S) rescaled to the global max,
 // then runs the detector (R-det) and the ladder (R-ladder) in double precision.
-__global__ void __launch_bounds__(256) entropy_kernel(DevState s, const void* logits, int ldt,
-                                                      float* entropy_out) {
-  const int split = blockIdx.x, b = blockIdx.y;
-  const int V = s.vocab;
-  const int seg = (V + kEntSplits - 1) / kEntSplits;
-  const int v0 = split * seg, v1 = min(V, v0 + seg);
-  const void* row = ldt == 0 ? (const void*)((const __nv_bfloat16*)logits + (long)b * V)
-                             : (const void*)((const float*)logits + (long)b * V);
-  const float invT = 1.0f / s.ent_temp;
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* x);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* x) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[2 * i] = __uint_as_float(w[i] << 16);
+    x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* x) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+__device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float tof(float v) { return v; }
+
+constexpr int kPreThreads = 512;
+
+// Partial (m, Z, S) of one split of row b; returns true in every thread of the block that
+// arrives last for the row (atomic ticket), after which the row's partials are complete.
+template <typename T>
+__device__ bool entropy_split(const DevState& s, const T* __restrict__ logits, int b, int split) {
   __shared__ float shm[32], shz[32], shs[32];
   __shared__ int last;
-  // pass 1: max
+  const int V = s.vocab;
+  const int seg = (((V + kEntSplits - 1) / kEntSplits) + 7) & ~7;   // multiple of 8 elements
+  const int v0 = min(V, split * seg), v1 = min(V, v0 + seg);
+  const T* row = logits + (long)b * V;
+  const bool vec = ((reinterpret_cast<uintptr_t>(row) & 31) == 0);
+  const float invT = 1.0f / s.ent_temp;
+  float x[8];
   float m = -INFINITY;
-  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) m = fmaxf(m, ldf(row, v, ldt) * invT);
+  const int v = v0 + (int)threadIdx.x * 8;   // one vector of 8 logits per thread
+  if (vec && v + 8 <= v1) {
+    load8<T>(row + v, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] *= invT;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] = (v + e < v1) ? tof(row[v + e]) * invT : -INFINITY;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m = fmaxf(m, x[e]);
+  // remainder (vocab > kEntSplits * 8 * kPreThreads)
+  for (int u = v0 + 8 * kPreThreads + (int)threadIdx.x; u < v1; u += kPreThreads) m = fmaxf(m, tof(row[u]) * invT);
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) shm[w] = m;
   __syncthreads();
   m = -INFINITY;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmaxf(m, shm[i]);
-  // pass 2: Z and S relative to the block max
+#pragma unroll
+  for (int k = 0; k < kPreThreads / 32; ++k) m = fmaxf(m, shm[k]);
   float z = 0.f, sx = 0.f;
-  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    float x = ldf(row, v, ldt) * invT - m;
-    float e = expf(x);
-    z += e;
-    sx += e * x;
+  if (m > -INFINITY) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = x[e] - m;   // -inf for padding -> ex = 0 (guarded product)
+      const float ex = expf(d);
+      z += ex;
+      sx += ex > 0.f ? ex * d : 0.f;
+    }
+    for (int u = v0 + 8 * kPreThreads + (int)threadIdx.x; u < v1; u += kPreThreads) {
+      const float d = tof(row[u]) * invT - m, ex = expf(d);
+      z += ex;
+      sx += ex * d;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     z += __shfl_xor_sync(0xffffffffu, z, o);
@@ -70,69 +112,86 @@ __global__ void __launch_bounds__(256) entropy_kernel(DevState s, const void* lo
   __syncthreads();
   if (threadIdx.x == 0) {
     z = 0.f; sx = 0.f;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { z += shz[i]; sx += shs[i]; }
+#pragma unroll
+    for (int k = 0; k < kPreThreads / 32; ++k) { z += shz[k]; sx += shs[k]; }
     float* ep = s.ent_part + ((long)b * kEntSplits + split) * 3;
     ep[0] = m; ep[1] = z; ep[2] = sx;
     __threadfence();
     last = atomicAdd(&s.ent_ticket[b], 1) == kEntSplits - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence();
-  // merge splits in order (double)
+  if (last) __threadfence();
+  return last;
+}
+
+// Warp 0 of the row's last block: merge the splits in a fixed order (double), H = ln Z - S/Z,
+// detector (R-det) and ladder (R-ladder).  Returns the recovery level in lane 0.
+__device__ int entropy_finish(const DevState& s, int b, float* entropy_out) {
+  const int lane = threadIdx.x & 31;
   const volatile float* ep = s.ent_part + (long)b * kEntSplits * 3;
+  double pm[kEntSplits / 32], pz[kEntSplits / 32], ps[kEntSplits / 32];
   double M = -INFINITY;
-  for (int i = 0; i < kEntSplits; ++i)
-    if (ep[i * 3 + 1] > 0.f) M = fmax(M, (double)ep[i * 3]);
-  double Z = 0.0, S = 0.0;
-  for (int i = 0; i < kEntSplits; ++i) {
-    double zi = ep[i * 3 + 1];
-    if (zi <= 0.0) continue;
-    double dm = (double)ep[i * 3] - M, f = exp(dm);
-    Z += zi * f;
-    S += f * ((double)ep[i * 3 + 2] + zi * dm);
+#pragma unroll
+  for (int k = 0; k < kEntSplits / 32; ++k) {
+    const int i = k * 32 + lane;
+    pm[k] = ep[i * 3]; pz[k] = ep[i * 3 + 1]; ps[k] = ep[i * 3 + 2];
+    if (pz[k] > 0.0) M = fmax(M, pm[k]);
   }
-  const double H = log(Z) - S / Z;
-  s.ent_ticket[b] = 0;
-  if (entropy_out) entropy_out[b] = (float)H;
-  SeqStats& st = s.stats[b];
-  st.entropy = (float)H;
-  st.entropy_valid = 1;
-  // detector: H > mean + z * max(sigma, floor) over the previous <= det_baseline values
+  for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  double Zl = 0.0, Sl = 0.0;
+#pragma unroll
+  for (int k = 0; k < kEntSplits / 32; ++k) {
+    if (pz[k] <= 0.0) continue;
+    const double dm = pm[k] - M, f = exp(dm);
+    Zl += pz[k] * f;
+    Sl += f * (ps[k] + pz[k] * dm);
+  }
+  for (int o = 16; o > 0; o >>= 1) {   // fixed-order tree over lanes (deterministic)
+    Zl += __shfl_xor_sync(0xffffffffu, Zl, o);
+    Sl += __shfl_xor_sync(0xffffffffu, Sl, o);
+  }
+  const double H = log(Zl) - Sl / Zl;
   DetState& ds = s.det[b];
   double* hist = s.hist + (long)b * s.det_baseline;
-  int trig = 0;
-  if (s.det_enable && ds.hist_len >= 2) {
-    double mu = 0.0;
-    for (int t = 0; t < ds.hist_len; ++t) mu += hist[t];
-    mu /= ds.hist_len;
-    double var = 0.0;
-    for (int t = 0; t < ds.hist_len; ++t) var += (hist[t] - mu) * (hist[t] - mu);
-    var /= ds.hist_len;
-    double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
-    trig = H > mu + (double)s.det_z * sd;
-  }
-  if (ds.hist_len < s.det_baseline) {
-    hist[ds.hist_len++] = H;
-  } else {
-    hist[ds.hist_head] = H;
-    ds.hist_head = (ds.hist_head + 1) % s.det_baseline;
-  }
+  const int hl = ds.hist_len;
+  double mu = 0.0, var = 0.0;
+  for (int t = lane; t < hl; t += 32) mu += hist[t];
+  for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+  mu = hl > 0 ? mu / hl : 0.0;
+  for (int t = lane; t < hl; t += 32) var += (hist[t] - mu) * (hist[t] - mu);
+  for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
   int level = 0;
-  if (trig) {
-    const int i = *s.step;
-    const int dt = i - ds.last_action_step;
-    if (ds.has_last && dt < s.det_cooldown) {
-      level = 0;  // absorbed
-    } else {
-      if (ds.has_last && dt < 2 * s.det_cooldown) level = ds.level < 4 ? ds.level + 1 : 4;
-      else level = 1;
-      ds.level = level;
-      ds.last_action_step = i;
-      ds.has_last = 1;
+  if (lane == 0) {
+    var = hl > 0 ? var / hl : 0.0;
+    int trig = 0;
+    if (s.det_enable && hl >= 2) {
+      const double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
+      trig = H > mu + (double)s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
     }
+    if (hl < s.det_baseline) {
+      hist[hl] = H;
+      ds.hist_len = hl + 1;
+    } else {
+      hist[ds.hist_head] = H;
+      ds.hist_head = (ds.hist_head + 1) % s.det_baseline;
+    }
+    if (trig) {
+      const int i = *s.step;
+      const int dt = i - ds.last_action_step;
+      if (!(ds.has_last && dt < s.det_cooldown)) {   // absorbed inside the cooldown
+        level = (ds.has_last && dt < 2 * s.det_cooldown) ? (ds.level < 4 ? ds.level + 1 : 4) : 1;
+        ds.level = level;
+        ds.last_action_step = i;
+        ds.has_last = 1;
+      }
+    }
+    s.ent_ticket[b] = 0;
+    if (entropy_out) entropy_out[b] = (float)H;
+    SeqStats& st = s.stats[b];
+    st.entropy = (float)H;
+    st.entropy_valid = 1;
   }
-  s.rec_action[b] = level;
+  return level;
 }
 
 // Recovery levels on one sequence's ledger: returns the restored count of this thread.
@@ -142,7 +201,7 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   int32_t* timer = s.timer + (long)b * s.max_ctx;
   const int32_t* fstep = s.fstep + (long)b * s.max_ctx;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    if (res[j] != 0) continue;
+    if (res_active(res[j])) continue;
     bool go = level == 1 ? timer[j] > 1 : level == 2 ? fstep[j] >= i - s.wr_window : true;
     if (go) {
       res[j] = 1;
@@ -157,67 +216,34 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   return restored;
 }
 
-// ------------------------------------------------------------------ (a0) + recovery + (a3) compaction
-// Blocks [0, B): the ledger of sequence b.  Blocks [B, B + B*L): append the new token's K/V rows
-// of (b, l) into its slot of the pool.
-template <typename T>
-__global__ void __launch_bounds__(kLedgerThreads) ledger_pre_kernel(DevState s, const T* k_new,
-                                                                    const T* v_new, int has_entropy) {
-  const int i = *s.step;
-  if ((int)blockIdx.x >= s.B) {  // ---- append K/V rows
-    const int r = blockIdx.x - s.B;
-    const int b = r / s.L, l = r % s.L;
-    const long pos = s.prompt_len[b] + i;
-    const long slot = (long)b * s.max_ctx + pos;
-    const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
-    T* dst = reinterpret_cast<T*>(s.kv) + (slot * s.L + l) * 2 * row;
-    const T* ks = k_new + ((long)b * s.L + l) * row;
-    const T* vs = v_new + ((long)b * s.L + l) * row;
-    const int vec = (int)(16 / sizeof(T));
-    if (row % vec == 0) {
-      const int nv = row / vec;
-      for (int t = threadIdx.x; t < 2 * nv; t += blockDim.x) {
-        const uint4* src = reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv);
-        reinterpret_cast<uint4*>(dst)[t] = *src;
-      }
-    } else {
-      for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) dst[t] = t < row ? ks[t] : vs[t - row];
-    }
-    return;
+// ------------------------------------------------------------------ (a3) compaction
+// A_i = sorted positions with residency Active, written by one block.  Thread t owns a contiguous
+// run of 16-position vectors (uint4 loads of the residency bytes; rows are 64-aligned and positions
+// >= n hold 0), counts, block-scans, then writes its positions.
+__device__ int active_mask16(uint4 u, uint32_t* m) {  // per byte: 1 iff residency == 1 (values 0..3)
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    m[k] = w[k] & 0x01010101u & ~((w[k] >> 1) & 0x01010101u);
+    c += __popc(m[k]);
   }
-  // ---- ledger of sequence b
-  __shared__ int sh[32];
+  return c;
+}
+
+__device__ void compact_block(const DevState& s, int b, int n) {
   __shared__ int wsum[32];
-  const int b = blockIdx.x;
-  const int n = s.prompt_len[b] + i + 1;  // total after the append
   const long base = (long)b * s.max_ctx;
-  SeqStats& st = s.stats[b];
-  if (threadIdx.x == 0) {
-    const int j = n - 1;  // the token produced by the previous step (Alg. 1 line 16)
-    s.res[base + j] = 1;
-    s.timer[base + j] = 0;
-    s.count[base + j] = 0;
-    s.fstep[base + j] = -1;
-  }
-  int level = has_entropy ? s.rec_action[b] : 0;
-  int restored = 0;
-  if (level > 0) restored = apply_level(s, b, n - 1, level, i);
-  restored = block_sum_int(restored, sh);  // includes a __syncthreads
-  if (threadIdx.x == 0) {
-    st.restored_this_step = st.pending_restored + restored;
-    st.pending_restored = 0;
-    st.recovery_action = level;
-    st.rewalk_requested = level == 4;
-    if (!has_entropy) st.entropy_valid = 0;
-    st.frozen_this_step = 0;
-  }
-  // compaction: each thread owns a contiguous segment of positions
-  const int seg = (n + blockDim.x - 1) / blockDim.x;
-  const int j0 = min(n, (int)threadIdx.x * seg), j1 = min(n, j0 + seg);
   const uint8_t* res = s.res + base;
+  const int nvec = (n + 15) >> 4;
+  const int per = (nvec + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int v0 = min(nvec, (int)threadIdx.x * per), v1 = min(nvec, v0 + per);
   int cnt = 0;
-  for (int j = j0; j < j1; ++j) cnt += res[j];
-  // exclusive block scan of cnt
+#pragma unroll 4
+  for (int v = v0; v < v1; ++v) {
+    uint32_t m[4];
+    cnt += active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
+  }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int incl = cnt;
   for (int o = 1; o < 32; o <<= 1) {
@@ -238,13 +264,127 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_pre_kernel(DevState s, 
   __syncthreads();
   int off = wsum[w] + incl - cnt;
   int32_t* out = s.act_pos + base;
-  for (int j = j0; j < j1; ++j)
-    if (res[j]) out[off++] = j;
+  for (int v = v0; v < v1; ++v) {
+    uint32_t m[4];
+    active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      while (m[k]) {
+        const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
+        out[off++] = v * 16 + k * 4 + (bit >> 3);
+        m[k] &= m[k] - 1;
+      }
+  }
   if (threadIdx.x == blockDim.x - 1) {
     s.act_len[b] = off;
-    st.attended = off;
+    s.stats[b].attended = off;
     if (off == 0) atomicOr(s.err, kErrEmptyActive);
   }
+  __syncthreads();
+}
+
+// Meeting point of the compaction block and the entropy block of sequence b: returns true (in all
+// threads) for the second arriver.
+__device__ bool pre_meet(const DevState& s, int b) {
+  __shared__ int second;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    second = atomicAdd(&s.pre_ticket[b], 1) == 1;
+    if (second) s.pre_ticket[b] = 0;
+    __threadfence();
+  }
+  __syncthreads();
+  return second;
+}
+
+// ------------------------------------------------------------------ pre_kernel
+// (a6) entropy + detector + ladder + recovery, (a0) append and (a3) compaction in one launch:
+//   blocks [0, B*S)          S = kEntSplits splits of each logits row (none without logits); the last
+//                            split block of row b finishes H, runs the detector and the ladder and
+//                            applies the recovery level to the ledger;
+//   blocks [B*S, B*S + B)    sequence b: ledger entry of the appended position n-1, then compaction
+//                            of A_i in parallel with the entropy (recovery is rare: whichever of the
+//                            two blocks of b arrives second recompacts when a level was applied);
+//   blocks [.., + B*L)       copy the new token's K/V rows of (b, l) into its slot.
+template <typename TL, typename TK>
+__global__ void __launch_bounds__(kPreThreads) pre_kernel(DevState s, const TL* logits, float* entropy_out,
+                                                             const TK* k_new, const TK* v_new) {
+  pdl_trigger();   // the attention kernel may start its (independent) prologue now
+  const int i = *s.step;
+  const int S = logits ? kEntSplits : 0;
+  const int blk = blockIdx.x;
+  if (blk >= s.B * S + s.B) {  // ---- append K/V rows
+    const int r = blk - s.B * S - s.B;
+    const int b = r / s.L, l = r % s.L;
+    const long pos = s.prompt_len[b] + i;
+    const long slot = (long)b * s.max_ctx + pos;
+    const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
+    TK* dst = reinterpret_cast<TK*>(s.kv) + (slot * s.L + l) * 2 * row;
+    const TK* ks = k_new + ((long)b * s.L + l) * row;
+    const TK* vs = v_new + ((long)b * s.L + l) * row;
+    const int vec = (int)(16 / sizeof(TK));
+    if (row % vec == 0) {
+      const int nv = row / vec;
+      for (int t = threadIdx.x; t < 2 * nv; t += blockDim.x) {
+        const uint4* src = reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv);
+        reinterpret_cast<uint4*>(dst)[t] = *src;
+      }
+    } else {
+      for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) dst[t] = t < row ? ks[t] : vs[t - row];
+    }
+    return;
+  }
+  if (blk >= s.B * S) {  // ---- compaction block of sequence b
+    const int b = blk - s.B * S;
+    const int n = s.prompt_len[b] + i + 1;  // total after the append
+    const long base = (long)b * s.max_ctx;
+    if (threadIdx.x == 0) {
+      const int j = n - 1;  // the token produced by the previous step (Alg. 1 line 16)
+      s.res[base + j] = 1;
+      s.timer[base + j] = 0;
+      s.count[base + j] = 0;
+      s.fstep[base + j] = -1;
+      SeqStats& st = s.stats[b];
+      st.restored_pre = st.pending_restored;
+      st.pending_restored = 0;
+      st.restored_tick = 0;
+      st.frozen_this_step = 0;
+      if (!logits) {
+        st.recovery_action = 0;
+        st.rewalk_requested = 0;
+        st.entropy_valid = 0;
+        st.restored_rec = 0;
+      }
+    }
+    __syncthreads();
+    compact_block(s, b, n);
+    if (logits && pre_meet(s, b) && s.rec_action[b] > 0) compact_block(s, b, n);
+    return;
+  }
+  // ---- entropy split of row b
+  __shared__ int sh[32];
+  __shared__ int sh_level;
+  const int b = blk / S;
+  if (!entropy_split<TL>(s, logits, b, blk % S)) return;   // block-uniform
+  if (threadIdx.x < 32) {
+    const int lv = entropy_finish(s, b, entropy_out);
+    if (threadIdx.x == 0) sh_level = lv;
+  }
+  __syncthreads();
+  const int level = sh_level;
+  const int n = s.prompt_len[b] + i + 1;
+  int restored = 0;
+  if (level > 0) restored = apply_level(s, b, n - 1, level, i);
+  restored = block_sum_int(restored, sh);
+  if (threadIdx.x == 0) {
+    SeqStats& st = s.stats[b];
+    st.restored_rec = restored;
+    st.recovery_action = level;
+    st.rewalk_requested = level == 4;
+    s.rec_action[b] = level;
+  }
+  if (pre_meet(s, b) && level > 0) compact_block(s, b, n);
 }
 
 // ------------------------------------------------------------------ (a2) decide + tick
@@ -265,9 +405,13 @@ __device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
   return m;
 }
 
-__global__ void __launch_bounds__(kLedgerThreads) decide_kernel(DevState s) {
+// Grid (decide_blocks, B).  Block x of sequence b handles a slice of the attended list (Alg. 1
+// lines 3-9 + the R0 tick of the tokens it freezes) and a slice of the positions (lines 10-15 for
+// tokens frozen at earlier steps).  The two index sets are disjoint (A_i = the tokens Active at the
+// step start), and tokens frozen in this step carry the step-parity tag res_tag(i), so the blocks
+// need no ordering between them.
+__device__ void decide_block(const DevState& s, int b, int x, int X, int nblocks_total) {
   __shared__ int sh[32];
-  const int b = blockIdx.x;
   const int i = *s.step;
   const int n = s.prompt_len[b] + i + 1;
   const long base = (long)b * s.max_ctx;
@@ -278,12 +422,25 @@ __global__ void __launch_bounds__(kLedgerThreads) decide_kernel(DevState s) {
   int32_t* fstep = s.fstep + base;
   const float inv = 1.0f / (float)(s.L * s.Hq);
   const float inv_sqrt_d = rsqrtf((float)s.d);
-  // Alg. 1 lines 3-9 (each attended token is visited by exactly one thread)
-  int frozen_now = 0;
-  for (int a = threadIdx.x; a < A; a += blockDim.x) {
+  const uint8_t tag_now = res_tag(i);
+  int frozen_now = 0, restored = 0;
+  // ---- lines 3-9 over this block's slice of A_i
+  const int per_a = (A + X - 1) / X;
+  const int a_end = min(A, (x + 1) * per_a);
+  for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
     const int j = s.act_pos[base + a];
+    // sum over layers in order l = 0..L-1; loads issued 8 at a time so their latencies overlap
+    const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
     float sum = 0.f;
-    for (int l = 0; l < s.L; ++l) sum += s.score_part[((long)b * s.L + l) * s.max_ctx + a];
+    int l = 0;
+    for (; l + 8 <= s.L; l += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = sp[(long)(l + u) * s.max_ctx];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; l < s.L; ++l) sum += sp[(long)l * s.max_ctx];
     float sj = sum * inv;               // Eq. 2: mean over the L*Hq (layer, head) pairs
     if (s.score_scaled) sj *= inv_sqrt_d;
     s.score[base + a] = sj;
@@ -292,20 +449,26 @@ __global__ void __launch_bounds__(kLedgerThreads) decide_kernel(DevState s) {
       cnt[j] = c;
       const int dd = duration(c, s.softness, s.softness_int);  // line 5
       if (dd > 0) {                     // lines 6-7
-        res[j] = 0;
-        timer[j] = dd;
-        fstep[j] = i;
         frozen_now++;
+        fstep[j] = i;
+        const int t = s.tick_skip_new ? dd : dd - 1;   // R0: this step's tick applies too
+        if (t <= 0) {
+          timer[j] = 0;                 // frozen and restored by the same tick (no absence)
+          restored++;
+        } else {
+          timer[j] = t;
+          res[j] = tag_now;
+        }
       }
     }
   }
-  __syncthreads();
-  // Alg. 1 lines 10-15: tick every frozen token (R0: including those frozen above)
-  int restored = 0;
+  // ---- lines 10-15 for tokens frozen before this step
   uint32_t err = 0;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    if (res[j] != 0) continue;
-    if (s.tick_skip_new && fstep[j] == i) continue;
+  const int per_n = (n + X - 1) / X;
+  const int n_end = min(n, (x + 1) * per_n);
+  for (int j = x * per_n + threadIdx.x; j < n_end; j += blockDim.x) {
+    const uint8_t r = res[j];
+    if (r == 1 || r == tag_now) continue;
     const int t = timer[j] - 1;
     if (t <= 0) {
       res[j] = 1;
@@ -313,6 +476,7 @@ __global__ void __launch_bounds__(kLedgerThreads) decide_kernel(DevState s) {
       restored++;
     } else {
       timer[j] = t;
+      if (r != 0) res[j] = 0;           // drop the previous step's tag
       if (j >= n - s.window) err |= kErrFrozenInWindow;
     }
   }
@@ -321,15 +485,88 @@ __global__ void __launch_bounds__(kLedgerThreads) decide_kernel(DevState s) {
   restored = block_sum_int(restored, sh);
   if (threadIdx.x == 0) {
     SeqStats& st = s.stats[b];
-    st.frozen_this_step = frozen_now;
-    st.restored_this_step += restored;
-    st.active_post = A - frozen_now + restored;
+    if (frozen_now) atomicAdd(&st.frozen_this_step, frozen_now);
+    if (restored) atomicAdd(&st.restored_tick, restored);
     __threadfence();
-    if (atomicAdd(s.ticket, 1) == (int)gridDim.x - 1) {  // last sequence: advance the step
+    if (atomicAdd(s.ticket, 1) == nblocks_total - 1) {  // last decide block: advance the step
       *s.ticket = 0;
       *s.step = i + 1;
     }
   }
+}
+
+// Combine: one warp per (b, l, h); lane c < nch reads split c's (m, l); each lane owns d/32
+// output elements.  Fixed split order -> deterministic.
+__device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) {
+  const int lane = threadIdx.x & 31;
+  const int h = wid % s.Hq;
+  const int l = (wid / s.Hq) % s.L;
+  const int b = wid / (s.Hq * s.L);
+  int chunk, nch;
+  chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+  const long it0 = s.item_start[b] + (long)l * nch;
+  float M = -INFINITY;
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, s.part_ml[((it0 + c) * s.Hq + h) * 2]);
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const int epl = s.d >= 32 ? s.d / 32 : 1;   // elements per lane (d <= 256 -> <= 8)
+  const bool on = lane * epl < s.d;
+  float num[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float den = 0.f;
+  for (int c0 = 0; c0 < nch; c0 += 32) {
+    float wl = 0.f, ll = 0.f;
+    if (c0 + lane < nch) {
+      const long pi = (it0 + c0 + lane) * s.Hq + h;
+      wl = exp2f(s.part_ml[pi * 2] - M);
+      ll = s.part_ml[pi * 2 + 1];
+    }
+    const int cn = min(32, nch - c0);
+    if (epl == 4) {
+      // 8 chunk vectors in flight at a time, accumulated in chunk order
+      for (int cb = 0; cb < cn; cb += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (cb + u < cn)
+            v[u] = *reinterpret_cast<const float4*>(s.part_acc + ((it0 + c0 + cb + u) * s.Hq + h) * (long)s.d +
+                                                    lane * 4);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (cb + u >= cn) break;
+          const float w = __shfl_sync(0xffffffffu, wl, cb + u);
+          den = fmaf(__shfl_sync(0xffffffffu, ll, cb + u), w, den);
+          num[0] = fmaf(v[u].x, w, num[0]); num[1] = fmaf(v[u].y, w, num[1]);
+          num[2] = fmaf(v[u].z, w, num[2]); num[3] = fmaf(v[u].w, w, num[3]);
+        }
+      }
+    } else {
+      for (int c = 0; c < cn; ++c) {
+        const float w = __shfl_sync(0xffffffffu, wl, c);
+        den = fmaf(__shfl_sync(0xffffffffu, ll, c), w, den);
+        if (on) {
+          const float* src = s.part_acc + ((it0 + c0 + c) * s.Hq + h) * (long)s.d + lane * epl;
+          for (int e = 0; e < epl; ++e) num[e] = fmaf(src[e], w, num[e]);
+        }
+      }
+    }
+  }
+  if (on) {
+    float* dst = o + (((long)b * s.L + l) * s.Hq + h) * s.d + lane * epl;
+    const float inv = 1.0f / den;
+    for (int e = 0; e < epl; ++e) dst[e] = num[e] * inv;
+  }
+}
+
+// Blocks [0, decide_blocks * B): decide + tick (block x of sequence b); the remaining blocks:
+// combine, one warp per (b, l, h).
+__global__ void __launch_bounds__(kDecideThreads) post_kernel(DevState s, float* __restrict__ o) {
+  pdl_wait();      // every input comes from the attention kernel
+  const int nd = s.decide_blocks * s.B;
+  if ((int)blockIdx.x < nd) {
+    decide_block(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, nd);
+    return;
+  }
+  const int wid = ((int)blockIdx.x - nd) * (kDecideThreads / 32) + (threadIdx.x >> 5);
+  if (wid < s.B * s.L * s.Hq) combine_warp(s, wid, o);
 }
 
 // Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.
@@ -345,32 +582,36 @@ __global__ void __launch_bounds__(kLedgerThreads) restore_kernel(DevState s, int
 
 }  // namespace
 
-cudaError_t launch_entropy(const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
-                           cudaStream_t st) {
-  entropy_kernel<<<dim3(kEntSplits, s.B), 256, 0, st>>>(s, logits, logits_dtype, entropy_out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_ledger_pre(const DevState& s, const void* k_new, const void* v_new, int has_entropy,
-                              cudaStream_t st) {
-  const int grid = s.B + s.B * s.L;
+void node_pre(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
+              const void* k_new, const void* v_new) {
+  n.s = s;
+  n.set(0, logits);
+  n.set(1, entropy_out);
+  n.set(2, k_new);
+  n.set(3, v_new);
+  const bool lf = logits && logits_dtype == 1;
+  const void* f;
   if (s.dtype == 0)
-    ledger_pre_kernel<__nv_bfloat16><<<grid, kLedgerThreads, 0, st>>>(
-        s, (const __nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new, has_entropy);
+    f = lf ? (const void*)pre_kernel<float, __nv_bfloat16> : (const void*)pre_kernel<__nv_bfloat16, __nv_bfloat16>;
   else
-    ledger_pre_kernel<float><<<grid, kLedgerThreads, 0, st>>>(s, (const float*)k_new, (const float*)v_new,
-                                                              has_entropy);
-  return cudaGetLastError();
+    f = lf ? (const void*)pre_kernel<float, float> : (const void*)pre_kernel<__nv_bfloat16, float>;
+  const int S = logits ? kEntSplits : 0;
+  n.finalize(f, dim3(s.B * S + s.B + s.B * s.L), dim3(kPreThreads), 0);
 }
 
-cudaError_t launch_decide(const DevState& s, cudaStream_t st) {
-  decide_kernel<<<s.B, kLedgerThreads, 0, st>>>(s);
-  return cudaGetLastError();
+void node_post(KNode& n, const DevState& s, float* o) {
+  n.s = s;
+  n.set(0, o);
+  const int warps = s.B * s.L * s.Hq;
+  const int wpb = kDecideThreads / 32;
+  n.finalize((const void*)post_kernel, dim3(s.decide_blocks * s.B + (warps + wpb - 1) / wpb), dim3(kDecideThreads), 0);
 }
 
-cudaError_t launch_restore(const DevState& s, int seq, int level, cudaStream_t st) {
-  restore_kernel<<<seq >= 0 ? 1 : s.B, kLedgerThreads, 0, st>>>(s, seq, level);
-  return cudaGetLastError();
+void node_restore(KNode& n, const DevState& s, int seq, int level) {
+  n.s = s;
+  n.set(0, seq);
+  n.set(1, level);
+  n.finalize((const void*)restore_kernel, dim3(seq >= 0 ? 1 : s.B), dim3(kLedgerThreads), 0);
 }
 
 }  // namespace asr
