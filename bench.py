@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps (for ncu)")
+    ap.add_argument("--timeline", action="store_true", help="device timeline of 8 extra steps (ASR_TIMELINE)")
     return ap.parse_args()
 
 
@@ -176,12 +177,14 @@ def run_asr(a, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if a.timeline:
+        os.environ["ASR_TIMELINE"] = "1"
     B = a.batch
     P = a.window
     grow = a.context - P - 1                     # steps before the measured region starts
     W, K = a.warmup, a.steps
     e2e_steps = 0 if a.no_e2e else K
-    max_ctx = a.context + W + 2 * K + e2e_steps + 4
+    max_ctx = a.context + W + 2 * K + e2e_steps + 16
     g = gen_params(a, rank)
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=0,
@@ -221,7 +224,18 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     LG = torch.empty((n_meas, B, VOCAB), dtype=bf, device=dev)
     for t in range(n_meas):
         inputs(grow + t, Q[t], KN[t], VN[t], LG[t])
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # L2 flush between timed steps (outside the events): write a 256 MiB buffer (> 126 MB L2), then
+    # read another 256 MiB buffer so the flush's dirty lines are written back before the step starts
+    flush_w = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_acc = torch.empty((), dtype=torch.float32, device=dev)
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            flush_w.zero_()
+            torch.sum(flush_r, dim=0, out=flush_acc)
+    flush = _Flush()
     st = torch.cuda.current_stream()
     for t in range(W):
         flush.zero_()
@@ -261,6 +275,15 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     stage_ms, launches = ctx.stage_times()
     ctx.set_profile(False)
     stats_p = [ctx.stats(b) for b in range(B)]
+    timeline = None
+    if a.timeline:
+        tls = []
+        for t in range(8):
+            flush.zero_()
+            ctx.step(Q[W + t], KN[W + t], VN[W + t], o, logits_prev=LG[W + t], entropy=ent)
+            tls.append(ctx.timeline())
+        timeline = {"pre_start_end_attn_start_end_post_start_end_us": [statistics.median(x) for x in zip(*tls)]}
+        print("timeline (us):", json.dumps(tls), file=sys.stderr)
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below
     att_last = sum(s["attended"] for s in stats)
@@ -334,7 +357,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}",
                    "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": 0.5, "k": 2,
-                   "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed (256 MiB write) between timed steps",
+                   "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
                    "parallelism": f"sequence-sharded x{world} (no hot-path collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "attention+score (split-KV over A_i)",
@@ -349,6 +372,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                    "compression": stats[0]["compression"],
                    "stage_ms_per_step_profiled": {n: v / K for n, v in zip(STAGES, stage_ms)},
                    "profiled_launches": launches,
+                   "timeline": timeline,
                    "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
                    "wall_s_timed": t_wall, "grow_s": t_grow,
                    "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES},

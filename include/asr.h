@@ -158,6 +158,11 @@ asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launche
  * (no programmatic dependent launch); off is the production configuration. */
 asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
 
+/* Diagnostic: device timeline of the last step (needs ASR_TIMELINE=1 in the environment at
+ * asr_create): us[2k], us[2k+1] = first-block start and last-block end of stage k (pre, attention,
+ * post) in microseconds relative to the pre kernel's start (%globaltimer).  n >= 6.  Synchronises. */
+asr_status asr_timeline(asr_ctx* ctx, double* us, int32_t n);
+
 /* Synchronise and free everything the context owns. */
 asr_status asr_destroy(asr_ctx* ctx);
 

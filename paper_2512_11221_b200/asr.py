@@ -65,7 +65,7 @@ class asr_ledger_view(ctypes.Structure):
 
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
-           "asr_stage_times", "asr_set_profile", "asr_destroy", "asr_last_error")
+           "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_destroy", "asr_last_error")
 
 _lib = None
 
@@ -88,8 +88,9 @@ def lib() -> ctypes.CDLL:
         L.asr_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32, ctypes.POINTER(ctypes.c_int64)]
         L.asr_destroy.argtypes = [vp]
         L.asr_set_profile.argtypes = [vp, i32]
+        L.asr_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
-                  "asr_set_profile", "asr_destroy"):
+                  "asr_set_profile", "asr_timeline", "asr_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -227,6 +228,12 @@ def asr_stage_times(ctx):
     return list(ms), int(n.value)
 
 
+def asr_timeline(ctx) -> list:
+    us = (ctypes.c_double * 6)()
+    _check(lib().asr_timeline(ctx, us, 6))
+    return list(us)
+
+
 def asr_set_profile(ctx, on: bool) -> None:
     _check(lib().asr_set_profile(ctx, int(bool(on))))
 
@@ -256,6 +263,9 @@ class Context:
 
     def stage_times(self):
         return asr_stage_times(self._h)
+
+    def timeline(self):
+        return asr_timeline(self._h)
 
     def set_profile(self, on: bool):
         asr_set_profile(self._h, on)

@@ -304,6 +304,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
     const char* ng = getenv("ASR_NO_GRAPH");
     c->use_graph = !(ng && ng[0] == '1');
+    const char* tlenv = getenv("ASR_TIMELINE");
+    if (tlenv && tlenv[0] == '1') {
+      CUDA_TRY(c->alloc(&s.tl, sizeof(unsigned long long) * 2 * asr::kStages));
+    }
     const char* np = getenv("ASR_NO_PDL");
     c->use_pdl = !(np && np[0] == '1');
     c->last_stream = st;
@@ -391,6 +395,11 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     c->prof_pending.push_back(c->prof_free.back());
     c->prof_free.pop_back();
     ev = &c->prof_pending.back();
+  }
+  if (s.tl) {   // diagnostic timeline of this step: start stamps = +inf, end stamps = 0
+    unsigned long long init[2 * asr::kStages];
+    for (int k = 0; k < asr::kStages; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
+    CUDA_TRY(cudaMemcpyAsync(s.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   // the step as kernel descriptions, one per stage
   asr::KNode kn_list[asr::kStages];
@@ -596,6 +605,18 @@ asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches)
   c->prof_pending.clear();
   if (launches) *launches = c->launches;
   c->launches = 0;
+  return ASR_OK;
+}
+
+asr_status asr_timeline(asr_ctx* c, double* us, int32_t n) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!c->s.tl) return fail(ASR_E_STATE, "timeline off (set ASR_TIMELINE=1 before asr_create)");
+  if (!us || n < 2 * asr::kStages) return fail(ASR_E_INVALID, "us must hold 6 values");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaStreamSynchronize(c->last_stream));
+  unsigned long long t[2 * asr::kStages];
+  CUDA_TRY(cudaMemcpy(t, c->s.tl, sizeof(t), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 2 * asr::kStages; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
   return ASR_OK;
 }
 

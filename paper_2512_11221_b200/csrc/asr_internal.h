@@ -83,13 +83,34 @@ struct DevState {
   uint32_t* err;              // [1]
   int32_t* ticket;            // [1]
   int32_t* pre_ticket;        // [B] compaction / recovery meeting point in the pre kernel
+  unsigned long long* tl;     // [2*kStages] diagnostic timeline (globaltimer ns), NULL = off
 };
 
+#ifdef __CUDACC__
 // Programmatic dependent launch (PDL): a kernel may let its dependent start early, and a dependent
 // waits for its programmatic upstream before touching the upstream's outputs.  Both are no-ops
 // without a programmatic edge (direct launches, profiled graphs).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Diagnostic timeline: thread 0 of every block stamps %globaltimer at entry (atomicMin) and exit
+// (atomicMax) into tl[2*stage], tl[2*stage+1].  Only when DevState::tl is set (ASR_TIMELINE=1).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct Stamp {
+  unsigned long long* tl;
+  int stage;
+  __device__ Stamp(unsigned long long* t, int k) : tl(t), stage(k) {
+    if (tl && threadIdx.x == 0) atomicMin(&tl[2 * stage], gtimer());
+  }
+  __device__ ~Stamp() {
+    if (tl && threadIdx.x == 0) atomicMax(&tl[2 * stage + 1], gtimer());
+  }
+};
+#endif  // __CUDACC__
 
 __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, int* chunk, int* nch) {
   int c = (A + max_splits - 1) / max_splits;

@@ -86,6 +86,7 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
   constexpr int ACT = D >= 32 ? 32 : D;
   pdl_wait();
   pdl_trigger();
+  Stamp stamp(s.tl, 1);
   const int total = build_items(s, sh_start);
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = s.Hq / s.Hkv;

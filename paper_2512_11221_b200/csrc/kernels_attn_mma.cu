@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Stamp stamp(s.tl, 1);
 
   // ---- prologue independent of the upstream kernel (overlaps it under PDL): barriers and a zeroed
   //      ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN would poison O)

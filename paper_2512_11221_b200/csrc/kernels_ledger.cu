@@ -9,7 +9,11 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "asr_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace asr {
 namespace {
@@ -55,145 +59,6 @@ __device__ __forceinline__ float tof(float v) { return v; }
 
 constexpr int kPreThreads = 512;
 
-// Partial (m, Z, S) of one split of row b; returns true in every thread of the block that
-// arrives last for the row (atomic ticket), after which the row's partials are complete.
-template <typename T>
-__device__ bool entropy_split(const DevState& s, const T* __restrict__ logits, int b, int split) {
-  __shared__ float shm[32], shz[32], shs[32];
-  __shared__ int last;
-  const int V = s.vocab;
-  const int seg = (((V + kEntSplits - 1) / kEntSplits) + 7) & ~7;   // multiple of 8 elements
-  const int v0 = min(V, split * seg), v1 = min(V, v0 + seg);
-  const T* row = logits + (long)b * V;
-  const bool vec = ((reinterpret_cast<uintptr_t>(row) & 31) == 0);
-  const float invT = 1.0f / s.ent_temp;
-  float x[8];
-  float m = -INFINITY;
-  const int v = v0 + (int)threadIdx.x * 8;   // one vector of 8 logits per thread
-  if (vec && v + 8 <= v1) {
-    load8<T>(row + v, x);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] *= invT;
-  } else {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) x[e] = (v + e < v1) ? tof(row[v + e]) * invT : -INFINITY;
-  }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) m = fmaxf(m, x[e]);
-  // remainder (vocab > kEntSplits * 8 * kPreThreads)
-  for (int u = v0 + 8 * kPreThreads + (int)threadIdx.x; u < v1; u += kPreThreads) m = fmaxf(m, tof(row[u]) * invT);
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) shm[w] = m;
-  __syncthreads();
-  m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < kPreThreads / 32; ++k) m = fmaxf(m, shm[k]);
-  float z = 0.f, sx = 0.f;
-  if (m > -INFINITY) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float d = x[e] - m;   // -inf for padding -> ex = 0 (guarded product)
-      const float ex = expf(d);
-      z += ex;
-      sx += ex > 0.f ? ex * d : 0.f;
-    }
-    for (int u = v0 + 8 * kPreThreads + (int)threadIdx.x; u < v1; u += kPreThreads) {
-      const float d = tof(row[u]) * invT - m, ex = expf(d);
-      z += ex;
-      sx += ex * d;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    z += __shfl_xor_sync(0xffffffffu, z, o);
-    sx += __shfl_xor_sync(0xffffffffu, sx, o);
-  }
-  if (lane == 0) { shz[w] = z; shs[w] = sx; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    z = 0.f; sx = 0.f;
-#pragma unroll
-    for (int k = 0; k < kPreThreads / 32; ++k) { z += shz[k]; sx += shs[k]; }
-    float* ep = s.ent_part + ((long)b * kEntSplits + split) * 3;
-    ep[0] = m; ep[1] = z; ep[2] = sx;
-    __threadfence();
-    last = atomicAdd(&s.ent_ticket[b], 1) == kEntSplits - 1;
-  }
-  __syncthreads();
-  if (last) __threadfence();
-  return last;
-}
-
-// Warp 0 of the row's last block: merge the splits in a fixed order (double), H = ln Z - S/Z,
-// detector (R-det) and ladder (R-ladder).  Returns the recovery level in lane 0.
-__device__ int entropy_finish(const DevState& s, int b, float* entropy_out) {
-  const int lane = threadIdx.x & 31;
-  const volatile float* ep = s.ent_part + (long)b * kEntSplits * 3;
-  double pm[kEntSplits / 32], pz[kEntSplits / 32], ps[kEntSplits / 32];
-  double M = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < kEntSplits / 32; ++k) {
-    const int i = k * 32 + lane;
-    pm[k] = ep[i * 3]; pz[k] = ep[i * 3 + 1]; ps[k] = ep[i * 3 + 2];
-    if (pz[k] > 0.0) M = fmax(M, pm[k]);
-  }
-  for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
-  double Zl = 0.0, Sl = 0.0;
-#pragma unroll
-  for (int k = 0; k < kEntSplits / 32; ++k) {
-    if (pz[k] <= 0.0) continue;
-    const double dm = pm[k] - M, f = exp(dm);
-    Zl += pz[k] * f;
-    Sl += f * (ps[k] + pz[k] * dm);
-  }
-  for (int o = 16; o > 0; o >>= 1) {   // fixed-order tree over lanes (deterministic)
-    Zl += __shfl_xor_sync(0xffffffffu, Zl, o);
-    Sl += __shfl_xor_sync(0xffffffffu, Sl, o);
-  }
-  const double H = log(Zl) - Sl / Zl;
-  DetState& ds = s.det[b];
-  double* hist = s.hist + (long)b * s.det_baseline;
-  const int hl = ds.hist_len;
-  double mu = 0.0, var = 0.0;
-  for (int t = lane; t < hl; t += 32) mu += hist[t];
-  for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
-  mu = hl > 0 ? mu / hl : 0.0;
-  for (int t = lane; t < hl; t += 32) var += (hist[t] - mu) * (hist[t] - mu);
-  for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-  int level = 0;
-  if (lane == 0) {
-    var = hl > 0 ? var / hl : 0.0;
-    int trig = 0;
-    if (s.det_enable && hl >= 2) {
-      const double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
-      trig = H > mu + (double)s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
-    }
-    if (hl < s.det_baseline) {
-      hist[hl] = H;
-      ds.hist_len = hl + 1;
-    } else {
-      hist[ds.hist_head] = H;
-      ds.hist_head = (ds.hist_head + 1) % s.det_baseline;
-    }
-    if (trig) {
-      const int i = *s.step;
-      const int dt = i - ds.last_action_step;
-      if (!(ds.has_last && dt < s.det_cooldown)) {   // absorbed inside the cooldown
-        level = (ds.has_last && dt < 2 * s.det_cooldown) ? (ds.level < 4 ? ds.level + 1 : 4) : 1;
-        ds.level = level;
-        ds.last_action_step = i;
-        ds.has_last = 1;
-      }
-    }
-    s.ent_ticket[b] = 0;
-    if (entropy_out) entropy_out[b] = (float)H;
-    SeqStats& st = s.stats[b];
-    st.entropy = (float)H;
-    st.entropy_valid = 1;
-  }
-  return level;
-}
-
 // Recovery levels on one sequence's ledger: returns the restored count of this thread.
 __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   int restored = 0;
@@ -216,11 +81,39 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   return restored;
 }
 
-// ------------------------------------------------------------------ (a3) compaction
-// A_i = sorted positions with residency Active, written by one block.  Thread t owns a contiguous
-// run of 16-position vectors (uint4 loads of the residency bytes; rows are 64-aligned and positions
-// >= n hold 0), counts, block-scans, then writes its positions.
-__device__ int active_mask16(uint4 u, uint32_t* m) {  // per byte: 1 iff residency == 1 (values 0..3)
+// ------------------------------------------------------------------ pre_kernel
+// (a6) entropy + detector + ladder + recovery, (a0) append and (a3) compaction in one launch.
+// Sequence b is handled by one thread-block cluster of kCl CTAs (B200 clusters: the partial results
+// meet in distributed shared memory behind hardware cluster barriers, no global atomics/fences):
+//   every CTA r:  entropy partial (m, Z, S) of vocab slice r; active count of position slice r
+//   barrier;      rank 0 merges the kCl entropy partials (fixed order), runs the detector and the
+//                 ladder (R-det, R-ladder) and publishes the recovery level
+//   barrier;      if a level fired (rare): every CTA applies it to its slice and recounts (+barrier)
+//                 every CTA writes its slice of A_i at the offset of the lower ranks' counts
+// Clusters >= B copy the new token's K/V rows, one (b, l) per CTA.
+constexpr int kCl = 8;
+
+struct PreShared {
+  float em, ez, es;     // entropy partial of this CTA
+  int cnt;              // Active positions in this CTA's slice
+  int restored;         // restored by recovery in this CTA's slice
+  int level;            // recovery level (rank 0 publishes)
+  int wsum[32];
+  float wm[32], wz[32], ws[32];
+  double hist[kMaxDetBaseline];
+};
+
+__device__ __forceinline__ void tri_merge(float& m, float& z, float& sx, float om, float oz, float os) {
+  // merge (m, Z, S) triples of the single-pass entropy: rescale both to M = max(m, om)
+  const float M = fmaxf(m, om);
+  float nz = 0.f, ns = 0.f;
+  if (z > 0.f) { const float f = __expf(m - M); nz += z * f; ns += f * (sx + z * (m - M)); }
+  if (oz > 0.f) { const float f = __expf(om - M); nz += oz * f; ns += f * (os + oz * (om - M)); }
+  m = M; z = nz; sx = ns;
+}
+
+// Active positions of [p0, p1) (p0 multiple of 16): per-thread runs of 16-position vectors.
+__device__ __forceinline__ int active_mask16(uint4 u, uint32_t* m) {  // 1 per byte iff residency == 1
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
   int c = 0;
 #pragma unroll
@@ -231,13 +124,9 @@ __device__ int active_mask16(uint4 u, uint32_t* m) {  // per byte: 1 iff residen
   return c;
 }
 
-__device__ void compact_block(const DevState& s, int b, int n) {
-  __shared__ int wsum[32];
-  const long base = (long)b * s.max_ctx;
-  const uint8_t* res = s.res + base;
-  const int nvec = (n + 15) >> 4;
-  const int per = (nvec + (int)blockDim.x - 1) / (int)blockDim.x;
-  const int v0 = min(nvec, (int)threadIdx.x * per), v1 = min(nvec, v0 + per);
+// Block count + exclusive scan of this CTA's slice: returns the thread's exclusive offset, writes the
+// CTA total to ps.cnt.  Thread t owns vectors [v0, v1).
+__device__ int slice_scan(const uint8_t* res, int v0, int v1, PreShared& ps, int* my_cnt) {
   int cnt = 0;
 #pragma unroll 4
   for (int v = v0; v < v1; ++v) {
@@ -250,73 +139,34 @@ __device__ void compact_block(const DevState& s, int b, int n) {
     int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  if (lane == 31) wsum[w] = incl;
+  if (lane == 31) ps.wsum[w] = incl;
   __syncthreads();
   if (w == 0) {
-    int x = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+    int x = lane < (int)(blockDim.x >> 5) ? ps.wsum[lane] : 0;
     int xi = x;
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, xi, o);
       if (lane >= o) xi += y;
     }
-    wsum[lane] = xi - x;  // exclusive warp offsets
+    ps.wsum[lane] = xi - x;  // exclusive warp offsets
+    if (lane == 31) ps.cnt = xi;
   }
   __syncthreads();
-  int off = wsum[w] + incl - cnt;
-  int32_t* out = s.act_pos + base;
-  for (int v = v0; v < v1; ++v) {
-    uint32_t m[4];
-    active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      while (m[k]) {
-        const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
-        out[off++] = v * 16 + k * 4 + (bit >> 3);
-        m[k] &= m[k] - 1;
-      }
-  }
-  if (threadIdx.x == blockDim.x - 1) {
-    s.act_len[b] = off;
-    s.stats[b].attended = off;
-    if (off == 0) atomicOr(s.err, kErrEmptyActive);
-  }
-  __syncthreads();
+  *my_cnt = cnt;
+  return ps.wsum[w] + incl - cnt;
 }
 
-// Meeting point of the compaction block and the entropy block of sequence b: returns true (in all
-// threads) for the second arriver.
-__device__ bool pre_meet(const DevState& s, int b) {
-  __shared__ int second;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    second = atomicAdd(&s.pre_ticket[b], 1) == 1;
-    if (second) s.pre_ticket[b] = 0;
-    __threadfence();
-  }
-  __syncthreads();
-  return second;
-}
-
-// ------------------------------------------------------------------ pre_kernel
-// (a6) entropy + detector + ladder + recovery, (a0) append and (a3) compaction in one launch:
-//   blocks [0, B*S)          S = kEntSplits splits of each logits row (none without logits); the last
-//                            split block of row b finishes H, runs the detector and the ladder and
-//                            applies the recovery level to the ledger;
-//   blocks [B*S, B*S + B)    sequence b: ledger entry of the appended position n-1, then compaction
-//                            of A_i in parallel with the entropy (recovery is rare: whichever of the
-//                            two blocks of b arrives second recompacts when a level was applied);
-//   blocks [.., + B*L)       copy the new token's K/V rows of (b, l) into its slot.
 template <typename TL, typename TK>
-__global__ void __launch_bounds__(kPreThreads) pre_kernel(DevState s, const TL* logits, float* entropy_out,
-                                                             const TK* k_new, const TK* v_new) {
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kPreThreads, 1)
+    pre_kernel(DevState s, const TL* logits, float* entropy_out, const TK* k_new, const TK* v_new) {
   pdl_trigger();   // the attention kernel may start its (independent) prologue now
+  Stamp stamp(s.tl, 0);
   const int i = *s.step;
-  const int S = logits ? kEntSplits : 0;
-  const int blk = blockIdx.x;
-  if (blk >= s.B * S + s.B) {  // ---- append K/V rows
-    const int r = blk - s.B * S - s.B;
-    const int b = r / s.L, l = r % s.L;
+  const int cid = blockIdx.x / kCl;
+  if (cid >= s.B) {  // ---- append K/V rows of (b, l) (whole clusters take this branch)
+    const int a = blockIdx.x - kCl * s.B;
+    if (a >= s.B * s.L) return;
+    const int b = a / s.L, l = a % s.L;
     const long pos = s.prompt_len[b] + i;
     const long slot = (long)b * s.max_ctx + pos;
     const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
@@ -335,56 +185,196 @@ __global__ void __launch_bounds__(kPreThreads) pre_kernel(DevState s, const TL* 
     }
     return;
   }
-  if (blk >= s.B * S) {  // ---- compaction block of sequence b
-    const int b = blk - s.B * S;
-    const int n = s.prompt_len[b] + i + 1;  // total after the append
-    const long base = (long)b * s.max_ctx;
-    if (threadIdx.x == 0) {
-      const int j = n - 1;  // the token produced by the previous step (Alg. 1 line 16)
-      s.res[base + j] = 1;
-      s.timer[base + j] = 0;
-      s.count[base + j] = 0;
-      s.fstep[base + j] = -1;
-      SeqStats& st = s.stats[b];
-      st.restored_pre = st.pending_restored;
-      st.pending_restored = 0;
-      st.restored_tick = 0;
-      st.frozen_this_step = 0;
-      if (!logits) {
-        st.recovery_action = 0;
-        st.rewalk_requested = 0;
-        st.entropy_valid = 0;
-        st.restored_rec = 0;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  __shared__ PreShared ps;
+  const int b = cid;
+  const int n = s.prompt_len[b] + i + 1;  // total after the append
+  const long base = (long)b * s.max_ctx;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  DetState& ds = s.det[b];
+  // ---- rank 0 prefetches the detector history; the owner of position n-1 appends its ledger entry
+  if (rank == 0 && logits)
+    for (int t = threadIdx.x; t < ds.hist_len; t += blockDim.x) ps.hist[t] = s.hist[(long)b * s.det_baseline + t];
+  const int nvec = (n + 15) >> 4;
+  const int vr = (nvec + kCl - 1) / kCl;                    // vectors per rank
+  const int rv0 = min(nvec, rank * vr), rv1 = min(nvec, rv0 + vr);
+  if (threadIdx.x == 0 && (n - 1) >= rv0 * 16 && (n - 1) < rv1 * 16) {
+    const long j = base + n - 1;   // the token produced by the previous step (Alg. 1 line 16)
+    s.res[j] = 1;
+    s.timer[j] = 0;
+    s.count[j] = 0;
+    s.fstep[j] = -1;
+  }
+  // ---- entropy partial of vocab slice `rank` (single pass, online (m, Z, S))
+  if (logits) {
+    const int V = s.vocab;
+    const int vs = ((((V + kCl - 1) / kCl) + 7) & ~7);
+    const int e0 = min(V, rank * vs), e1 = min(V, e0 + vs);
+    const TL* row = logits + (long)b * V;
+    const bool vecok = (reinterpret_cast<uintptr_t>(row) & 31) == 0;
+    const float invT = 1.0f / s.ent_temp;
+    float m = -INFINITY, z = 0.f, sx = 0.f;
+    for (int v = e0 + (int)threadIdx.x * 8; v < e1; v += (int)blockDim.x * 8) {
+      float x[8];
+      if (vecok && v + 8 <= e1) {
+        load8<TL>(row + v, x);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = (v + e < e1) ? tof(row[v + e]) : -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { x[e] *= invT; mx = fmaxf(mx, x[e]); }
+      if (mx > m) {   // rescale the running sums to the new max
+        if (z > 0.f) { const float f = __expf(m - mx); sx = f * (sx + z * (m - mx)); z *= f; }
+        m = mx;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = x[e] - m;
+        const float ex = __expf(d);
+        z += ex;
+        sx += ex > 0.f ? ex * d : 0.f;
       }
     }
+    for (int o = 16; o > 0; o >>= 1)
+      tri_merge(m, z, sx, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, z, o),
+                __shfl_xor_sync(0xffffffffu, sx, o));
+    if (lane == 0) { ps.wm[w] = m; ps.wz[w] = z; ps.ws[w] = sx; }
     __syncthreads();
-    compact_block(s, b, n);
-    if (logits && pre_meet(s, b) && s.rec_action[b] > 0) compact_block(s, b, n);
-    return;
+    if (threadIdx.x == 0) {
+      float M = -INFINITY, Z = 0.f, S = 0.f;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tri_merge(M, Z, S, ps.wm[k], ps.wz[k], ps.ws[k]);
+      ps.em = M; ps.ez = Z; ps.es = S;
+    }
   }
-  // ---- entropy split of row b
-  __shared__ int sh[32];
-  __shared__ int sh_level;
-  const int b = blk / S;
-  if (!entropy_split<TL>(s, logits, b, blk % S)) return;   // block-uniform
-  if (threadIdx.x < 32) {
-    const int lv = entropy_finish(s, b, entropy_out);
-    if (threadIdx.x == 0) sh_level = lv;
+  // ---- count the Active positions of this rank's slice
+  const uint8_t* res = s.res + base;
+  const int per = (rv1 - rv0 + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int v0 = min(rv1, rv0 + (int)threadIdx.x * per), v1 = min(rv1, v0 + per);
+  __syncthreads();   // the appended entry is visible to the counting threads of this CTA
+  int my_cnt;
+  int my_off = slice_scan(res, v0, v1, ps, &my_cnt);
+  if (threadIdx.x == 0) ps.restored = 0;
+  cl.sync();
+  // ---- rank 0: H, detector, ladder
+  if (rank == 0 && w == 0) {
+    int level = 0;
+    if (logits) {
+      double M = -INFINITY, Z = 0.0, S = 0.0;
+      if (lane == 0) {
+        for (int r = 0; r < kCl; ++r) {   // fixed rank order
+          const PreShared* o = cl.map_shared_rank(&ps, r);
+          const double om = o->em, oz = o->ez, os = o->es;
+          if (oz <= 0.0) continue;
+          const double Mn = fmax(M, om);
+          double nz = 0.0, ns = 0.0;
+          if (Z > 0.0) { const double f = exp(M - Mn); nz += Z * f; ns += f * (S + Z * (M - Mn)); }
+          const double f = exp(om - Mn);
+          nz += oz * f;
+          ns += f * (os + oz * (om - Mn));
+          M = Mn; Z = nz; S = ns;
+        }
+      }
+      const double H = __shfl_sync(0xffffffffu, log(Z) - S / Z, 0);
+      const int hl = ds.hist_len;
+      double mu = 0.0, var = 0.0;
+      for (int t = lane; t < hl; t += 32) mu += ps.hist[t];
+      for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      mu = hl > 0 ? mu / hl : 0.0;
+      for (int t = lane; t < hl; t += 32) var += (ps.hist[t] - mu) * (ps.hist[t] - mu);
+      for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+      if (lane == 0) {
+        var = hl > 0 ? var / hl : 0.0;
+        int trig = 0;
+        if (s.det_enable && hl >= 2) {
+          const double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
+          trig = H > mu + (double)s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
+        }
+        double* hist = s.hist + (long)b * s.det_baseline;
+        if (hl < s.det_baseline) {
+          hist[hl] = H;
+          ds.hist_len = hl + 1;
+        } else {
+          hist[ds.hist_head] = H;
+          ds.hist_head = (ds.hist_head + 1) % s.det_baseline;
+        }
+        if (trig) {
+          const int dt = i - ds.last_action_step;
+          if (!(ds.has_last && dt < s.det_cooldown)) {   // absorbed inside the cooldown
+            level = (ds.has_last && dt < 2 * s.det_cooldown) ? (ds.level < 4 ? ds.level + 1 : 4) : 1;
+            ds.level = level;
+            ds.last_action_step = i;
+            ds.has_last = 1;
+          }
+        }
+        if (entropy_out) entropy_out[b] = (float)H;
+        s.stats[b].entropy = (float)H;
+      }
+    }
+    if (lane == 0) ps.level = level;
   }
-  __syncthreads();
-  const int level = sh_level;
-  const int n = s.prompt_len[b] + i + 1;
-  int restored = 0;
-  if (level > 0) restored = apply_level(s, b, n - 1, level, i);
-  restored = block_sum_int(restored, sh);
-  if (threadIdx.x == 0) {
+  cl.sync();
+  const int level = cl.map_shared_rank(&ps, 0)->level;
+  if (level > 0) {   // rare: recovery restores in every slice, then recount
+    int r = 0;
+    int32_t* timer = s.timer + base;
+    const int32_t* fstep = s.fstep + base;
+    uint8_t* resw = s.res + base;
+    const int p0 = rv0 * 16, p1 = min(n - 1, rv1 * 16);
+    for (int j = p0 + (int)threadIdx.x; j < p1; j += blockDim.x) {
+      if (res_active(resw[j])) continue;
+      const bool go = level == 1 ? timer[j] > 1 : level == 2 ? fstep[j] >= i - s.wr_window : true;
+      if (go) { resw[j] = 1; timer[j] = 0; r++; }
+    }
+    if (level >= 3 && s.fr_clear_counts)
+      for (int j = p0 + (int)threadIdx.x; j < p1; j += blockDim.x) s.count[base + j] = 0;
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    __syncthreads();
+    if (lane == 0) atomicAdd(&ps.restored, r);
+    __syncthreads();
+    my_off = slice_scan(res, v0, v1, ps, &my_cnt);
+    cl.sync();
+  }
+  // ---- write this slice of A_i at the offset of the lower ranks
+  int off0 = 0, total = 0, restored = 0;
+  for (int r = 0; r < kCl; ++r) {
+    const PreShared* o = cl.map_shared_rank(&ps, r);
+    const int c = o->cnt;
+    if (r < rank) off0 += c;
+    total += c;
+    restored += o->restored;
+  }
+  int off = off0 + my_off;
+  int32_t* out = s.act_pos + base;
+  for (int v = v0; v < v1; ++v) {
+    uint32_t m[4];
+    active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      while (m[k]) {
+        const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
+        out[off++] = v * 16 + k * 4 + (bit >> 3);
+        m[k] &= m[k] - 1;
+      }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    s.act_len[b] = total;
+    if (total == 0) atomicOr(s.err, kErrEmptyActive);
     SeqStats& st = s.stats[b];
+    st.attended = total;
+    st.restored_pre = st.pending_restored;
+    st.pending_restored = 0;
+    st.restored_tick = 0;
+    st.frozen_this_step = 0;
     st.restored_rec = restored;
     st.recovery_action = level;
     st.rewalk_requested = level == 4;
+    st.entropy_valid = logits ? 1 : 0;
     s.rec_action[b] = level;
   }
-  if (pre_meet(s, b) && level > 0) compact_block(s, b, n);
+  cl.sync();   // keep every CTA's shared memory alive until the whole cluster has read it
 }
 
 // ------------------------------------------------------------------ (a2) decide + tick
@@ -412,6 +402,7 @@ __device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
 // need no ordering between them.
 __device__ void decide_block(const DevState& s, int b, int x, int X, int nblocks_total) {
   __shared__ int sh[32];
+  __shared__ int sh2[32];
   const int i = *s.step;
   const int n = s.prompt_len[b] + i + 1;
   const long base = (long)b * s.max_ctx;
@@ -423,8 +414,21 @@ __device__ void decide_block(const DevState& s, int b, int x, int X, int nblocks
   const float inv = 1.0f / (float)(s.L * s.Hq);
   const float inv_sqrt_d = rsqrtf((float)s.d);
   const uint8_t tag_now = res_tag(i);
+  // ---- prefetch the tick's ledger entries of this block's position slice (independent of the
+  //      freeze loop: tokens of A_i read Active here and are skipped by the tick below)
+  constexpr int kPF = 4;
+  const int per_n = (n + X - 1) / X;
+  const int n0 = x * per_n, n_end = min(n, n0 + per_n);
+  uint8_t pr[kPF];
+  int pt[kPF];
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    pr[k] = j < n_end ? res[j] : (uint8_t)1;
+    pt[k] = j < n_end ? timer[j] : 0;
+  }
   int frozen_now = 0, restored = 0;
-  // ---- lines 3-9 over this block's slice of A_i
+  // ---- Alg. 1 lines 3-9 over this block's slice of A_i
   const int per_a = (A + X - 1) / X;
   const int a_end = min(A, (x + 1) * per_a);
   for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
@@ -464,12 +468,13 @@ __device__ void decide_block(const DevState& s, int b, int x, int X, int nblocks
   }
   // ---- lines 10-15 for tokens frozen before this step
   uint32_t err = 0;
-  const int per_n = (n + X - 1) / X;
-  const int n_end = min(n, (x + 1) * per_n);
-  for (int j = x * per_n + threadIdx.x; j < n_end; j += blockDim.x) {
-    const uint8_t r = res[j];
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    if (j >= n_end) continue;
+    const uint8_t r = pr[k];
     if (r == 1 || r == tag_now) continue;
-    const int t = timer[j] - 1;
+    const int t = pt[k] - 1;
     if (t <= 0) {
       res[j] = 1;
       timer[j] = 0;
@@ -480,13 +485,36 @@ __device__ void decide_block(const DevState& s, int b, int x, int X, int nblocks
       if (j >= n - s.window) err |= kErrFrozenInWindow;
     }
   }
+  for (int j = n0 + (int)threadIdx.x + kPF * (int)blockDim.x; j < n_end; j += blockDim.x) {   // n > kPF*threads*X
+    const uint8_t r = res[j];
+    if (r == 1 || r == tag_now) continue;
+    const int t = timer[j] - 1;
+    if (t <= 0) {
+      res[j] = 1;
+      timer[j] = 0;
+      restored++;
+    } else {
+      timer[j] = t;
+      if (r != 0) res[j] = 0;
+      if (j >= n - s.window) err |= kErrFrozenInWindow;
+    }
+  }
   if (err) atomicOr(s.err, err);
-  frozen_now = block_sum_int(frozen_now, sh);
-  restored = block_sum_int(restored, sh);
+  // block sums of the two counters in one pass
+  int f = frozen_now, r = restored;
+  for (int o = 16; o > 0; o >>= 1) {
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sh[w] = f; sh2[w] = r; }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    f = 0; r = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { f += sh[k]; r += sh2[k]; }
     SeqStats& st = s.stats[b];
-    if (frozen_now) atomicAdd(&st.frozen_this_step, frozen_now);
-    if (restored) atomicAdd(&st.restored_tick, restored);
+    if (f) atomicAdd(&st.frozen_this_step, f);
+    if (r) atomicAdd(&st.restored_tick, r);
     __threadfence();
     if (atomicAdd(s.ticket, 1) == nblocks_total - 1) {  // last decide block: advance the step
       *s.ticket = 0;
@@ -560,6 +588,7 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
 // combine, one warp per (b, l, h).
 __global__ void __launch_bounds__(kDecideThreads) post_kernel(DevState s, float* __restrict__ o) {
   pdl_wait();      // every input comes from the attention kernel
+  Stamp stamp(s.tl, 2);
   const int nd = s.decide_blocks * s.B;
   if ((int)blockIdx.x < nd) {
     decide_block(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, nd);
@@ -595,8 +624,8 @@ void node_pre(KNode& n, const DevState& s, const void* logits, int logits_dtype,
     f = lf ? (const void*)pre_kernel<float, __nv_bfloat16> : (const void*)pre_kernel<__nv_bfloat16, __nv_bfloat16>;
   else
     f = lf ? (const void*)pre_kernel<float, float> : (const void*)pre_kernel<__nv_bfloat16, float>;
-  const int S = logits ? kEntSplits : 0;
-  n.finalize(f, dim3(s.B * S + s.B + s.B * s.L), dim3(kPreThreads), 0);
+  const int blocks = kCl * s.B + s.B * s.L;
+  n.finalize(f, dim3((blocks + kCl - 1) / kCl * kCl), dim3(kPreThreads), 0);
 }
 
 void node_post(KNode& n, const DevState& s, float* o) {
