@@ -147,10 +147,11 @@ asr_status asr_stats(asr_ctx* ctx, int32_t seq, asr_stats_t* out, asr_ledger_vie
 asr_status asr_read_kv(asr_ctx* ctx, int32_t seq, int32_t pos, int32_t from_mirror, void* k_out,
                        void* v_out);
 
-/* Accumulated device time per stage since the last call (needs profile_stages = 1):
- * ms[0] entropy + detector + ladder + append + recovery + compaction, ms[1] attention + fused
- * score, ms[2] combine + decide + tick; *launches = kernel launches of the library in that
- * period.  n >= 3.  Synchronises. */
+/* Accumulated device time since the last call (needs profiling on: profile_stages or
+ * asr_set_profile): ms[0] entropy + detector + ladder + append + recovery + compaction, ms[1]
+ * attention + fused score, ms[2] combine + decide + tick, ms[3] whole steps (CUDA events around the
+ * step's kernels).  With the fused single-kernel step, ms[0..2] are its phases (%globaltimer).
+ * *launches = kernel launches of the library in that period.  n >= 4.  Synchronises. */
 asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launches);
 
 /* Switch stage profiling (the events asr_stage_times reads) on or off for the following steps.

@@ -22,7 +22,7 @@ ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, A
 KV_BF16, KV_F32 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 SR, WR, FR = 1, 2, 3
-STAGES = ("entropy_append_recover_compact", "attention_score", "combine_decide_tick")
+STAGES = ("entropy_append_recover_compact", "attention_score", "combine_decide_tick", "step_total")
 
 
 class AsrError(RuntimeError):

@@ -73,6 +73,10 @@ struct asr_ctx {
   StepGraph graphs[2];
   bool use_graph = true;
   bool use_pdl = true;
+  bool use_mega = false;        // persistent single-kernel step
+  int mega_grid = 0;
+  bool timeline_on = false;     // ASR_TIMELINE=1
+  unsigned long long* tl_buf = nullptr;
   // stage profiling
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_pending;
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_free;
@@ -304,9 +308,26 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
     const char* ng = getenv("ASR_NO_GRAPH");
     c->use_graph = !(ng && ng[0] == '1');
+    CUDA_TRY(c->alloc(&s.gbar, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(s.gbar, 0, 2 * sizeof(unsigned), st));
+    // device timeline: [2*kStages] stamps + [kStages] accumulated phase ns + [1] step count
+    CUDA_TRY(c->alloc(&c->tl_buf, sizeof(unsigned long long) * (3 * asr::kStages + 1)));
+    CUDA_TRY(cudaMemsetAsync(c->tl_buf, 0, sizeof(unsigned long long) * (3 * asr::kStages + 1), st));
     const char* tlenv = getenv("ASR_TIMELINE");
-    if (tlenv && tlenv[0] == '1') {
-      CUDA_TRY(c->alloc(&s.tl, sizeof(unsigned long long) * 2 * asr::kStages));
+    c->timeline_on = tlenv && tlenv[0] == '1';
+    s.tl = nullptr;
+    // the persistent single-kernel step (cooperative launch, one CTA per SM) for the LLaMA bf16 shape:
+    // opt-in (ASR_MEGA=1) — measured slower than the 4-kernel graph with PDL at batch 1 (its four
+    // grid barriers cost more than the kernel boundaries they replace; profiles/README.md)
+    const char* nm = getenv("ASR_MEGA");
+    int coop = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg->device));
+    c->use_mega = asr::attention_mma_supported(s) && coop && (nm && nm[0] == '1');
+    if (c->use_mega) {
+      CUDA_TRY(asr::attention_mma_prepare());
+      const int g = asr::step_kernel_max_grid(c->num_sms);
+      c->mega_grid = g < c->num_sms ? g : c->num_sms;
+      if (c->mega_grid < 1) c->use_mega = false;
     }
     const char* np = getenv("ASR_NO_PDL");
     c->use_pdl = !(np && np[0] == '1');
@@ -396,31 +417,41 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     c->prof_free.pop_back();
     ev = &c->prof_pending.back();
   }
-  if (s.tl) {   // diagnostic timeline of this step: start stamps = +inf, end stamps = 0
+  const bool prof = ev != nullptr;
+  DevState sd = s;   // the step's view: timeline stamps when profiling the fused kernel or on request
+  if (c->timeline_on || (prof && c->use_mega)) sd.tl = c->tl_buf;
+  if (sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0
     unsigned long long init[2 * asr::kStages];
     for (int k = 0; k < asr::kStages; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
-    CUDA_TRY(cudaMemcpyAsync(s.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
-  // the step as kernel descriptions, one per stage
-  asr::KNode kn_list[asr::kStages];
-  int stage_of[asr::kStages];
+  // the step as kernel descriptions with their stage (0 ledger pre, 1 attention, 2 decide/combine)
+  asr::KNode kn_list[4];
+  int stage_of[4];
   int nk = 0;
-  asr::node_pre(kn_list[nk], s, has_logits ? lg : nullptr, io->logits_dtype, has_logits ? ent : nullptr, kn, vn);
-  stage_of[nk++] = 0;
-  asr::node_attention(kn_list[nk], s, q, c->attn_grid);
-  stage_of[nk++] = 1;
-  asr::node_post(kn_list[nk], s, o);
-  stage_of[nk++] = 2;
+  const void* lgp = has_logits ? lg : nullptr;
+  if (c->use_mega) {
+    asr::node_step(kn_list[nk], sd, lgp, io->logits_dtype, has_logits ? ent : nullptr, kn, vn, q, o, c->mega_grid);
+    stage_of[nk++] = 0;
+  } else {
+    asr::node_phaseA(kn_list[nk], sd, lgp, io->logits_dtype, kn, vn);
+    stage_of[nk++] = 0;
+    asr::node_phaseB(kn_list[nk], sd, has_logits ? 1 : 0, has_logits ? ent : nullptr);
+    stage_of[nk++] = 0;
+    asr::node_attention(kn_list[nk], sd, q, c->attn_grid);
+    stage_of[nk++] = 1;
+    asr::node_phaseD(kn_list[nk], sd, o);
+    stage_of[nk++] = 2;
+  }
   if (!c->use_graph) {
     int k = 0;
     for (int stg = 0; stg < asr::kStages; ++stg) {
       CUDA_TRY(prof_mark(c, ev, stg, st));
-      if (k < nk && stage_of[k] == stg) CUDA_TRY(kn_list[k++].launch(st));
+      while (k < nk && stage_of[k] == stg) CUDA_TRY(kn_list[k++].launch(st));
     }
     CUDA_TRY(prof_mark(c, ev, asr::kStages, st));
   } else {
     asr_ctx::StepGraph& G = c->graphs[has_logits ? 1 : 0];
-    const bool prof = ev != nullptr;
     if (G.x && G.profiled != prof) {
       cudaGraphExecDestroy(G.x);
       cudaGraphDestroy(G.g);
@@ -438,11 +469,16 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
           G.evnodes.push_back(e);
           prev = e;
         }
-        if (stg < asr::kStages && k < nk && stage_of[k] == stg) {
+        while (stg < asr::kStages && k < nk && stage_of[k] == stg) {
           cudaGraphNode_t kn_node;
           const bool pdl = c->use_pdl && !prof && prev != nullptr;
           CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
                                           &kn_list[k].p));
+          if (kn_list[k].cooperative) {
+            cudaKernelNodeAttrValue v{};
+            v.cooperative = 1;
+            CUDA_TRY(cudaGraphKernelNodeSetAttribute(kn_node, cudaLaunchAttributeCooperative, &v));
+          }
           if (pdl) {
             // programmatic edge: the kernel may launch before its upstream completes; it calls
             // griddepcontrol.wait before reading the upstream's results
@@ -590,7 +626,7 @@ asr_status asr_read_kv(asr_ctx* c, int32_t seq, int32_t pos, int32_t from_mirror
 
 asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
-  if (!ms || n < asr::kStages) return fail(ASR_E_INVALID, "ms must hold 3 values");
+  if (!ms || n < asr::kStages + 1) return fail(ASR_E_INVALID, "ms must hold 4 values");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   for (int k = 0; k < n; ++k) ms[k] = 0.0;
@@ -600,9 +636,18 @@ asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches)
       CUDA_TRY(cudaEventElapsedTime(&t, a[k], a[k + 1]));
       ms[k] += t;
     }
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, a[0], a[asr::kStages]));
+    ms[asr::kStages] += t;
     c->prof_free.push_back(a);
   }
   c->prof_pending.clear();
+  if (c->use_mega) {   // phases of the fused kernel: accumulated %globaltimer durations
+    unsigned long long acc[asr::kStages + 1];
+    CUDA_TRY(cudaMemcpy(acc, c->tl_buf + 2 * asr::kStages, sizeof(acc), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < asr::kStages; ++k) ms[k] = (double)acc[k] * 1e-6;
+    CUDA_TRY(cudaMemset(c->tl_buf + 2 * asr::kStages, 0, sizeof(acc)));
+  }
   if (launches) *launches = c->launches;
   c->launches = 0;
   return ASR_OK;
@@ -610,12 +655,12 @@ asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches)
 
 asr_status asr_timeline(asr_ctx* c, double* us, int32_t n) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
-  if (!c->s.tl) return fail(ASR_E_STATE, "timeline off (set ASR_TIMELINE=1 before asr_create)");
+  if (!c->timeline_on) return fail(ASR_E_STATE, "timeline off (set ASR_TIMELINE=1 before asr_create)");
   if (!us || n < 2 * asr::kStages) return fail(ASR_E_INVALID, "us must hold 6 values");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   unsigned long long t[2 * asr::kStages];
-  CUDA_TRY(cudaMemcpy(t, c->s.tl, sizeof(t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(t, c->tl_buf, sizeof(t), cudaMemcpyDeviceToHost));
   for (int k = 0; k < 2 * asr::kStages; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
   return ASR_OK;
 }

@@ -84,6 +84,7 @@ struct DevState {
   int32_t* ticket;            // [1]
   int32_t* pre_ticket;        // [B] compaction / recovery meeting point in the pre kernel
   unsigned long long* tl;     // [2*kStages] diagnostic timeline (globaltimer ns), NULL = off
+  unsigned* gbar;             // [2] grid barrier of the persistent step kernel (arrivals, generation)
 };
 
 #ifdef __CUDACC__
@@ -126,11 +127,12 @@ __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, i
 struct KNode {
   cudaKernelNodeParams p{};
   DevState s{};
-  uint64_t extra[4] = {0, 0, 0, 0};   // pointer / int arguments after DevState (8-byte slots)
-  void* argv[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  uint64_t extra[6] = {0, 0, 0, 0, 0, 0};   // pointer / int arguments after DevState (8-byte slots)
+  void* argv[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool cooperative = false;                  // needs all CTAs co-resident (grid barriers)
   void finalize(const void* func, dim3 grid, dim3 block, unsigned smem) {
     argv[0] = &s;
-    for (int k = 0; k < 4; ++k) argv[k + 1] = &extra[k];
+    for (int k = 0; k < 6; ++k) argv[k + 1] = &extra[k];
     p.func = const_cast<void*>(func);
     p.gridDim = grid;
     p.blockDim = block;
@@ -145,15 +147,21 @@ struct KNode {
     memcpy(&extra[k], &v, sizeof(P));
   }
   cudaError_t launch(cudaStream_t st) const {
+    if (cooperative)
+      return cudaLaunchCooperativeKernel(p.func, p.gridDim, p.blockDim, const_cast<void**>(argv), p.sharedMemBytes, st);
     return cudaLaunchKernel(p.func, p.gridDim, p.blockDim, const_cast<void**>(argv), p.sharedMemBytes, st);
   }
 };
 
 // Node builders (kernels_*.cu).
-void node_pre(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
-              const void* k_new, const void* v_new);
+void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dtype, const void* k_new,
+                 const void* v_new);
+void node_phaseB(KNode& n, const DevState& s, int has_logits, float* entropy_out);
 void node_attention(KNode& n, const DevState& s, const void* q, int grid);
-void node_post(KNode& n, const DevState& s, float* o);
+void node_phaseD(KNode& n, const DevState& s, float* o);
+void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
+               const void* k_new, const void* v_new, const void* q, float* o, int grid);
+int step_kernel_max_grid(int num_sms);
 void node_restore(KNode& n, const DevState& s, int seq, int level);
 int attention_grid(const DevState& s, int num_sms);
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head

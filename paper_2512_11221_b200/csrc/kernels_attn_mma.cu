@@ -23,7 +23,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
-#include "asr_internal.h"
+#include "step_units.cuh"
 
 namespace asr {
 namespace {
@@ -144,14 +144,9 @@ struct TileIt {
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  Stamp stamp(s.tl, 1);
-
-  // ---- prologue independent of the upstream kernel (overlaps it under PDL): barriers and a zeroed
-  //      ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN would poison O)
+// Barriers and a zeroed ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN
+// would poison O).  Once per launch, before any phase touches the ring.
+__device__ void attention_prologue(Smem& sm) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesRing; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -163,15 +158,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  {
-    uint4* z = reinterpret_cast<uint4*>(&sm.kv[0][0]);
-    const int nz = (int)(sizeof(sm.kv) / sizeof(uint4));
-    for (int i = threadIdx.x; i < nz; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    // order the generic-proxy zero fill before the async-proxy (bulk copy) writes to the same rows
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  pdl_wait();      // A_i, |A_i|, q and the appended K/V come from the pre kernel
-  pdl_trigger();   // the post kernel may be scheduled as CTAs retire
+  uint4* z = reinterpret_cast<uint4*>(&sm.kv[0][0]);
+  const int nz = (int)(sizeof(sm.kv) / sizeof(uint4));
+  for (int i = threadIdx.x; i < nz; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  // order the generic-proxy zero fill before the async-proxy (bulk copy) writes to the same rows
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
+__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q, Smem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
@@ -186,6 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
   }
   __syncthreads();
   const int total = sm.start[s.B];
+  const long row_elems = (long)kHK * kD;  // per token-layer K (or V)
+  (void)row_elems;
 
   if (warp == kHK) {
     // ================================================================== producer warp
@@ -254,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
       __syncwarp();
       epilogue(stage, pend[stage]);
     }
-    return;
+    return;   // the producer warp is done with this phase
   }
 
   // ==================================================================== consumer warps (KV head = warp)
@@ -376,6 +374,83 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const
   }
 }
 
+
+// Standalone attention kernel (multi-kernel schedule, ASR_NO_MEGA=1).
+__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  Stamp stamp(s.tl, 1);
+  attention_prologue(sm);
+  pdl_wait();      // A_i, |A_i|, q and the appended K/V come from the upstream kernels
+  pdl_trigger();
+  attention_phase(s, q, sm);
+}
+
+__device__ __forceinline__ void stamp_min(const DevState& s, int k) {
+  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[k], gtimer());
+}
+__device__ __forceinline__ void stamp_max(const DevState& s, int k) {
+  if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[k], gtimer());
+}
+
+// The whole step as ONE persistent cooperative kernel (one CTA per SM): phases A, B (ledger units),
+// C (attention + score), D (decide + combine) separated by grid barriers; the step counter advances
+// after the last barrier.  Replaces 3-4 dependent launches whose latency chains dominated batch-1
+// steps.
+template <typename TL>
+__global__ void __launch_bounds__(kThreads, 1)
+    step_kernel(DevState s, const TL* logits, float* entropy_out, const __nv_bfloat16* k_new,
+                const __nv_bfloat16* v_new, const __nv_bfloat16* __restrict__ q, float* o) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  __shared__ units::UnitShm u;
+  stamp_min(s, 0);
+  attention_prologue(sm);
+  const int i = *s.step;
+  // ---- phase A: entropy splits, append, speculative compaction
+  const int nA = units::phaseA_units(s, logits != nullptr);
+  for (int unit = blockIdx.x; unit < nA; unit += gridDim.x) {
+    units::run_phaseA_unit<TL, __nv_bfloat16>(s, unit, i, logits, k_new, v_new, u);
+    __syncthreads();
+  }
+  units::grid_sync(s.gbar);
+  // ---- phase B: entropy, detector, ladder, recovery (+ recompaction)
+  for (int b = blockIdx.x; b < s.B; b += gridDim.x) {
+    units::unit_finish(s, b, i, logits != nullptr, entropy_out, u);
+    __syncthreads();
+  }
+  units::grid_sync(s.gbar);
+  stamp_max(s, 1);
+  stamp_min(s, 2);
+  // ---- phase C: attention + fused Eq. 2 score
+  attention_phase(s, q, sm);
+  units::grid_sync(s.gbar);
+  stamp_max(s, 3);
+  stamp_min(s, 4);
+  // ---- phase D: decide + tick, combine
+  const int nd = s.decide_blocks * s.B;
+  const int wpb = kThreads / 32;
+  const int nc = (s.B * s.L * s.Hq + wpb - 1) / wpb;
+  for (int unit = blockIdx.x; unit < nd + nc; unit += gridDim.x) {
+    if (unit < nd) {
+      units::unit_decide(s, unit / s.decide_blocks, unit % s.decide_blocks, s.decide_blocks, i, u);
+    } else {
+      const int wid = (unit - nd) * wpb + (threadIdx.x >> 5);
+      if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
+    }
+    __syncthreads();
+  }
+  stamp_max(s, 5);
+  units::grid_sync(s.gbar);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *s.step = i + 1;
+    if (s.tl) {   // accumulate the phase durations (asr_stage_times)
+      for (int k = 0; k < kStages; ++k) s.tl[2 * kStages + k] += s.tl[2 * k + 1] - s.tl[2 * k];
+      s.tl[3 * kStages] += 1;
+    }
+  }
+}
+
 }  // namespace
 
 bool attention_mma_supported(const DevState& s) {
@@ -383,10 +458,36 @@ bool attention_mma_supported(const DevState& s) {
 }
 
 cudaError_t attention_mma_prepare() {
-  return cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(step_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
 }
 const void* attention_mma_func() { return (const void*)attn_mma_kernel; }
 unsigned attention_mma_smem() { return (unsigned)sizeof(Smem); }
 int attention_mma_threads() { return kThreads; }
+
+int step_kernel_max_grid(int num_sms) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<__nv_bfloat16>, kThreads, sizeof(Smem)) !=
+      cudaSuccess)
+    return 0;
+  return per_sm * num_sms;
+}
+
+void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
+               const void* k_new, const void* v_new, const void* q, float* o, int grid) {
+  n.s = s;
+  n.set(0, logits);
+  n.set(1, entropy_out);
+  n.set(2, k_new);
+  n.set(3, v_new);
+  n.set(4, q);
+  n.set(5, o);
+  const void* f = (logits && logits_dtype == 1) ? (const void*)step_kernel<float> : (const void*)step_kernel<__nv_bfloat16>;
+  n.finalize(f, dim3(grid), dim3(kThreads), sizeof(Smem));
+  n.cooperative = true;
+}
 
 }  // namespace asr

@@ -1,0 +1,560 @@
+// paper_2512_11221_b200/csrc/step_units.cuh — the ledger-side work units of one ASR-KF-EGR step,
+// written once and scheduled two ways: by the persistent step kernel (kernels_attn_mma.cu, one
+// cooperative launch per step, phases separated by grid barriers) and by the generic multi-kernel
+// path (kernels_ledger.cu).  Every unit uses the whole thread block (any blockDim multiple of 32,
+// <= 1024) and is followed by a __syncthreads() in its scheduler.
+//
+//   phase A  unit_entropy_split   (a6) partial (m, Z, S) of one split of a logits row
+//            unit_compact         (a0) ledger entry of the appended position, (a3) A_i (speculative:
+//                                 assumes no recovery this step)
+//            unit_append          (a0) the new token's K/V rows of (b, l) -> its slot
+//   phase B  unit_finish          (a6) H = ln Z - S/Z, detector (R-det), ladder (R-ladder) and, when
+//                                 a level fires (rare), the level (Sec 3.6) + recompaction
+//   phase C  attention            (a4)+(a1) — kernels_attn_mma.cu / kernels_attn.cu
+//   phase D  unit_decide          (a2) Eq. 2 finish, threshold, Eq. 3, freeze, R0 tick (Alg. 1 3-15)
+//            combine_warp         (a4') fixed-order combine of the split-KV partials -> O
+// Floating-point reductions are in a fixed order, so a step is bitwise deterministic.
+#pragma once
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "asr_internal.h"
+
+namespace asr {
+namespace units {
+namespace {   // internal linkage: this header is compiled into several translation units
+
+struct UnitShm {
+  int sh[32], sh2[32], wsum[32];
+  float wm[32], wz[32], ws[32];
+  int level;
+  int total;
+};
+
+__device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float tof(float v) { return v; }
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* x);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* x) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[2 * i] = __uint_as_float(w[i] << 16);
+    x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* x) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+
+// ---------------------------------------------------------------------------------- grid barrier
+// Sense-reversing barrier over all CTAs of a cooperative launch (bar[0] arrivals, bar[1] generation).
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------- (a6) entropy
+// merge (m, Z, S) triples of the single-pass entropy (Z = sum e^{x-m}, S = sum e^{x-m}(x-m)),
+// rescaled to M = max(m, om)
+__device__ __forceinline__ void tri_merge(float& m, float& z, float& sx, float om, float oz, float os) {
+  const float M = fmaxf(m, om);
+  float nz = 0.f, ns = 0.f;
+  if (z > 0.f) { const float f = __expf(m - M); nz += z * f; ns += f * (sx + z * (m - M)); }
+  if (oz > 0.f) { const float f = __expf(om - M); nz += oz * f; ns += f * (os + oz * (om - M)); }
+  m = M; z = nz; sx = ns;
+}
+
+template <typename TL>
+__device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ logits, int b, int split, UnitShm& u) {
+  const int V = s.vocab;
+  const int seg = (((V + kEntSplits - 1) / kEntSplits) + 7) & ~7;   // multiple of 8 elements
+  const int e0 = min(V, split * seg), e1 = min(V, e0 + seg);
+  const TL* row = logits + (long)b * V;
+  const bool vecok = (reinterpret_cast<uintptr_t>(row) & 31) == 0;
+  const float invT = 1.0f / s.ent_temp;
+  float m = -INFINITY, z = 0.f, sx = 0.f;
+  for (int v = e0 + (int)threadIdx.x * 8; v < e1; v += (int)blockDim.x * 8) {
+    float x[8];
+    if (vecok && v + 8 <= e1) {
+      load8<TL>(row + v, x);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = (v + e < e1) ? tof(row[v + e]) : -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { x[e] *= invT; mx = fmaxf(mx, x[e]); }
+    if (mx > m) {   // rescale the running sums to the new max
+      if (z > 0.f) { const float f = __expf(m - mx); sx = f * (sx + z * (m - mx)); z *= f; }
+      m = mx;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = x[e] - m;
+      const float ex = __expf(d);
+      z += ex;
+      sx += ex > 0.f ? ex * d : 0.f;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1)
+    tri_merge(m, z, sx, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, z, o),
+              __shfl_xor_sync(0xffffffffu, sx, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { u.wm[w] = m; u.wz[w] = z; u.ws[w] = sx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = -INFINITY, Z = 0.f, S = 0.f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tri_merge(M, Z, S, u.wm[k], u.wz[k], u.ws[k]);
+    float* ep = s.ent_part + ((long)b * kEntSplits + split) * 3;
+    ep[0] = M; ep[1] = Z; ep[2] = S;
+  }
+}
+
+// ---------------------------------------------------------------------------------- (a3) compaction
+__device__ __forceinline__ int active_mask16(uint4 x, uint32_t* m) {  // 1 per byte iff residency == 1
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    m[k] = w[k] & 0x01010101u & ~((w[k] >> 1) & 0x01010101u);
+    c += __popc(m[k]);
+  }
+  return c;
+}
+
+// A_i = sorted Active positions of [0, n) (rows are 64-aligned, positions >= n hold 0).
+__device__ void compact_positions(const DevState& s, int b, int n, UnitShm& u) {
+  const long base = (long)b * s.max_ctx;
+  const uint8_t* res = s.res + base;
+  const int nvec = (n + 15) >> 4;
+  const int per = (nvec + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int v0 = min(nvec, (int)threadIdx.x * per), v1 = min(nvec, v0 + per);
+  int cnt = 0;
+#pragma unroll 4
+  for (int v = v0; v < v1; ++v) {
+    uint32_t m[4];
+    cnt += active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) u.wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < (int)(blockDim.x >> 5) ? u.wsum[lane] : 0;
+    int xi = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    u.wsum[lane] = xi - x;  // exclusive warp offsets
+    if (lane == 31) u.total = xi;
+  }
+  __syncthreads();
+  int off = u.wsum[w] + incl - cnt;
+  int32_t* out = s.act_pos + base;
+  for (int v = v0; v < v1; ++v) {
+    uint32_t m[4];
+    active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      while (m[k]) {
+        const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
+        out[off++] = v * 16 + k * 4 + (bit >> 3);
+        m[k] &= m[k] - 1;
+      }
+  }
+  if (threadIdx.x == 0) {
+    s.act_len[b] = u.total;
+    s.stats[b].attended = u.total;
+    if (u.total == 0) atomicOr(s.err, kErrEmptyActive);
+  }
+}
+
+__device__ void unit_compact(const DevState& s, int b, int i, UnitShm& u) {
+  const int n = s.prompt_len[b] + i + 1;  // total after the append
+  if (threadIdx.x == 0) {
+    const long j = (long)b * s.max_ctx + n - 1;   // the token produced by the previous step (Alg. 1 line 16)
+    s.res[j] = 1;
+    s.timer[j] = 0;
+    s.count[j] = 0;
+    s.fstep[j] = -1;
+    SeqStats& st = s.stats[b];
+    st.restored_pre = st.pending_restored;
+    st.pending_restored = 0;
+    st.restored_tick = 0;
+    st.frozen_this_step = 0;
+  }
+  __syncthreads();
+  compact_positions(s, b, n, u);
+}
+
+template <typename TK>
+__device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __restrict__ k_new,
+                            const TK* __restrict__ v_new) {
+  const long pos = s.prompt_len[b] + i;
+  const long slot = (long)b * s.max_ctx + pos;
+  const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
+  TK* dst = reinterpret_cast<TK*>(s.kv) + (slot * s.L + l) * 2 * row;
+  const TK* ks = k_new + ((long)b * s.L + l) * row;
+  const TK* vs = v_new + ((long)b * s.L + l) * row;
+  const int vec = (int)(16 / sizeof(TK));
+  if (row % vec == 0) {
+    const int nv = row / vec;
+    for (int t = threadIdx.x; t < 2 * nv; t += blockDim.x) {
+      const uint4* src = reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv);
+      reinterpret_cast<uint4*>(dst)[t] = *src;
+    }
+  } else {
+    for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) dst[t] = t < row ? ks[t] : vs[t - row];
+  }
+}
+
+// Recovery levels on one sequence's ledger over positions [0, n): returns this thread's
+// restored count.  SR: frozen with d > 1; WR: frozen at step >= i - N; FR: every frozen token.
+__device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
+  int restored = 0;
+  uint8_t* res = s.res + (long)b * s.max_ctx;
+  int32_t* timer = s.timer + (long)b * s.max_ctx;
+  const int32_t* fstep = s.fstep + (long)b * s.max_ctx;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    if (res_active(res[j])) continue;
+    bool go = level == 1 ? timer[j] > 1 : level == 2 ? fstep[j] >= i - s.wr_window : true;
+    if (go) {
+      res[j] = 1;
+      timer[j] = 0;
+      restored++;
+    }
+  }
+  if (level >= 3 && s.fr_clear_counts) {
+    uint32_t* cnt = s.count + (long)b * s.max_ctx;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) cnt[j] = 0;
+  }
+  return restored;
+}
+
+__device__ int block_sum_int(int v, UnitShm& u) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) u.sh[w] = v;
+  __syncthreads();
+  int t = 0;
+  for (int k = 0; k < nw; ++k) t += u.sh[k];
+  __syncthreads();
+  return t;
+}
+
+// Phase B for sequence b: entropy of logits_prev (if given), detector, ladder, recovery.
+__device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, float* entropy_out, UnitShm& u) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w == 0) {
+    int level = 0;
+    if (has_logits) {
+      const float* ep = s.ent_part + (long)b * kEntSplits * 3;
+      double pm[kEntSplits / 32], pz[kEntSplits / 32], ps[kEntSplits / 32];
+      double M = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kEntSplits / 32; ++k) {
+        const int sp = k * 32 + lane;
+        pm[k] = ep[sp * 3]; pz[k] = ep[sp * 3 + 1]; ps[k] = ep[sp * 3 + 2];
+        if (pz[k] > 0.0) M = fmax(M, pm[k]);
+      }
+      for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+      double Zl = 0.0, Sl = 0.0;
+#pragma unroll
+      for (int k = 0; k < kEntSplits / 32; ++k) {
+        if (pz[k] <= 0.0) continue;
+        const double dm = pm[k] - M, f = exp(dm);
+        Zl += pz[k] * f;
+        Sl += f * (ps[k] + pz[k] * dm);
+      }
+      for (int o = 16; o > 0; o >>= 1) {   // fixed-order tree over lanes (deterministic)
+        Zl += __shfl_xor_sync(0xffffffffu, Zl, o);
+        Sl += __shfl_xor_sync(0xffffffffu, Sl, o);
+      }
+      const double H = log(Zl) - Sl / Zl;
+      DetState& ds = s.det[b];
+      double* hist = s.hist + (long)b * s.det_baseline;
+      const int hl = ds.hist_len;
+      double mu = 0.0, var = 0.0;
+      for (int t = lane; t < hl; t += 32) mu += hist[t];
+      for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
+      mu = hl > 0 ? mu / hl : 0.0;
+      for (int t = lane; t < hl; t += 32) var += (hist[t] - mu) * (hist[t] - mu);
+      for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+      if (lane == 0) {
+        var = hl > 0 ? var / hl : 0.0;
+        int trig = 0;
+        if (s.det_enable && hl >= 2) {
+          const double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
+          trig = H > mu + (double)s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
+        }
+        if (hl < s.det_baseline) {
+          hist[hl] = H;
+          ds.hist_len = hl + 1;
+        } else {
+          hist[ds.hist_head] = H;
+          ds.hist_head = (ds.hist_head + 1) % s.det_baseline;
+        }
+        if (trig) {
+          const int dt = i - ds.last_action_step;
+          if (!(ds.has_last && dt < s.det_cooldown)) {   // absorbed inside the cooldown
+            level = (ds.has_last && dt < 2 * s.det_cooldown) ? (ds.level < 4 ? ds.level + 1 : 4) : 1;
+            ds.level = level;
+            ds.last_action_step = i;
+            ds.has_last = 1;
+          }
+        }
+        if (entropy_out) entropy_out[b] = (float)H;
+        s.stats[b].entropy = (float)H;
+      }
+    }
+    if (lane == 0) u.level = level;
+  }
+  __syncthreads();
+  const int level = u.level;
+  int restored = 0;
+  if (level > 0) {   // rare: apply the level, then recompact A_i
+    const int n = s.prompt_len[b] + i + 1;
+    restored = block_sum_int(apply_level(s, b, n - 1, level, i), u);
+    compact_positions(s, b, n, u);
+  }
+  if (threadIdx.x == 0) {
+    SeqStats& st = s.stats[b];
+    st.restored_rec = restored;
+    st.recovery_action = level;
+    st.rewalk_requested = level == 4;
+    st.entropy_valid = has_logits ? 1 : 0;
+    s.rec_action[b] = level;
+  }
+}
+
+// ---------------------------------------------------------------------------------- (a2) decide
+__device__ __forceinline__ uint32_t isqrt_u32(uint32_t c) {
+  uint32_t r = (uint32_t)sqrtf((float)c);
+  while ((uint64_t)r * r > c) --r;
+  while ((uint64_t)(r + 1) * (r + 1) <= c) ++r;
+  return r;
+}
+
+// Eq. 3: d = floor(sqrt(c) / k) (exact, worked values P:72).
+__device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
+  if (kint > 0) return (int)(isqrt_u32(c) / (uint32_t)kint);
+  const double kd = k;
+  int m = (int)(sqrt((double)c) / kd);
+  while (m > 0 && ((double)m * kd) * ((double)m * kd) > (double)c) --m;
+  while (((double)(m + 1) * kd) * ((double)(m + 1) * kd) <= (double)c) ++m;
+  return m;
+}
+
+// Unit x of X for sequence b: a slice of the attended list (Alg. 1 lines 3-9 + the R0 tick of the
+// tokens it freezes) and a slice of the positions (lines 10-15 for tokens frozen at earlier steps).
+// The two index sets are disjoint (A_i = the tokens Active at the step start) and tokens frozen in
+// this step carry the step-parity tag res_tag(i), so units need no ordering between them.
+__device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
+  const int n = s.prompt_len[b] + i + 1;
+  const long base = (long)b * s.max_ctx;
+  const int A = s.act_len[b];
+  uint8_t* res = s.res + base;
+  int32_t* timer = s.timer + base;
+  uint32_t* cnt = s.count + base;
+  int32_t* fstep = s.fstep + base;
+  const float inv = 1.0f / (float)(s.L * s.Hq);
+  const float inv_sqrt_d = rsqrtf((float)s.d);
+  const uint8_t tag_now = res_tag(i);
+  // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
+  // loop: tokens of A_i read Active here and are skipped by the tick below)
+  constexpr int kPF = 8;
+  const int per_n = (n + X - 1) / X;
+  const int n0 = x * per_n, n_end = min(n, n0 + per_n);
+  uint8_t pr[kPF];
+  int pt[kPF];
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    pr[k] = j < n_end ? res[j] : (uint8_t)1;
+    pt[k] = j < n_end ? timer[j] : 0;
+  }
+  int frozen_now = 0, restored = 0;
+  const int per_a = (A + X - 1) / X;
+  const int a_end = min(A, (x + 1) * per_a);
+  for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
+    const int j = s.act_pos[base + a];
+    // Eq. 2: sum over layers in order l = 0..L-1 (loads issued 8 at a time)
+    const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
+    float sum = 0.f;
+    int l = 0;
+    for (; l + 8 <= s.L; l += 8) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = sp[(long)(l + q) * s.max_ctx];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += v[q];
+    }
+    for (; l < s.L; ++l) sum += sp[(long)l * s.max_ctx];
+    float sj = sum * inv;               // mean over the L*Hq (layer, head) pairs
+    if (s.score_scaled) sj *= inv_sqrt_d;
+    s.score[base + a] = sj;
+    if (j < n - s.window && j >= s.pinned && sj < s.tau) {
+      const uint32_t c = cnt[j] + 1;    // line 4
+      cnt[j] = c;
+      const int dd = duration(c, s.softness, s.softness_int);  // line 5
+      if (dd > 0) {                     // lines 6-7
+        frozen_now++;
+        fstep[j] = i;
+        const int t = s.tick_skip_new ? dd : dd - 1;   // R0: this step's tick applies too
+        if (t <= 0) {
+          timer[j] = 0;                 // frozen and restored by the same tick (no absence)
+          restored++;
+        } else {
+          timer[j] = t;
+          res[j] = tag_now;
+        }
+      }
+    }
+  }
+  // lines 10-15 for tokens frozen before this step
+  uint32_t err = 0;
+  auto tick = [&](int j, uint8_t r, int tm) {
+    if (r == 1 || r == tag_now) return;
+    const int t = tm - 1;
+    if (t <= 0) {
+      res[j] = 1;
+      timer[j] = 0;
+      restored++;
+    } else {
+      timer[j] = t;
+      if (r != 0) res[j] = 0;           // drop the previous step's tag
+      if (j >= n - s.window) err |= kErrFrozenInWindow;
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    if (j < n_end) tick(j, pr[k], pt[k]);
+  }
+  for (int j = n0 + (int)threadIdx.x + kPF * (int)blockDim.x; j < n_end; j += blockDim.x) tick(j, res[j], timer[j]);
+  if (err) atomicOr(s.err, err);
+  int f = frozen_now, r = restored;
+  for (int o = 16; o > 0; o >>= 1) {
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { u.sh[w] = f; u.sh2[w] = r; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    f = 0; r = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { f += u.sh[k]; r += u.sh2[k]; }
+    SeqStats& st = s.stats[b];
+    if (f) atomicAdd(&st.frozen_this_step, f);
+    if (r) atomicAdd(&st.restored_tick, r);
+  }
+}
+
+// ---------------------------------------------------------------------------------- (a4') combine
+// One warp per (b, l, h): lane c < nch reads split c's (m, l); each lane owns d/32 output elements;
+// fixed split order -> deterministic.
+__device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) {
+  const int lane = threadIdx.x & 31;
+  const int h = wid % s.Hq;
+  const int l = (wid / s.Hq) % s.L;
+  const int b = wid / (s.Hq * s.L);
+  int chunk, nch;
+  chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+  const long it0 = s.item_start[b] + (long)l * nch;
+  float M = -INFINITY;
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, s.part_ml[((it0 + c) * s.Hq + h) * 2]);
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const int epl = s.d >= 32 ? s.d / 32 : 1;   // elements per lane (d <= 256 -> <= 8)
+  const bool on = lane * epl < s.d;
+  float num[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float den = 0.f;
+  for (int c0 = 0; c0 < nch; c0 += 32) {
+    float wl = 0.f, ll = 0.f;
+    if (c0 + lane < nch) {
+      const long pi = (it0 + c0 + lane) * s.Hq + h;
+      wl = exp2f(s.part_ml[pi * 2] - M);
+      ll = s.part_ml[pi * 2 + 1];
+    }
+    const int cn = min(32, nch - c0);
+    if (epl == 4) {
+      for (int cb = 0; cb < cn; cb += 8) {   // 8 chunk vectors in flight, accumulated in chunk order
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (cb + q < cn)
+            v[q] = *reinterpret_cast<const float4*>(s.part_acc + ((it0 + c0 + cb + q) * s.Hq + h) * (long)s.d +
+                                                    lane * 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (cb + q >= cn) break;
+          const float w = __shfl_sync(0xffffffffu, wl, cb + q);
+          den = fmaf(__shfl_sync(0xffffffffu, ll, cb + q), w, den);
+          num[0] = fmaf(v[q].x, w, num[0]); num[1] = fmaf(v[q].y, w, num[1]);
+          num[2] = fmaf(v[q].z, w, num[2]); num[3] = fmaf(v[q].w, w, num[3]);
+        }
+      }
+    } else {
+      for (int c = 0; c < cn; ++c) {
+        const float w = __shfl_sync(0xffffffffu, wl, c);
+        den = fmaf(__shfl_sync(0xffffffffu, ll, c), w, den);
+        if (on) {
+          const float* src = s.part_acc + ((it0 + c0 + c) * s.Hq + h) * (long)s.d + lane * epl;
+          for (int e = 0; e < epl; ++e) num[e] = fmaf(src[e], w, num[e]);
+        }
+      }
+    }
+  }
+  if (on) {
+    float* dst = o + (((long)b * s.L + l) * s.Hq + h) * s.d + lane * epl;
+    const float inv = 1.0f / den;
+    for (int e = 0; e < epl; ++e) dst[e] = num[e] * inv;
+  }
+}
+
+// Work-unit counts of the phases.
+__host__ __device__ inline int phaseA_units(const DevState& s, bool has_logits) {
+  return (has_logits ? s.B * kEntSplits : 0) + s.B + s.B * s.L;
+}
+template <typename TL, typename TK>
+__device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* logits, const TK* k_new,
+                                const TK* v_new, UnitShm& u) {
+  const int ne = logits ? s.B * kEntSplits : 0;
+  if (unit < ne) {
+    unit_entropy_split<TL>(s, logits, unit / kEntSplits, unit % kEntSplits, u);
+  } else if (unit < ne + s.B) {
+    unit_compact(s, unit - ne, i, u);
+  } else {
+    const int a = unit - ne - s.B;
+    unit_append<TK>(s, a / s.L, a % s.L, i, k_new, v_new);
+  }
+}
+
+}  // namespace
+}  // namespace units
+}  // namespace asr
