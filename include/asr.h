@@ -71,6 +71,15 @@ typedef struct {
   int32_t host_mirror;    /* 1 = keep the write-once pinned host copy of every token's KV */
   int32_t profile_stages; /* 1 = record CUDA events around every stage (asr_stage_times) */
   int32_t device;         /* CUDA device ordinal */
+  int32_t evict_min_absence; /* pressure mode: a token frozen for >= this many more steps gives up its
+                                device slot at freeze time (default 2) */
+  int32_t reserved0;
+  int64_t pool_tokens;    /* 0: full residency (every token keeps its device slot; freezing only flips
+                           * its residency bit).  > 0: pressure mode (Sec 3.3, "moves the token's
+                           * KV pair from GPU to CPU"): the device holds pool_tokens token slots; frozen
+                           * tokens are evicted to the pinned host mirror and prefetched back one step
+                           * before their timer expires; entropy-triggered / explicit restores of
+                           * evicted tokens are copied back on demand.  Needs host_mirror = 1. */
 } asr_config;
 
 /* Fills *cfg with the paper's defaults (K=32, tau=0.5, k=2: P:112) and LLaMA-3-8B shape. */
@@ -106,6 +115,10 @@ typedef struct {
   int32_t rewalk_requested;   /* RR: the caller should regenerate (needs the model; out of scope) */
   int64_t bytes_h2d, bytes_d2h; /* host-link bytes moved by the library for this context so far */
   uint32_t device_error;      /* latched invariant flags (0 = none) */
+  int64_t resident;           /* tokens of this sequence holding a device slot (pressure mode; else total) */
+  int64_t evicted_this_step;  /* device slots released by this step's freezes (pressure mode) */
+  int64_t prefetched_this_step; /* tokens copied host -> device ahead of their timer expiry */
+  int64_t demand_restored_this_step; /* evicted tokens copied back on demand (recovery / asr_restore) */
 } asr_stats_t;
 
 /* Host buffers for a full ledger snapshot of one sequence (any pointer may be NULL). */

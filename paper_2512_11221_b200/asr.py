@@ -40,7 +40,8 @@ class asr_config(ctypes.Structure):
                 ("vocab", ctypes.c_int32), ("entropy_temperature", ctypes.c_float), ("det_enable", ctypes.c_int32),
                 ("det_baseline", ctypes.c_int32), ("det_cooldown", ctypes.c_int32), ("wr_window", ctypes.c_int32),
                 ("det_z", ctypes.c_float), ("det_sigma_floor", ctypes.c_float), ("fr_clear_counts", ctypes.c_int32),
-                ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("evict_min_absence", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("pool_tokens", ctypes.c_int64)]
 
 
 class asr_step_io(ctypes.Structure):
@@ -55,7 +56,9 @@ class asr_stats_t(ctypes.Structure):
                 ("restored_this_step", ctypes.c_int64), ("compression", ctypes.c_double),
                 ("entropy", ctypes.c_float), ("entropy_valid", ctypes.c_int32),
                 ("recovery_action", ctypes.c_int32), ("rewalk_requested", ctypes.c_int32),
-                ("bytes_h2d", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64), ("device_error", ctypes.c_uint32)]
+                ("bytes_h2d", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64), ("device_error", ctypes.c_uint32),
+                ("resident", ctypes.c_int64), ("evicted_this_step", ctypes.c_int64),
+                ("prefetched_this_step", ctypes.c_int64), ("demand_restored_this_step", ctypes.c_int64)]
 
 
 class asr_ledger_view(ctypes.Structure):
@@ -132,6 +135,9 @@ class Config:
     host_mirror: int = 1
     profile_stages: int = 0
     device: int = 0
+    evict_min_absence: int = 2
+    reserved0: int = 0
+    pool_tokens: int = 0             # 0 = full residency; > 0 = pressure mode (device slot pool)
 
     def c(self) -> asr_config:
         v = dataclasses.asdict(self)

@@ -142,6 +142,9 @@ void asr_config_defaults(asr_config* c) {
   c->host_mirror = 1;
   c->profile_stages = 0;
   c->device = 0;
+  c->evict_min_absence = 2;
+  c->reserved0 = 0;
+  c->pool_tokens = 0;
 }
 
 static asr_status validate(const asr_config* c) {
@@ -170,6 +173,9 @@ static asr_status validate(const asr_config* c) {
   if (c->det_baseline < 1 || c->det_baseline > asr::kMaxDetBaseline)
     return fail(ASR_E_INVALID, "det_baseline out of range [1,256]");
   if (c->det_cooldown < 0 || c->wr_window < 0) return fail(ASR_E_INVALID, "det_cooldown / wr_window < 0");
+  if (c->pool_tokens < 0) return fail(ASR_E_INVALID, "pool_tokens < 0");
+  if (c->pool_tokens > 0 && !c->host_mirror) return fail(ASR_E_INVALID, "pool_tokens > 0 needs host_mirror = 1");
+  if (c->pool_tokens > ((int64_t)1 << 31) - 1) return fail(ASR_E_INVALID, "pool_tokens too large");
   return ASR_OK;
 }
 
@@ -189,6 +195,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     pmax = prompt_len[b] > pmax ? prompt_len[b] : pmax;
   }
   if (pmax > 0 && (!prompt_k || !prompt_v)) return fail(ASR_E_INVALID, "prompt_k / prompt_v is NULL");
+  int64_t prompt_total = 0;
+  for (int b = 0; b < cfg->batch; ++b) prompt_total += prompt_len[b];
+  if (cfg->pool_tokens > 0 && cfg->pool_tokens < prompt_total + 2 * (int64_t)cfg->batch)
+    return fail(ASR_E_INVALID, "pool_tokens must hold every prompt token plus two slots per sequence");
   CUDA_TRY(cudaSetDevice(cfg->device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
 
@@ -239,8 +249,40 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
 
     c->kv_elem = s.dtype == ASR_KV_BF16 ? 2 : 4;
     c->tok_bytes = (size_t)s.L * 2 * s.Hkv * s.d * c->kv_elem;
+    s.tok_bytes = (long)c->tok_bytes;
     const size_t BT = (size_t)s.B * s.max_ctx;
-    CUDA_TRY(c->alloc(&s.kv, BT * c->tok_bytes));
+    s.pool_mode = cfg->pool_tokens > 0 ? 1 : 0;
+    s.evict_min = cfg->evict_min_absence > 0 ? cfg->evict_min_absence : 2;
+    const size_t slots = s.pool_mode ? (size_t)cfg->pool_tokens : BT;
+    CUDA_TRY(c->alloc(&s.kv, slots * c->tok_bytes));
+    CUDA_TRY(c->alloc(&s.act_slot, BT * 4));
+    std::vector<size_t> slot0(s.B, 0);   // first slot of each sequence's prompt
+    for (int b = 0; b < s.B; ++b) slot0[b] = s.pool_mode ? (b ? slot0[b - 1] + prompt_len[b - 1] : 0) : (size_t)b * s.max_ctx;
+    if (s.pool_mode) {
+      const int64_t used = prompt_total;
+      CUDA_TRY(c->alloc(&s.slot_of, BT * 4));
+      CUDA_TRY(c->alloc(&s.spare, (size_t)s.B * 4));
+      CUDA_TRY(c->alloc(&s.free_stack, slots * 4));
+      CUDA_TRY(c->alloc(&s.free_top, 4));
+      CUDA_TRY(c->alloc(&s.pf_list, 2 * BT * 4));
+      CUDA_TRY(c->alloc(&s.pf_count, 2 * (size_t)s.B * 4));
+      CUDA_TRY(c->alloc(&s.cp_list, BT * 4));
+      CUDA_TRY(c->alloc(&s.cp_count, (size_t)s.B * 4));
+      CUDA_TRY(c->alloc(&s.h2d, 8));
+      std::vector<int32_t> so(BT, -1), sp(s.B), fs;
+      for (int b = 0; b < s.B; ++b)
+        for (int p = 0; p < prompt_len[b]; ++p) so[(size_t)b * s.max_ctx + p] = (int32_t)(slot0[b] + p);
+      for (int b = 0; b < s.B; ++b) sp[b] = (int32_t)(used + b);
+      for (int64_t k = (int64_t)slots - 1; k >= used + s.B; --k) fs.push_back((int32_t)k);
+      const int32_t top = (int32_t)fs.size();
+      CUDA_TRY(cudaMemcpy(s.slot_of, so.data(), BT * 4, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(s.spare, sp.data(), (size_t)s.B * 4, cudaMemcpyHostToDevice));
+      if (top) CUDA_TRY(cudaMemcpy(s.free_stack, fs.data(), (size_t)top * 4, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(s.free_top, &top, 4, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemset(s.pf_count, 0, 2 * (size_t)s.B * 4));
+      CUDA_TRY(cudaMemset(s.cp_count, 0, (size_t)s.B * 4));
+      CUDA_TRY(cudaMemset(s.h2d, 0, 8));
+    }
     CUDA_TRY(c->alloc(&s.res, BT));
     CUDA_TRY(c->alloc(&s.timer, BT * 4));
     CUDA_TRY(c->alloc(&s.count, BT * 4));
@@ -281,8 +323,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     for (int b = 0; b < s.B; ++b)
       if (prompt_len[b] > 0) CUDA_TRY(cudaMemsetAsync(s.res + (size_t)b * s.max_ctx, 1, prompt_len[b], st));
     if (cfg->host_mirror) {
-      cudaError_t e = cudaHostAlloc(&c->host_mirror, BT * c->tok_bytes, cudaHostAllocPortable);
+      cudaError_t e = cudaHostAlloc(&c->host_mirror, BT * c->tok_bytes,
+                                    cudaHostAllocPortable | (s.pool_mode ? cudaHostAllocMapped : 0));
       if (e != cudaSuccess) return fail(ASR_E_OOM, "pinned host mirror allocation failed");
+      if (s.pool_mode) CUDA_TRY(cudaHostGetDevicePointer((void**)&s.host_kv, c->host_mirror, 0));
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
@@ -294,7 +338,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       if (prompt_len[b] == 0) continue;
       const size_t rows = (size_t)prompt_len[b] * s.L;
       const size_t src_off = (size_t)b * prompt_stride * s.L * row;
-      char* dst = (char*)s.kv + (size_t)b * s.max_ctx * c->tok_bytes;
+      char* dst = (char*)s.kv + slot0[b] * c->tok_bytes;
       CUDA_TRY(cudaMemcpy2DAsync(dst, 2 * row, (const char*)prompt_k + src_off, row, row, rows, kind, st));
       CUDA_TRY(cudaMemcpy2DAsync(dst + row, 2 * row, (const char*)prompt_v + src_off, row, row, rows, kind, st));
       if (c->host_mirror) {
@@ -426,8 +470,8 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     CUDA_TRY(cudaMemcpyAsync(sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   // the step as kernel descriptions with their stage (0 ledger pre, 1 attention, 2 decide/combine)
-  asr::KNode kn_list[4];
-  int stage_of[4];
+  asr::KNode kn_list[5];
+  int stage_of[5];
   int nk = 0;
   const void* lgp = has_logits ? lg : nullptr;
   if (c->use_mega) {
@@ -438,6 +482,11 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     stage_of[nk++] = 0;
     asr::node_phaseB(kn_list[nk], sd, has_logits ? 1 : 0, has_logits ? ent : nullptr);
     stage_of[nk++] = 0;
+    if (s.pool_mode) {   // prefetch copies: a branch beside the attention kernel
+      asr::node_copy(kn_list[nk], sd, 32);
+      kn_list[nk].branch = true;
+      stage_of[nk++] = 1;
+    }
     asr::node_attention(kn_list[nk], sd, q, c->attn_grid);
     stage_of[nk++] = 1;
     asr::node_phaseD(kn_list[nk], sd, o);
@@ -471,6 +520,13 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
         }
         while (stg < asr::kStages && k < nk && stage_of[k] == stg) {
           cudaGraphNode_t kn_node;
+          if (kn_list[k].branch) {   // parallel branch: depends on the previous kernel, nothing waits on it
+            CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, prev ? &prev : nullptr, prev ? 1 : 0, &kn_list[k].p));
+            G.knodes.push_back(kn_node);
+            G.last.push_back(kn_list[k]);
+            ++k;
+            continue;
+          }
           const bool pdl = c->use_pdl && !prof && prev != nullptr;
           CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
                                           &kn_list[k].p));
@@ -509,7 +565,9 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   }
   c->launches += nk;
   // (a5) write-once host mirror of the appended token (side stream, overlapped with compute)
-  if (c->host_mirror) {
+  if (c->host_mirror && s.pool_mode) {
+    c->bytes_d2h += (int64_t)s.B * c->tok_bytes;   // written by the append units (mapped mirror)
+  } else if (c->host_mirror) {
     CUDA_TRY(cudaEventRecord(c->ev_append, st));
     CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_append, 0));
     const size_t pitch = (size_t)s.max_ctx * c->tok_bytes;
@@ -582,6 +640,20 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
   out->bytes_h2d = c->bytes_h2d;
   out->bytes_d2h = c->bytes_d2h;
   out->device_error = err;
+  out->resident = n;
+  if (s.pool_mode) {
+    unsigned long long h2d = 0;
+    CUDA_TRY(cudaMemcpy(&h2d, s.h2d, 8, cudaMemcpyDeviceToHost));
+    out->bytes_h2d += (int64_t)h2d;
+    std::vector<int32_t> so(n);
+    if (n) CUDA_TRY(cudaMemcpy(so.data(), s.slot_of + (size_t)seq * s.max_ctx, n * 4, cudaMemcpyDeviceToHost));
+    int64_t r = 0;
+    for (int64_t j = 0; j < n; ++j) r += so[j] >= 0;
+    out->resident = r;
+    out->evicted_this_step = st.evicted;
+    out->prefetched_this_step = st.prefetched;
+    out->demand_restored_this_step = st.demand;
+  }
   if (detail) {
     if (detail->capacity < n) return fail(ASR_E_INVALID, "detail->capacity < total");
     const size_t base = (size_t)seq * s.max_ctx;
@@ -614,8 +686,18 @@ asr_status asr_read_kv(asr_ctx* c, int32_t seq, int32_t pos, int32_t from_mirror
   CUDA_TRY(cudaStreamSynchronize(c->side));
   std::vector<char> tok(c->tok_bytes);
   const size_t off = ((size_t)seq * s.max_ctx + pos) * c->tok_bytes;
-  if (from_mirror) memcpy(tok.data(), (const char*)c->host_mirror + off, c->tok_bytes);
-  else CUDA_TRY(cudaMemcpy(tok.data(), (const char*)s.kv + off, c->tok_bytes, cudaMemcpyDeviceToHost));
+  if (from_mirror) {
+    memcpy(tok.data(), (const char*)c->host_mirror + off, c->tok_bytes);
+  } else {
+    size_t doff = off;
+    if (s.pool_mode) {
+      int32_t slot = -1;
+      CUDA_TRY(cudaMemcpy(&slot, s.slot_of + (size_t)seq * s.max_ctx + pos, 4, cudaMemcpyDeviceToHost));
+      if (slot < 0) return fail(ASR_E_INVALID, "token is not resident on the device (evicted)");
+      doff = (size_t)slot * c->tok_bytes;
+    }
+    CUDA_TRY(cudaMemcpy(tok.data(), (const char*)s.kv + doff, c->tok_bytes, cudaMemcpyDeviceToHost));
+  }
   const size_t row = (size_t)s.Hkv * s.d * c->kv_elem;
   for (int l = 0; l < s.L; ++l) {
     if (k_out) memcpy((char*)k_out + l * row, tok.data() + (2 * l) * row, row);

@@ -30,7 +30,12 @@ struct SeqStats {
   int32_t rewalk_requested;
   int32_t entropy_valid;
   float entropy;
-  int32_t pad[2];
+  int32_t evicted;            // pressure mode: slots released by this step's freezes
+  int32_t prefetched;         // pressure mode: slots allocated for next-step restores (copied this step)
+  int32_t demand;             // pressure mode: evicted tokens copied back on demand this step
+  int32_t resident;           // pressure mode: tokens holding a slot (after the step)
+  int32_t pending_demand;     // pressure mode: demand copies by asr_restore since the last step
+  int32_t pad[1];
 };
 
 // Detector / ladder state per sequence (R-det, R-ladder).
@@ -44,6 +49,8 @@ enum : uint32_t {
   kErrFrozenInWindow = 1u,   // a frozen token inside the protected window
   kErrEmptyActive = 2u,      // |A_i| == 0 (the current token is always active)
   kErrTimer = 4u,            // Active token with timer != 0 or Frozen with timer < 1
+  kErrPoolEmpty = 8u,        // pressure mode: no free device slot (pool_tokens too small)
+  kErrNotResident = 16u,     // pressure mode: an Active token without a device slot
 };
 
 // Everything a kernel may need; passed by value (all pointers are device pointers).
@@ -59,6 +66,20 @@ struct DevState {
   float det_z, det_sigma_floor;
   int max_splits, chunk_min;
   int decide_blocks;          // blocks per sequence of the decide kernel
+  // pressure mode (pool_tokens > 0)
+  int pool_mode;              // 0 full residency (slot = b*max_ctx + pos), 1 slot pool
+  int evict_min;              // evict at freeze when the remaining absence >= evict_min
+  long tok_bytes;             // bytes of one token (all layers, K and V)
+  int32_t* slot_of;           // [B][max_ctx] device slot of each position, -1 = evicted (pool mode)
+  int32_t* spare;             // [B] slot reserved for the next appended token (pool mode)
+  int32_t* free_stack;        // [pool] free slots
+  int32_t* free_top;          // [1] number of free slots
+  char* host_kv;              // device-mapped pointer of the pinned host mirror (pool mode)
+  int32_t* pf_list;           // [2][B][max_ctx] positions to prefetch (timer reached 1), by step parity
+  int32_t* pf_count;          // [2][B]
+  int32_t* cp_list;           // [B][max_ctx] positions whose slot the copy kernel fills this step
+  int32_t* cp_count;          // [B]
+  unsigned long long* h2d;    // [1] bytes copied host -> device by the kernels (prefetch + demand)
 
   void* kv;                   // pool [B*max_ctx][L][2][Hkv][d]
   uint8_t* res;               // [B][max_ctx] 1 Active / 0 Frozen
@@ -68,6 +89,7 @@ struct DevState {
   int32_t* prompt_len;        // [B]
   int32_t* step;              // [1] index of the next (or current) step
   int32_t* act_pos;           // [B][max_ctx]
+  int32_t* act_slot;          // [B][max_ctx] device slot of each attended position
   int32_t* act_len;           // [B]
   int32_t* item_start;        // [B+1]
   float* score_part;          // [B][L][max_ctx] per-layer Eq. 2 head sums per attended index
@@ -130,6 +152,7 @@ struct KNode {
   uint64_t extra[6] = {0, 0, 0, 0, 0, 0};   // pointer / int arguments after DevState (8-byte slots)
   void* argv[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool cooperative = false;                  // needs all CTAs co-resident (grid barriers)
+  bool branch = false;                       // graph: parallel branch (nothing depends on it)
   void finalize(const void* func, dim3 grid, dim3 block, unsigned smem) {
     argv[0] = &s;
     for (int k = 0; k < 6; ++k) argv[k + 1] = &extra[k];
@@ -163,6 +186,7 @@ void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype
                const void* k_new, const void* v_new, const void* q, float* o, int grid);
 int step_kernel_max_grid(int num_sms);
 void node_restore(KNode& n, const DevState& s, int seq, int level);
+void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies
 int attention_grid(const DevState& s, int num_sms);
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head
 cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory

@@ -101,7 +101,7 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
     const int r = item - sh_start[b];
     const int l = r / nch, c = r % nch;
     const int a0 = c * chunk, a1 = min(A, a0 + chunk);
-    const int* act = s.act_pos + (long)b * s.max_ctx;
+    const int* act = s.act_slot + (long)b * s.max_ctx;   // device slots of A_i
     // q slice of the G heads of this warp's KV head
     float qr[kMaxG][EPL];
     float m[kMaxG], lsum[kMaxG], acc[kMaxG][EPL];
@@ -117,7 +117,7 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
     for (int t0 = a0; t0 < a1; t0 += 32) {
       const int tn = min(32, a1 - t0);
       for (int tt = 0; tt < tn; ++tt) {
-        const long slot = (long)b * s.max_ctx + act[t0 + tt];
+        const long slot = max(0, act[t0 + tt]);
         const T* kp = reinterpret_cast<const T*>(s.kv) + (slot * s.L + l) * 2 * row + (long)g * D;
         const T* vp = kp + row;
         float kr[EPL], vr[EPL];

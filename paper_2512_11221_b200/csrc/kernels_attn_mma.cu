@@ -204,7 +204,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     if (cur.valid(total)) cur.it = decode_item(s, sm.start, cur.item);
     auto load_idx = [&](const TileIt& t) -> int {
       if (!t.valid(total) || lane >= min(kTM, t.it.n - t.t0)) return 0;
-      return __ldg(s.act_pos + (long)t.it.b * s.max_ctx + t.it.a0 + t.t0 + lane);
+      return max(0, __ldg(s.act_slot + (long)t.it.b * s.max_ctx + t.it.a0 + t.t0 + lane));   // device slot
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
@@ -235,7 +235,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
       __syncwarp();
       if (lane < cnt) {
-        const long slot = (long)it.b * s.max_ctx + j_cur;
+        const long slot = j_cur;
         bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + it.l) * (long)kTokBytes, kTokBytes,
                  &sm.full[stage]);
       }

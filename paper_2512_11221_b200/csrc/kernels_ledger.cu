@@ -53,14 +53,29 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
   if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
 }
 
-// Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.
+// Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.  In pressure
+// mode the evicted tokens it restores are copied back before it returns.
 __global__ void __launch_bounds__(1024) restore_kernel(DevState s, int seq, int level) {
   __shared__ units::UnitShm u;
   const int b = seq >= 0 ? seq : (int)blockIdx.x;
   const int i = *s.step;
   const int n = s.prompt_len[b] + i;  // tokens currently held
+  if (s.pool_mode && threadIdx.x == 0) s.cp_count[b] = 0;
+  __syncthreads();
   const int r = units::block_sum_int(units::apply_level(s, b, n, level, i), u);
-  if (threadIdx.x == 0) s.stats[b].pending_restored += r;
+  const int d = s.pool_mode ? units::demand_copies(s, b) : 0;
+  if (threadIdx.x == 0) {
+    s.stats[b].pending_restored += r;
+    s.stats[b].pending_demand += d;
+  }
+}
+
+// Pressure mode: fill the slots phase B allocated for next-step restores (graph branch beside the
+// attention kernel; reads the pinned host mirror over the host link).
+constexpr int kCopyThreads = 256;
+__global__ void __launch_bounds__(kCopyThreads) copy_kernel(DevState s) {
+  __shared__ int start[4097];
+  units::prefetch_copies(s, start);
 }
 
 }  // namespace
@@ -93,6 +108,11 @@ void node_phaseD(KNode& n, const DevState& s, float* o) {
   const int warps = s.B * s.L * s.Hq;
   const int wpb = kUnitThreads / 32;
   n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + (warps + wpb - 1) / wpb), dim3(kUnitThreads), 0);
+}
+
+void node_copy(KNode& n, const DevState& s, int grid) {
+  n.s = s;
+  n.finalize((const void*)copy_kernel, dim3(grid), dim3(kCopyThreads), 0);
 }
 
 void node_restore(KNode& n, const DevState& s, int seq, int level) {

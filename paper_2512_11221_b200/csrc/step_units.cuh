@@ -73,6 +73,45 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------------- (a5) slot pool
+// Pressure mode (pool_tokens > 0): device token slots come from a free stack.  Pops happen only in
+// phase B (and asr_restore), pushes only in phase D, so the stack never sees both at once.
+__device__ __forceinline__ int pool_pop(const DevState& s) {
+  const int idx = atomicSub(s.free_top, 1) - 1;
+  if (idx < 0) {
+    atomicAdd(s.free_top, 1);
+    atomicOr(s.err, kErrPoolEmpty);
+    return -1;
+  }
+  return s.free_stack[idx];
+}
+__device__ __forceinline__ void pool_push(const DevState& s, int slot) {
+  const int idx = atomicAdd(s.free_top, 1);
+  s.free_stack[idx] = slot;
+}
+// Block-cooperative copy of one token (all layers, K and V) from the pinned host mirror (mapped,
+// read over the host link) into its device slot.
+__device__ void copy_token_h2d(const DevState& s, int b, int pos, int slot) {
+  if (slot < 0) return;
+  const uint4* src = reinterpret_cast<const uint4*>(s.host_kv + ((long)b * s.max_ctx + pos) * s.tok_bytes);
+  uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s.kv) + (long)slot * s.tok_bytes);
+  const int nv = (int)(s.tok_bytes / 16);
+  for (int v0 = (int)threadIdx.x; v0 < nv; v0 += 8 * (int)blockDim.x) {
+    uint4 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int v = v0 + k * (int)blockDim.x;
+      if (v < nv) x[k] = src[v];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int v = v0 + k * (int)blockDim.x;
+      if (v < nv) dst[v] = x[k];
+    }
+  }
+  if (threadIdx.x == 0) atomicAdd(s.h2d, (unsigned long long)s.tok_bytes);
+}
+
 // ---------------------------------------------------------------------------------- (a6) entropy
 // merge (m, Z, S) triples of the single-pass entropy (Z = sum e^{x-m}, S = sum e^{x-m}(x-m)),
 // rescaled to M = max(m, om)
@@ -176,6 +215,8 @@ __device__ void compact_positions(const DevState& s, int b, int n, UnitShm& u) {
   __syncthreads();
   int off = u.wsum[w] + incl - cnt;
   int32_t* out = s.act_pos + base;
+  int32_t* out_slot = s.act_slot + base;
+  const int32_t* slot_of = s.slot_of + base;
   for (int v = v0; v < v1; ++v) {
     uint32_t m[4];
     active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
@@ -183,7 +224,10 @@ __device__ void compact_positions(const DevState& s, int b, int n, UnitShm& u) {
     for (int k = 0; k < 4; ++k)
       while (m[k]) {
         const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
-        out[off++] = v * 16 + k * 4 + (bit >> 3);
+        const int j = v * 16 + k * 4 + (bit >> 3);
+        out[off] = j;
+        out_slot[off] = s.pool_mode ? slot_of[j] : (int)(base + j);
+        ++off;
         m[k] &= m[k] - 1;
       }
   }
@@ -202,7 +246,14 @@ __device__ void unit_compact(const DevState& s, int b, int i, UnitShm& u) {
     s.timer[j] = 0;
     s.count[j] = 0;
     s.fstep[j] = -1;
+    if (s.pool_mode) {
+      s.slot_of[j] = s.spare[b];                      // the slot reserved by the previous step
+      s.pf_count[(i & 1) * s.B + b] = 0;              // this step's decide fills list i & 1
+    }
     SeqStats& st = s.stats[b];
+    st.evicted = 0;
+    st.demand = st.pending_demand;
+    st.pending_demand = 0;
     st.restored_pre = st.pending_restored;
     st.pending_restored = 0;
     st.restored_tick = 0;
@@ -216,20 +267,29 @@ template <typename TK>
 __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __restrict__ k_new,
                             const TK* __restrict__ v_new) {
   const long pos = s.prompt_len[b] + i;
-  const long slot = (long)b * s.max_ctx + pos;
+  const long slot = s.pool_mode ? (long)s.spare[b] : (long)b * s.max_ctx + pos;
+  if (slot < 0) return;   // pool exhausted (latched by the pop)
   const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
   TK* dst = reinterpret_cast<TK*>(s.kv) + (slot * s.L + l) * 2 * row;
+  // pressure mode: the write-once host mirror is written here too (mapped pinned memory), so a
+  // token's bytes are off-GPU before it can ever be evicted
+  TK* mir = s.pool_mode ? reinterpret_cast<TK*>(s.host_kv) + (((long)b * s.max_ctx + pos) * s.L + l) * 2 * row : nullptr;
   const TK* ks = k_new + ((long)b * s.L + l) * row;
   const TK* vs = v_new + ((long)b * s.L + l) * row;
   const int vec = (int)(16 / sizeof(TK));
   if (row % vec == 0) {
     const int nv = row / vec;
     for (int t = threadIdx.x; t < 2 * nv; t += blockDim.x) {
-      const uint4* src = reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv);
-      reinterpret_cast<uint4*>(dst)[t] = *src;
+      const uint4 x = *(reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv));
+      reinterpret_cast<uint4*>(dst)[t] = x;
+      if (mir) reinterpret_cast<uint4*>(mir)[t] = x;
     }
   } else {
-    for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) dst[t] = t < row ? ks[t] : vs[t - row];
+    for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) {
+      const TK x = t < row ? ks[t] : vs[t - row];
+      dst[t] = x;
+      if (mir) mir[t] = x;
+    }
   }
 }
 
@@ -247,6 +307,10 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
       res[j] = 1;
       timer[j] = 0;
       restored++;
+      if (s.pool_mode && s.slot_of[(long)b * s.max_ctx + j] < 0) {   // evicted: copy back on demand
+        s.slot_of[(long)b * s.max_ctx + j] = pool_pop(s);
+        s.cp_list[(long)b * s.max_ctx + atomicAdd(&s.cp_count[b], 1)] = j;
+      }
     }
   }
   if (level >= 3 && s.fr_clear_counts) {
@@ -254,6 +318,21 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) cnt[j] = 0;
   }
   return restored;
+}
+
+// Copy back (synchronously, whole block) every token apply_level listed for sequence b; returns
+// the count.  Runs with no concurrent pushes (phase B / asr_restore).
+__device__ int demand_copies(const DevState& s, int b) {
+  __syncthreads();
+  const int nd = s.cp_count[b];
+  for (int k = 0; k < nd; ++k) {
+    const int j = s.cp_list[(long)b * s.max_ctx + k];
+    copy_token_h2d(s, b, j, s.slot_of[(long)b * s.max_ctx + j]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s.cp_count[b] = 0;
+  __syncthreads();
+  return nd;
 }
 
 __device__ int block_sum_int(int v, UnitShm& u) {
@@ -271,6 +350,7 @@ __device__ int block_sum_int(int v, UnitShm& u) {
 // Phase B for sequence b: entropy of logits_prev (if given), detector, ladder, recovery.
 __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, float* entropy_out, UnitShm& u) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (s.pool_mode && threadIdx.x == 0) s.cp_count[b] = 0;   // the previous step's copies are done
   if (w == 0) {
     int level = 0;
     if (has_logits) {
@@ -337,14 +417,35 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
   }
   __syncthreads();
   const int level = u.level;
-  int restored = 0;
-  if (level > 0) {   // rare: apply the level, then recompact A_i
+  int restored = 0, demand = 0;
+  if (level > 0) {   // rare: apply the level (copy evicted tokens back), then recompact A_i
     const int n = s.prompt_len[b] + i + 1;
     restored = block_sum_int(apply_level(s, b, n - 1, level, i), u);
+    if (s.pool_mode) demand = demand_copies(s, b);
     compact_positions(s, b, n, u);
+  }
+  int prefetched = 0;
+  if (s.pool_mode) {
+    // tokens whose timer reached 1 in the previous step's tick are restored by this step's tick
+    // and attended next step: give them slots now; the copy kernel fills them during this step
+    const int r = ((i + 1) & 1) * s.B + b;
+    const int np = i > 0 ? s.pf_count[r] : 0;
+    const int32_t* pl = s.pf_list + (long)r * s.max_ctx;
+    int32_t* slot_of = s.slot_of + (long)b * s.max_ctx;
+    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+      const int j = pl[k];
+      if (slot_of[j] >= 0) continue;   // already back (recovery demand copy)
+      slot_of[j] = pool_pop(s);
+      s.cp_list[(long)b * s.max_ctx + atomicAdd(&s.cp_count[b], 1)] = j;
+    }
+    __syncthreads();
+    prefetched = s.cp_count[b];
+    if (threadIdx.x == 0) s.spare[b] = pool_pop(s);   // slot of the token the next step appends
   }
   if (threadIdx.x == 0) {
     SeqStats& st = s.stats[b];
+    st.prefetched = prefetched;
+    st.demand += demand;
     st.restored_rec = restored;
     st.recovery_action = level;
     st.rewalk_requested = level == 4;
@@ -399,7 +500,8 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     pr[k] = j < n_end ? res[j] : (uint8_t)1;
     pt[k] = j < n_end ? timer[j] : 0;
   }
-  int frozen_now = 0, restored = 0;
+  int frozen_now = 0, restored = 0, evicted = 0;
+  const int pf_row = (i & 1) * s.B + b;   // prefetch list written by this step
   const int per_a = (A + X - 1) / X;
   const int a_end = min(A, (x + 1) * per_a);
   for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
@@ -433,6 +535,13 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
         } else {
           timer[j] = t;
           res[j] = tag_now;
+          if (s.pool_mode && t >= s.evict_min && s.slot_of[base + j] >= 0) {   // (a5) offload
+            pool_push(s, s.slot_of[base + j]);
+            s.slot_of[base + j] = -1;
+            evicted++;
+          }
+          if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)
+            s.pf_list[(long)pf_row * s.max_ctx + atomicAdd(&s.pf_count[pf_row], 1)] = j;
         }
       }
     }
@@ -446,10 +555,13 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
       res[j] = 1;
       timer[j] = 0;
       restored++;
+      if (s.pool_mode && s.slot_of[base + j] < 0) err |= kErrNotResident;
     } else {
       timer[j] = t;
       if (r != 0) res[j] = 0;           // drop the previous step's tag
       if (j >= n - s.window) err |= kErrFrozenInWindow;
+      if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)   // back next step: prefetch it
+        s.pf_list[(long)pf_row * s.max_ctx + atomicAdd(&s.pf_count[pf_row], 1)] = j;
     }
   };
 #pragma unroll
@@ -473,6 +585,36 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     SeqStats& st = s.stats[b];
     if (f) atomicAdd(&st.frozen_this_step, f);
     if (r) atomicAdd(&st.restored_tick, r);
+  }
+  if (s.pool_mode) {
+    for (int o = 16; o > 0; o >>= 1) evicted += __shfl_xor_sync(0xffffffffu, evicted, o);
+    if (lane == 0 && evicted) atomicAdd(&s.stats[b].evicted, evicted);
+  }
+}
+
+// Pressure mode: copy the tokens phase B gave slots to (this step's prefetch list) from the host
+// mirror, one token per block at a time; runs beside the attention kernel (graph branch).
+__device__ void prefetch_copies(const DevState& s, int* start) {
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < s.B; ++b) {
+      start[b] = acc;
+      acc += s.cp_count[b];
+    }
+    start[s.B] = acc;
+  }
+  __syncthreads();
+  const int total = start[s.B];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    int lo = 0, hi = s.B - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const int b = lo;
+    const int j = s.cp_list[(long)b * s.max_ctx + (t - start[b])];
+    copy_token_h2d(s, b, j, s.slot_of[(long)b * s.max_ctx + j]);
   }
 }
 

@@ -52,6 +52,8 @@ class Case:
     host_io: bool = False          # pass host (numpy) buffers through the C ABI
     restore_at: dict = dataclasses.field(default_factory=dict)  # step -> (seq, level) explicit restore
     max_context: int = 0
+    pool_tokens: int = 0           # > 0: pressure mode (device slot pool, eviction / prefetch / demand)
+    evict_min: int = 2
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -75,7 +77,8 @@ def asr_cfg(c: Case):
     return Config(n_layers=c.L, n_q_heads=c.Hq, n_kv_heads=c.Hkv, head_dim=c.d, batch=c.B,
                   max_context=c.capacity(), kv_dtype=KV_BF16 if c.dtype == "bf16" else KV_F32,
                   window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
-                  score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window)
+                  score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window,
+                  pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min)
 
 
 def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:
@@ -113,6 +116,7 @@ def run(c: Case, check_o: bool = True) -> dict:
     ctx = Context(asr_cfg(c), to_t(pk), to_t(pv), P)
     orc = [oracle.OracleSeq(orc_cfg(c), cap, P[b]) for b in range(c.B)]
     worst_o, worst_h, frozen_total, restored_total = 0.0, 0.0, 0, 0
+    evicted_total = prefetched_total = demand_total = 0
     for i in range(c.steps):
         if i in c.restore_at:
             seq, level = c.restore_at[i]
@@ -166,7 +170,32 @@ def run(c: Case, check_o: bool = True) -> dict:
                 worst_o = max(worst_o, err)
             frozen_total += out["frozen_this_step"]
             restored_total += out["restored_this_step"]
+            if c.pool_tokens:
+                assert g["resident"] <= c.pool_tokens, where
+                # every attended token held a device slot (else the device would have latched an error)
+                assert g["resident"] >= g["active"], where
+                evicted_total += g["evicted_this_step"]
+                prefetched_total += g["prefetched_this_step"]
+                demand_total += g["demand_restored_this_step"]
+    # exact restoration ("no permanent information loss"): every stored token's bytes, on the
+    # device (resident tokens, including ones evicted and copied back) and in the host mirror, equal
+    # what was appended
+    for b in range(c.B):
+        n = P[b] + c.steps
+        led = ctx.stats(b, detail=True)["ledger"]
+        for j in range(n):
+            km, vm = ctx.read_kv(b, j, from_mirror=True)
+            np.testing.assert_array_equal(km, KV[b][0][j], err_msg=f"mirror K seq {b} pos {j}")
+            np.testing.assert_array_equal(vm, KV[b][1][j], err_msg=f"mirror V seq {b} pos {j}")
+            try:
+                kd, vd = ctx.read_kv(b, j)
+            except Exception:
+                assert c.pool_tokens and led["residency"][j] == 0, (b, j)   # only frozen tokens may be evicted
+                continue
+            np.testing.assert_array_equal(kd, KV[b][0][j], err_msg=f"device K seq {b} pos {j}")
+            np.testing.assert_array_equal(vd, KV[b][1][j], err_msg=f"device V seq {b} pos {j}")
     summary = {"worst_o": worst_o, "worst_h": worst_h, "frozen": frozen_total, "restored": restored_total,
+               "evicted": evicted_total, "prefetched": prefetched_total, "demand": demand_total,
                "final": [ctx.stats(b) for b in range(c.B)]}
     ctx.close()
     return summary

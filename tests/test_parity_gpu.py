@@ -87,3 +87,27 @@ def test_entropy_spikes_ladder():
 def test_host_memory_io():
     run(Case(L=2, Hq=8, Hkv=2, d=64, B=2, prompt=(50, 64), steps=30, window=8, hot_permille=300,
              vocab=3000, host_io=True, seed=51))
+
+
+# ------------------------------------------------------------------ (a5) pressure mode: real offload
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_pressure_mode_tiny(dtype):
+    # evict every freeze (evict_min=1): frozen tokens leave the device and are prefetched back one step
+    # before they return (early on the sublinear schedule gives 1-2 step absences, so the pool still
+    # needs ~n slots here); results identical to the oracle, bytes restored exactly
+    s = run(Case(prompt=(32,), steps=64, window=8, seed=61, dtype=dtype, pool_tokens=100, evict_min=1))
+    assert s["evicted"] > 0 and s["prefetched"] > 0
+
+
+def test_pressure_mode_llama_heads_and_recovery():
+    # MMA attention path with slot indirection; planted entropy spikes force demand copies (SR/WR/FR)
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=2, prompt=(40, 25), steps=110, window=8, vocab=128256, seed=71,
+             spike_first=50, spike_period=16, spike_count=4, pool_tokens=300, hot_permille=300, a_hot=64)
+    s = run(c)
+    assert s["evicted"] > 0 and s["prefetched"] > 0 and s["demand"] > 0
+
+
+def test_pressure_mode_explicit_restore_and_evict_threshold():
+    s = run(Case(B=2, prompt=(30, 12), steps=70, window=4, seed=81, pool_tokens=200, evict_min=1,
+                 restore_at={40: (-1, 3), 55: (0, 1)}))
+    assert s["evicted"] > 0 and s["demand"] > 0
