@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--nvtx", action="store_true", help="NVTX range 'timed' around the timed steps (for ncu)")
     ap.add_argument("--timeline", action="store_true", help="device timeline of 8 extra steps (ASR_TIMELINE)")
+    ap.add_argument("--pool-frac", type=float, default=0.0,
+                    help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
+    ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
+    ap.add_argument("--points", default="cfg3", help="comma list of extra workloads (POINTS) or '' for none")
     return ap.parse_args()
 
 
@@ -186,9 +190,10 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     e2e_steps = 0 if a.no_e2e else K
     max_ctx = a.context + W + 2 * K + e2e_steps + 16
     g = gen_params(a, rank)
+    pool = int(a.pool_frac * B * a.context) + 4 * B if a.pool_frac > 0 else 0
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=0,
-                 device=local_rank)
+                 device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, HKV, D), dtype=bf, device=dev)
     pv = torch.empty_like(pk)
@@ -245,6 +250,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    io0 = ctx.stats(0)
     if a.nvtx:
         torch.cuda.nvtx.range_push("timed")
     t_wall = time.perf_counter()
@@ -263,6 +269,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     total_ms = sum(step_ms)
     stats = [ctx.stats(b) for b in range(B)]
+    h2d_timed = stats[0]["bytes_h2d"] - io0["bytes_h2d"]    # context-wide counters
+    d2h_timed = stats[0]["bytes_d2h"] - io0["bytes_d2h"]
     launches_timed = 3 * K   # pre, attention, post per step (one CUDA-graph launch)
     # ---- the same K-step workload again with stage events (graph event nodes between the kernels, no
     #      programmatic overlap): per-stage device times and the attention kernel's duration (roofline)
@@ -344,8 +352,11 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     except Exception:
         pass
     value = B * K * world / (total_max / 1000.0)
+    ctx.close()
+    del Q, KN, VN, LG, flush_w, flush_r
+    torch.cuda.empty_cache()
     if rank != 0:
-        return
+        return None
     cpu = None
     if not a.no_cpu_baseline and world == 1:
         r = oracle_sample(a, a.cpu_seconds)
@@ -355,7 +366,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "value": value, "unit": "tok/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}",
+        "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
+                               + (f" pool{a.pool_frac:g}" if pool else ""),
                    "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": 0.5, "k": 2,
                    "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
                    "parallelism": f"sequence-sharded x{world} (no hot-path collective)"},
@@ -368,6 +380,13 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "gpu_launches": launches_timed,
         "cpu_baseline": cpu,
         "clocks": clk,
+        "offload": {"mode": "pressure" if pool else "full residency", "pool_tokens": pool,
+                    "evict_min_absence": a.evict_min if pool else None,
+                    "resident_tokens": sum(s_["resident"] for s_ in stats),
+                    "total_tokens": sum(s_["total"] for s_ in stats),
+                    "h2d_bytes_per_step": h2d_timed / K, "d2h_bytes_per_step": d2h_timed / K,
+                    "host_link_gbs": (h2d_timed + d2h_timed) / (total_max / 1000.0) / 1e9,
+                    "note": "H2D = prefetch + demand copies of evicted tokens; D2H = write-once mirror of appended tokens"},
         "detail": {"attended_per_step": att_last / B, "active_post": stats[0]["active"], "total": stats[0]["total"],
                    "compression": stats[0]["compression"],
                    "stage_ms_per_step_profiled": {n: v / K for n, v in zip(STAGES, stage_ms)},
@@ -377,7 +396,12 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                    "wall_s_timed": t_wall, "grow_s": t_grow,
                    "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES},
     }
-    print(json.dumps(line), flush=True)
+    return line
+
+
+POINTS = {   # extra workloads measured after the headline (BASELINE.json configs[2]: 8K, batch 64)
+    "cfg3": dict(batch=64, steps=16, warmup=4, pool_frac=0.0),
+}
 
 
 def main():
@@ -393,7 +417,23 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    run_asr(a, rank, world, local_rank)
+    line = run_asr(a, rank, world, local_rank)
+    points = {}
+    for name in [x for x in a.points.split(",") if x]:
+        b = argparse.Namespace(**vars(a))
+        for k, v in POINTS[name].items():
+            setattr(b, k, v)
+        b.no_e2e, b.no_cpu_baseline, b.timeline = True, True, False
+        r = run_asr(b, rank, world, local_rank)
+        if r is not None:
+            points[name] = {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
+                            "ms_per_step": r["ms_per_step"], "steps": r["steps"], "warmup": r["warmup"],
+                            "roofline": {k: r["roofline"][k] for k in ("achieved", "peak", "frac", "unit")},
+                            "offload": r["offload"], "clocks": r["clocks"]}
+    if line is not None:
+        if points:
+            line["points"] = points
+        print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -354,44 +354,38 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
   if (w == 0) {
     int level = 0;
     if (has_logits) {
+      // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
       const float* ep = s.ent_part + (long)b * kEntSplits * 3;
-      double pm[kEntSplits / 32], pz[kEntSplits / 32], ps[kEntSplits / 32];
-      double M = -INFINITY;
+      float M = -INFINITY, Zl = 0.f, Sl = 0.f;
 #pragma unroll
       for (int k = 0; k < kEntSplits / 32; ++k) {
         const int sp = k * 32 + lane;
-        pm[k] = ep[sp * 3]; pz[k] = ep[sp * 3 + 1]; ps[k] = ep[sp * 3 + 2];
-        if (pz[k] > 0.0) M = fmax(M, pm[k]);
+        tri_merge(M, Zl, Sl, ep[sp * 3], ep[sp * 3 + 1], ep[sp * 3 + 2]);
       }
-      for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
-      double Zl = 0.0, Sl = 0.0;
-#pragma unroll
-      for (int k = 0; k < kEntSplits / 32; ++k) {
-        if (pz[k] <= 0.0) continue;
-        const double dm = pm[k] - M, f = exp(dm);
-        Zl += pz[k] * f;
-        Sl += f * (ps[k] + pz[k] * dm);
-      }
-      for (int o = 16; o > 0; o >>= 1) {   // fixed-order tree over lanes (deterministic)
-        Zl += __shfl_xor_sync(0xffffffffu, Zl, o);
-        Sl += __shfl_xor_sync(0xffffffffu, Sl, o);
-      }
-      const double H = log(Zl) - Sl / Zl;
+      for (int o = 16; o > 0; o >>= 1)
+        tri_merge(M, Zl, Sl, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Zl, o),
+                  __shfl_xor_sync(0xffffffffu, Sl, o));
+      const float H = logf(Zl) - Sl / Zl;
       DetState& ds = s.det[b];
       double* hist = s.hist + (long)b * s.det_baseline;
       const int hl = ds.hist_len;
-      double mu = 0.0, var = 0.0;
-      for (int t = lane; t < hl; t += 32) mu += hist[t];
+      // detector statistics over the previous <= det_baseline entropies (fp32 is ample: the decision
+      // margin of R-det is >= 0.5 nats on the generator's rows and sigma_floor is 0.05)
+      const float hv0 = lane < hl ? (float)hist[lane] : 0.f;
+      const float hv1 = lane + 32 < hl ? (float)hist[lane + 32] : 0.f;
+      float mu = hv0 + hv1;
+      for (int t = lane + 64; t < hl; t += 32) mu += (float)hist[t];
       for (int o = 16; o > 0; o >>= 1) mu += __shfl_xor_sync(0xffffffffu, mu, o);
-      mu = hl > 0 ? mu / hl : 0.0;
-      for (int t = lane; t < hl; t += 32) var += (hist[t] - mu) * (hist[t] - mu);
+      mu = hl > 0 ? mu / hl : 0.f;
+      float var = (lane < hl ? (hv0 - mu) * (hv0 - mu) : 0.f) + (lane + 32 < hl ? (hv1 - mu) * (hv1 - mu) : 0.f);
+      for (int t = lane + 64; t < hl; t += 32) var += ((float)hist[t] - mu) * ((float)hist[t] - mu);
       for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
       if (lane == 0) {
-        var = hl > 0 ? var / hl : 0.0;
+        var = hl > 0 ? var / hl : 0.f;
         int trig = 0;
         if (s.det_enable && hl >= 2) {
-          const double sd = fmax(sqrt(var), (double)s.det_sigma_floor);
-          trig = H > mu + (double)s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
+          const float sd = fmaxf(sqrtf(var), s.det_sigma_floor);
+          trig = H > mu + s.det_z * sd;   // detector: H > mean + z * max(sigma, floor)
         }
         if (hl < s.det_baseline) {
           hist[hl] = H;
@@ -409,8 +403,8 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
             ds.has_last = 1;
           }
         }
-        if (entropy_out) entropy_out[b] = (float)H;
-        s.stats[b].entropy = (float)H;
+        if (entropy_out) entropy_out[b] = H;
+        s.stats[b].entropy = H;
       }
     }
     if (lane == 0) u.level = level;
