@@ -326,6 +326,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         e0.record(st)
         for t in range(e2e_steps):
             ctx.step(HQs[t], HKs[t], HVs[t], ho, logits_prev=HLs[t], entropy=he)
+        ctx.flush()   # the stream waits for the last step's outputs to land in host memory
         e1.record(st)
         torch.cuda.synchronize()
         e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -335,7 +336,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         d2h = B * (L * HQ * D * 4 + 4)
         e2e = {"value": B * e2e_steps * world / (float(e2e_ms.item()) / 1000.0), "unit": "tok/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region"}
+               "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region "
+                       "(the library overlaps them with neighbouring steps on two copy streams)"}
     # ---- roofline of the dominant kernel (attention + fused score), measured live via stage events
     attn_ms = stage_ms[1]
     # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);

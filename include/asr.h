@@ -85,10 +85,15 @@ typedef struct {
 /* Fills *cfg with the paper's defaults (K=32, tau=0.5, k=2: P:112) and LLaMA-3-8B shape. */
 void asr_config_defaults(asr_config* cfg);
 
-/* Per-step buffers, owned by the CALLER and valid until the stream passes the step.
- * memory = ASR_MEM_DEVICE: device pointers.  ASR_MEM_HOST: host pointers (pinned for
- * asynchrony); the library copies inputs in and o/entropy out on the stream (counted in
- * asr_stats_t.bytes_h2d / bytes_d2h). */
+/* Per-step buffers, owned by the CALLER.
+ * memory = ASR_MEM_DEVICE: device pointers, valid until the caller's stream passes the step; o and
+ *   entropy are complete at that point.
+ * memory = ASR_MEM_HOST: host pointers (pinned for asynchrony).  The library copies the inputs into
+ *   one of two device staging sets on its own copy stream as soon as the step is issued (overlapping
+ *   the previous step's kernels) and copies o / entropy back on a second copy stream while the next
+ *   step computes.  Inputs may be reused once the caller's stream passes the step; outputs are
+ *   complete after asr_flush() has been ordered on a stream and that stream passes it, or after
+ *   asr_stats() / asr_destroy().  Bytes are counted in asr_stats_t.bytes_h2d / bytes_d2h. */
 typedef struct {
   const void* q;           /* [B][L][Hq][d]  kv_dtype: the current query Q_i (Eq. 1-2) */
   const void* k_new;       /* [B][L][Hkv][d] kv_dtype: K of the token appended this step */
@@ -166,6 +171,10 @@ asr_status asr_read_kv(asr_ctx* ctx, int32_t seq, int32_t pos, int32_t from_mirr
  * step's kernels).  With the fused single-kernel step, ms[0..2] are its phases (%globaltimer).
  * *launches = kernel launches of the library in that period.  n >= 4.  Synchronises. */
 asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launches);
+
+/* Make cuda_stream wait (without blocking the host) until the host-memory outputs of every step
+ * issued so far have landed (ASR_MEM_HOST).  No-op otherwise. */
+asr_status asr_flush(asr_ctx* ctx, void* cuda_stream);
 
 /* Switch stage profiling (the events asr_stage_times reads) on or off for the following steps.
  * While it is on, stages are separated by event nodes, so the kernels of one step do not overlap

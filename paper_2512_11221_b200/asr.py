@@ -68,7 +68,7 @@ class asr_ledger_view(ctypes.Structure):
 
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
-           "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_destroy", "asr_last_error")
+           "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error")
 
 _lib = None
 
@@ -92,8 +92,9 @@ def lib() -> ctypes.CDLL:
         L.asr_destroy.argtypes = [vp]
         L.asr_set_profile.argtypes = [vp, i32]
         L.asr_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
+        L.asr_flush.argtypes = [vp, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
-                  "asr_set_profile", "asr_timeline", "asr_destroy"):
+                  "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -240,6 +241,10 @@ def asr_timeline(ctx) -> list:
     return list(us)
 
 
+def asr_flush(ctx, stream=None) -> None:
+    _check(lib().asr_flush(ctx, _stream(stream)))
+
+
 def asr_set_profile(ctx, on: bool) -> None:
     _check(lib().asr_set_profile(ctx, int(bool(on))))
 
@@ -272,6 +277,9 @@ class Context:
 
     def timeline(self):
         return asr_timeline(self._h)
+
+    def flush(self, stream=None):
+        asr_flush(self._h, stream)
 
     def set_profile(self, on: bool):
         asr_set_profile(self._h, on)

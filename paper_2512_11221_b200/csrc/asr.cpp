@@ -51,14 +51,22 @@ struct asr_ctx {
   cudaStream_t side = nullptr;   // mirror copies
   cudaEvent_t ev_append = nullptr, ev_mirror = nullptr;
   cudaStream_t last_stream = nullptr;
-  // ASR_MEM_HOST staging
-  void* st_q = nullptr;
-  void* st_k = nullptr;
-  void* st_v = nullptr;
-  void* st_logits = nullptr;
-  size_t st_logits_bytes = 0;
-  float* st_o = nullptr;
-  float* st_ent = nullptr;
+  // ASR_MEM_HOST: double-buffered device staging; inputs arrive on io_in while the previous step
+  // computes, outputs leave on io_out while the next step computes
+  struct Staging {
+    void* q = nullptr;
+    void* k = nullptr;
+    void* v = nullptr;
+    void* logits = nullptr;
+    size_t logits_bytes = 0;
+    float* o = nullptr;
+    float* ent = nullptr;
+    cudaEvent_t in_done = nullptr, graph_done = nullptr, out_done = nullptr;
+    bool used = false;
+  };
+  Staging stg[2];
+  cudaStream_t io_in = nullptr, io_out = nullptr;
+  cudaEvent_t last_out = nullptr;
   int64_t bytes_h2d = 0, bytes_d2h = 0;
   int64_t launches = 0;
   // CUDA graph of one step, per variant (with / without the entropy stage)
@@ -70,7 +78,7 @@ struct asr_ctx {
     std::vector<asr::KNode> last;
     std::vector<cudaGraphNode_t> evnodes;
   };
-  StepGraph graphs[2];
+  StepGraph graphs[6];  // [has_logits][device io | host io staging set 0 | 1]
   bool use_graph = true;
   bool use_pdl = true;
   bool use_mega = false;        // persistent single-kernel step
@@ -90,6 +98,11 @@ struct asr_ctx {
     for (void* p : allocs) cudaFree(p);
     if (host_mirror) cudaFreeHost(host_mirror);
     if (side) cudaStreamDestroy(side);
+    if (io_in) cudaStreamDestroy(io_in);
+    if (io_out) cudaStreamDestroy(io_out);
+    for (auto& x : stg)
+      for (cudaEvent_t e : {x.in_done, x.graph_done, x.out_done})
+        if (e) cudaEventDestroy(e);
     if (ev_append) cudaEventDestroy(ev_append);
     if (ev_mirror) cudaEventDestroy(ev_mirror);
     for (auto& a : prof_pending)
@@ -386,20 +399,27 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
   return ASR_OK;
 }
 
-static asr_status ensure_staging(asr_ctx* c, bool logits, int logits_dtype) {
+static asr_status ensure_staging(asr_ctx* c, asr_ctx::Staging& S, bool logits, int logits_dtype) {
   const DevState& s = c->s;
-  if (!c->st_q) {
-    CUDA_TRY(c->alloc(&c->st_q, (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem));
-    CUDA_TRY(c->alloc(&c->st_k, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
-    CUDA_TRY(c->alloc(&c->st_v, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
-    CUDA_TRY(c->alloc(&c->st_o, (size_t)s.B * s.L * s.Hq * s.d * 4));
-    CUDA_TRY(c->alloc(&c->st_ent, (size_t)s.B * 4));
+  if (!S.q) {
+    CUDA_TRY(c->alloc(&S.q, (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&S.k, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&S.v, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
+    CUDA_TRY(c->alloc(&S.o, (size_t)s.B * s.L * s.Hq * s.d * 4));
+    CUDA_TRY(c->alloc(&S.ent, (size_t)s.B * 4));
+    CUDA_TRY(cudaEventCreateWithFlags(&S.in_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&S.graph_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&S.out_done, cudaEventDisableTiming));
+  }
+  if (!c->io_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->io_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking));
   }
   if (logits) {
     size_t need = (size_t)s.B * s.vocab * (logits_dtype == ASR_KV_BF16 ? 2 : 4);
-    if (need > c->st_logits_bytes) {
-      CUDA_TRY(c->alloc(&c->st_logits, need));
-      c->st_logits_bytes = need;
+    if (need > S.logits_bytes) {
+      CUDA_TRY(c->alloc(&S.logits, need));
+      S.logits_bytes = need;
     }
   }
   return ASR_OK;
@@ -429,26 +449,35 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   const void* lg = io->logits_prev;
   float* o = io->o;
   float* ent = io->entropy;
-  if (io->memory == ASR_MEM_HOST) {
-    asr_status r = ensure_staging(c, has_logits, io->logits_dtype);
+  const bool host_io = io->memory == ASR_MEM_HOST;
+  asr_ctx::Staging& S = c->stg[c->step & 1];
+  if (host_io) {
+    asr_status r = ensure_staging(c, S, has_logits, io->logits_dtype);
     if (r) return r;
+    // inputs: copied on io_in as soon as the step is issued (overlapping the previous step's kernels),
+    // once the graph that last read this staging set is done
+    if (S.used) CUDA_TRY(cudaStreamWaitEvent(c->io_in, S.graph_done, 0));
     const size_t qb = (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem;
     const size_t kb = (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem;
-    CUDA_TRY(cudaMemcpyAsync(c->st_q, q, qb, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(c->st_k, kn, kb, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(c->st_v, vn, kb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(S.q, q, qb, cudaMemcpyHostToDevice, c->io_in));
+    CUDA_TRY(cudaMemcpyAsync(S.k, kn, kb, cudaMemcpyHostToDevice, c->io_in));
+    CUDA_TRY(cudaMemcpyAsync(S.v, vn, kb, cudaMemcpyHostToDevice, c->io_in));
     c->bytes_h2d += (int64_t)(qb + 2 * kb);
     if (has_logits) {
       const size_t lb = (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
-      CUDA_TRY(cudaMemcpyAsync(c->st_logits, lg, lb, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(S.logits, lg, lb, cudaMemcpyHostToDevice, c->io_in));
       c->bytes_h2d += (int64_t)lb;
-      lg = c->st_logits;
+      lg = S.logits;
     }
-    q = c->st_q;
-    kn = c->st_k;
-    vn = c->st_v;
-    o = c->st_o;
-    ent = ent ? c->st_ent : nullptr;
+    CUDA_TRY(cudaEventRecord(S.in_done, c->io_in));
+    CUDA_TRY(cudaStreamWaitEvent(st, S.in_done, 0));
+    // the outputs this staging set held two steps ago must have left before the kernels overwrite them
+    if (S.used) CUDA_TRY(cudaStreamWaitEvent(st, S.out_done, 0));
+    q = S.q;
+    kn = S.k;
+    vn = S.v;
+    o = S.o;
+    ent = ent ? S.ent : nullptr;
   }
   std::array<cudaEvent_t, asr::kStages + 1>* ev = nullptr;
   if (c->cfg.profile_stages) {
@@ -500,7 +529,7 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     }
     CUDA_TRY(prof_mark(c, ev, asr::kStages, st));
   } else {
-    asr_ctx::StepGraph& G = c->graphs[has_logits ? 1 : 0];
+    asr_ctx::StepGraph& G = c->graphs[(has_logits ? 3 : 0) + (host_io ? 1 + (int)(c->step & 1) : 0)];
     if (G.x && G.profiled != prof) {
       cudaGraphExecDestroy(G.x);
       cudaGraphDestroy(G.g);
@@ -584,14 +613,19 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     }
     c->bytes_d2h += (int64_t)s.B * c->tok_bytes;
   }
-  if (io->memory == ASR_MEM_HOST) {
+  if (host_io) {   // outputs leave on io_out while the next step computes (asr_flush / asr_stats)
+    CUDA_TRY(cudaEventRecord(S.graph_done, st));
+    CUDA_TRY(cudaStreamWaitEvent(c->io_out, S.graph_done, 0));
     const size_t ob = (size_t)s.B * s.L * s.Hq * s.d * 4;
-    CUDA_TRY(cudaMemcpyAsync(io->o, o, ob, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(io->o, o, ob, cudaMemcpyDeviceToHost, c->io_out));
     c->bytes_d2h += (int64_t)ob;
     if (io->entropy && has_logits) {
-      CUDA_TRY(cudaMemcpyAsync(io->entropy, ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(io->entropy, ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, c->io_out));
       c->bytes_d2h += (int64_t)s.B * 4;
     }
+    CUDA_TRY(cudaEventRecord(S.out_done, c->io_out));
+    c->last_out = S.out_done;
+    S.used = true;
   }
   c->step++;
   c->last_stream = st;
@@ -618,6 +652,7 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   CUDA_TRY(cudaStreamSynchronize(c->side));
+  if (c->io_out) CUDA_TRY(cudaStreamSynchronize(c->io_out));
   const DevState& s = c->s;
   asr::SeqStats st;
   uint32_t err = 0;
@@ -753,11 +788,20 @@ asr_status asr_set_profile(asr_ctx* c, int32_t on) {
   return ASR_OK;
 }
 
+asr_status asr_flush(asr_ctx* c, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  if (c->last_out) CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)cuda_stream, c->last_out, 0));
+  return ASR_OK;
+}
+
 asr_status asr_destroy(asr_ctx* c) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
   cudaSetDevice(c->cfg.device);
   cudaStreamSynchronize(c->last_stream);
   cudaStreamSynchronize(c->side);
+  if (c->io_in) cudaStreamSynchronize(c->io_in);
+  if (c->io_out) cudaStreamSynchronize(c->io_out);
   delete c;
   return ASR_OK;
 }
