@@ -80,6 +80,11 @@ typedef struct {
                            * tokens are evicted to the pinned host mirror and prefetched back one step
                            * before their timer expires; entropy-triggered / explicit restores of
                            * evicted tokens are copied back on demand.  Needs host_mirror = 1. */
+  int32_t score_heads;    /* head-sharded mode: H of Eq. 2's 1/H over ALL shards (the context holds only
+                           * n_q_heads of them); 0 = n_q_heads (unsharded).  The per-token partial sums
+                           * must then be summed across shards between asr_step_attend and
+                           * asr_step_decide (asr_attach_nccl does it inside asr_step). */
+  int32_t reserved1;
 } asr_config;
 
 /* Fills *cfg with the paper's defaults (K=32, tau=0.5, k=2: P:112) and LLaMA-3-8B shape. */
@@ -151,6 +156,23 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
 /* One generation step for every sequence (asynchronous on cuda_stream, no host sync).
  * ASR_E_CAPACITY if any sequence is full (nothing is changed). */
 asr_status asr_step(asr_ctx* ctx, const asr_step_io* io, void* cuda_stream);
+
+/* The two halves of asr_step, for head-sharded contexts (score_heads > n_q_heads):
+ * asr_step_attend runs append, entropy/recovery, compaction, attention + score and leaves this
+ * shard's per-token partial score sums (over its heads and all layers) in a device buffer;
+ * asr_step_decide runs combine + decide + tick reading the (summed) buffer.  Every shard must see the
+ * same inputs except q / k_new / v_new, which hold its own heads; their ledgers stay identical. */
+asr_status asr_step_attend(asr_ctx* ctx, const asr_step_io* io, void* cuda_stream);
+asr_status asr_step_decide(asr_ctx* ctx, void* cuda_stream);
+/* Device buffer of per-token partial score sums: [batch][row] fp32, row >= max_context (entries past
+ * |A_b| are unused); sum it element-wise across shards (e.g. an NCCL all-reduce). */
+asr_status asr_score_partials(asr_ctx* ctx, float** dev_ptr, int64_t* count);
+/* Head-sharded mode over NCCL (NVLink/NVSwitch): rank 0 creates an id (128 bytes), every rank
+ * passes it to asr_attach_nccl (collective; one GPU per rank); from then on asr_step runs attend,
+ * an in-place ncclAllReduce (sum) of the per-token partial sums on the step's stream, and decide.
+ * Needs libnccl.so.2 in the process (loaded with dlopen). */
+asr_status asr_nccl_unique_id(void* out, int32_t n);
+asr_status asr_attach_nccl(asr_ctx* ctx, const void* unique_id, int32_t nranks, int32_t rank);
 
 /* Explicit recovery at the boundary before the next step: SR restores frozen tokens with
  * d > 1, WR those frozen in the last wr_window steps, FR all.  seq = -1 applies to all. */

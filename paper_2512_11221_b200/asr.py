@@ -41,7 +41,8 @@ class asr_config(ctypes.Structure):
                 ("det_baseline", ctypes.c_int32), ("det_cooldown", ctypes.c_int32), ("wr_window", ctypes.c_int32),
                 ("det_z", ctypes.c_float), ("det_sigma_floor", ctypes.c_float), ("fr_clear_counts", ctypes.c_int32),
                 ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("evict_min_absence", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("pool_tokens", ctypes.c_int64)]
+                ("evict_min_absence", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("pool_tokens", ctypes.c_int64),
+                ("score_heads", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class asr_step_io(ctypes.Structure):
@@ -68,7 +69,8 @@ class asr_ledger_view(ctypes.Structure):
 
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
-           "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error")
+           "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
+           "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl")
 
 _lib = None
 
@@ -93,8 +95,14 @@ def lib() -> ctypes.CDLL:
         L.asr_set_profile.argtypes = [vp, i32]
         L.asr_timeline.argtypes = [vp, ctypes.POINTER(ctypes.c_double), i32]
         L.asr_flush.argtypes = [vp, vp]
+        L.asr_step_attend.argtypes = [vp, ctypes.POINTER(asr_step_io), vp]
+        L.asr_step_decide.argtypes = [vp, vp]
+        L.asr_score_partials.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64)]
+        L.asr_nccl_unique_id.argtypes = [vp, i32]
+        L.asr_attach_nccl.argtypes = [vp, vp, i32, i32]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
-                  "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy"):
+                  "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
+                  "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -139,6 +147,8 @@ class Config:
     evict_min_absence: int = 2
     reserved0: int = 0
     pool_tokens: int = 0             # 0 = full residency; > 0 = pressure mode (device slot pool)
+    score_heads: int = 0             # head-sharded mode: H of Eq. 2 over all shards (0 = n_q_heads)
+    reserved1: int = 0
 
     def c(self) -> asr_config:
         v = dataclasses.asdict(self)
@@ -192,6 +202,39 @@ def asr_step(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=Non
                      _dtype_code(logits_prev) if logits_prev is not None else 0,
                      MEM_HOST if _is_host(q) else MEM_DEVICE, _ptr(o), _ptr(entropy))
     _check(lib().asr_step(ctx, ctypes.byref(io), _stream(stream)))
+
+
+def _io(q, k_new, v_new, o, logits_prev, entropy):
+    return asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
+                       _dtype_code(logits_prev) if logits_prev is not None else 0,
+                       MEM_HOST if _is_host(q) else MEM_DEVICE, _ptr(o), _ptr(entropy))
+
+
+def asr_step_attend(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None) -> None:
+    io = _io(q, k_new, v_new, o, logits_prev, entropy)
+    _check(lib().asr_step_attend(ctx, ctypes.byref(io), _stream(stream)))
+
+
+def asr_step_decide(ctx, stream=None) -> None:
+    _check(lib().asr_step_decide(ctx, _stream(stream)))
+
+
+def asr_score_partials(ctx):
+    """(device pointer, element count) of the per-token partial score sums of a head shard."""
+    p, n = ctypes.c_void_p(), ctypes.c_int64()
+    _check(lib().asr_score_partials(ctx, ctypes.byref(p), ctypes.byref(n)))
+    return p.value, n.value
+
+
+def asr_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_char * 128)()
+    _check(lib().asr_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def asr_attach_nccl(ctx, unique_id: bytes, nranks: int, rank: int) -> None:
+    buf = (ctypes.c_char * 128).from_buffer_copy(unique_id)
+    _check(lib().asr_attach_nccl(ctx, buf, nranks, rank))
 
 
 def asr_restore(ctx, seq: int, level: int, stream=None) -> None:
@@ -262,6 +305,18 @@ class Context:
 
     def step(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None):
         asr_step(self._h, q, k_new, v_new, o, logits_prev, entropy, stream)
+
+    def attend(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None):
+        asr_step_attend(self._h, q, k_new, v_new, o, logits_prev, entropy, stream)
+
+    def decide(self, stream=None):
+        asr_step_decide(self._h, stream)
+
+    def score_partials(self):
+        return asr_score_partials(self._h)
+
+    def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        asr_attach_nccl(self._h, unique_id, nranks, rank)
 
     def restore(self, seq: int, level: int, stream=None):
         asr_restore(self._h, seq, level, stream)

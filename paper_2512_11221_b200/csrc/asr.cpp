@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <array>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -78,7 +79,11 @@ struct asr_ctx {
     std::vector<asr::KNode> last;
     std::vector<cudaGraphNode_t> evnodes;
   };
-  StepGraph graphs[6];  // [has_logits][device io | host io staging set 0 | 1]
+  StepGraph graphs[18];  // [has_logits][device io | host io set 0 | 1][full | attend | decide]
+  bool attend_pending = false;
+  std::unique_ptr<struct StepArgsBox> pending;
+  asr::NcclApi nccl;
+  void* nccl_comm = nullptr;
   bool use_graph = true;
   bool use_pdl = true;
   bool use_mega = false;        // persistent single-kernel step
@@ -90,7 +95,10 @@ struct asr_ctx {
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_free;
   std::vector<void*> allocs;
 
-  ~asr_ctx() {
+  ~asr_ctx();
+  void release() {
+    if (nccl_comm && nccl.comm_destroy) nccl.comm_destroy(nccl_comm);
+    nccl_comm = nullptr;
     for (auto& g : graphs) {
       if (g.x) cudaGraphExecDestroy(g.x);
       if (g.g) cudaGraphDestroy(g.g);
@@ -122,6 +130,8 @@ struct asr_ctx {
     return e;
   }
 };
+
+struct StepArgsBox;   // defined below (holds a StepArgs between asr_step_attend and asr_step_decide)
 
 extern "C" {
 
@@ -158,6 +168,8 @@ void asr_config_defaults(asr_config* c) {
   c->evict_min_absence = 2;
   c->reserved0 = 0;
   c->pool_tokens = 0;
+  c->score_heads = 0;
+  c->reserved1 = 0;
 }
 
 static asr_status validate(const asr_config* c) {
@@ -189,6 +201,8 @@ static asr_status validate(const asr_config* c) {
   if (c->pool_tokens < 0) return fail(ASR_E_INVALID, "pool_tokens < 0");
   if (c->pool_tokens > 0 && !c->host_mirror) return fail(ASR_E_INVALID, "pool_tokens > 0 needs host_mirror = 1");
   if (c->pool_tokens > ((int64_t)1 << 31) - 1) return fail(ASR_E_INVALID, "pool_tokens too large");
+  if (c->score_heads != 0 && c->score_heads < c->n_q_heads)
+    return fail(ASR_E_INVALID, "score_heads must be 0 or >= n_q_heads (the heads of all shards)");
   return ASR_OK;
 }
 
@@ -269,6 +283,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     const size_t slots = s.pool_mode ? (size_t)cfg->pool_tokens : BT;
     CUDA_TRY(c->alloc(&s.kv, slots * c->tok_bytes));
     CUDA_TRY(c->alloc(&s.act_slot, BT * 4));
+    s.score_heads = cfg->score_heads > 0 ? cfg->score_heads : s.Hq;
+    s.sharded = s.score_heads != s.Hq ? 1 : 0;
+    CUDA_TRY(c->alloc(&s.tok_score, BT * 4));
+    CUDA_TRY(cudaMemsetAsync(s.tok_score, 0, BT * 4, st));
     std::vector<size_t> slot0(s.B, 0);   // first slot of each sequence's prompt
     for (int b = 0; b < s.B; ++b) slot0[b] = s.pool_mode ? (b ? slot0[b - 1] + prompt_len[b - 1] : 0) : (size_t)b * s.max_ctx;
     if (s.pool_mode) {
@@ -430,155 +448,212 @@ static cudaError_t prof_mark(asr_ctx* c, std::array<cudaEvent_t, asr::kStages + 
   return cudaEventRecord((*ev)[k], st);
 }
 
-asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
-  if (!c) return fail(ASR_E_STATE, "context is NULL");
+// ---------------------------------------------------------------------------------------- one step
+// A step is prepared (inputs staged, profiling events), launched in one or two parts (the full step,
+// or attend + decide around the head-sharded all-reduce), then finished (mirror, outputs, counters).
+enum Part { kPartFull = 0, kPartAttend = 1, kPartDecide = 2 };
+
+struct StepArgs {
+  bool has_logits = false, host_io = false;
+  int logits_dtype = 0;
+  const void *q = nullptr, *kn = nullptr, *vn = nullptr, *lg = nullptr;
+  float *o = nullptr, *ent = nullptr;           // device outputs (staging in host-io mode)
+  float *o_user = nullptr, *ent_user = nullptr;  // caller's outputs
+  std::array<cudaEvent_t, asr::kStages + 1>* ev = nullptr;
+  bool ev_done[asr::kStages + 1] = {false, false, false, false};
+  DevState sd{};
+};
+
+struct StepArgsBox {
+  StepArgs a;
+};
+asr_ctx::~asr_ctx() { release(); }
+
+static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t st, StepArgs& a) {
   if (!io || !io->q || !io->k_new || !io->v_new || !io->o) return fail(ASR_E_INVALID, "io has NULL q/k_new/v_new/o");
   if (io->memory != ASR_MEM_DEVICE && io->memory != ASR_MEM_HOST) return fail(ASR_E_INVALID, "io->memory");
   const DevState& s = c->s;
-  const bool has_logits = io->logits_prev != nullptr && s.vocab > 0;
-  if (has_logits && io->logits_dtype != ASR_KV_BF16 && io->logits_dtype != ASR_KV_F32)
+  a.has_logits = io->logits_prev != nullptr && s.vocab > 0;
+  a.logits_dtype = io->logits_dtype;
+  if (a.has_logits && io->logits_dtype != ASR_KV_BF16 && io->logits_dtype != ASR_KV_F32)
     return fail(ASR_E_INVALID, "logits_dtype");
   for (int b = 0; b < s.B; ++b)
     if (c->prompt_len[b] + c->step + 1 > c->cfg.max_context)
       return fail(ASR_E_CAPACITY, "sequence " + std::to_string(b) + " is at max_context");
-  cudaStream_t st = (cudaStream_t)cuda_stream;
   CUDA_TRY(cudaSetDevice(c->cfg.device));
-  const void* q = io->q;
-  const void* kn = io->k_new;
-  const void* vn = io->v_new;
-  const void* lg = io->logits_prev;
-  float* o = io->o;
-  float* ent = io->entropy;
-  const bool host_io = io->memory == ASR_MEM_HOST;
+  a.q = io->q;
+  a.kn = io->k_new;
+  a.vn = io->v_new;
+  a.lg = io->logits_prev;
+  a.o = a.o_user = io->o;
+  a.ent = a.ent_user = io->entropy;
+  a.host_io = io->memory == ASR_MEM_HOST;
   asr_ctx::Staging& S = c->stg[c->step & 1];
-  if (host_io) {
-    asr_status r = ensure_staging(c, S, has_logits, io->logits_dtype);
+  if (a.host_io) {
+    asr_status r = ensure_staging(c, S, a.has_logits, io->logits_dtype);
     if (r) return r;
     // inputs: copied on io_in as soon as the step is issued (overlapping the previous step's kernels),
     // once the graph that last read this staging set is done
     if (S.used) CUDA_TRY(cudaStreamWaitEvent(c->io_in, S.graph_done, 0));
     const size_t qb = (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem;
     const size_t kb = (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem;
-    CUDA_TRY(cudaMemcpyAsync(S.q, q, qb, cudaMemcpyHostToDevice, c->io_in));
-    CUDA_TRY(cudaMemcpyAsync(S.k, kn, kb, cudaMemcpyHostToDevice, c->io_in));
-    CUDA_TRY(cudaMemcpyAsync(S.v, vn, kb, cudaMemcpyHostToDevice, c->io_in));
+    CUDA_TRY(cudaMemcpyAsync(S.q, a.q, qb, cudaMemcpyHostToDevice, c->io_in));
+    CUDA_TRY(cudaMemcpyAsync(S.k, a.kn, kb, cudaMemcpyHostToDevice, c->io_in));
+    CUDA_TRY(cudaMemcpyAsync(S.v, a.vn, kb, cudaMemcpyHostToDevice, c->io_in));
     c->bytes_h2d += (int64_t)(qb + 2 * kb);
-    if (has_logits) {
+    if (a.has_logits) {
       const size_t lb = (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
-      CUDA_TRY(cudaMemcpyAsync(S.logits, lg, lb, cudaMemcpyHostToDevice, c->io_in));
+      CUDA_TRY(cudaMemcpyAsync(S.logits, a.lg, lb, cudaMemcpyHostToDevice, c->io_in));
       c->bytes_h2d += (int64_t)lb;
-      lg = S.logits;
+      a.lg = S.logits;
     }
     CUDA_TRY(cudaEventRecord(S.in_done, c->io_in));
     CUDA_TRY(cudaStreamWaitEvent(st, S.in_done, 0));
     // the outputs this staging set held two steps ago must have left before the kernels overwrite them
     if (S.used) CUDA_TRY(cudaStreamWaitEvent(st, S.out_done, 0));
-    q = S.q;
-    kn = S.k;
-    vn = S.v;
-    o = S.o;
-    ent = ent ? S.ent : nullptr;
+    a.q = S.q;
+    a.kn = S.k;
+    a.vn = S.v;
+    a.o = S.o;
+    a.ent = a.ent ? S.ent : nullptr;
   }
-  std::array<cudaEvent_t, asr::kStages + 1>* ev = nullptr;
   if (c->cfg.profile_stages) {
     if (c->prof_free.empty()) {
-      std::array<cudaEvent_t, asr::kStages + 1> a;
-      for (auto& e : a) CUDA_TRY(cudaEventCreate(&e));
-      c->prof_free.push_back(a);
+      std::array<cudaEvent_t, asr::kStages + 1> e;
+      for (auto& x : e) CUDA_TRY(cudaEventCreate(&x));
+      c->prof_free.push_back(e);
     }
     c->prof_pending.push_back(c->prof_free.back());
     c->prof_free.pop_back();
-    ev = &c->prof_pending.back();
+    a.ev = &c->prof_pending.back();
   }
-  const bool prof = ev != nullptr;
-  DevState sd = s;   // the step's view: timeline stamps when profiling the fused kernel or on request
-  if (c->timeline_on || (prof && c->use_mega)) sd.tl = c->tl_buf;
-  if (sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0
+  a.sd = s;   // the step's view: timeline stamps when profiling the fused kernel or on request
+  if (c->timeline_on || (a.ev && c->use_mega)) a.sd.tl = c->tl_buf;
+  if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0
     unsigned long long init[2 * asr::kStages];
     for (int k = 0; k < asr::kStages; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
-    CUDA_TRY(cudaMemcpyAsync(sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(a.sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
-  // the step as kernel descriptions with their stage (0 ledger pre, 1 attention, 2 decide/combine)
-  asr::KNode kn_list[5];
-  int stage_of[5];
+  return ASR_OK;
+}
+
+static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st) {
+  const DevState& s = c->s;
+  const DevState& sd = a.sd;
+  const bool prof = a.ev != nullptr;
+  // the part's kernels with their stage (0 ledger pre, 1 attention, 2 decide/combine)
+  asr::KNode kn_list[6];
+  int stage_of[6];
   int nk = 0;
-  const void* lgp = has_logits ? lg : nullptr;
+  const void* lgp = a.has_logits ? a.lg : nullptr;
   if (c->use_mega) {
-    asr::node_step(kn_list[nk], sd, lgp, io->logits_dtype, has_logits ? ent : nullptr, kn, vn, q, o, c->mega_grid);
+    asr::node_step(kn_list[nk], sd, lgp, a.logits_dtype, a.has_logits ? a.ent : nullptr, a.kn, a.vn, a.q, a.o,
+                   c->mega_grid);
     stage_of[nk++] = 0;
   } else {
-    asr::node_phaseA(kn_list[nk], sd, lgp, io->logits_dtype, kn, vn);
-    stage_of[nk++] = 0;
-    asr::node_phaseB(kn_list[nk], sd, has_logits ? 1 : 0, has_logits ? ent : nullptr);
-    stage_of[nk++] = 0;
-    if (s.pool_mode) {   // prefetch copies: a branch beside the attention kernel
-      asr::node_copy(kn_list[nk], sd, 32);
-      kn_list[nk].branch = true;
+    if (part != kPartDecide) {
+      asr::node_phaseA(kn_list[nk], sd, lgp, a.logits_dtype, a.kn, a.vn);
+      stage_of[nk++] = 0;
+      asr::node_phaseB(kn_list[nk], sd, a.has_logits ? 1 : 0, a.has_logits ? a.ent : nullptr);
+      stage_of[nk++] = 0;
+      if (s.pool_mode) {   // prefetch copies: a branch beside the attention kernel
+        asr::node_copy(kn_list[nk], sd, 32);
+        kn_list[nk].branch = true;
+        stage_of[nk++] = 1;
+      }
+      asr::node_attention(kn_list[nk], sd, a.q, c->attn_grid);
       stage_of[nk++] = 1;
+      if (s.sharded) {
+        asr::node_scoresum(kn_list[nk], sd);
+        stage_of[nk++] = 2;
+      }
     }
-    asr::node_attention(kn_list[nk], sd, q, c->attn_grid);
-    stage_of[nk++] = 1;
-    asr::node_phaseD(kn_list[nk], sd, o);
-    stage_of[nk++] = 2;
+    if (part != kPartAttend) {
+      asr::node_phaseD(kn_list[nk], sd, a.o);
+      stage_of[nk++] = 2;
+    }
   }
+  const bool last_part = part != kPartAttend;
+  auto record = [&](int k) -> cudaError_t {   // event k once per step
+    if (!prof || a.ev_done[k]) return cudaSuccess;
+    a.ev_done[k] = true;
+    return cudaEventRecord((*a.ev)[k], st);
+  };
   if (!c->use_graph) {
-    int k = 0;
-    for (int stg = 0; stg < asr::kStages; ++stg) {
-      CUDA_TRY(prof_mark(c, ev, stg, st));
-      while (k < nk && stage_of[k] == stg) CUDA_TRY(kn_list[k++].launch(st));
+    for (int k = 0; k < nk; ++k) {
+      for (int e = 0; e <= stage_of[k]; ++e) CUDA_TRY(record(e));
+      CUDA_TRY(kn_list[k].launch(st));
     }
-    CUDA_TRY(prof_mark(c, ev, asr::kStages, st));
+    if (last_part)
+      for (int e = 0; e <= asr::kStages; ++e) CUDA_TRY(record(e));
   } else {
-    asr_ctx::StepGraph& G = c->graphs[(has_logits ? 3 : 0) + (host_io ? 1 + (int)(c->step & 1) : 0)];
+    const int variant = (a.has_logits ? 9 : 0) + (a.host_io ? 3 * (1 + (int)(c->step & 1)) : 0) + part;
+    asr_ctx::StepGraph& G = c->graphs[variant];
     if (G.x && G.profiled != prof) {
       cudaGraphExecDestroy(G.x);
       cudaGraphDestroy(G.g);
       G = asr_ctx::StepGraph();
     }
+    // the events this part records (stage boundaries it crosses)
+    std::vector<int> evs;
+    if (prof) {
+      bool done[asr::kStages + 1];
+      for (int e = 0; e <= asr::kStages; ++e) done[e] = a.ev_done[e];
+      for (int k = 0; k < nk; ++k)
+        for (int e = 0; e <= stage_of[k]; ++e)
+          if (!done[e]) { evs.push_back(e); done[e] = true; }
+      if (last_part)
+        for (int e = 0; e <= asr::kStages; ++e)
+          if (!done[e]) { evs.push_back(e); done[e] = true; }
+    }
     if (!G.x) {
       CUDA_TRY(cudaGraphCreate(&G.g, 0));
       G.profiled = prof;
       cudaGraphNode_t prev = nullptr;
-      int k = 0;
-      for (int stg = 0; stg <= asr::kStages; ++stg) {
-        if (prof) {
+      size_t ei = 0;
+      auto add_events_upto = [&](int stage) -> asr_status {   // event nodes for boundaries <= stage
+        while (ei < evs.size() && evs[ei] <= stage) {
           cudaGraphNode_t e;
-          CUDA_TRY(cudaGraphAddEventRecordNode(&e, G.g, prev ? &prev : nullptr, prev ? 1 : 0, (*ev)[stg]));
+          CUDA_TRY(cudaGraphAddEventRecordNode(&e, G.g, prev ? &prev : nullptr, prev ? 1 : 0, (*a.ev)[evs[ei]]));
           G.evnodes.push_back(e);
           prev = e;
+          ++ei;
         }
-        while (stg < asr::kStages && k < nk && stage_of[k] == stg) {
-          cudaGraphNode_t kn_node;
-          if (kn_list[k].branch) {   // parallel branch: depends on the previous kernel, nothing waits on it
-            CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, prev ? &prev : nullptr, prev ? 1 : 0, &kn_list[k].p));
-            G.knodes.push_back(kn_node);
-            G.last.push_back(kn_list[k]);
-            ++k;
-            continue;
-          }
-          const bool pdl = c->use_pdl && !prof && prev != nullptr;
-          CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
-                                          &kn_list[k].p));
-          if (kn_list[k].cooperative) {
-            cudaKernelNodeAttrValue v{};
-            v.cooperative = 1;
-            CUDA_TRY(cudaGraphKernelNodeSetAttribute(kn_node, cudaLaunchAttributeCooperative, &v));
-          }
-          if (pdl) {
-            // programmatic edge: the kernel may launch before its upstream completes; it calls
-            // griddepcontrol.wait before reading the upstream's results
-            cudaGraphEdgeData ed{};
-            ed.from_port = cudaGraphKernelNodePortProgrammatic;
-            ed.to_port = 0;
-            ed.type = cudaGraphDependencyTypeProgrammatic;
-            CUDA_TRY(cudaGraphAddDependencies_v2(G.g, &prev, &kn_node, &ed, 1));
-          }
+        return ASR_OK;
+      };
+      for (int k = 0; k < nk; ++k) {
+        asr_status r = add_events_upto(stage_of[k]);
+        if (r) return r;
+        cudaGraphNode_t kn_node;
+        if (kn_list[k].branch) {   // parallel branch: depends on the previous kernel, nothing waits on it
+          CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, prev ? &prev : nullptr, prev ? 1 : 0, &kn_list[k].p));
           G.knodes.push_back(kn_node);
           G.last.push_back(kn_list[k]);
-          prev = kn_node;
-          ++k;
+          continue;
         }
+        const bool pdl = c->use_pdl && !prof && prev != nullptr;
+        CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
+                                        &kn_list[k].p));
+        if (kn_list[k].cooperative) {
+          cudaKernelNodeAttrValue v{};
+          v.cooperative = 1;
+          CUDA_TRY(cudaGraphKernelNodeSetAttribute(kn_node, cudaLaunchAttributeCooperative, &v));
+        }
+        if (pdl) {
+          // programmatic edge: the kernel may launch before its upstream completes; it calls
+          // griddepcontrol.wait before reading the upstream's results
+          cudaGraphEdgeData ed{};
+          ed.from_port = cudaGraphKernelNodePortProgrammatic;
+          ed.to_port = 0;
+          ed.type = cudaGraphDependencyTypeProgrammatic;
+          CUDA_TRY(cudaGraphAddDependencies_v2(G.g, &prev, &kn_node, &ed, 1));
+        }
+        G.knodes.push_back(kn_node);
+        G.last.push_back(kn_list[k]);
+        prev = kn_node;
       }
+      asr_status r = add_events_upto(asr::kStages);
+      if (r) return r;
       CUDA_TRY(cudaGraphInstantiate(&G.x, G.g, 0));
     } else {
       for (int k = 0; k < nk; ++k) {
@@ -587,12 +662,18 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
           memcpy(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra));
         }
       }
-      if (prof)
-        for (int e = 0; e <= asr::kStages; ++e) CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.x, G.evnodes[e], (*ev)[e]));
+      for (size_t e = 0; e < evs.size(); ++e)
+        CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.x, G.evnodes[e], (*a.ev)[evs[e]]));
     }
+    for (int e : evs) a.ev_done[e] = true;
     CUDA_TRY(cudaGraphLaunch(G.x, st));
   }
   c->launches += nk;
+  return ASR_OK;
+}
+
+static asr_status step_finish(asr_ctx* c, StepArgs& a, cudaStream_t st) {
+  const DevState& s = c->s;
   // (a5) write-once host mirror of the appended token (side stream, overlapped with compute)
   if (c->host_mirror && s.pool_mode) {
     c->bytes_d2h += (int64_t)s.B * c->tok_bytes;   // written by the append units (mapped mirror)
@@ -613,14 +694,15 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
     }
     c->bytes_d2h += (int64_t)s.B * c->tok_bytes;
   }
-  if (host_io) {   // outputs leave on io_out while the next step computes (asr_flush / asr_stats)
+  if (a.host_io) {   // outputs leave on io_out while the next step computes (asr_flush / asr_stats)
+    asr_ctx::Staging& S = c->stg[c->step & 1];
     CUDA_TRY(cudaEventRecord(S.graph_done, st));
     CUDA_TRY(cudaStreamWaitEvent(c->io_out, S.graph_done, 0));
     const size_t ob = (size_t)s.B * s.L * s.Hq * s.d * 4;
-    CUDA_TRY(cudaMemcpyAsync(io->o, o, ob, cudaMemcpyDeviceToHost, c->io_out));
+    CUDA_TRY(cudaMemcpyAsync(a.o_user, a.o, ob, cudaMemcpyDeviceToHost, c->io_out));
     c->bytes_d2h += (int64_t)ob;
-    if (io->entropy && has_logits) {
-      CUDA_TRY(cudaMemcpyAsync(io->entropy, ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, c->io_out));
+    if (a.ent_user && a.has_logits) {
+      CUDA_TRY(cudaMemcpyAsync(a.ent_user, a.ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, c->io_out));
       c->bytes_d2h += (int64_t)s.B * 4;
     }
     CUDA_TRY(cudaEventRecord(S.out_done, c->io_out));
@@ -629,6 +711,96 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   }
   c->step++;
   c->last_stream = st;
+  return ASR_OK;
+}
+
+asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (c->attend_pending) return fail(ASR_E_STATE, "asr_step_attend without asr_step_decide");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (c->s.sharded && !c->nccl_comm)
+    return fail(ASR_E_STATE, "head-sharded context: use asr_step_attend / asr_step_decide or asr_attach_nccl");
+  StepArgs a;
+  asr_status r = step_prepare(c, io, st, a);
+  if (r) return r;
+  if (c->s.sharded) {
+    r = step_launch(c, a, kPartAttend, st);
+    if (r) return r;
+    // sum the shards' per-token partial scores in place (NCCL over NVLink / NVSwitch)
+    const int rc = c->nccl.all_reduce(c->s.tok_score, c->s.tok_score, (size_t)c->s.B * c->s.max_ctx, 7 /*ncclFloat32*/,
+                                      0 /*ncclSum*/, c->nccl_comm, st);
+    if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclAllReduce: ") + c->nccl.err(rc));
+    r = step_launch(c, a, kPartDecide, st);
+  } else {
+    r = step_launch(c, a, kPartFull, st);
+  }
+  if (r) return r;
+  return step_finish(c, a, st);
+}
+
+asr_status asr_step_attend(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (c->attend_pending) return fail(ASR_E_STATE, "asr_step_attend twice without asr_step_decide");
+  if (c->use_mega) return fail(ASR_E_STATE, "split steps are not available with ASR_MEGA=1");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  c->pending = std::make_unique<StepArgsBox>();
+  asr_status r = step_prepare(c, io, st, c->pending->a);
+  if (r) return r;
+  r = step_launch(c, c->pending->a, kPartAttend, st);
+  if (r) return r;
+  c->attend_pending = true;
+  c->last_stream = st;
+  return ASR_OK;
+}
+
+asr_status asr_step_decide(asr_ctx* c, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!c->attend_pending) return fail(ASR_E_STATE, "asr_step_decide without asr_step_attend");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  asr_status r = step_launch(c, c->pending->a, kPartDecide, st);
+  if (r) return r;
+  c->attend_pending = false;
+  r = step_finish(c, c->pending->a, st);
+  c->pending.reset();
+  return r;
+}
+
+asr_status asr_score_partials(asr_ctx* c, float** dev_ptr, int64_t* count) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!dev_ptr || !count) return fail(ASR_E_INVALID, "NULL output");
+  *dev_ptr = c->s.tok_score;
+  *count = (int64_t)c->s.B * c->s.max_ctx;
+  return ASR_OK;
+}
+
+asr_status asr_nccl_unique_id(void* out, int32_t n) {
+  if (!out || n < 128) return fail(ASR_E_INVALID, "out must hold 128 bytes");
+  asr::NcclApi& api = asr::nccl_api();
+  if (!api.ok) return fail(ASR_E_CUDA, "libnccl.so.2 not loadable");
+  const int rc = api.get_unique_id(out);
+  if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclGetUniqueId: ") + api.err(rc));
+  return ASR_OK;
+}
+
+asr_status asr_attach_nccl(asr_ctx* c, const void* unique_id, int32_t nranks, int32_t rank) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(ASR_E_INVALID, "bad NCCL rank arguments");
+  asr::NcclApi& api = asr::nccl_api();
+  if (!api.ok) return fail(ASR_E_CUDA, "libnccl.so.2 not loadable");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  void* comm = nullptr;
+  const int rc = api.comm_init_rank(&comm, nranks, unique_id, rank);
+  if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclCommInitRank: ") + api.err(rc));
+  c->nccl = api;
+  c->nccl_comm = comm;
+  // from now on every step runs attend -> all-reduce -> decide; cached graphs captured the
+  // unsharded kernel arguments
+  c->s.sharded = 1;
+  for (auto& g : c->graphs) {
+    if (g.x) cudaGraphExecDestroy(g.x);
+    if (g.g) cudaGraphDestroy(g.g);
+    g = asr_ctx::StepGraph();
+  }
   return ASR_OK;
 }
 

@@ -80,6 +80,10 @@ struct DevState {
   int32_t* cp_list;           // [B][max_ctx] positions whose slot the copy kernel fills this step
   int32_t* cp_count;          // [B]
   unsigned long long* h2d;    // [1] bytes copied host -> device by the kernels (prefetch + demand)
+  // head-sharded mode
+  int sharded;                // 1: decide reads tok_score (summed across shards) instead of score_part
+  int score_heads;            // H of Eq. 2 (all shards)
+  float* tok_score;           // [B][max_ctx] per-token score sums over this shard's heads, all layers
 
   void* kv;                   // pool [B*max_ctx][L][2][Hkv][d]
   uint8_t* res;               // [B][max_ctx] 1 Active / 0 Frozen
@@ -176,6 +180,19 @@ struct KNode {
   }
 };
 
+// NCCL entry points, resolved with dlopen at first use (nccl_dl.cpp); head-sharded mode only.
+struct NcclApi {
+  bool ok = false;
+  int (*get_unique_id)(void* out128) = nullptr;
+  int (*comm_init_rank)(void** comm, int nranks, const void* id128, int rank) = nullptr;
+  int (*all_reduce)(const void* send, void* recv, size_t count, int dtype, int op, void* comm,
+                    cudaStream_t st) = nullptr;
+  int (*comm_destroy)(void* comm) = nullptr;
+  const char* (*get_error)(int rc) = nullptr;
+  const char* err(int rc) const { return get_error ? get_error(rc) : "nccl error"; }
+};
+NcclApi& nccl_api();
+
 // Node builders (kernels_*.cu).
 void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dtype, const void* k_new,
                  const void* v_new);
@@ -187,6 +204,7 @@ void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype
 int step_kernel_max_grid(int num_sms);
 void node_restore(KNode& n, const DevState& s, int seq, int level);
 void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies
+void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: layer sums -> tok_score
 int attention_grid(const DevState& s, int num_sms);
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head
 cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory

@@ -53,6 +53,12 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
   if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
 }
 
+// Head-sharded mode: per-token partial score sums of this shard (grid decide_blocks x B).
+__global__ void __launch_bounds__(kUnitThreads) scoresum_kernel(DevState s) {
+  pdl_wait();
+  units::unit_score_sum(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks);
+}
+
 // Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.  In pressure
 // mode the evicted tokens it restores are copied back before it returns.
 __global__ void __launch_bounds__(1024) restore_kernel(DevState s, int seq, int level) {
@@ -108,6 +114,11 @@ void node_phaseD(KNode& n, const DevState& s, float* o) {
   const int warps = s.B * s.L * s.Hq;
   const int wpb = kUnitThreads / 32;
   n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + (warps + wpb - 1) / wpb), dim3(kUnitThreads), 0);
+}
+
+void node_scoresum(KNode& n, const DevState& s) {
+  n.s = s;
+  n.finalize((const void*)scoresum_kernel, dim3(s.decide_blocks * s.B), dim3(kUnitThreads), 0);
 }
 
 void node_copy(KNode& n, const DevState& s, int grid) {

@@ -466,6 +466,32 @@ __device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
   return m;
 }
 
+// Eq. 2 numerator of attended index a: sum over layers in order l = 0..L-1 of the per-layer head sums
+// (loads issued 8 at a time so their latencies overlap).
+__device__ __forceinline__ float layer_sum(const DevState& s, int b, int a) {
+  const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
+  float sum = 0.f;
+  int l = 0;
+  for (; l + 8 <= s.L; l += 8) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = sp[(long)(l + q) * s.max_ctx];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sum += v[q];
+  }
+  for (; l < s.L; ++l) sum += sp[(long)l * s.max_ctx];
+  return sum;
+}
+
+// Head-sharded mode: this shard's per-token sums (its heads, all layers) for a slice of A_b.
+__device__ void unit_score_sum(const DevState& s, int b, int x, int X) {
+  const int A = s.act_len[b];
+  const int per_a = (A + X - 1) / X;
+  const int a_end = min(A, (x + 1) * per_a);
+  for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x)
+    s.tok_score[(long)b * s.max_ctx + a] = layer_sum(s, b, a);
+}
+
 // Unit x of X for sequence b: a slice of the attended list (Alg. 1 lines 3-9 + the R0 tick of the
 // tokens it freezes) and a slice of the positions (lines 10-15 for tokens frozen at earlier steps).
 // The two index sets are disjoint (A_i = the tokens Active at the step start) and tokens frozen in
@@ -478,7 +504,7 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   int32_t* timer = s.timer + base;
   uint32_t* cnt = s.count + base;
   int32_t* fstep = s.fstep + base;
-  const float inv = 1.0f / (float)(s.L * s.Hq);
+  const float inv = 1.0f / (float)(s.L * s.score_heads);
   const float inv_sqrt_d = rsqrtf((float)s.d);
   const uint8_t tag_now = res_tag(i);
   // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
@@ -500,18 +526,7 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   const int a_end = min(A, (x + 1) * per_a);
   for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
     const int j = s.act_pos[base + a];
-    // Eq. 2: sum over layers in order l = 0..L-1 (loads issued 8 at a time)
-    const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
-    float sum = 0.f;
-    int l = 0;
-    for (; l + 8 <= s.L; l += 8) {
-      float v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = sp[(long)(l + q) * s.max_ctx];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) sum += v[q];
-    }
-    for (; l < s.L; ++l) sum += sp[(long)l * s.max_ctx];
+    const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
     float sj = sum * inv;               // mean over the L*Hq (layer, head) pairs
     if (s.score_scaled) sj *= inv_sqrt_d;
     s.score[base + a] = sj;

@@ -45,3 +45,22 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def head_shard(Hq: int, Hkv: int, rank: int, world: int) -> tuple[int, int, int, int]:
+    """Head-sharded mode: (q_lo, q_hi, kv_lo, kv_hi) of this rank.  KV heads are split evenly and each
+    rank keeps the query heads that read them (GQA groups stay whole)."""
+    if Hkv % world or Hq % Hkv:
+        raise ValueError("need n_kv_heads % world == 0 and n_q_heads % n_kv_heads == 0")
+    hk = Hkv // world
+    g = Hq // Hkv
+    return rank * hk * g, (rank + 1) * hk * g, rank * hk, (rank + 1) * hk
+
+
+def share_nccl_id(make_id) -> bytes:
+    """Rank 0 calls make_id() (e.g. asr_nccl_unique_id) and broadcasts the 128 bytes to every rank over
+    the torch.distributed process group (plumbing; any backend)."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]

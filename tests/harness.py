@@ -54,6 +54,7 @@ class Case:
     max_context: int = 0
     pool_tokens: int = 0           # > 0: pressure mode (device slot pool, eviction / prefetch / demand)
     evict_min: int = 2
+    nccl_world1: bool = False      # attach a one-rank NCCL communicator (attend -> all-reduce -> decide)
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -114,6 +115,9 @@ def run(c: Case, check_o: bool = True) -> dict:
         return t if c.host_io else t.cuda()
 
     ctx = Context(asr_cfg(c), to_t(pk), to_t(pv), P)
+    if c.nccl_world1:
+        from paper_2512_11221_b200 import asr_nccl_unique_id
+        ctx.attach_nccl(asr_nccl_unique_id(), 1, 0)
     orc = [oracle.OracleSeq(orc_cfg(c), cap, P[b]) for b in range(c.B)]
     worst_o, worst_h, frozen_total, restored_total = 0.0, 0.0, 0, 0
     evicted_total = prefetched_total = demand_total = 0

@@ -66,6 +66,47 @@ def test_gloo_world2_reductions():
     assert [(r[3], r[4]) for r in res] == [(0, 4), (4, 3)]
 
 
+def _id_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2512_11221_b200.dist import head_shard, share_nccl_id
+    uid = share_nccl_id(lambda: bytes(range(128)))
+    q.put((rank, uid, head_shard(32, 8, rank, world)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_head_shard_setup():
+    # every rank receives rank 0's NCCL id; the KV heads (and their GQA query heads) are partitioned
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == bytes(range(128)) for r in res)
+    assert [r[2] for r in res] == [(0, 16, 0, 4), (16, 32, 4, 8)]
+
+
+def test_head_shard_partition():
+    from paper_2512_11221_b200.dist import head_shard
+    for world in (1, 2, 4, 8):
+        kv, qh = [], []
+        for r in range(world):
+            q0, q1, k0, k1 = head_shard(32, 8, r, world)
+            kv.extend(range(k0, k1))
+            qh.extend(range(q0, q1))
+            assert all(h // 4 in range(k0, k1) for h in range(q0, q1))   # GQA groups stay whole
+        assert kv == list(range(8)) and qh == list(range(32))
+    with pytest.raises(ValueError):
+        head_shard(32, 8, 0, 3)
+
+
 def test_sharded_batch_equals_whole_batch_on_oracle():
     import gen
     import oracle

@@ -59,6 +59,17 @@ def build_gen_dev(force: bool = False) -> str:
     return out
 
 
+def _nccl_include() -> str:
+    """nccl.h of the NCCL that torch ships (headers only: libasr.so dlopens libnccl.so.2)."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+    except Exception:
+        import site
+        base = os.path.join(site.getsitepackages()[0], "nvidia", "nccl")
+    return os.path.join(base, "include")
+
+
 def build_asr(force: bool = False) -> str:
     pkg = os.path.join(ROOT, "paper_2512_11221_b200")
     out = os.path.join(pkg, "libasr.so")
@@ -78,11 +89,12 @@ def build_asr(force: bool = False) -> str:
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-warn-spills", *common, "-c", s, "-o", o])
         objs.append(o)
+    nccl_inc = _nccl_include()
     for s in cpp:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", *common, "-c", s, "-o", o])
+        _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", *common, "-I", nccl_inc, "-c", s, "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs, "-ldl"])
     return out
 
 
