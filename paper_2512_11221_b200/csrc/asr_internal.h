@@ -206,10 +206,8 @@ void node_restore(KNode& n, const DevState& s, int seq, int level);
 void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies
 void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: layer sums -> tok_score
 int attention_grid(const DevState& s, int num_sms);
-bool attention_mma_supported(const DevState& s);   // bf16, d=128, 8 KV heads, 4 q heads per KV head
+bool attention_mma_supported(const DevState& s);   // bf16, d=128, 1/2/4/8 KV heads, <= 4 (8) q heads per KV head
 cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory
-const void* attention_mma_func();
-unsigned attention_mma_smem();
-int attention_mma_threads();
+void attention_mma_launch_shape(const DevState& s, const void** func, int* threads, unsigned* smem);
 
 }  // namespace asr

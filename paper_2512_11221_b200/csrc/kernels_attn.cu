@@ -195,7 +195,11 @@ void node_attention(KNode& n, const DevState& s, const void* q, int grid) {
   n.s = s;
   n.set(0, q);
   if (attention_mma_supported(s)) {
-    n.finalize(attention_mma_func(), dim3(grid), dim3(attention_mma_threads()), attention_mma_smem());
+    const void* f;
+    int threads;
+    unsigned smem;
+    attention_mma_launch_shape(s, &f, &threads, &smem);
+    n.finalize(f, dim3(grid), dim3(threads), smem);
     return;
   }
   const unsigned smem = (unsigned)(sizeof(int) * (s.B + 1) + sizeof(float) * 32 * s.Hkv);

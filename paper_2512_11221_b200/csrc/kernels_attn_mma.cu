@@ -29,28 +29,43 @@ namespace asr {
 namespace {
 
 constexpr int kD = 128;
-constexpr int kG = 4;                 // query heads per KV head
-constexpr int kHK = 8;                // KV heads (consumer warps)
 constexpr int kTM = 16;               // tokens per stage
-constexpr int kStagesRing = 3;
-constexpr int kRowBytes = kHK * kD * 2;         // 2048: one token-layer K (or V) row, all heads
-constexpr int kTokBytes = 2 * kRowBytes;        // 4096: K row then V row (contiguous in the pool)
-constexpr int kTokPad = kTokBytes + 16;         // 4112: ldmatrix conflict-free stride
-constexpr int kStageBytes = kTM * kTokPad;
-constexpr int kThreads = (kHK + 1) * 32;
-constexpr int kMaxB = 1024;                     // sequences per context on this path
-constexpr int kQBytes = kHK * kG * kD * 2;      // 8 KiB: q of one (b, l), all heads
+constexpr int kMaxB = 1024;           // sequences per context on this path
 
-struct Smem {
-  alignas(128) uint8_t kv[kStagesRing][kStageBytes];
-  alignas(128) uint8_t q[2][kQBytes];    // q of the current / next work item
-  float sc[kStagesRing][kHK][kTM];      // per-warp head sums |S| of each token
-  int start[kMaxB + 1];                 // work list: first item of each sequence
-  alignas(8) uint64_t full[kStagesRing];
-  alignas(8) uint64_t empty[kStagesRing];
-  alignas(8) uint64_t qfull[2];
-  alignas(8) uint64_t qempty[2];
+// Geometry of the kernel for HK KV heads (= consumer warps) and up to kGMax query heads per KV head.
+// Smaller HK means smaller token rows, so the ring gets more stages to keep ~200 KB in flight.
+template <int HK>
+struct Geo {
+  static constexpr int kHK = HK;
+  static constexpr int kGMax = HK == 8 ? 4 : 8;
+  static constexpr int kStagesRing = HK == 8 ? 3 : (HK == 4 ? 6 : 12);
+  static constexpr int kRowBytes = HK * kD * 2;       // one token-layer K (or V) row, all heads
+  static constexpr int kTokBytes = 2 * kRowBytes;     // K row then V row (contiguous in the pool)
+  static constexpr int kTokPad = kTokBytes + 16;      // ldmatrix conflict-free stride
+  static constexpr int kStageBytes = kTM * kTokPad;
+  static constexpr int kThreads = (HK + 1) * 32;
+  static constexpr int kQBytes = HK * kGMax * kD * 2; // q of one (b, l), all heads (upper bound)
+  struct Smem {
+    alignas(128) uint8_t kv[kStagesRing][kStageBytes];
+    alignas(128) uint8_t q[2][kQBytes];    // q of the current / next work item
+    float sc[kStagesRing][HK][kTM];       // per-warp head sums |S| of each token
+    int start[kMaxB + 1];                 // work list: first item of each sequence
+    alignas(8) uint64_t full[kStagesRing];
+    alignas(8) uint64_t empty[kStagesRing];
+    alignas(8) uint64_t qfull[2];
+    alignas(8) uint64_t qempty[2];
+  };
 };
+
+#define ASR_GEO(HK)                                        \
+  using Smem = typename Geo<HK>::Smem;                     \
+  constexpr int kHK = Geo<HK>::kHK;                        \
+  constexpr int kStagesRing = Geo<HK>::kStagesRing;        \
+  constexpr int kRowBytes = Geo<HK>::kRowBytes;            \
+  constexpr int kTokBytes = Geo<HK>::kTokBytes;            \
+  constexpr int kTokPad = Geo<HK>::kTokPad;                \
+  constexpr int kStageBytes = Geo<HK>::kStageBytes;        \
+  (void)kHK; (void)kStagesRing; (void)kRowBytes; (void)kTokBytes; (void)kTokPad; (void)kStageBytes
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -146,7 +161,9 @@ struct TileIt {
 
 // Barriers and a zeroed ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN
 // would poison O).  Once per launch, before any phase touches the ring.
-__device__ void attention_prologue(Smem& sm) {
+template <int HK>
+__device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
+  ASR_GEO(HK);
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesRing; ++i) {
       mbar_init(&sm.full[i], 1);
@@ -166,7 +183,11 @@ __device__ void attention_prologue(Smem& sm) {
 }
 
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
-__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q, Smem& sm) {
+template <int HK>
+__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q, typename Geo<HK>::Smem& sm) {
+  ASR_GEO(HK);
+  const int G = s.Hq / s.Hkv;               // query heads per KV head (<= Geo<HK>::kGMax)
+  const int qbytes = s.Hq * kD * 2;         // q of one (b, l)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -218,8 +239,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
         const int qs = it_local & 1;
         mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
         if (lane == 0) {
-          mbar_expect_tx(&sm.qfull[qs], kQBytes);
-          bulk_g2s(&sm.q[qs][0], q + ((long)it.b * s.L + it.l) * s.Hq * kD, kQBytes, &sm.qfull[qs]);
+          mbar_expect_tx(&sm.qfull[qs], (uint32_t)qbytes);
+          bulk_g2s(&sm.q[qs][0], q + ((long)it.b * s.L + it.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
         }
       }
       const int stage = g % kStagesRing;
@@ -272,13 +293,13 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     mbar_wait(&sm.qfull[qs], (uint32_t)(it_local >> 1) & 1u);
     uint32_t qa[8][2];
     {
-      const __nv_bfloat16* qh = reinterpret_cast<const __nv_bfloat16*>(&sm.q[qs][0]) + (warp * kG + (r & 3)) * kD;
+      const __nv_bfloat16* qh = reinterpret_cast<const __nv_bfloat16*>(&sm.q[qs][0]) + (warp * G + (r < G ? r : 0)) * kD;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         uint32_t lo = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 2 * qd);
         uint32_t hi = *reinterpret_cast<const uint32_t*>(qh + ks * 16 + 8 + 2 * qd);
-        qa[ks][0] = r < kG ? lo : 0u;
-        qa[ks][1] = r < kG ? hi : 0u;
+        qa[ks][0] = r < G ? lo : 0u;
+        qa[ks][1] = r < G ? hi : 0u;
       }
     }
     __syncwarp();
@@ -306,10 +327,10 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       // tokens of this thread's columns: n0 = 2qd, n0+1 (tile 0), 8+2qd, 9+2qd (tile 1)
       const int n0 = 2 * qd;
       const bool v00 = n0 < cnt, v01 = n0 + 1 < cnt, v10 = n0 + 8 < cnt, v11 = n0 + 9 < cnt;
-      // ---- Eq. 2 head sum: |S| over the 4 valid rows (lanes 0..15) -> lanes 0..3
+      // ---- Eq. 2 head sum: |S| over the G valid rows (rows >= G hold exact zeros: their q is zero)
       float s00 = fabsf(c0[0]), s01 = fabsf(c0[1]), s10 = fabsf(c1[0]), s11 = fabsf(c1[1]);
 #pragma unroll
-      for (int o = 4; o <= 8; o <<= 1) {
+      for (int o = 4; o <= 16; o <<= 1) {
         s00 += __shfl_xor_sync(0xffffffffu, s00, o);
         s01 += __shfl_xor_sync(0xffffffffu, s01, o);
         s10 += __shfl_xor_sync(0xffffffffu, s10, o);
@@ -361,8 +382,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     // ---- partial outputs of this item: rows 0..3 (lanes 0..15)
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    if (r < kG) {
-      const long pi = (long)item * s.Hq + warp * kG + r;
+    if (r < G) {
+      const long pi = (long)item * s.Hq + warp * G + r;
       if (qd == 0) {
         s.part_ml[pi * 2] = m_run;
         s.part_ml[pi * 2 + 1] = l_run;
@@ -376,14 +397,15 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 
 
 // Standalone attention kernel (multi-kernel schedule, ASR_NO_MEGA=1).
-__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
+template <int HK>
+__global__ void __launch_bounds__(Geo<HK>::kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  auto& sm = *reinterpret_cast<typename Geo<HK>::Smem*>(smem_raw);
   Stamp stamp(s.tl, 1);
-  attention_prologue(sm);
+  attention_prologue<HK>(sm);
   pdl_wait();      // A_i, |A_i|, q and the appended K/V come from the upstream kernels
   pdl_trigger();
-  attention_phase(s, q, sm);
+  attention_phase<HK>(s, q, sm);
 }
 
 __device__ __forceinline__ void stamp_min(const DevState& s, int k) {
@@ -398,14 +420,15 @@ __device__ __forceinline__ void stamp_max(const DevState& s, int k) {
 // after the last barrier.  Replaces 3-4 dependent launches whose latency chains dominated batch-1
 // steps.
 template <typename TL>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Geo<8>::kThreads, 1)
     step_kernel(DevState s, const TL* logits, float* entropy_out, const __nv_bfloat16* k_new,
                 const __nv_bfloat16* v_new, const __nv_bfloat16* __restrict__ q, float* o) {
+  constexpr int kThreads = Geo<8>::kThreads;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  auto& sm = *reinterpret_cast<Geo<8>::Smem*>(smem_raw);
   __shared__ units::UnitShm u;
   stamp_min(s, 0);
-  attention_prologue(sm);
+  attention_prologue<8>(sm);
   const int i = *s.step;
   // ---- phase A: entropy splits, append, speculative compaction
   const int nA = units::phaseA_units(s, logits != nullptr);
@@ -423,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   stamp_max(s, 1);
   stamp_min(s, 2);
   // ---- phase C: attention + fused Eq. 2 score
-  attention_phase(s, q, sm);
+  attention_phase<8>(s, q, sm);
   units::grid_sync(s.gbar);
   stamp_max(s, 3);
   stamp_min(s, 4);
@@ -453,24 +476,50 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+template <int HK>
+int gmax() { return Geo<HK>::kGMax; }
+
 bool attention_mma_supported(const DevState& s) {
-  return s.dtype == 0 && s.d == kD && s.Hkv == kHK && s.Hq == kHK * kG && s.B <= kMaxB;
+  if (s.dtype != 0 || s.d != kD || s.B > kMaxB || s.Hq % s.Hkv) return false;
+  const int G = s.Hq / s.Hkv;
+  switch (s.Hkv) {
+    case 8: return G <= gmax<8>();
+    case 4: return G <= gmax<4>();
+    case 2: return G <= gmax<2>();
+    case 1: return G <= gmax<1>();
+    default: return false;
+  }
+}
+
+template <int HK>
+cudaError_t prep_one() {
+  return cudaFuncSetAttribute(attn_mma_kernel<HK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(typename Geo<HK>::Smem));
 }
 
 cudaError_t attention_mma_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  cudaError_t e;
+  if ((e = prep_one<8>()) != cudaSuccess || (e = prep_one<4>()) != cudaSuccess || (e = prep_one<2>()) != cudaSuccess ||
+      (e = prep_one<1>()) != cudaSuccess)
+    return e;
+  e = cudaFuncSetAttribute(step_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Geo<8>::Smem));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(step_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  return cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Geo<8>::Smem));
 }
-const void* attention_mma_func() { return (const void*)attn_mma_kernel; }
-unsigned attention_mma_smem() { return (unsigned)sizeof(Smem); }
-int attention_mma_threads() { return kThreads; }
+
+void attention_mma_launch_shape(const DevState& s, const void** func, int* threads, unsigned* smem) {
+  switch (s.Hkv) {
+    case 8: *func = (const void*)attn_mma_kernel<8>; *threads = Geo<8>::kThreads; *smem = sizeof(Geo<8>::Smem); break;
+    case 4: *func = (const void*)attn_mma_kernel<4>; *threads = Geo<4>::kThreads; *smem = sizeof(Geo<4>::Smem); break;
+    case 2: *func = (const void*)attn_mma_kernel<2>; *threads = Geo<2>::kThreads; *smem = sizeof(Geo<2>::Smem); break;
+    default: *func = (const void*)attn_mma_kernel<1>; *threads = Geo<1>::kThreads; *smem = sizeof(Geo<1>::Smem); break;
+  }
+}
 
 int step_kernel_max_grid(int num_sms) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<__nv_bfloat16>, kThreads, sizeof(Smem)) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<__nv_bfloat16>, Geo<8>::kThreads,
+                                                    sizeof(Geo<8>::Smem)) !=
       cudaSuccess)
     return 0;
   return per_sm * num_sms;
@@ -486,7 +535,7 @@ void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype
   n.set(4, q);
   n.set(5, o);
   const void* f = (logits && logits_dtype == 1) ? (const void*)step_kernel<float> : (const void*)step_kernel<__nv_bfloat16>;
-  n.finalize(f, dim3(grid), dim3(kThreads), sizeof(Smem));
+  n.finalize(f, dim3(grid), dim3(Geo<8>::kThreads), sizeof(Geo<8>::Smem));
   n.cooperative = true;
 }
 

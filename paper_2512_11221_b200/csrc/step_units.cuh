@@ -504,8 +504,8 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   int32_t* timer = s.timer + base;
   uint32_t* cnt = s.count + base;
   int32_t* fstep = s.fstep + base;
-  const float inv = 1.0f / (float)(s.L * s.score_heads);
-  const float inv_sqrt_d = rsqrtf((float)s.d);
+  const float heads = (float)(s.L * s.score_heads);   // Eq. 2's H over all layers (R-layer)
+  const float sqrt_d = sqrtf((float)s.d);
   const uint8_t tag_now = res_tag(i);
   // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
   // loop: tokens of A_i read Active here and are skipped by the tick below)
@@ -527,8 +527,8 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
     const int j = s.act_pos[base + a];
     const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
-    float sj = sum * inv;               // mean over the L*Hq (layer, head) pairs
-    if (s.score_scaled) sj *= inv_sqrt_d;
+    float sj = sum / heads;             // mean over the L*Hq (layer, head) pairs (correctly rounded)
+    if (s.score_scaled) sj = sj / sqrt_d;
     s.score[base + a] = sj;
     if (j < n - s.window && j >= s.pinned && sj < s.tau) {
       const uint32_t c = cnt[j] + 1;    // line 4

@@ -150,8 +150,10 @@ def run(c: Case, check_o: bool = True) -> dict:
             g = stats[b]
             where = f"step {i} seq {b}"
             np.testing.assert_array_equal(g["active_list"], act, err_msg=where)
-            assert np.array_equal(g["scores"].astype(np.float64), scores), \
-                f"{where}: scores differ at {np.flatnonzero(g['scores'] != scores)[:5]}"
+            # the sums are exact on LAT inputs; the mean is one correctly rounded fp32 division
+            sc32 = scores.astype(np.float32)
+            assert np.array_equal(g["scores"], sc32), \
+                f"{where}: scores differ at {np.flatnonzero(g['scores'] != sc32)[:5]}"
             led = orc[b].ledger()
             for key in ("residency", "timer", "count", "freeze_step"):
                 np.testing.assert_array_equal(g["ledger"][key], led[key], err_msg=f"{where} {key}")

@@ -75,7 +75,7 @@ def test_needle_restore_ladder_32k(pool):
                 O, act, scores, out = orc[b].step(qn[b], KVs[b][0], KVs[b][1], None if lg is None else lg[b])
                 rel = (np.abs(o[b] - O).max(-1) / np.abs(O).max(-1)).max()
                 assert rel <= 2e-3, (i, b, rel)
-                np.testing.assert_array_equal(g["scores"].astype(np.float64), scores)
+                np.testing.assert_array_equal(g["scores"], scores.astype(np.float32))
             else:
                 H = oracle.entropy(lg[b]) if lg is not None else None
                 # class labels of the LAT construction: every eligible token scores below tau except the

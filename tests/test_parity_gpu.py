@@ -111,3 +111,11 @@ def test_pressure_mode_explicit_restore_and_evict_threshold():
     s = run(Case(B=2, prompt=(30, 12), steps=70, window=4, seed=81, pool_tokens=200, evict_min=1,
                  restore_at={40: (-1, 3), 55: (0, 1)}))
     assert s["evicted"] > 0 and s["demand"] > 0
+
+
+@pytest.mark.parametrize("hq,hkv", [(28, 4), (16, 2), (8, 1), (16, 4), (32, 8)])
+def test_mma_path_gqa_layouts(hq, hkv):
+    # the tensor-core attention kernel covers 1/2/4/8 KV heads and up to 8 (4 for 8 KV heads) query
+    # heads per KV head: Qwen2-7B-like (28 q / 4 KV), head shards of LLaMA-3-8B (16/4, 8/2 ...), G = 8
+    run(Case(L=2, Hq=hq, Hkv=hkv, d=128, B=2, prompt=(90, 37), steps=20, window=16, hot_permille=300, a_hot=64,
+             seed=3000 + hq + hkv, vocab=2048))
