@@ -52,6 +52,8 @@ def parse():
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
     ap.add_argument("--points", default="cfg3", help="comma list of extra workloads (POINTS) or '' for none")
+    ap.add_argument("--head-shard", action="store_true",
+                    help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
     return ap.parse_args()
 
 
@@ -181,6 +183,9 @@ def run_asr(a, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    # head-sharded mode: this rank holds hkv_r of the KV heads (and their query heads) of every sequence
+    # and the per-token partial scores are all-reduced over NCCL inside asr_step
+    hq_r, hkv_r = (HQ // world, HKV // world) if a.head_shard else (HQ, HKV)
     if a.timeline:
         os.environ["ASR_TIMELINE"] = "1"
     B = a.batch
@@ -189,23 +194,38 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     W, K = a.warmup, a.steps
     e2e_steps = 0 if a.no_e2e else K
     max_ctx = a.context + W + 2 * K + e2e_steps + 16
-    g = gen_params(a, rank)
+    g = gen_params(a, 0 if a.head_shard else rank)
+    g.Hq, g.Hkv = hq_r, hkv_r
     pool = int(a.pool_frac * B * a.context) + 4 * B if a.pool_frac > 0 else 0
-    cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
+    cfg = Config(n_layers=L, n_q_heads=hq_r, n_kv_heads=hkv_r, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=0,
-                 device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min)
+                 device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min,
+                 score_heads=HQ if a.head_shard else 0)
     bf = torch.bfloat16
-    pk = torch.empty((B, P, L, HKV, D), dtype=bf, device=dev)
+    pk = torch.empty((B, P, L, hkv_r, D), dtype=bf, device=dev)
     pv = torch.empty_like(pk)
     gen.dev_kv(g, B, 0, P, pk, pv)
     torch.cuda.synchronize()
     ctx = Context(cfg, pk, pv, [P] * B)
+    if a.head_shard:
+        from paper_2512_11221_b200 import asr_nccl_unique_id
+        from paper_2512_11221_b200.dist import share_nccl_id
+        uid = share_nccl_id(asr_nccl_unique_id) if world > 1 else asr_nccl_unique_id()
+        # NCCL prints its version banner on stdout at init; keep stdout for the one JSON line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            ctx.attach_nccl(uid, world, rank)
+        finally:
+            os.dup2(saved, 1)
+            os.close(saved)
     del pk, pv
-    q = torch.empty((B, L, HQ, D), dtype=bf, device=dev)
-    kn = torch.empty((B, L, HKV, D), dtype=bf, device=dev)
+    q = torch.empty((B, L, hq_r, D), dtype=bf, device=dev)
+    kn = torch.empty((B, L, hkv_r, D), dtype=bf, device=dev)
     vn = torch.empty_like(kn)
     lg = torch.empty((B, VOCAB), dtype=bf, device=dev)
-    o = torch.empty((B, L, HQ, D), dtype=torch.float32, device=dev)
+    o = torch.empty((B, L, hq_r, D), dtype=torch.float32, device=dev)
     ent = torch.empty((B,), dtype=torch.float32, device=dev)
     pos_dev = torch.full((B,), P, dtype=torch.int32, device=dev)
 
@@ -223,8 +243,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     t_grow = time.perf_counter() - t_grow
     # inputs of the measured steps (warm-up, timed, profiled), resident in HBM before timing
     n_meas = W + 2 * K
-    Q = torch.empty((n_meas, B, L, HQ, D), dtype=bf, device=dev)
-    KN = torch.empty((n_meas, B, L, HKV, D), dtype=bf, device=dev)
+    Q = torch.empty((n_meas, B, L, hq_r, D), dtype=bf, device=dev)
+    KN = torch.empty((n_meas, B, L, hkv_r, D), dtype=bf, device=dev)
     VN = torch.empty_like(KN)
     LG = torch.empty((n_meas, B, VOCAB), dtype=bf, device=dev)
     for t in range(n_meas):
@@ -303,17 +323,17 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     # ---- e2e through the C ABI with HOST buffers (copies inside the timed region)
     e2e = None
     if e2e_steps:
-        hq = [torch.empty((B, L, HQ, D), dtype=bf).pin_memory() for _ in range(2)]
-        hk = [torch.empty((B, L, HKV, D), dtype=bf).pin_memory() for _ in range(2)]
-        hv = [torch.empty((B, L, HKV, D), dtype=bf).pin_memory() for _ in range(2)]
+        hq = [torch.empty((B, L, hq_r, D), dtype=bf).pin_memory() for _ in range(2)]
+        hk = [torch.empty((B, L, hkv_r, D), dtype=bf).pin_memory() for _ in range(2)]
+        hv = [torch.empty((B, L, hkv_r, D), dtype=bf).pin_memory() for _ in range(2)]
         hl = [torch.empty((B, VOCAB), dtype=bf).pin_memory() for _ in range(2)]
-        ho = torch.empty((B, L, HQ, D), dtype=torch.float32).pin_memory()
+        ho = torch.empty((B, L, hq_r, D), dtype=torch.float32).pin_memory()
         he = torch.empty((B,), dtype=torch.float32).pin_memory()
         base = grow + n_meas
-        HQs, HKs, HVs, HLs = [], [], [], []
+        hq_rs, HKs, HVs, HLs = [], [], [], []
         for t in range(e2e_steps):
             inputs(base + t, q, kn, vn, lg)
-            HQs.append(q.cpu().pin_memory()); HKs.append(kn.cpu().pin_memory())
+            hq_rs.append(q.cpu().pin_memory()); HKs.append(kn.cpu().pin_memory())
             HVs.append(vn.cpu().pin_memory()); HLs.append(lg.cpu().pin_memory())
         # one untimed host-I/O step allocates the library's staging buffers
         inputs(base + e2e_steps, q, kn, vn, lg)
@@ -325,16 +345,16 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for t in range(e2e_steps):
-            ctx.step(HQs[t], HKs[t], HVs[t], ho, logits_prev=HLs[t], entropy=he)
+            ctx.step(hq_rs[t], HKs[t], HVs[t], ho, logits_prev=HLs[t], entropy=he)
         ctx.flush()   # the stream waits for the last step's outputs to land in host memory
         e1.record(st)
         torch.cuda.synchronize()
         e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        h2d = B * (L * HQ * D * 2 + 2 * L * HKV * D * 2 + VOCAB * 2)
-        d2h = B * (L * HQ * D * 4 + 4)
-        e2e = {"value": B * e2e_steps * world / (float(e2e_ms.item()) / 1000.0), "unit": "tok/s",
+        h2d = B * (L * hq_r * D * 2 + 2 * L * hkv_r * D * 2 + VOCAB * 2)
+        d2h = B * (L * hq_r * D * 4 + 4)
+        e2e = {"value": B * e2e_steps * (1 if a.head_shard else world) / (float(e2e_ms.item()) / 1000.0), "unit": "tok/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region "
                        "(the library overlaps them with neighbouring steps on two copy streams)"}
@@ -342,7 +362,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     attn_ms = stage_ms[1]
     # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);
     # per (sequence, layer): q (Hq*d*2 B).  |A_i| per step ~ att_last (drifts < 0.5 % over the window).
-    bytes_per_step = L * att_prof * (2 * HKV * D * 2 + 8) + B * L * HQ * D * 2
+    bytes_per_step = L * att_prof * (2 * hkv_r * D * 2 + 8) + B * L * hq_r * D * 2
     achieved = bytes_per_step * K / (attn_ms / 1000.0) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = None
@@ -353,7 +373,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                 traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
-    value = B * K * world / (total_max / 1000.0)
+    # sequence sharding: every rank decodes its own batch; head sharding: all ranks decode one batch
+    value = B * K * (1 if a.head_shard else world) / (total_max / 1000.0)
     ctx.close()
     del Q, KN, VN, LG, flush_w, flush_r
     torch.cuda.empty_cache()
@@ -366,13 +387,15 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     line = {
         "metric": "decode tokens/s at LLaMA-3-8B shape (8K context, window 512)",
         "value": value, "unit": "tok/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "strong" if a.head_shard else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
                                + (f" pool{a.pool_frac:g}" if pool else ""),
                    "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": 0.5, "k": 2,
                    "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
-                   "parallelism": f"sequence-sharded x{world} (no hot-path collective)"},
+                   "parallelism": (f"head-sharded x{world} (NCCL all-reduce of per-token partial scores)" if a.head_shard
+                                   else f"sequence-sharded x{world} (no hot-path collective)")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "attention+score (split-KV over A_i)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
