@@ -260,6 +260,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.det_sigma_floor = cfg->det_sigma_floor;
     CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
     // split-KV policy: enough work items to fill the SMs; fp32 KV keeps chunks <= 256 tokens
+    // split-KV policy: enough work items to fill the SMs (a balanced split into 37-token chunks at
+    // batch 1 measured slower: partial tiles shrink the bytes in flight; profiles/README.md)
     s.chunk_min = 64;
     long want = (8L * c->num_sms + (long)s.B * s.L - 1) / ((long)s.B * s.L);
     if (s.dtype == ASR_KV_F32) {

@@ -141,7 +141,7 @@ struct Stamp {
 
 __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, int* chunk, int* nch) {
   int c = (A + max_splits - 1) / max_splits;
-  c = (c + 15) & ~15;
+  c = (c + 15) & ~15;   // whole 16-token tiles: a partial tile shrinks the bytes in flight of its stage
   if (c < chunk_min) c = chunk_min;
   *chunk = c;
   *nch = (A + c - 1) / c;

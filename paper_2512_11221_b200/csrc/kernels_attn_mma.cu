@@ -159,8 +159,7 @@ struct TileIt {
   }
 };
 
-// Barriers and a zeroed ring (masked tail rows must hold finite values: P = 0 there and 0 * NaN
-// would poison O).  Once per launch, before any phase touches the ring.
+// Barriers, once per launch before any phase touches the ring.
 template <int HK>
 __device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
   ASR_GEO(HK);
@@ -175,11 +174,6 @@ __device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint4* z = reinterpret_cast<uint4*>(&sm.kv[0][0]);
-  const int nz = (int)(sizeof(sm.kv) / sizeof(uint4));
-  for (int i = threadIdx.x; i < nz; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-  // order the generic-proxy zero fill before the async-proxy (bulk copy) writes to the same rows
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
@@ -253,6 +247,15 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 #pragma unroll
       for (int i = 0; i < kStagesRing; ++i)
         if (i == stage) pend[i] = tile;
+      if (cnt < kTM) {
+        // masked tail rows: their P is 0, but 0 * NaN would poison O, so their V slices get zeros
+        // (generic-proxy stores, ordered before later bulk copies into the same rows by the fence)
+        uint4* z = reinterpret_cast<uint4*>(&sm.kv[stage][0]);
+        const int per_row = kRowBytes / 16;
+        for (int t = cnt; t < kTM; ++t)
+          for (int k = lane; k < per_row; k += 32) z[(t * kTokPad + kRowBytes) / 16 + k] = make_uint4(0, 0, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
       if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
       __syncwarp();
       if (lane < cnt) {
