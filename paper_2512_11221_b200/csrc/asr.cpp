@@ -327,7 +327,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.item_start, (size_t)(s.B + 1) * 4));
     CUDA_TRY(c->alloc(&s.score_part, BT * s.L * 4));
     CUDA_TRY(c->alloc(&s.score, BT * 4));
-    const size_t max_items = (size_t)s.B * s.L * s.max_splits;
+    size_t max_items = (size_t)s.B * s.L * s.max_splits;
+    if (max_items < (size_t)s.B * s.L + c->num_sms) max_items = (size_t)s.B * s.L + c->num_sms;   // stream-K
     CUDA_TRY(c->alloc(&s.part_ml, max_items * s.Hq * 2 * 4));
     CUDA_TRY(c->alloc(&s.part_acc, max_items * s.Hq * s.d * 4));
     CUDA_TRY(c->alloc(&s.ent_part, (size_t)s.B * asr::kEntSplits * 3 * 4));
@@ -406,6 +407,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       c->mega_grid = g < c->num_sms ? g : c->num_sms;
       if (c->mega_grid < 1) c->use_mega = false;
     }
+    s.sk_grid = asr::attention_mma_supported(s) ? (c->use_mega ? c->mega_grid : c->attn_grid) : 0;
     const char* np = getenv("ASR_NO_PDL");
     c->use_pdl = !(np && np[0] == '1');
     c->last_stream = st;

@@ -66,6 +66,7 @@ struct DevState {
   float det_z, det_sigma_floor;
   int max_splits, chunk_min;
   int decide_blocks;          // blocks per sequence of the decide kernel
+  int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
   // pressure mode (pool_tokens > 0)
   int pool_mode;              // 0 full residency (slot = b*max_ctx + pos), 1 slot pool
   int evict_min;              // evict at freeze when the remaining absence >= evict_min
@@ -146,6 +147,17 @@ __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, i
   *chunk = c;
   *nch = (A + c - 1) / c;
 }
+
+// Stream-K split of the tensor-core attention (DevState::sk_grid = G > 0).  The L * ceil(A_b / 16)
+// 16-token tiles of all (b, l) items, in (b, l, tile) order, T in total, are cut into G contiguous
+// ranges [floor(cT/G), floor((c+1)T/G)), one per CTA, so every CTA streams the same number of tiles
+// (+-1); G = sk_span(T, grid) = min(grid, T) keeps every range non-empty (CTAs >= G idle).  The part of item i = b*L + l that CTA c covers writes its softmax partial to slot i + c
+// (unique: both indices grow along the tile order), so item i's partials are the consecutive slots
+// i + sk_cta_of(S_i) .. i + sk_cta_of(S_i + tiles_b - 1), S_i = item_start[b] + l * tiles_b, and there
+// are at most B*L + G of them.  sk_cta_of(t) = the CTA whose range holds tile t.
+constexpr int kSkTile = 16;
+__host__ __device__ inline int sk_span(long T, int grid) { return T < grid ? (int)T : grid; }
+__host__ __device__ inline int sk_cta_of(long t, long T, int G) { return (int)(((t + 1) * (long)G - 1) / T); }
 
 // One kernel launch described as data, so the same description serves a direct launch
 // (cudaLaunchKernel) and a CUDA-graph kernel node (cudaGraphAddKernelNode /

@@ -124,39 +124,38 @@ struct ItemInfo {
   int b, l, a0, n;  // sequence, layer, first compact index, tokens
 };
 
-__device__ __forceinline__ ItemInfo decode_item(const DevState& s, const int* start, int item) {
-  int lo = 0, hi = s.B - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (start[mid] <= item) lo = mid;
-    else hi = mid - 1;
+// Position in the stream-K tile order (asr_internal.h): tile t = tile ti of item (b, l), whose
+// sequence has A active tokens in `tiles` tiles.  `start` = per-sequence first tile (prefix sums).
+struct Cursor {
+  int t, b, l, ti, tiles, A;
+  __device__ void seek(const DevState& s, const int* start, int tt) {
+    t = tt;
+    int lo = 0, hi = s.B - 1;   // last sequence whose first tile is <= t (skips empty sequences)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= tt) lo = mid;
+      else hi = mid - 1;
+    }
+    b = lo;
+    A = s.act_len[b];
+    tiles = (A + kTM - 1) / kTM;
+    const int r = tt - start[b];
+    l = r / tiles;
+    ti = r - l * tiles;
   }
-  ItemInfo it;
-  it.b = lo;
-  const int A = s.act_len[lo];
-  int chunk, nch;
-  chunking(A, s.max_splits, s.chunk_min, &chunk, &nch);
-  const int r = item - start[lo];
-  it.l = r / nch;
-  const int c = r % nch;
-  it.a0 = c * chunk;
-  it.n = min(A, it.a0 + chunk) - it.a0;
-  return it;
-}
-
-// Iterator over this CTA's tiles: items blockIdx.x, blockIdx.x + gridDim.x, ...; 16 tokens a tile.
-struct TileIt {
-  int item, t0;
-  ItemInfo it;
-  __device__ bool valid(int total) const { return item < total; }
-  __device__ void advance(const DevState& s, const int* start, int total) {
-    t0 += kTM;
-    if (t0 >= it.n) {
-      item += gridDim.x;
-      t0 = 0;
-      if (item < total) it = decode_item(s, start, item);
+  __device__ void next(const DevState& s) {   // one tile forward
+    ++t;
+    if (++ti < tiles) return;
+    ti = 0;
+    if (++l < s.L) return;
+    l = 0;
+    for (++b; b < s.B; ++b) {
+      A = s.act_len[b];
+      tiles = (A + kTM - 1) / kTM;
+      if (tiles) break;
     }
   }
+  __device__ int cnt() const { return min(kTM, A - ti * kTM); }
 };
 
 // Barriers, once per launch before any phase touches the ring.
@@ -187,18 +186,18 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       sm.start[b] = acc;
-      int chunk, nch;
-      chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
-      acc += s.L * nch;
+      acc += s.L * ((s.act_len[b] + kTM - 1) / kTM);
     }
     sm.start[s.B] = acc;
     if (blockIdx.x == 0)
       for (int b = 0; b <= s.B; ++b) s.item_start[b] = sm.start[b];
   }
   __syncthreads();
-  const int total = sm.start[s.B];
-  const long row_elems = (long)kHK * kD;  // per token-layer K (or V)
-  (void)row_elems;
+  // this CTA's contiguous range of the stream-K tile order over sk_span(T, G) CTAs (gridDim.x == s.sk_grid)
+  const long T = sm.start[s.B];
+  const int Ge = sk_span(T, gridDim.x);
+  const int t_begin = blockIdx.x < Ge ? (int)((long)blockIdx.x * T / Ge) : 0;
+  const int t_end = blockIdx.x < Ge ? (int)((long)(blockIdx.x + 1) * T / Ge) : 0;
 
   if (warp == kHK) {
     // ================================================================== producer warp
@@ -215,26 +214,26 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       }
     };
     const char* kvb = reinterpret_cast<const char*>(s.kv);
-    TileIt cur{(int)blockIdx.x, 0, {}};
-    if (cur.valid(total)) cur.it = decode_item(s, sm.start, cur.item);
-    auto load_idx = [&](const TileIt& t) -> int {
-      if (!t.valid(total) || lane >= min(kTM, t.it.n - t.t0)) return 0;
-      return max(0, __ldg(s.act_slot + (long)t.it.b * s.max_ctx + t.it.a0 + t.t0 + lane));   // device slot
+    Cursor cur;
+    if (t_begin < t_end) cur.seek(s, sm.start, t_begin);
+    else cur.t = t_end;
+    auto load_idx = [&](const Cursor& c) -> int {
+      if (c.t >= t_end || lane >= c.cnt()) return 0;
+      return max(0, __ldg(s.act_slot + (long)c.b * s.max_ctx + c.ti * kTM + lane));   // device slot
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
-    while (cur.valid(total)) {
-      TileIt nxt = cur;
-      nxt.advance(s, sm.start, total);
+    while (cur.t < t_end) {
+      Cursor nxt = cur;
+      nxt.next(s);
       const int j_next = load_idx(nxt);   // in flight while this tile waits for its stage
-      const ItemInfo& it = cur.it;
-      if (cur.t0 == 0) {                  // new work item: stage its q (8 KiB) in the q ring
+      if (cur.t == t_begin || cur.ti == 0) {   // new piece: stage its q (Hq x 256 B) in the q ring
         ++it_local;
         const int qs = it_local & 1;
         mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
         if (lane == 0) {
           mbar_expect_tx(&sm.qfull[qs], (uint32_t)qbytes);
-          bulk_g2s(&sm.q[qs][0], q + ((long)it.b * s.L + it.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
+          bulk_g2s(&sm.q[qs][0], q + ((long)cur.b * s.L + cur.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
         }
       }
       const int stage = g % kStagesRing;
@@ -242,8 +241,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       mbar_wait(&sm.empty[stage], ph ^ 1u);
       __syncwarp();
       epilogue(stage, pend[stage]);
-      const int cnt = min(kTM, it.n - cur.t0);
-      ItemInfo tile{it.b, it.l, it.a0 + cur.t0, cnt};
+      const int cnt = cur.cnt();
+      ItemInfo tile{cur.b, cur.l, cur.ti * kTM, cnt};
 #pragma unroll
       for (int i = 0; i < kStagesRing; ++i)
         if (i == stage) pend[i] = tile;
@@ -260,7 +259,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       __syncwarp();
       if (lane < cnt) {
         const long slot = j_cur;
-        bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + it.l) * (long)kTokBytes, kTokBytes,
+        bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
                  &sm.full[stage]);
       }
       j_cur = j_next;
@@ -288,8 +287,11 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
   const uint32_t k_lane = (uint32_t)((ri + (mi >> 1) * 8) * kTokPad + warp * kD * 2 + (mi & 1) * 16);
   const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kTokPad + kRowBytes + warp * kD * 2 + (mi >> 1) * 16);
   int g = 0, it_local = -1;
-  for (int item = blockIdx.x; item < total; item += gridDim.x) {
-    const ItemInfo it = decode_item(s, sm.start, item);
+  Cursor cur;
+  if (t_begin < t_end) cur.seek(s, sm.start, t_begin);
+  else cur.t = t_end;
+  while (cur.t < t_end) {   // one piece (the part of one (b, l) item in this CTA's range) per pass
+    const long piece = (long)cur.b * s.L + cur.l + blockIdx.x;
     // q fragments from the q ring (rows 0..3 = the 4 query heads of this KV head, rows 4..15 zero)
     ++it_local;
     const int qs = it_local & 1;
@@ -311,10 +313,13 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int t0 = 0; t0 < it.n; t0 += kTM, ++g) {
+    for (bool more = true; more; ++g) {
       const int stage = g % kStagesRing;
       const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
-      const int cnt = min(kTM, it.n - t0);
+      const int cnt = cur.cnt();
+      more = cur.ti + 1 < cur.tiles;   // the piece ends with its item's last tile or the range's end
+      cur.next(s);
+      more = more && cur.t < t_end;
       mbar_wait(&sm.full[stage], ph);
       const uint32_t ks_addr = kvbase + stage * kStageBytes + k_lane;
       const uint32_t vs_addr = kvbase + stage * kStageBytes + v_lane;
@@ -386,7 +391,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     if (r < G) {
-      const long pi = (long)item * s.Hq + warp * G + r;
+      const long pi = piece * s.Hq + warp * G + r;
       if (qd == 0) {
         s.part_ml[pi * 2] = m_run;
         s.part_ml[pi * 2 + 1] = l_run;

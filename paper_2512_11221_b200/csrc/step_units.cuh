@@ -635,9 +635,20 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   const int h = wid % s.Hq;
   const int l = (wid / s.Hq) % s.L;
   const int b = wid / (s.Hq * s.L);
-  int chunk, nch;
-  chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
-  const long it0 = s.item_start[b] + (long)l * nch;
+  int nch;
+  long it0;
+  if (s.sk_grid) {   // stream-K pieces (asr_internal.h)
+    const int tiles = (s.act_len[b] + kSkTile - 1) / kSkTile;
+    const long T = s.item_start[s.B], S = s.item_start[b] + (long)l * tiles;
+    const int G = sk_span(T, s.sk_grid);
+    const int cf = tiles ? sk_cta_of(S, T, G) : 0;
+    nch = tiles ? sk_cta_of(S + tiles - 1, T, G) - cf + 1 : 0;
+    it0 = (long)b * s.L + l + cf;
+  } else {
+    int chunk;
+    chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+    it0 = s.item_start[b] + (long)l * nch;
+  }
   float M = -INFINITY;
   for (int c = lane; c < nch; c += 32) M = fmaxf(M, s.part_ml[((it0 + c) * s.Hq + h) * 2]);
   for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
