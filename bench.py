@@ -310,7 +310,9 @@ def run_asr(a, rank: int, world: int, local_rank: int):
             flush.zero_()
             ctx.step(Q[W + t], KN[W + t], VN[W + t], o, logits_prev=LG[W + t], entropy=ent)
             tls.append(ctx.timeline())
-        timeline = {"pre_start_end_attn_start_end_post_start_end_us": [statistics.median(x) for x in zip(*tls)]}
+        med = [round(statistics.median(x), 3) for x in zip(*tls)]
+        timeline = {"pre_start_end_attn_start_end_post_start_end_us": med[:6],
+                    "post_decide_end_next_list_end_combine_end_released_us": med[6:10]}
         print("timeline (us):", json.dumps(tls), file=sys.stderr)
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below

@@ -279,8 +279,10 @@ def asr_stage_times(ctx):
 
 
 def asr_timeline(ctx) -> list:
-    us = (ctypes.c_double * 6)()
-    _check(lib().asr_timeline(ctx, us, 6))
+    """[pre start, end, attention start, end, post start, end, decide end, next-A end, combine end,
+    post released] (us)."""
+    us = (ctypes.c_double * 10)()
+    _check(lib().asr_timeline(ctx, us, 10))
     return list(us)
 
 

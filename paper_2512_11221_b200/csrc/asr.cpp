@@ -86,8 +86,6 @@ struct asr_ctx {
   void* nccl_comm = nullptr;
   bool use_graph = true;
   bool use_pdl = true;
-  bool use_mega = false;        // persistent single-kernel step
-  int mega_grid = 0;
   bool timeline_on = false;     // ASR_TIMELINE=1
   unsigned long long* tl_buf = nullptr;
   // stage profiling
@@ -241,6 +239,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.Hkv = cfg->n_kv_heads;
     s.d = cfg->head_dim;
     s.max_ctx = (cfg->max_context + 63) & ~63;   // row stride of every per-sequence array (aligned)
+    s.cap = cfg->max_context;
     s.dtype = cfg->kv_dtype;
     s.window = cfg->window;
     s.pinned = cfg->pinned_prefix;
@@ -272,8 +271,12 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.max_splits = (int)(want < 1 ? 1 : want > cap ? cap : want);
     if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
     {
+      // decide blocks per sequence: ~2K positions each; X > 1 only if all B*X blocks are co-resident
+      // (one per SM), since they meet at a barrier to compact A_{i+1} together
       int db = (s.max_ctx + 2047) / 2048;
-      s.decide_blocks = db < 1 ? 1 : db > 32 ? 32 : db;
+      db = db < 1 ? 1 : db > 32 ? 32 : db;
+      if ((long)s.B * db > c->num_sms) db = 1;
+      s.decide_blocks = db;
     }
 
     c->kv_elem = s.dtype == ASR_KV_BF16 ? 2 : 4;
@@ -284,7 +287,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.evict_min = cfg->evict_min_absence > 0 ? cfg->evict_min_absence : 2;
     const size_t slots = s.pool_mode ? (size_t)cfg->pool_tokens : BT;
     CUDA_TRY(c->alloc(&s.kv, slots * c->tok_bytes));
-    CUDA_TRY(c->alloc(&s.act_slot, BT * 4));
+    CUDA_TRY(c->alloc(&s.act_slot, 2 * BT * 4));
     s.score_heads = cfg->score_heads > 0 ? cfg->score_heads : s.Hq;
     s.sharded = s.score_heads != s.Hq ? 1 : 0;
     CUDA_TRY(c->alloc(&s.tok_score, BT * 4));
@@ -322,8 +325,13 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.fstep, BT * 4));
     CUDA_TRY(c->alloc(&s.prompt_len, (size_t)s.B * 4));
     CUDA_TRY(c->alloc(&s.step, 4));
-    CUDA_TRY(c->alloc(&s.act_pos, BT * 4));
-    CUDA_TRY(c->alloc(&s.act_len, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.act_pos, 2 * BT * 4));
+    CUDA_TRY(c->alloc(&s.act_len, 2 * (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.dticket, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&s.dagg, (size_t)s.B * 32 * 8));
+    CUDA_TRY(c->alloc(&s.redo, 4));
+    CUDA_TRY(c->alloc(&s.pre_done, 4));
+    CUDA_TRY(c->alloc(&s.gbar, 8));
     CUDA_TRY(c->alloc(&s.item_start, (size_t)(s.B + 1) * 4));
     CUDA_TRY(c->alloc(&s.score_part, BT * s.L * 4));
     CUDA_TRY(c->alloc(&s.score, BT * 4));
@@ -353,6 +361,12 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(cudaMemsetAsync(s.err, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.ticket, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.pre_ticket, 0, (size_t)s.B * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.dticket, 0, (size_t)s.B * 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.dagg, 0, (size_t)s.B * 32 * 8, st));
+    CUDA_TRY(cudaMemsetAsync(s.redo, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.pre_done, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(s.gbar, 0, 8, st));
+    CUDA_TRY(cudaMemsetAsync(s.act_len, 0, 2 * (size_t)s.B * 4, st));
     CUDA_TRY(cudaMemcpyAsync(s.prompt_len, prompt_len, (size_t)s.B * 4, cudaMemcpyHostToDevice, st));
     for (int b = 0; b < s.B; ++b)
       if (prompt_len[b] > 0) CUDA_TRY(cudaMemsetAsync(s.res + (size_t)b * s.max_ctx, 1, prompt_len[b], st));
@@ -386,28 +400,27 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
     const char* ng = getenv("ASR_NO_GRAPH");
     c->use_graph = !(ng && ng[0] == '1');
-    CUDA_TRY(c->alloc(&s.gbar, 2 * sizeof(unsigned)));
-    CUDA_TRY(cudaMemsetAsync(s.gbar, 0, 2 * sizeof(unsigned), st));
     // device timeline: [2*kStages] stamps + [kStages] accumulated phase ns + [1] step count
-    CUDA_TRY(c->alloc(&c->tl_buf, sizeof(unsigned long long) * (3 * asr::kStages + 1)));
-    CUDA_TRY(cudaMemsetAsync(c->tl_buf, 0, sizeof(unsigned long long) * (3 * asr::kStages + 1), st));
+    CUDA_TRY(c->alloc(&c->tl_buf, sizeof(unsigned long long) * asr::kTimelineSlots));
+    CUDA_TRY(cudaMemsetAsync(c->tl_buf, 0, sizeof(unsigned long long) * asr::kTimelineSlots, st));
     const char* tlenv = getenv("ASR_TIMELINE");
     c->timeline_on = tlenv && tlenv[0] == '1';
     s.tl = nullptr;
-    // the persistent single-kernel step (cooperative launch, one CTA per SM) for the LLaMA bf16 shape:
-    // opt-in (ASR_MEGA=1) — measured slower than the 4-kernel graph with PDL at batch 1 (its four
-    // grid barriers cost more than the kernel boundaries they replace; profiles/README.md)
-    const char* nm = getenv("ASR_MEGA");
-    int coop = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, cfg->device));
-    c->use_mega = asr::attention_mma_supported(s) && coop && (nm && nm[0] == '1');
-    if (c->use_mega) {
-      CUDA_TRY(asr::attention_mma_prepare());
-      const int g = asr::step_kernel_max_grid(c->num_sms);
-      c->mega_grid = g < c->num_sms ? g : c->num_sms;
-      if (c->mega_grid < 1) c->use_mega = false;
+    s.sk_grid = asr::attention_mma_supported(s) ? c->attn_grid : 0;
+    {   // batch 1: phase A inside the attention kernel (one unit per CTA; not with the slot pool,
+        // whose prefetch copies must follow phase B)
+      const char* pa = getenv("ASR_PRE_KERNEL");
+      const bool force_kernel = pa && pa[0] == '1';
+      s.pre_in_attn = s.sk_grid && !s.pool_mode && !force_kernel &&
+                      asr::kEntSplits * s.B + s.L * s.B <= c->attn_grid;
     }
-    s.sk_grid = asr::attention_mma_supported(s) ? (c->use_mega ? c->mega_grid : c->attn_grid) : 0;
+    // A_0 of every sequence (the ledger entry of the first appended position + compaction)
+    {
+      asr::KNode pn;
+      asr::node_prepare(pn, s);
+      CUDA_TRY(pn.launch(st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
     const char* np = getenv("ASR_NO_PDL");
     c->use_pdl = !(np && np[0] == '1');
     c->last_stream = st;
@@ -532,50 +545,65 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
     a.ev = &c->prof_pending.back();
   }
   a.sd = s;   // the step's view: timeline stamps when profiling the fused kernel or on request
-  if (c->timeline_on || (a.ev && c->use_mega)) a.sd.tl = c->tl_buf;
-  if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0
-    unsigned long long init[2 * asr::kStages];
-    for (int k = 0; k < asr::kStages; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
+  if (c->timeline_on) a.sd.tl = c->tl_buf;
+  if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0 (+ phase D detail)
+    unsigned long long init[asr::kTimelineSlots];
+    for (int k = 0; k < asr::kTimelineSlots; ++k)
+      init[k] = ((k < 2 * asr::kStages && !(k & 1)) || k == asr::kTimelineSlots - 1) ? ~0ull : 0ull;
     CUDA_TRY(cudaMemcpyAsync(a.sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   return ASR_OK;
 }
 
+// The step's kernels and their dependencies (A_i was compacted by the previous step's phase D).
+//  batch 1, tensor-core path (DevState::pre_in_attn): 2 kernels
+//     attention (phase A + B on an extra warp of CTAs 0..95; a second pass inside the kernel only if
+//     recovery recompacted A_i) --full edge--> phase D   (--PDL--> scoresum --PDL--> in head-shard mode)
+//  otherwise:
+//     phase A (+B) --PDL--> attention --PDL--> [scoresum] --PDL--> phase D, and in pressure mode the
+//     prefetch copy kernel as a branch after phase A (nothing waits on it within the step).
+// A profiled step (event nodes between the stages) runs the same kernels as a chain.
 static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st) {
   const DevState& s = c->s;
   const DevState& sd = a.sd;
   const bool prof = a.ev != nullptr;
-  // the part's kernels with their stage (0 ledger pre, 1 attention, 2 decide/combine)
   asr::KNode kn_list[6];
-  int stage_of[6];
+  int stage_of[6];   // 0 ledger pre, 1 attention, 2 decide/combine (profiling events)
   int nk = 0;
   const void* lgp = a.has_logits ? a.lg : nullptr;
-  if (c->use_mega) {
-    asr::node_step(kn_list[nk], sd, lgp, a.logits_dtype, a.has_logits ? a.ent : nullptr, a.kn, a.vn, a.q, a.o,
-                   c->mega_grid);
-    stage_of[nk++] = 0;
-  } else {
-    if (part != kPartDecide) {
-      asr::node_phaseA(kn_list[nk], sd, lgp, a.logits_dtype, a.kn, a.vn);
+  float* entp = a.has_logits ? a.ent : nullptr;
+  if (part != kPartDecide) {
+    if (s.pre_in_attn) {
+      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, lgp, a.logits_dtype, entp);
+      stage_of[nk++] = 1;
+    } else {
+      const int kA = nk;
+      asr::node_phaseA(kn_list[nk], sd, lgp, a.logits_dtype, a.kn, a.vn, entp);
       stage_of[nk++] = 0;
-      asr::node_phaseB(kn_list[nk], sd, a.has_logits ? 1 : 0, a.has_logits ? a.ent : nullptr);
-      stage_of[nk++] = 0;
-      if (s.pool_mode) {   // prefetch copies: a branch beside the attention kernel
+      if (s.pool_mode) {
         asr::node_copy(kn_list[nk], sd, 32);
-        kn_list[nk].branch = true;
+        kn_list[nk].dep_full[0] = kA;
         stage_of[nk++] = 1;
       }
-      asr::node_attention(kn_list[nk], sd, a.q, c->attn_grid);
+      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, nullptr, 0, nullptr);
+      kn_list[nk].dep_prog = kA;
       stage_of[nk++] = 1;
-      if (s.sharded) {
-        asr::node_scoresum(kn_list[nk], sd);
-        stage_of[nk++] = 2;
-      }
     }
-    if (part != kPartAttend) {
-      asr::node_phaseD(kn_list[nk], sd, a.o);
+    if (s.sharded) {
+      asr::node_scoresum(kn_list[nk], sd);
+      kn_list[nk].dep_prog = nk - 1;
       stage_of[nk++] = 2;
     }
+  }
+  if (part != kPartAttend) {
+    asr::node_phaseD(kn_list[nk], sd, a.o);
+    if (part == kPartFull) {   // after the last attention-side kernel
+      // batch-1 path: a full edge — phase D launched early beside the attention measured slower
+      // (its blocks wait for whole SMs and then run its latency chain slower than a fresh launch)
+      if (s.pre_in_attn && nk == 1) kn_list[nk].dep_full[0] = nk - 1;
+      else kn_list[nk].dep_prog = nk - 1;
+    }
+    stage_of[nk++] = 2;
   }
   const bool last_part = part != kPartAttend;
   auto record = [&](int k) -> cudaError_t {   // event k once per step
@@ -583,7 +611,7 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
     a.ev_done[k] = true;
     return cudaEventRecord((*a.ev)[k], st);
   };
-  if (!c->use_graph) {
+  if (!c->use_graph) {   // direct launches in list order (a chain on the stream)
     for (int k = 0; k < nk; ++k) {
       for (int e = 0; e <= stage_of[k]; ++e) CUDA_TRY(record(e));
       CUDA_TRY(kn_list[k].launch(st));
@@ -613,7 +641,8 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
     if (!G.x) {
       CUDA_TRY(cudaGraphCreate(&G.g, 0));
       G.profiled = prof;
-      cudaGraphNode_t prev = nullptr;
+      std::vector<cudaGraphNode_t> node(nk, nullptr);
+      cudaGraphNode_t prev = nullptr;   // profiled chain
       size_t ei = 0;
       auto add_events_upto = [&](int stage) -> asr_status {   // event nodes for boundaries <= stage
         while (ei < evs.size() && evs[ei] <= stage) {
@@ -626,38 +655,38 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
         return ASR_OK;
       };
       for (int k = 0; k < nk; ++k) {
-        asr_status r = add_events_upto(stage_of[k]);
-        if (r) return r;
-        cudaGraphNode_t kn_node;
-        if (kn_list[k].branch) {   // parallel branch: depends on the previous kernel, nothing waits on it
-          CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, prev ? &prev : nullptr, prev ? 1 : 0, &kn_list[k].p));
-          G.knodes.push_back(kn_node);
-          G.last.push_back(kn_list[k]);
+        if (prof) {   // serial chain with event nodes at the stage boundaries, no PDL
+          asr_status r = add_events_upto(stage_of[k]);
+          if (r) return r;
+          CUDA_TRY(cudaGraphAddKernelNode(&node[k], G.g, prev ? &prev : nullptr, prev ? 1 : 0, &kn_list[k].p));
+          prev = node[k];
+        } else {
+          CUDA_TRY(cudaGraphAddKernelNode(&node[k], G.g, nullptr, 0, &kn_list[k].p));
+        }
+        G.knodes.push_back(node[k]);
+        G.last.push_back(kn_list[k]);
+      }
+      for (int k = 0; k < nk && !prof; ++k) {   // edges (a dependency may be listed after its dependent)
+        for (int f : kn_list[k].dep_full)
+          if (f >= 0) CUDA_TRY(cudaGraphAddDependencies(G.g, &node[f], &node[k], 1));
+        const int pg = kn_list[k].dep_prog;
+        if (pg < 0) continue;
+        if (!c->use_pdl) {
+          CUDA_TRY(cudaGraphAddDependencies(G.g, &node[pg], &node[k], 1));
           continue;
         }
-        const bool pdl = c->use_pdl && !prof && prev != nullptr;
-        CUDA_TRY(cudaGraphAddKernelNode(&kn_node, G.g, (prev && !pdl) ? &prev : nullptr, (prev && !pdl) ? 1 : 0,
-                                        &kn_list[k].p));
-        if (kn_list[k].cooperative) {
-          cudaKernelNodeAttrValue v{};
-          v.cooperative = 1;
-          CUDA_TRY(cudaGraphKernelNodeSetAttribute(kn_node, cudaLaunchAttributeCooperative, &v));
-        }
-        if (pdl) {
-          // programmatic edge: the kernel may launch before its upstream completes; it calls
-          // griddepcontrol.wait before reading the upstream's results
-          cudaGraphEdgeData ed{};
-          ed.from_port = cudaGraphKernelNodePortProgrammatic;
-          ed.to_port = 0;
-          ed.type = cudaGraphDependencyTypeProgrammatic;
-          CUDA_TRY(cudaGraphAddDependencies_v2(G.g, &prev, &kn_node, &ed, 1));
-        }
-        G.knodes.push_back(kn_node);
-        G.last.push_back(kn_list[k]);
-        prev = kn_node;
+        // programmatic edge: the kernel may launch once its upstream triggered (griddepcontrol.
+        // launch_dependents); it calls griddepcontrol.wait before reading the upstream's results
+        cudaGraphEdgeData ed{};
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.to_port = 0;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+        CUDA_TRY(cudaGraphAddDependencies_v2(G.g, &node[pg], &node[k], &ed, 1));
       }
-      asr_status r = add_events_upto(asr::kStages);
-      if (r) return r;
+      if (prof) {
+        asr_status r = add_events_upto(asr::kStages);
+        if (r) return r;
+      }
       CUDA_TRY(cudaGraphInstantiate(&G.x, G.g, 0));
     } else {
       for (int k = 0; k < nk; ++k) {
@@ -745,7 +774,6 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
 asr_status asr_step_attend(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
   if (c->attend_pending) return fail(ASR_E_STATE, "asr_step_attend twice without asr_step_decide");
-  if (c->use_mega) return fail(ASR_E_STATE, "split steps are not available with ASR_MEGA=1");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   c->pending = std::make_unique<StepArgsBox>();
   asr_status r = step_prepare(c, io, st, c->pending->a);
@@ -876,10 +904,13 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
     if (detail->count) CUDA_TRY(cudaMemcpy(detail->count, s.count + base, n * 4, cudaMemcpyDeviceToHost));
     if (detail->freeze_step) CUDA_TRY(cudaMemcpy(detail->freeze_step, s.fstep + base, n * 4, cudaMemcpyDeviceToHost));
     int32_t A = 0;
-    CUDA_TRY(cudaMemcpy(&A, s.act_len + seq, 4, cudaMemcpyDeviceToHost));
+    const int p = (int)((c->step - 1) & 1);   // parity of the last step's A_i
+    CUDA_TRY(cudaMemcpy(&A, s.act_len + (size_t)p * s.B + seq, 4, cudaMemcpyDeviceToHost));
     if (c->step == 0) A = 0;
     if (detail->active_len) *detail->active_len = A;
-    if (detail->active_list && A) CUDA_TRY(cudaMemcpy(detail->active_list, s.act_pos + base, (size_t)A * 4, cudaMemcpyDeviceToHost));
+    if (detail->active_list && A)
+      CUDA_TRY(cudaMemcpy(detail->active_list, s.act_pos + asr::act_off(s, p) + base, (size_t)A * 4,
+                          cudaMemcpyDeviceToHost));
     if (detail->scores && A) CUDA_TRY(cudaMemcpy(detail->scores, s.score + base, (size_t)A * 4, cudaMemcpyDeviceToHost));
   }
   if (err) return fail(ASR_E_INVARIANT, "device invariant violation, flags=" + std::to_string(err));
@@ -935,12 +966,6 @@ asr_status asr_stage_times(asr_ctx* c, double* ms, int32_t n, int64_t* launches)
     c->prof_free.push_back(a);
   }
   c->prof_pending.clear();
-  if (c->use_mega) {   // phases of the fused kernel: accumulated %globaltimer durations
-    unsigned long long acc[asr::kStages + 1];
-    CUDA_TRY(cudaMemcpy(acc, c->tl_buf + 2 * asr::kStages, sizeof(acc), cudaMemcpyDeviceToHost));
-    for (int k = 0; k < asr::kStages; ++k) ms[k] = (double)acc[k] * 1e-6;
-    CUDA_TRY(cudaMemset(c->tl_buf + 2 * asr::kStages, 0, sizeof(acc)));
-  }
   if (launches) *launches = c->launches;
   c->launches = 0;
   return ASR_OK;
@@ -952,9 +977,10 @@ asr_status asr_timeline(asr_ctx* c, double* us, int32_t n) {
   if (!us || n < 2 * asr::kStages) return fail(ASR_E_INVALID, "us must hold 6 values");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
-  unsigned long long t[2 * asr::kStages];
+  unsigned long long t[asr::kTimelineSlots];
   CUDA_TRY(cudaMemcpy(t, c->tl_buf, sizeof(t), cudaMemcpyDeviceToHost));
-  for (int k = 0; k < 2 * asr::kStages; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
+  const int m = n < asr::kTimelineSlots ? n : asr::kTimelineSlots;
+  for (int k = 0; k < m; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
   return ASR_OK;
 }
 

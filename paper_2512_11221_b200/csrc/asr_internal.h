@@ -7,7 +7,11 @@
 
 namespace asr {
 
-constexpr int kStages = 3;          // pre (entropy+append+recovery+compaction), attention, post (combine+decide)
+constexpr int kStages = 3;          // pre (entropy+append+recovery), attention, post (combine+decide+next A)
+// diagnostic timeline slots: [2k], [2k+1] = start / end of stage k; then phase D detail: end of the
+// decide blocks, end of the next-step preparation (A_{i+1}), end of the combine, release of phase D
+// (its first block past griddepcontrol.wait)
+constexpr int kTimelineSlots = 2 * kStages + 4;
 constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
 constexpr int kLedgerThreads = 1024;
 constexpr int kDecideThreads = 512;
@@ -51,11 +55,13 @@ enum : uint32_t {
   kErrTimer = 4u,            // Active token with timer != 0 or Frozen with timer < 1
   kErrPoolEmpty = 8u,        // pressure mode: no free device slot (pool_tokens too small)
   kErrNotResident = 16u,     // pressure mode: an Active token without a device slot
+  kErrStall = 32u,           // a wait inside the attention kernel timed out (phase B never finished)
 };
 
 // Everything a kernel may need; passed by value (all pointers are device pointers).
 struct DevState {
   int B, L, Hq, Hkv, d, max_ctx;
+  int cap;                    // max_context (tokens a sequence may hold)
   int dtype;                  // 0 bf16, 1 f32
   int window, pinned, tick_skip_new, score_scaled;
   float tau, softness;
@@ -67,6 +73,7 @@ struct DevState {
   int max_splits, chunk_min;
   int decide_blocks;          // blocks per sequence of the decide kernel
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
+  int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
   // pressure mode (pool_tokens > 0)
   int pool_mode;              // 0 full residency (slot = b*max_ctx + pos), 1 slot pool
   int evict_min;              // evict at freeze when the remaining absence >= evict_min
@@ -93,10 +100,12 @@ struct DevState {
   int32_t* fstep;             // [B][max_ctx]
   int32_t* prompt_len;        // [B]
   int32_t* step;              // [1] index of the next (or current) step
-  int32_t* act_pos;           // [B][max_ctx]
-  int32_t* act_slot;          // [B][max_ctx] device slot of each attended position
-  int32_t* act_len;           // [B]
-  int32_t* item_start;        // [B+1]
+  // A_i by step parity p = i & 1 (act_* below): phase D of step i compacts A_{i+1} into parity p^1
+  // while step i's kernels still read parity p; recovery and asr_restore recompact parity p in place
+  int32_t* act_pos;           // [2][B][max_ctx]
+  int32_t* act_slot;          // [2][B][max_ctx] device slot of each attended position
+  int32_t* act_len;           // [2][B]
+  int32_t* item_start;        // [B+1] attention work list: first item / tile of each sequence
   float* score_part;          // [B][L][max_ctx] per-layer Eq. 2 head sums per attended index
   float* score;               // [B][max_ctx]   s_j per attended index (last step)
   float* part_ml;             // [max_items][Hq][2] (m in log2 domain, l)
@@ -109,10 +118,17 @@ struct DevState {
   SeqStats* stats;            // [B]
   uint32_t* err;              // [1]
   int32_t* ticket;            // [1]
-  int32_t* pre_ticket;        // [B] compaction / recovery meeting point in the pre kernel
-  unsigned long long* tl;     // [2*kStages] diagnostic timeline (globaltimer ns), NULL = off
-  unsigned* gbar;             // [2] grid barrier of the persistent step kernel (arrivals, generation)
+  int32_t* pre_ticket;        // [B] last phase-A unit of a sequence runs its phase B (unit_finish)
+  int32_t* dticket;           // [B] arrivals of the decide blocks of a sequence, over all steps
+  unsigned long long* dagg;   // [B][32] per decide block: (step + 1) << 32 | its count of A_{i+1}
+  int32_t* redo;              // [1] recovery changed some A_i after the attention started (pre_in_attn)
+  int32_t* pre_done;          // [1] = step + 1 once phase B of the step is done (pre_in_attn)
+  unsigned* gbar;             // [2] grid barrier of the attention kernel's redo pass
+  unsigned long long* tl;     // [kTimelineSlots] diagnostic timeline (globaltimer ns), NULL = off
 };
+
+// Offset of the parity-p copy of the act_* lists.
+__host__ __device__ inline long act_off(const DevState& s, int p) { return (long)(p & 1) * s.B * s.max_ctx; }
 
 #ifdef __CUDACC__
 // Programmatic dependent launch (PDL): a kernel may let its dependent start early, and a dependent
@@ -167,8 +183,10 @@ struct KNode {
   DevState s{};
   uint64_t extra[6] = {0, 0, 0, 0, 0, 0};   // pointer / int arguments after DevState (8-byte slots)
   void* argv[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  bool cooperative = false;                  // needs all CTAs co-resident (grid barriers)
-  bool branch = false;                       // graph: parallel branch (nothing depends on it)
+  // step-graph dependencies (indices into the step's node list): full edges and at most one
+  // programmatic (PDL) edge; a node with none is a root of the graph
+  int dep_full[2] = {-1, -1};
+  int dep_prog = -1;
   void finalize(const void* func, dim3 grid, dim3 block, unsigned smem) {
     argv[0] = &s;
     for (int k = 0; k < 6; ++k) argv[k + 1] = &extra[k];
@@ -186,8 +204,6 @@ struct KNode {
     memcpy(&extra[k], &v, sizeof(P));
   }
   cudaError_t launch(cudaStream_t st) const {
-    if (cooperative)
-      return cudaLaunchCooperativeKernel(p.func, p.gridDim, p.blockDim, const_cast<void**>(argv), p.sharedMemBytes, st);
     return cudaLaunchKernel(p.func, p.gridDim, p.blockDim, const_cast<void**>(argv), p.sharedMemBytes, st);
   }
 };
@@ -207,19 +223,17 @@ NcclApi& nccl_api();
 
 // Node builders (kernels_*.cu).
 void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dtype, const void* k_new,
-                 const void* v_new);
-void node_phaseB(KNode& n, const DevState& s, int has_logits, float* entropy_out);
-void node_attention(KNode& n, const DevState& s, const void* q, int grid);
+                 const void* v_new, float* entropy_out);
+void node_attention(KNode& n, const DevState& s, const void* q, const void* k_new, const void* v_new, int grid,
+                    const void* pre_logits, int logits_dtype, float* entropy_out);
 void node_phaseD(KNode& n, const DevState& s, float* o);
-void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
-               const void* k_new, const void* v_new, const void* q, float* o, int grid);
-int step_kernel_max_grid(int num_sms);
+void node_prepare(KNode& n, const DevState& s);            // A_0 at asr_create
 void node_restore(KNode& n, const DevState& s, int seq, int level);
 void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies
 void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: layer sums -> tok_score
 int attention_grid(const DevState& s, int num_sms);
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 1/2/4/8 KV heads, <= 4 (8) q heads per KV head
 cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory
-void attention_mma_launch_shape(const DevState& s, const void** func, int* threads, unsigned* smem);
+void attention_mma_launch_shape(const DevState& s, bool logits_f32, const void** func, int* threads, unsigned* smem);
 
 }  // namespace asr

@@ -47,14 +47,14 @@ struct Vec<__nv_bfloat16> {
 };
 
 // Work-list prologue shared by every CTA: item_start[b] = sum_{b'<b} L * nch(b').
-__device__ int build_items(const DevState& s, int* sh_start) {
+__device__ int build_items(const DevState& s, const int* alen, int* sh_start) {
   // B <= 4096 sequences: serial scan by thread 0 is fine (a few microseconds at most once per CTA)
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       sh_start[b] = acc;
       int chunk, nch;
-      chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+      chunking(alen[b], s.max_splits, s.chunk_min, &chunk, &nch);
       acc += s.L * nch;
     }
     sh_start[s.B] = acc;
@@ -87,7 +87,9 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
   pdl_wait();
   pdl_trigger();
   Stamp stamp(s.tl, 1);
-  const int total = build_items(s, sh_start);
+  const int p = *s.step & 1;   // A_i lists of this step
+  const int* alen = s.act_len + p * s.B;
+  const int total = build_items(s, alen, sh_start);
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = s.Hq / s.Hkv;
   const bool lane_on = lane < ACT;
@@ -95,13 +97,13 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
   const long row = (long)s.Hkv * D;                              // K (or V) elements per token-layer
   for (int item = blockIdx.x; item < total; item += gridDim.x) {
     const int b = find_seq(sh_start, s.B, item);
-    const int A = s.act_len[b];
+    const int A = alen[b];
     int chunk, nch;
     chunking(A, s.max_splits, s.chunk_min, &chunk, &nch);
     const int r = item - sh_start[b];
     const int l = r / nch, c = r % nch;
     const int a0 = c * chunk, a1 = min(A, a0 + chunk);
-    const int* act = s.act_slot + (long)b * s.max_ctx;   // device slots of A_i
+    const int* act = s.act_slot + act_off(s, p) + (long)b * s.max_ctx;   // device slots of A_i
     // q slice of the G heads of this warp's KV head
     float qr[kMaxG][EPL];
     float m[kMaxG], lsum[kMaxG], acc[kMaxG][EPL];
@@ -191,14 +193,19 @@ int attention_grid(const DevState& s, int num_sms) {
   return (int)(max_items < g ? max_items : g);
 }
 
-void node_attention(KNode& n, const DevState& s, const void* q, int grid) {
+void node_attention(KNode& n, const DevState& s, const void* q, const void* k_new, const void* v_new, int grid,
+                    const void* pre_logits, int logits_dtype, float* entropy_out) {
   n.s = s;
   n.set(0, q);
   if (attention_mma_supported(s)) {
+    n.set(1, k_new);
+    n.set(2, v_new);
+    n.set(3, pre_logits);
+    n.set(4, entropy_out);
     const void* f;
     int threads;
     unsigned smem;
-    attention_mma_launch_shape(s, &f, &threads, &smem);
+    attention_mma_launch_shape(s, pre_logits && logits_dtype == 1, &f, &threads, &smem);
     n.finalize(f, dim3(grid), dim3(threads), smem);
     return;
   }

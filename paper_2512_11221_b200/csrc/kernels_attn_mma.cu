@@ -23,6 +23,10 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+// phase A units inside the attention kernel run on one dedicated warp (the last of the CTA)
+#define ASR_UNIT_THREADS() 32u
+#define ASR_UNIT_TID() (threadIdx.x & 31u)
+#define ASR_UNIT_SYNC() __syncwarp()
 #include "step_units.cuh"
 
 namespace asr {
@@ -43,7 +47,7 @@ struct Geo {
   static constexpr int kTokBytes = 2 * kRowBytes;     // K row then V row (contiguous in the pool)
   static constexpr int kTokPad = kTokBytes + 16;      // ldmatrix conflict-free stride
   static constexpr int kStageBytes = kTM * kTokPad;
-  static constexpr int kThreads = (HK + 1) * 32;
+  static constexpr int kThreads = (HK + 2) * 32;   // HK consumers, 1 producer, 1 phase-A warp
   static constexpr int kQBytes = HK * kGMax * kD * 2; // q of one (b, l), all heads (upper bound)
   struct Smem {
     alignas(128) uint8_t kv[kStagesRing][kStageBytes];
@@ -128,7 +132,7 @@ struct ItemInfo {
 // sequence has A active tokens in `tiles` tiles.  `start` = per-sequence first tile (prefix sums).
 struct Cursor {
   int t, b, l, ti, tiles, A;
-  __device__ void seek(const DevState& s, const int* start, int tt) {
+  __device__ void seek(const DevState& s, const int* __restrict__ alen, const int* start, int tt) {
     t = tt;
     int lo = 0, hi = s.B - 1;   // last sequence whose first tile is <= t (skips empty sequences)
     while (lo < hi) {
@@ -137,20 +141,20 @@ struct Cursor {
       else hi = mid - 1;
     }
     b = lo;
-    A = s.act_len[b];
+    A = alen[b];
     tiles = (A + kTM - 1) / kTM;
     const int r = tt - start[b];
     l = r / tiles;
     ti = r - l * tiles;
   }
-  __device__ void next(const DevState& s) {   // one tile forward
+  __device__ void next(const DevState& s, const int* __restrict__ alen) {   // one tile forward
     ++t;
     if (++ti < tiles) return;
     ti = 0;
     if (++l < s.L) return;
     l = 0;
     for (++b; b < s.B; ++b) {
-      A = s.act_len[b];
+      A = alen[b];
       tiles = (A + kTM - 1) / kTM;
       if (tiles) break;
     }
@@ -176,9 +180,18 @@ __device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
 }
 
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
-template <int HK>
-__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q, typename Geo<HK>::Smem& sm) {
+// With do_pre (batch 1, DevState::pre_in_attn) the CTA's extra warp runs its phase-A unit (entropy
+// split or append; the last unit of the sequence also runs phase B) beside the attention warps.
+template <int HK, typename TL>
+__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q,
+                                const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
+                                typename Geo<HK>::Smem& sm, bool do_pre, const TL* pre_logits, float* entropy_out,
+                                units::UnitShm& u) {
   ASR_GEO(HK);
+  const int step = *s.step;
+  const int p = step & 1;                    // A_i lists of this step
+  const int* __restrict__ alen = s.act_len + p * s.B;
+  const int* __restrict__ aslot = s.act_slot + act_off(s, p);
   const int G = s.Hq / s.Hkv;               // query heads per KV head (<= Geo<HK>::kGMax)
   const int qbytes = s.Hq * kD * 2;         // q of one (b, l)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -186,7 +199,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       sm.start[b] = acc;
-      acc += s.L * ((s.act_len[b] + kTM - 1) / kTM);
+      acc += s.L * ((alen[b] + kTM - 1) / kTM);
     }
     sm.start[s.B] = acc;
     if (blockIdx.x == 0)
@@ -215,17 +228,17 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     };
     const char* kvb = reinterpret_cast<const char*>(s.kv);
     Cursor cur;
-    if (t_begin < t_end) cur.seek(s, sm.start, t_begin);
+    if (t_begin < t_end) cur.seek(s, alen, sm.start, t_begin);
     else cur.t = t_end;
     auto load_idx = [&](const Cursor& c) -> int {
       if (c.t >= t_end || lane >= c.cnt()) return 0;
-      return max(0, __ldg(s.act_slot + (long)c.b * s.max_ctx + c.ti * kTM + lane));   // device slot
+      return max(0, __ldg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));   // device slot
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
     while (cur.t < t_end) {
       Cursor nxt = cur;
-      nxt.next(s);
+      nxt.next(s, alen);
       const int j_next = load_idx(nxt);   // in flight while this tile waits for its stage
       if (cur.t == t_begin || cur.ti == 0) {   // new piece: stage its q (Hq x 256 B) in the q ring
         ++it_local;
@@ -258,9 +271,17 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
       __syncwarp();
       if (lane < cnt) {
-        const long slot = j_cur;
-        bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
-                 &sm.full[stage]);
+        if (cur.ti * kTM + lane == cur.A - 1) {
+          // the token this step appends (always last in A_i): read from the caller's k_new / v_new, so
+          // the attention does not wait for phase A's append
+          const long r = ((long)cur.b * s.L + cur.l) * (kRowBytes / 2);
+          bulk_g2s(&sm.kv[stage][lane * kTokPad], k_new + r, kRowBytes, &sm.full[stage]);
+          bulk_g2s(&sm.kv[stage][lane * kTokPad + kRowBytes], v_new + r, kRowBytes, &sm.full[stage]);
+        } else {
+          const long slot = j_cur;
+          bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
+                   &sm.full[stage]);
+        }
       }
       j_cur = j_next;
       cur = nxt;
@@ -277,6 +298,15 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     }
     return;   // the producer warp is done with this phase
   }
+  if (warp == kHK + 1) {
+    // ================================================================== phase-A warp (batch 1)
+    if (do_pre && (int)blockIdx.x < units::phaseA_units(s, pre_logits != nullptr)) {
+      if (s.tl && lane == 0) atomicMin(&s.tl[0], gtimer());
+      units::phaseA_block<TL, __nv_bfloat16>(s, blockIdx.x, step, pre_logits, k_new, v_new, entropy_out, u);
+      if (s.tl && lane == 0) atomicMax(&s.tl[1], gtimer());
+    }
+    return;
+  }
 
   // ==================================================================== consumer warps (KV head = warp)
   const float scale = 1.4426950408889634f * 0.08838834764831845f;  // log2(e) / sqrt(128)
@@ -288,7 +318,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
   const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kTokPad + kRowBytes + warp * kD * 2 + (mi >> 1) * 16);
   int g = 0, it_local = -1;
   Cursor cur;
-  if (t_begin < t_end) cur.seek(s, sm.start, t_begin);
+  if (t_begin < t_end) cur.seek(s, alen, sm.start, t_begin);
   else cur.t = t_end;
   while (cur.t < t_end) {   // one piece (the part of one (b, l) item in this CTA's range) per pass
     const long piece = (long)cur.b * s.L + cur.l + blockIdx.x;
@@ -318,7 +348,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
       const int cnt = cur.cnt();
       more = cur.ti + 1 < cur.tiles;   // the piece ends with its item's last tile or the range's end
-      cur.next(s);
+      cur.next(s, alen);
       more = more && cur.t < t_end;
       mbar_wait(&sm.full[stage], ph);
       const uint32_t ks_addr = kvbase + stage * kStageBytes + k_lane;
@@ -404,82 +434,76 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 }
 
 
-// Standalone attention kernel (multi-kernel schedule, ASR_NO_MEGA=1).
-template <int HK>
-__global__ void __launch_bounds__(Geo<HK>::kThreads, 1) attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q) {
+// Sense-reversing barrier over the CTAs of the attention grid (one CTA per SM, all resident once
+// the kernel has triggered its dependents); used only when recovery forces a second pass.
+__device__ void grid_sync(unsigned* bar, uint32_t* err) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const unsigned long long t0 = gtimer();
+      while (*vgen == gen) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
+          atomicOr(err, kErrStall);
+          break;
+        }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The attention kernel over A_i as phase D of the previous step compacted it.  With pre_in_attn
+// (batch 1) the CTAs' extra warps also run phase A and B of the step; since recovery (phase B) may
+// recompact A_i while the attention runs, every CTA then waits for phase B (*pre_done) and, only if
+// recovery fired (*redo, rare), all CTAs pass a grid barrier and redo the attention over the new A_i.
+template <int HK, typename TL>
+__global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
+    attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_new,
+                    const __nv_bfloat16* __restrict__ v_new, const TL* logits, float* entropy_out) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   auto& sm = *reinterpret_cast<typename Geo<HK>::Smem*>(smem_raw);
-  Stamp stamp(s.tl, 1);
-  attention_prologue<HK>(sm);
-  pdl_wait();      // A_i, |A_i|, q and the appended K/V come from the upstream kernels
-  pdl_trigger();
-  attention_phase<HK>(s, q, sm);
-}
-
-__device__ __forceinline__ void stamp_min(const DevState& s, int k) {
-  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[k], gtimer());
-}
-__device__ __forceinline__ void stamp_max(const DevState& s, int k) {
-  if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[k], gtimer());
-}
-
-// The whole step as ONE persistent cooperative kernel (one CTA per SM): phases A, B (ledger units),
-// C (attention + score), D (decide + combine) separated by grid barriers; the step counter advances
-// after the last barrier.  Replaces 3-4 dependent launches whose latency chains dominated batch-1
-// steps.
-template <typename TL>
-__global__ void __launch_bounds__(Geo<8>::kThreads, 1)
-    step_kernel(DevState s, const TL* logits, float* entropy_out, const __nv_bfloat16* k_new,
-                const __nv_bfloat16* v_new, const __nv_bfloat16* __restrict__ q, float* o) {
-  constexpr int kThreads = Geo<8>::kThreads;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  auto& sm = *reinterpret_cast<Geo<8>::Smem*>(smem_raw);
   __shared__ units::UnitShm u;
-  stamp_min(s, 0);
-  attention_prologue<8>(sm);
-  const int i = *s.step;
-  // ---- phase A: entropy splits, append, speculative compaction
-  const int nA = units::phaseA_units(s, logits != nullptr);
-  for (int unit = blockIdx.x; unit < nA; unit += gridDim.x) {
-    units::run_phaseA_unit<TL, __nv_bfloat16>(s, unit, i, logits, k_new, v_new, u);
-    __syncthreads();
+  __shared__ int redo;
+  attention_prologue<HK>(sm);
+  pdl_wait();      // upstream results (phase A when it runs as its own kernel)
+  pdl_trigger();
+  const bool do_pre = s.pre_in_attn;
+  const int step = *s.step;
+  {
+    Stamp stamp(s.tl, 1);
+    attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u);
   }
-  units::grid_sync(s.gbar);
-  // ---- phase B: entropy, detector, ladder, recovery (+ recompaction)
-  for (int b = blockIdx.x; b < s.B; b += gridDim.x) {
-    units::unit_finish(s, b, i, logits != nullptr, entropy_out, u);
-    __syncthreads();
-  }
-  units::grid_sync(s.gbar);
-  stamp_max(s, 1);
-  stamp_min(s, 2);
-  // ---- phase C: attention + fused Eq. 2 score
-  attention_phase<8>(s, q, sm);
-  units::grid_sync(s.gbar);
-  stamp_max(s, 3);
-  stamp_min(s, 4);
-  // ---- phase D: decide + tick, combine
-  const int nd = s.decide_blocks * s.B;
-  const int wpb = kThreads / 32;
-  const int nc = (s.B * s.L * s.Hq + wpb - 1) / wpb;
-  for (int unit = blockIdx.x; unit < nd + nc; unit += gridDim.x) {
-    if (unit < nd) {
-      units::unit_decide(s, unit / s.decide_blocks, unit % s.decide_blocks, s.decide_blocks, i, u);
-    } else {
-      const int wid = (unit - nd) * wpb + (threadIdx.x >> 5);
-      if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
+  if (!do_pre) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const volatile int* done = s.pre_done;
+    const unsigned long long t0 = gtimer();
+    bool ok = true;
+    while (*done != step + 1) {
+      __nanosleep(64);
+      if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
+        atomicOr(s.err, kErrStall);
+        ok = false;
+        break;
+      }
     }
-    __syncthreads();
+    __threadfence();
+    redo = ok ? *reinterpret_cast<const volatile int*>(s.redo) : 0;
   }
-  stamp_max(s, 5);
-  units::grid_sync(s.gbar);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *s.step = i + 1;
-    if (s.tl) {   // accumulate the phase durations (asr_stage_times)
-      for (int k = 0; k < kStages; ++k) s.tl[2 * kStages + k] += s.tl[2 * k + 1] - s.tl[2 * k];
-      s.tl[3 * kStages] += 1;
-    }
-  }
+  __syncthreads();
+  if (!redo) return;
+  grid_sync(s.gbar, s.err);    // every CTA is past its first pass
+  attention_prologue<HK>(sm);  // fresh ring barriers
+  attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u);
 }
 
 }  // namespace
@@ -501,7 +525,10 @@ bool attention_mma_supported(const DevState& s) {
 
 template <int HK>
 cudaError_t prep_one() {
-  return cudaFuncSetAttribute(attn_mma_kernel<HK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<HK, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(typename Geo<HK>::Smem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(attn_mma_kernel<HK, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(typename Geo<HK>::Smem));
 }
 
@@ -510,41 +537,23 @@ cudaError_t attention_mma_prepare() {
   if ((e = prep_one<8>()) != cudaSuccess || (e = prep_one<4>()) != cudaSuccess || (e = prep_one<2>()) != cudaSuccess ||
       (e = prep_one<1>()) != cudaSuccess)
     return e;
-  e = cudaFuncSetAttribute(step_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Geo<8>::Smem));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(step_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Geo<8>::Smem));
+  return cudaSuccess;
 }
 
-void attention_mma_launch_shape(const DevState& s, const void** func, int* threads, unsigned* smem) {
+template <int HK>
+void shape_of(bool lf, const void** func, int* threads, unsigned* smem) {
+  *func = lf ? (const void*)attn_mma_kernel<HK, float> : (const void*)attn_mma_kernel<HK, __nv_bfloat16>;
+  *threads = Geo<HK>::kThreads;
+  *smem = sizeof(typename Geo<HK>::Smem);
+}
+
+void attention_mma_launch_shape(const DevState& s, bool logits_f32, const void** func, int* threads, unsigned* smem) {
   switch (s.Hkv) {
-    case 8: *func = (const void*)attn_mma_kernel<8>; *threads = Geo<8>::kThreads; *smem = sizeof(Geo<8>::Smem); break;
-    case 4: *func = (const void*)attn_mma_kernel<4>; *threads = Geo<4>::kThreads; *smem = sizeof(Geo<4>::Smem); break;
-    case 2: *func = (const void*)attn_mma_kernel<2>; *threads = Geo<2>::kThreads; *smem = sizeof(Geo<2>::Smem); break;
-    default: *func = (const void*)attn_mma_kernel<1>; *threads = Geo<1>::kThreads; *smem = sizeof(Geo<1>::Smem); break;
+    case 8: shape_of<8>(logits_f32, func, threads, smem); break;
+    case 4: shape_of<4>(logits_f32, func, threads, smem); break;
+    case 2: shape_of<2>(logits_f32, func, threads, smem); break;
+    default: shape_of<1>(logits_f32, func, threads, smem); break;
   }
-}
-
-int step_kernel_max_grid(int num_sms) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<__nv_bfloat16>, Geo<8>::kThreads,
-                                                    sizeof(Geo<8>::Smem)) !=
-      cudaSuccess)
-    return 0;
-  return per_sm * num_sms;
-}
-
-void node_step(KNode& n, const DevState& s, const void* logits, int logits_dtype, float* entropy_out,
-               const void* k_new, const void* v_new, const void* q, float* o, int grid) {
-  n.s = s;
-  n.set(0, logits);
-  n.set(1, entropy_out);
-  n.set(2, k_new);
-  n.set(3, v_new);
-  n.set(4, q);
-  n.set(5, o);
-  const void* f = (logits && logits_dtype == 1) ? (const void*)step_kernel<float> : (const void*)step_kernel<__nv_bfloat16>;
-  n.finalize(f, dim3(grid), dim3(Geo<8>::kThreads), sizeof(Geo<8>::Smem));
-  n.cooperative = true;
 }
 
 }  // namespace asr

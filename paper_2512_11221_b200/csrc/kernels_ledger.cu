@@ -1,49 +1,50 @@
-// paper_2512_11221_b200/csrc/kernels_ledger.cu — the generic multi-kernel schedule of the ledger
-// units (step_units.cuh), used for every shape the persistent step kernel does not cover (fp32 KV,
-// head_dim != 128, other GQA groupings):
-//   phaseA_kernel   (a6) entropy splits, (a0) append, (a3) speculative compaction — one unit per block
-//   phaseB_kernel   (a6) H, detector, ladder, recovery levels (+ recompaction)    — one block per sequence
-//   [attention]     kernels_attn.cu
-//   phaseD_kernel   (a2) decide + tick and (a4') combine; the last decide block advances the step
-//   restore_kernel  explicit SR / WR / FR (asr_restore)
+// paper_2512_11221_b200/csrc/kernels_ledger.cu — the ledger kernels of a step (units in step_units.cuh):
+//   phaseA_kernel   (a6) entropy splits, (a0) append; the last unit of each sequence runs its phase B
+//                   (entropy, detector, ladder, recovery + recompaction)
+//   [attention]     kernels_attn_mma.cu / kernels_attn.cu
+//   phaseD_kernel   (a2) decide + tick, A_{i+1} (last decide block of a sequence) and (a4') combine;
+//                   the last decide block overall advances the step
+//   prepare_kernel  A_0 at asr_create;  restore_kernel  explicit SR / WR / FR (asr_restore)
 #include "step_units.cuh"
 
 namespace asr {
 namespace {
 
 constexpr int kUnitThreads = 512;
+constexpr int kPhaseAThreads = 256;   // 16K registers: a phase-A block fits beside an attention CTA
 
+// One phase-A unit per block (+ phase B of its sequence if it finishes last).
 template <typename TL, typename TK>
-__global__ void __launch_bounds__(kUnitThreads) phaseA_kernel(DevState s, const TL* logits, const TK* k_new,
-                                                              const TK* v_new) {
+__global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, const TL* logits, const TK* k_new,
+                                                                const TK* v_new, float* entropy_out) {
   pdl_trigger();
   Stamp stamp(s.tl, 0);
   __shared__ units::UnitShm u;
-  units::run_phaseA_unit<TL, TK>(s, blockIdx.x, *s.step, logits, k_new, v_new, u);
+  units::phaseA_block<TL, TK>(s, blockIdx.x, *s.step, logits, k_new, v_new, entropy_out, u);
 }
 
-__global__ void __launch_bounds__(kUnitThreads) phaseB_kernel(DevState s, int has_logits, float* entropy_out) {
-  pdl_wait();
-  pdl_trigger();
-  Stamp stamp(s.tl, 0);
-  __shared__ units::UnitShm u;
-  units::unit_finish(s, blockIdx.x, *s.step, has_logits != 0, entropy_out, u);
-}
-
-// Blocks [0, decide_blocks * B): decide + tick (unit x of sequence b); the remaining blocks: combine,
-// one warp per (b, l, h).  The last decide block (atomic ticket) advances the step counter.
+// Blocks [0, decide_blocks * B): decide + tick (unit x of sequence b), then together A_{i+1} into the
+// other parity (unit_next_list); the last decide block overall advances the step counter and clears
+// the redo flag.  The remaining blocks: combine, one warp per (b, l, h).
 __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float* __restrict__ o) {
-  pdl_wait();      // every input comes from the attention kernel
   Stamp stamp(s.tl, 2);
+  pdl_wait();      // every input comes from the attention kernel(s) and phase A
+  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[kTimelineSlots - 1], gtimer());
   __shared__ units::UnitShm u;
   const int nd = s.decide_blocks * s.B;
   if ((int)blockIdx.x < nd) {
     const int i = *s.step;
-    units::unit_decide(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
+    const int b = blockIdx.x / s.decide_blocks;
+    units::unit_decide(s, b, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
+    __syncthreads();
+    if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[2 * kStages], gtimer());
+    units::unit_next_list(s, b, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
+    if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[2 * kStages + 1], gtimer());
     if (threadIdx.x == 0) {
       __threadfence();
-      if (atomicAdd(s.ticket, 1) == nd - 1) {
+      if (atomicAdd(s.ticket, 1) == nd - 1) {   // the last decide block of the step
         *s.ticket = 0;
+        *s.redo = 0;
         *s.step = i + 1;
       }
     }
@@ -51,12 +52,22 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
   }
   const int wid = ((int)blockIdx.x - nd) * (kUnitThreads / 32) + (threadIdx.x >> 5);
   if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
+  if (s.tl) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&s.tl[2 * kStages + 2], gtimer());
+  }
+}
+
+// A_0 of every sequence (asr_create): one block per sequence.
+__global__ void __launch_bounds__(kUnitThreads) prepare_kernel(DevState s) {
+  __shared__ units::UnitShm u;
+  units::unit_prepare(s, blockIdx.x, u);
 }
 
 // Head-sharded mode: per-token partial score sums of this shard (grid decide_blocks x B).
 __global__ void __launch_bounds__(kUnitThreads) scoresum_kernel(DevState s) {
   pdl_wait();
-  units::unit_score_sum(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks);
+  units::unit_score_sum(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, *s.step);
 }
 
 // Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.  In pressure
@@ -74,6 +85,7 @@ __global__ void __launch_bounds__(1024) restore_kernel(DevState s, int seq, int 
     s.stats[b].pending_restored += r;
     s.stats[b].pending_demand += d;
   }
+  if (n + 1 <= s.cap) units::compact_positions(s, b, n + 1, i, u);   // A_i with the restored tokens
 }
 
 // Pressure mode: fill the slots phase B allocated for next-step restores (graph branch beside the
@@ -87,25 +99,19 @@ __global__ void __launch_bounds__(kCopyThreads) copy_kernel(DevState s) {
 }  // namespace
 
 void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dtype, const void* k_new,
-                 const void* v_new) {
+                 const void* v_new, float* entropy_out) {
   n.s = s;
   n.set(0, logits);
   n.set(1, k_new);
   n.set(2, v_new);
+  n.set(3, entropy_out);
   const bool lf = logits && logits_dtype == 1;
   const void* f;
   if (s.dtype == 0)
     f = lf ? (const void*)phaseA_kernel<float, __nv_bfloat16> : (const void*)phaseA_kernel<__nv_bfloat16, __nv_bfloat16>;
   else
     f = lf ? (const void*)phaseA_kernel<float, float> : (const void*)phaseA_kernel<__nv_bfloat16, float>;
-  n.finalize(f, dim3(units::phaseA_units(s, logits != nullptr)), dim3(kUnitThreads), 0);
-}
-
-void node_phaseB(KNode& n, const DevState& s, int has_logits, float* entropy_out) {
-  n.s = s;
-  n.set(0, has_logits);
-  n.set(1, entropy_out);
-  n.finalize((const void*)phaseB_kernel, dim3(s.B), dim3(kUnitThreads), 0);
+  n.finalize(f, dim3(units::phaseA_units(s, logits != nullptr)), dim3(kPhaseAThreads), 0);
 }
 
 void node_phaseD(KNode& n, const DevState& s, float* o) {
@@ -114,6 +120,11 @@ void node_phaseD(KNode& n, const DevState& s, float* o) {
   const int warps = s.B * s.L * s.Hq;
   const int wpb = kUnitThreads / 32;
   n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + (warps + wpb - 1) / wpb), dim3(kUnitThreads), 0);
+}
+
+void node_prepare(KNode& n, const DevState& s) {
+  n.s = s;
+  n.finalize((const void*)prepare_kernel, dim3(s.B), dim3(kUnitThreads), 0);
 }
 
 void node_scoresum(KNode& n, const DevState& s) {

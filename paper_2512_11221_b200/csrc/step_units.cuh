@@ -1,20 +1,27 @@
-// paper_2512_11221_b200/csrc/step_units.cuh — the ledger-side work units of one ASR-KF-EGR step,
-// written once and scheduled two ways: by the persistent step kernel (kernels_attn_mma.cu, one
-// cooperative launch per step, phases separated by grid barriers) and by the generic multi-kernel
-// path (kernels_ledger.cu).  Every unit uses the whole thread block (any blockDim multiple of 32,
-// <= 1024) and is followed by a __syncthreads() in its scheduler.
+// paper_2512_11221_b200/csrc/step_units.cuh — the ledger-side work units of one ASR-KF-EGR step.
+// A unit runs on a team of ASR_UNIT_THREADS() threads (a multiple of 32, <= 1024; team rank
+// ASR_UNIT_TID()) that synchronise with ASR_UNIT_SYNC(): the whole block in kernels_ledger.cu, one
+// dedicated warp of the attention CTA in kernels_attn_mma.cu (where phase A of a batch-1 step runs
+// inside the attention kernel, beside the producer and consumer warps).
 //
 //   phase A  unit_entropy_split   (a6) partial (m, Z, S) of one split of a logits row
-//            unit_compact         (a0) ledger entry of the appended position, (a3) A_i (speculative:
-//                                 assumes no recovery this step)
 //            unit_append          (a0) the new token's K/V rows of (b, l) -> its slot
-//   phase B  unit_finish          (a6) H = ln Z - S/Z, detector (R-det), ladder (R-ladder) and, when
-//                                 a level fires (rare), the level (Sec 3.6) + recompaction
-//   phase C  attention            (a4)+(a1) — kernels_attn_mma.cu / kernels_attn.cu
+//            unit_finish          (a6) H = ln Z - S/Z, detector (R-det), ladder (R-ladder) and, when
+//                                 a level fires (rare), the level (Sec 3.6) + recompaction of A_i;
+//                                 run by the last phase-A unit of the sequence
+//   phase C  attention            (a4)+(a1) — kernels_attn_mma.cu / kernels_attn.cu (A_i is known before
+//                                 the step; at batch 1 phase A runs inside the tensor-core kernel)
 //   phase D  unit_decide          (a2) Eq. 2 finish, threshold, Eq. 3, freeze, R0 tick (Alg. 1 3-15)
+//            unit_prepare         (a0) ledger entry of the next appended position, (a3) A_{i+1} — run
+//                                 by the last decide block of the sequence
 //            combine_warp         (a4') fixed-order combine of the split-KV partials -> O
 // Floating-point reductions are in a fixed order, so a step is bitwise deterministic.
 #pragma once
+#ifndef ASR_UNIT_THREADS
+#define ASR_UNIT_THREADS() blockDim.x
+#define ASR_UNIT_TID() threadIdx.x
+#define ASR_UNIT_SYNC() __syncthreads()
+#endif
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -29,6 +36,7 @@ struct UnitShm {
   float wm[32], wz[32], ws[32];
   int level;
   int total;
+  int last;
 };
 
 __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
@@ -51,26 +59,6 @@ __device__ __forceinline__ void load8<float>(const float* p, float* x) {
   const float4 a = __ldg(reinterpret_cast<const float4*>(p));
   const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
   x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-}
-
-// ---------------------------------------------------------------------------------- grid barrier
-// Sense-reversing barrier over all CTAs of a cooperative launch (bar[0] arrivals, bar[1] generation).
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------------- (a5) slot pool
@@ -96,20 +84,20 @@ __device__ void copy_token_h2d(const DevState& s, int b, int pos, int slot) {
   const uint4* src = reinterpret_cast<const uint4*>(s.host_kv + ((long)b * s.max_ctx + pos) * s.tok_bytes);
   uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s.kv) + (long)slot * s.tok_bytes);
   const int nv = (int)(s.tok_bytes / 16);
-  for (int v0 = (int)threadIdx.x; v0 < nv; v0 += 8 * (int)blockDim.x) {
+  for (int v0 = (int)ASR_UNIT_TID(); v0 < nv; v0 += 8 * (int)ASR_UNIT_THREADS()) {
     uint4 x[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int v = v0 + k * (int)blockDim.x;
+      const int v = v0 + k * (int)ASR_UNIT_THREADS();
       if (v < nv) x[k] = src[v];
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int v = v0 + k * (int)blockDim.x;
+      const int v = v0 + k * (int)ASR_UNIT_THREADS();
       if (v < nv) dst[v] = x[k];
     }
   }
-  if (threadIdx.x == 0) atomicAdd(s.h2d, (unsigned long long)s.tok_bytes);
+  if (ASR_UNIT_TID() == 0) atomicAdd(s.h2d, (unsigned long long)s.tok_bytes);
 }
 
 // ---------------------------------------------------------------------------------- (a6) entropy
@@ -132,7 +120,7 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
   const bool vecok = (reinterpret_cast<uintptr_t>(row) & 31) == 0;
   const float invT = 1.0f / s.ent_temp;
   float m = -INFINITY, z = 0.f, sx = 0.f;
-  for (int v = e0 + (int)threadIdx.x * 8; v < e1; v += (int)blockDim.x * 8) {
+  for (int v = e0 + (int)ASR_UNIT_TID() * 8; v < e1; v += (int)ASR_UNIT_THREADS() * 8) {
     float x[8];
     if (vecok && v + 8 <= e1) {
       load8<TL>(row + v, x);
@@ -158,109 +146,140 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
   for (int o = 16; o > 0; o >>= 1)
     tri_merge(m, z, sx, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, z, o),
               __shfl_xor_sync(0xffffffffu, sx, o));
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = ASR_UNIT_TID() >> 5, lane = ASR_UNIT_TID() & 31;
   if (lane == 0) { u.wm[w] = m; u.wz[w] = z; u.ws[w] = sx; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  ASR_UNIT_SYNC();
+  if (ASR_UNIT_TID() == 0) {
     float M = -INFINITY, Z = 0.f, S = 0.f;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tri_merge(M, Z, S, u.wm[k], u.wz[k], u.ws[k]);
+    for (int k = 0; k < (int)(ASR_UNIT_THREADS() >> 5); ++k) tri_merge(M, Z, S, u.wm[k], u.wz[k], u.ws[k]);
     float* ep = s.ent_part + ((long)b * kEntSplits + split) * 3;
     ep[0] = M; ep[1] = Z; ep[2] = S;
   }
 }
 
 // ---------------------------------------------------------------------------------- (a3) compaction
-__device__ __forceinline__ int active_mask16(uint4 x, uint32_t* m) {  // 1 per byte iff residency == 1
-  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    m[k] = w[k] & 0x01010101u & ~((w[k] >> 1) & 0x01010101u);
-    c += __popc(m[k]);
-  }
-  return c;
+// A_i = sorted Active positions into the parity-p lists.  A team compacts the positions [lo, hi) of
+// a row (lo a multiple of 128) in 128-position groups: lane k of a warp reads the 4 residency bytes of
+// positions 4k..4k+3 of a group (one coalesced 128-byte load per group); a warp scan of the per-lane
+// counts gives every lane its output offset, so the writes of a group are contiguous too.
+// Residency (and slots) are read through L2 (ld.global.cg): other blocks of the same kernel wrote
+// them (decide slices, recovery), and this block's L1 may hold older lines.
+__device__ __forceinline__ uint32_t active_bits4(const uint32_t* res4, int q, int n) {
+  // bit k set iff position 4q + k < n is Active (residency byte == 1)
+  if (4 * q >= n) return 0u;
+  const uint32_t e = __vcmpeq4(__ldcg(res4 + q), 0x01010101u);   // 0xff per byte equal to 1
+  uint32_t m = ((e >> 7) & 1u) | ((e >> 14) & 2u) | ((e >> 21) & 4u) | ((e >> 28) & 8u);
+  const int left = n - 4 * q;
+  if (left < 4) m &= (1u << left) - 1u;
+  return m;
 }
 
-// A_i = sorted Active positions of [0, n) (rows are 64-aligned, positions >= n hold 0).
-__device__ void compact_positions(const DevState& s, int b, int n, UnitShm& u) {
-  const long base = (long)b * s.max_ctx;
-  const uint8_t* res = s.res + base;
-  const int nvec = (n + 15) >> 4;
-  const int per = (nvec + (int)blockDim.x - 1) / (int)blockDim.x;
-  const int v0 = min(nvec, (int)threadIdx.x * per), v1 = min(nvec, v0 + per);
-  int cnt = 0;
+struct Compactor {
+  static constexpr int kKeep = 8;   // masks of a warp's first kKeep groups stay in registers
+  const uint32_t* res4;
+  int lo, hi, g0, g1;
+  uint32_t keep[kKeep];
+  // count pass: returns the team's total; u.wsum[w] = exclusive offset of warp w within the team
+  __device__ int count(const DevState& s, int b, int lo_, int hi_, UnitShm& u) {
+    res4 = reinterpret_cast<const uint32_t*>(s.res + (long)b * s.max_ctx);   // rows are 64-byte aligned
+    lo = lo_;
+    hi = hi_;
+    const int tid = (int)ASR_UNIT_TID(), lane = tid & 31, w = tid >> 5, nw = (int)ASR_UNIT_THREADS() >> 5;
+    const int ngrp = hi > lo ? (hi - lo + 127) >> 7 : 0;
+    const int per = (ngrp + nw - 1) / nw;
+    g0 = min(ngrp, w * per);
+    g1 = min(ngrp, g0 + per);
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kKeep; ++k) {
+      keep[k] = g0 + k < g1 ? active_bits4(res4, (lo >> 2) + (g0 + k) * 32 + lane, hi) : 0u;
+      cnt += __popc(keep[k]);
+    }
 #pragma unroll 4
-  for (int v = v0; v < v1; ++v) {
-    uint32_t m[4];
-    cnt += active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int incl = cnt;
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) u.wsum[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    int x = lane < (int)(blockDim.x >> 5) ? u.wsum[lane] : 0;
-    int xi = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, xi, o);
-      if (lane >= o) xi += y;
-    }
-    u.wsum[lane] = xi - x;  // exclusive warp offsets
-    if (lane == 31) u.total = xi;
-  }
-  __syncthreads();
-  int off = u.wsum[w] + incl - cnt;
-  int32_t* out = s.act_pos + base;
-  int32_t* out_slot = s.act_slot + base;
-  const int32_t* slot_of = s.slot_of + base;
-  for (int v = v0; v < v1; ++v) {
-    uint32_t m[4];
-    active_mask16(*reinterpret_cast<const uint4*>(res + v * 16), m);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      while (m[k]) {
-        const int bit = __ffs(m[k]) - 1;   // bit 8*q of byte q
-        const int j = v * 16 + k * 4 + (bit >> 3);
-        out[off] = j;
-        out_slot[off] = s.pool_mode ? slot_of[j] : (int)(base + j);
-        ++off;
-        m[k] &= m[k] - 1;
+    for (int g = g0 + kKeep; g < g1; ++g) cnt += __popc(active_bits4(res4, (lo >> 2) + g * 32 + lane, hi));
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) u.wsum[w] = cnt;
+    ASR_UNIT_SYNC();
+    if (w == 0) {
+      const int x = lane < nw ? u.wsum[lane] : 0;
+      int xi = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += y;
       }
+      u.wsum[lane] = xi - x;  // exclusive warp offsets
+      if (lane == 31) u.total = xi;
+    }
+    ASR_UNIT_SYNC();
+    return u.total;
   }
-  if (threadIdx.x == 0) {
-    s.act_len[b] = u.total;
-    s.stats[b].attended = u.total;
-    if (u.total == 0) atomicOr(s.err, kErrEmptyActive);
+  // write pass: the team's positions go to compact indices base, base + 1, ... of the parity-p lists
+  __device__ void write(const DevState& s, int b, int p, int base_idx, const UnitShm& u) {
+    const int tid = (int)ASR_UNIT_TID(), lane = tid & 31, w = tid >> 5;
+    const long row = (long)b * s.max_ctx;
+    int32_t* out = s.act_pos + act_off(s, p) + row;
+    int32_t* out_slot = s.act_slot + act_off(s, p) + row;
+    const int32_t* slot_of = s.slot_of + row;
+    int off = base_idx + u.wsum[w];
+    for (int g = g0; g < g1; ++g) {
+      const int q = (lo >> 2) + g * 32 + lane;
+      uint32_t m = 0u;
+      if (g - g0 < kKeep) {
+#pragma unroll
+        for (int k = 0; k < kKeep; ++k)
+          if (g - g0 == k) m = keep[k];
+      } else {
+        m = active_bits4(res4, q, hi);
+      }
+      const int c = __popc(m);
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int o = off + incl - c;
+      while (m) {
+        const int j = 4 * q + __ffs(m) - 1;
+        out[o] = j;
+        out_slot[o] = s.pool_mode ? __ldcg(slot_of + j) : (int)(row + j);
+        ++o;
+        m &= m - 1;
+      }
+      off += __shfl_sync(0xffffffffu, incl, 31);
+    }
   }
+};
+
+// A_i of [0, n) by one team.
+__device__ void compact_positions(const DevState& s, int b, int n, int p, UnitShm& u) {
+  Compactor c;
+  const int total = c.count(s, b, 0, n, u);
+  c.write(s, b, p, 0, u);
+  if (ASR_UNIT_TID() == 0) {
+    s.act_len[(p & 1) * s.B + b] = total;
+    if (total == 0) atomicOr(s.err, kErrEmptyActive);
+  }
+  ASR_UNIT_SYNC();
 }
 
-__device__ void unit_compact(const DevState& s, int b, int i, UnitShm& u) {
-  const int n = s.prompt_len[b] + i + 1;  // total after the append
-  if (threadIdx.x == 0) {
-    const long j = (long)b * s.max_ctx + n - 1;   // the token produced by the previous step (Alg. 1 line 16)
-    s.res[j] = 1;
-    s.timer[j] = 0;
-    s.count[j] = 0;
-    s.fstep[j] = -1;
-    if (s.pool_mode) {
-      s.slot_of[j] = s.spare[b];                      // the slot reserved by the previous step
-      s.pf_count[(i & 1) * s.B + b] = 0;              // this step's decide fills list i & 1
-    }
-    SeqStats& st = s.stats[b];
-    st.evicted = 0;
-    st.demand = st.pending_demand;
-    st.pending_demand = 0;
-    st.restored_pre = st.pending_restored;
-    st.pending_restored = 0;
-    st.restored_tick = 0;
-    st.frozen_this_step = 0;
-  }
-  __syncthreads();
-  compact_positions(s, b, n, u);
+// Ledger entry of position j = the token step i appends (Alg. 1 line 16 of the previous step:
+// Active, c = 0, timer 0, its reserved slot in pressure mode).
+__device__ __forceinline__ void ledger_entry_new(const DevState& s, int b, int j) {
+  const long k = (long)b * s.max_ctx + j;
+  s.res[k] = 1;
+  s.timer[k] = 0;
+  s.count[k] = 0;
+  s.fstep[k] = -1;
+  if (s.pool_mode) s.slot_of[k] = s.spare[b];   // the slot reserved by phase B
+}
+
+// At asr_create: the ledger entry of the position step 0 appends and A_0 (parity 0).
+__device__ void unit_prepare(const DevState& s, int b, UnitShm& u) {
+  const int n = s.prompt_len[b] + 1;  // tokens after step 0's append
+  if (n > s.cap) return;
+  if (ASR_UNIT_TID() == 0) ledger_entry_new(s, b, n - 1);
+  ASR_UNIT_SYNC();
+  compact_positions(s, b, n, 0, u);
 }
 
 template <typename TK>
@@ -279,13 +298,13 @@ __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __
   const int vec = (int)(16 / sizeof(TK));
   if (row % vec == 0) {
     const int nv = row / vec;
-    for (int t = threadIdx.x; t < 2 * nv; t += blockDim.x) {
+    for (int t = ASR_UNIT_TID(); t < 2 * nv; t += ASR_UNIT_THREADS()) {
       const uint4 x = *(reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv));
       reinterpret_cast<uint4*>(dst)[t] = x;
       if (mir) reinterpret_cast<uint4*>(mir)[t] = x;
     }
   } else {
-    for (int t = threadIdx.x; t < 2 * row; t += blockDim.x) {
+    for (int t = ASR_UNIT_TID(); t < 2 * row; t += ASR_UNIT_THREADS()) {
       const TK x = t < row ? ks[t] : vs[t - row];
       dst[t] = x;
       if (mir) mir[t] = x;
@@ -300,7 +319,7 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   uint8_t* res = s.res + (long)b * s.max_ctx;
   int32_t* timer = s.timer + (long)b * s.max_ctx;
   const int32_t* fstep = s.fstep + (long)b * s.max_ctx;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  for (int j = ASR_UNIT_TID(); j < n; j += ASR_UNIT_THREADS()) {
     if (res_active(res[j])) continue;
     bool go = level == 1 ? timer[j] > 1 : level == 2 ? fstep[j] >= i - s.wr_window : true;
     if (go) {
@@ -315,7 +334,7 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   }
   if (level >= 3 && s.fr_clear_counts) {
     uint32_t* cnt = s.count + (long)b * s.max_ctx;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) cnt[j] = 0;
+    for (int j = ASR_UNIT_TID(); j < n; j += ASR_UNIT_THREADS()) cnt[j] = 0;
   }
   return restored;
 }
@@ -323,44 +342,57 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
 // Copy back (synchronously, whole block) every token apply_level listed for sequence b; returns
 // the count.  Runs with no concurrent pushes (phase B / asr_restore).
 __device__ int demand_copies(const DevState& s, int b) {
-  __syncthreads();
+  ASR_UNIT_SYNC();
   const int nd = s.cp_count[b];
   for (int k = 0; k < nd; ++k) {
     const int j = s.cp_list[(long)b * s.max_ctx + k];
     copy_token_h2d(s, b, j, s.slot_of[(long)b * s.max_ctx + j]);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) s.cp_count[b] = 0;
-  __syncthreads();
+  ASR_UNIT_SYNC();
+  if (ASR_UNIT_TID() == 0) s.cp_count[b] = 0;
+  ASR_UNIT_SYNC();
   return nd;
 }
 
 __device__ int block_sum_int(int v, UnitShm& u) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __syncthreads();
+  const int w = ASR_UNIT_TID() >> 5, lane = ASR_UNIT_TID() & 31, nw = ASR_UNIT_THREADS() >> 5;
+  ASR_UNIT_SYNC();
   if (lane == 0) u.sh[w] = v;
-  __syncthreads();
+  ASR_UNIT_SYNC();
   int t = 0;
   for (int k = 0; k < nw; ++k) t += u.sh[k];
-  __syncthreads();
+  ASR_UNIT_SYNC();
   return t;
 }
 
 // Phase B for sequence b: entropy of logits_prev (if given), detector, ladder, recovery.
 __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, float* entropy_out, UnitShm& u) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (s.pool_mode && threadIdx.x == 0) s.cp_count[b] = 0;   // the previous step's copies are done
+  const int lane = ASR_UNIT_TID() & 31, w = ASR_UNIT_TID() >> 5;
+  if (ASR_UNIT_TID() == 0) {   // per-step counters (phase D of this step adds to them)
+    if (s.pool_mode) {
+      s.cp_count[b] = 0;                              // the previous step's copies are done
+      s.pf_count[(i & 1) * s.B + b] = 0;              // this step's decide fills list i & 1
+    }
+    SeqStats& st = s.stats[b];
+    st.evicted = 0;
+    st.demand = st.pending_demand;
+    st.pending_demand = 0;
+    st.restored_pre = st.pending_restored;
+    st.pending_restored = 0;
+    st.restored_tick = 0;
+    st.frozen_this_step = 0;
+  }
   if (w == 0) {
     int level = 0;
     if (has_logits) {
       // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
-      const float* ep = s.ent_part + (long)b * kEntSplits * 3;
+      const float* ep = s.ent_part + (long)b * kEntSplits * 3;   // written by other blocks: via L2
       float M = -INFINITY, Zl = 0.f, Sl = 0.f;
 #pragma unroll
       for (int k = 0; k < kEntSplits / 32; ++k) {
         const int sp = k * 32 + lane;
-        tri_merge(M, Zl, Sl, ep[sp * 3], ep[sp * 3 + 1], ep[sp * 3 + 2]);
+        tri_merge(M, Zl, Sl, __ldcg(ep + sp * 3), __ldcg(ep + sp * 3 + 1), __ldcg(ep + sp * 3 + 2));
       }
       for (int o = 16; o > 0; o >>= 1)
         tri_merge(M, Zl, Sl, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Zl, o),
@@ -409,14 +441,15 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
     }
     if (lane == 0) u.level = level;
   }
-  __syncthreads();
+  ASR_UNIT_SYNC();
   const int level = u.level;
   int restored = 0, demand = 0;
   if (level > 0) {   // rare: apply the level (copy evicted tokens back), then recompact A_i
     const int n = s.prompt_len[b] + i + 1;
     restored = block_sum_int(apply_level(s, b, n - 1, level, i), u);
     if (s.pool_mode) demand = demand_copies(s, b);
-    compact_positions(s, b, n, u);
+    compact_positions(s, b, n, i, u);
+    if (ASR_UNIT_TID() == 0) *s.redo = 1;   // a speculative attention pass over the old A_i is void
   }
   int prefetched = 0;
   if (s.pool_mode) {
@@ -426,17 +459,17 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
     const int np = i > 0 ? s.pf_count[r] : 0;
     const int32_t* pl = s.pf_list + (long)r * s.max_ctx;
     int32_t* slot_of = s.slot_of + (long)b * s.max_ctx;
-    for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    for (int k = ASR_UNIT_TID(); k < np; k += ASR_UNIT_THREADS()) {
       const int j = pl[k];
       if (slot_of[j] >= 0) continue;   // already back (recovery demand copy)
       slot_of[j] = pool_pop(s);
       s.cp_list[(long)b * s.max_ctx + atomicAdd(&s.cp_count[b], 1)] = j;
     }
-    __syncthreads();
+    ASR_UNIT_SYNC();
     prefetched = s.cp_count[b];
-    if (threadIdx.x == 0) s.spare[b] = pool_pop(s);   // slot of the token the next step appends
+    if (ASR_UNIT_TID() == 0) s.spare[b] = pool_pop(s);   // slot of the token the next step appends
   }
-  if (threadIdx.x == 0) {
+  if (ASR_UNIT_TID() == 0) {
     SeqStats& st = s.stats[b];
     st.prefetched = prefetched;
     st.demand += demand;
@@ -444,6 +477,7 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
     st.recovery_action = level;
     st.rewalk_requested = level == 4;
     st.entropy_valid = has_logits ? 1 : 0;
+    st.attended = s.act_len[(i & 1) * s.B + b];
     s.rec_action[b] = level;
   }
 }
@@ -467,28 +501,27 @@ __device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
 }
 
 // Eq. 2 numerator of attended index a: sum over layers in order l = 0..L-1 of the per-layer head sums
-// (loads issued 8 at a time so their latencies overlap).
+// (the loads of up to 32 layers are issued before the first add, so their latencies overlap).
 __device__ __forceinline__ float layer_sum(const DevState& s, int b, int a) {
   const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
   float sum = 0.f;
-  int l = 0;
-  for (; l + 8 <= s.L; l += 8) {
-    float v[8];
+  for (int l0 = 0; l0 < s.L; l0 += 32) {
+    float v[32];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = sp[(long)(l + q) * s.max_ctx];
+    for (int q = 0; q < 32; ++q) v[q] = l0 + q < s.L ? sp[(long)(l0 + q) * s.max_ctx] : 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) sum += v[q];
+    for (int q = 0; q < 32; ++q)
+      if (l0 + q < s.L) sum += v[q];
   }
-  for (; l < s.L; ++l) sum += sp[(long)l * s.max_ctx];
   return sum;
 }
 
 // Head-sharded mode: this shard's per-token sums (its heads, all layers) for a slice of A_b.
-__device__ void unit_score_sum(const DevState& s, int b, int x, int X) {
-  const int A = s.act_len[b];
+__device__ void unit_score_sum(const DevState& s, int b, int x, int X, int i) {
+  const int A = s.act_len[(i & 1) * s.B + b];
   const int per_a = (A + X - 1) / X;
   const int a_end = min(A, (x + 1) * per_a);
-  for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x)
+  for (int a = x * per_a + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS())
     s.tok_score[(long)b * s.max_ctx + a] = layer_sum(s, b, a);
 }
 
@@ -499,7 +532,8 @@ __device__ void unit_score_sum(const DevState& s, int b, int x, int X) {
 __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
   const int n = s.prompt_len[b] + i + 1;
   const long base = (long)b * s.max_ctx;
-  const int A = s.act_len[b];
+  const int A = s.act_len[(i & 1) * s.B + b];
+  const int32_t* act_pos = s.act_pos + act_off(s, i) + base;
   uint8_t* res = s.res + base;
   int32_t* timer = s.timer + base;
   uint32_t* cnt = s.count + base;
@@ -516,7 +550,7 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   int pt[kPF];
 #pragma unroll
   for (int k = 0; k < kPF; ++k) {
-    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    const int j = n0 + (int)ASR_UNIT_TID() + k * (int)ASR_UNIT_THREADS();
     pr[k] = j < n_end ? res[j] : (uint8_t)1;
     pt[k] = j < n_end ? timer[j] : 0;
   }
@@ -524,8 +558,8 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   const int pf_row = (i & 1) * s.B + b;   // prefetch list written by this step
   const int per_a = (A + X - 1) / X;
   const int a_end = min(A, (x + 1) * per_a);
-  for (int a = x * per_a + threadIdx.x; a < a_end; a += blockDim.x) {
-    const int j = s.act_pos[base + a];
+  for (int a = x * per_a + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS()) {
+    const int j = act_pos[a];
     const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
     float sj = sum / heads;             // mean over the L*Hq (layer, head) pairs (correctly rounded)
     if (s.score_scaled) sj = sj / sqrt_d;
@@ -575,22 +609,22 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   };
 #pragma unroll
   for (int k = 0; k < kPF; ++k) {
-    const int j = n0 + (int)threadIdx.x + k * (int)blockDim.x;
+    const int j = n0 + (int)ASR_UNIT_TID() + k * (int)ASR_UNIT_THREADS();
     if (j < n_end) tick(j, pr[k], pt[k]);
   }
-  for (int j = n0 + (int)threadIdx.x + kPF * (int)blockDim.x; j < n_end; j += blockDim.x) tick(j, res[j], timer[j]);
+  for (int j = n0 + (int)ASR_UNIT_TID() + kPF * (int)ASR_UNIT_THREADS(); j < n_end; j += ASR_UNIT_THREADS()) tick(j, res[j], timer[j]);
   if (err) atomicOr(s.err, err);
   int f = frozen_now, r = restored;
   for (int o = 16; o > 0; o >>= 1) {
     f += __shfl_xor_sync(0xffffffffu, f, o);
     r += __shfl_xor_sync(0xffffffffu, r, o);
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = ASR_UNIT_TID() >> 5, lane = ASR_UNIT_TID() & 31;
   if (lane == 0) { u.sh[w] = f; u.sh2[w] = r; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  ASR_UNIT_SYNC();
+  if (ASR_UNIT_TID() == 0) {
     f = 0; r = 0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { f += u.sh[k]; r += u.sh2[k]; }
+    for (int k = 0; k < (int)(ASR_UNIT_THREADS() >> 5); ++k) { f += u.sh[k]; r += u.sh2[k]; }
     SeqStats& st = s.stats[b];
     if (f) atomicAdd(&st.frozen_this_step, f);
     if (r) atomicAdd(&st.restored_tick, r);
@@ -601,10 +635,87 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   }
 }
 
+// After unit_decide of step i (whole ledger of sequence b final for this step): A_{i+1} into parity
+// (i+1) & 1, by the X decide blocks of b together — block x compacts positions [x*P, (x+1)*P)
+// (P = ceil(n/X) rounded up to 128; the last block also appends position n, the token step i+1
+// appends).  The blocks first meet at a per-sequence barrier (dticket counts arrivals over all steps;
+// the host only uses X > 1 when every decide block is co-resident), then each publishes its count
+// in dagg[b][x] tagged with the step and adds up its predecessors' counts (decoupled look-back
+// without a chain) to place its part.
+__device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
+  const int n = s.prompt_len[b] + i + 1;    // tokens held after step i
+  const bool next = n + 1 <= s.cap;         // step i+1 can run
+  const int tid = (int)ASR_UNIT_TID();
+  if (X > 1) {
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&s.dticket[b], 1);
+      const volatile int* c = s.dticket + b;
+      const int want = (i + 1) * X;
+      const unsigned long long t0 = gtimer();
+      while (*c < want) {
+        __nanosleep(32);
+        if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
+          atomicOr(s.err, kErrStall);
+          break;
+        }
+      }
+      __threadfence();
+    }
+  }
+  const int per = (((n + X - 1) / X) + 127) & ~127;
+  const int lo = min(n, x * per);
+  int hi = x == X - 1 ? n : min(n, lo + per);
+  if (x == X - 1 && next) {
+    if (tid == 0) ledger_entry_new(s, b, n);
+    hi = n + 1;
+  }
+  ASR_UNIT_SYNC();
+  Compactor c;
+  const int cnt = c.count(s, b, lo, hi, u);
+  const unsigned long long tag = (unsigned long long)(unsigned)(i + 1) << 32;
+  if (X > 1) {
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(&s.dagg[(long)b * 32 + x], tag | (unsigned)cnt);
+    }
+    if (tid < 32) {   // warp 0: lane k waits for predecessor k's count
+      int pre = 0;
+      if (tid < x) {
+        const volatile unsigned long long* a = s.dagg + (long)b * 32 + tid;
+        unsigned long long v = *a;
+        const unsigned long long t0 = gtimer();
+        while ((v & 0xffffffff00000000ull) != tag) {
+          __nanosleep(32);
+          v = *a;
+          if (gtimer() - t0 > 2000000000ull) {
+            atomicOr(s.err, kErrStall);
+            break;
+          }
+        }
+        pre = (int)(v & 0xffffffffu);
+      }
+      for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+      if (tid == 0) u.level = pre;
+    }
+    ASR_UNIT_SYNC();
+  } else if (tid == 0) {
+    u.level = 0;
+  }
+  if (X == 1) ASR_UNIT_SYNC();
+  const int base = u.level;
+  if (next) c.write(s, b, (i + 1) & 1, base, u);
+  if (tid == 0 && x == X - 1 && next) {
+    s.act_len[((i + 1) & 1) * s.B + b] = base + cnt;
+    if (base + cnt == 0) atomicOr(s.err, kErrEmptyActive);
+  }
+  ASR_UNIT_SYNC();
+}
+
 // Pressure mode: copy the tokens phase B gave slots to (this step's prefetch list) from the host
 // mirror, one token per block at a time; runs beside the attention kernel (graph branch).
 __device__ void prefetch_copies(const DevState& s, int* start) {
-  if (threadIdx.x == 0) {
+  if (ASR_UNIT_TID() == 0) {
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       start[b] = acc;
@@ -612,7 +723,7 @@ __device__ void prefetch_copies(const DevState& s, int* start) {
     }
     start[s.B] = acc;
   }
-  __syncthreads();
+  ASR_UNIT_SYNC();
   const int total = start[s.B];
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     int lo = 0, hi = s.B - 1;
@@ -631,22 +742,22 @@ __device__ void prefetch_copies(const DevState& s, int* start) {
 // One warp per (b, l, h): lane c < nch reads split c's (m, l); each lane owns d/32 output elements;
 // fixed split order -> deterministic.
 __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) {
-  const int lane = threadIdx.x & 31;
+  const int lane = ASR_UNIT_TID() & 31;
   const int h = wid % s.Hq;
   const int l = (wid / s.Hq) % s.L;
   const int b = wid / (s.Hq * s.L);
   int nch;
   long it0;
+  const int per_seq = (s.item_start[b + 1] - s.item_start[b]) / s.L;   // tiles (or chunks) per layer
   if (s.sk_grid) {   // stream-K pieces (asr_internal.h)
-    const int tiles = (s.act_len[b] + kSkTile - 1) / kSkTile;
+    const int tiles = per_seq;
     const long T = s.item_start[s.B], S = s.item_start[b] + (long)l * tiles;
     const int G = sk_span(T, s.sk_grid);
     const int cf = tiles ? sk_cta_of(S, T, G) : 0;
     nch = tiles ? sk_cta_of(S + tiles - 1, T, G) - cf + 1 : 0;
     it0 = (long)b * s.L + l + cf;
   } else {
-    int chunk;
-    chunking(s.act_len[b], s.max_splits, s.chunk_min, &chunk, &nch);
+    nch = per_seq;
     it0 = s.item_start[b] + (long)l * nch;
   }
   float M = -INFINITY;
@@ -699,9 +810,17 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   }
 }
 
-// Work-unit counts of the phases.
+// Work units of phase A: entropy splits (with logits), then one append unit per (b, l).
 __host__ __device__ inline int phaseA_units(const DevState& s, bool has_logits) {
-  return (has_logits ? s.B * kEntSplits : 0) + s.B + s.B * s.L;
+  return (has_logits ? s.B * kEntSplits : 0) + s.B * s.L;
+}
+// Sequence of phase-A unit `unit`, and how many units each sequence has.
+__host__ __device__ inline int phaseA_seq(const DevState& s, bool has_logits, int unit) {
+  const int ne = has_logits ? s.B * kEntSplits : 0;
+  return unit < ne ? unit / kEntSplits : (unit - ne) / s.L;
+}
+__host__ __device__ inline int phaseA_units_per_seq(const DevState& s, bool has_logits) {
+  return (has_logits ? kEntSplits : 0) + s.L;
 }
 template <typename TL, typename TK>
 __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* logits, const TK* k_new,
@@ -709,11 +828,37 @@ __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* lo
   const int ne = logits ? s.B * kEntSplits : 0;
   if (unit < ne) {
     unit_entropy_split<TL>(s, logits, unit / kEntSplits, unit % kEntSplits, u);
-  } else if (unit < ne + s.B) {
-    unit_compact(s, unit - ne, i, u);
   } else {
-    const int a = unit - ne - s.B;
+    const int a = unit - ne;
     unit_append<TK>(s, a / s.L, a % s.L, i, k_new, v_new);
+  }
+}
+
+// Phase A unit `unit` of step i and, when it is the last unit of its sequence to finish (per-sequence
+// ticket, threadfence pattern), phase B of that sequence (unit_finish) — no dependent launch between.
+template <typename TL, typename TK>
+__device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logits, const TK* k_new, const TK* v_new,
+                             float* entropy_out, UnitShm& u) {
+  const bool has_logits = logits != nullptr;
+  run_phaseA_unit<TL, TK>(s, unit, i, logits, k_new, v_new, u);
+  const int b = phaseA_seq(s, has_logits, unit);
+  ASR_UNIT_SYNC();
+  if (ASR_UNIT_TID() == 0) {
+    __threadfence();   // this unit's results before the ticket
+    u.last = atomicAdd(&s.pre_ticket[b], 1) == phaseA_units_per_seq(s, has_logits) - 1;
+    if (u.last) {
+      s.pre_ticket[b] = 0;
+      __threadfence();
+    }
+  }
+  ASR_UNIT_SYNC();
+  if (u.last) {
+    unit_finish(s, b, i, has_logits, entropy_out, u);
+    ASR_UNIT_SYNC();
+    if (ASR_UNIT_TID() == 0) {
+      __threadfence();
+      *s.pre_done = i + 1;   // the attention kernel's CTAs wait for this when phase A runs inside it
+    }
   }
 }
 
