@@ -272,7 +272,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
     {
       // decide blocks per sequence: ~2K positions each; X > 1 only if all B*X blocks are co-resident
-      // (one per SM), since they meet at a barrier to compact A_{i+1} together
+      // (one per SM), since a block waits for its predecessors' counts to place its part of A_{i+1}
       int db = (s.max_ctx + 2047) / 2048;
       db = db < 1 ? 1 : db > 32 ? 32 : db;
       if ((long)s.B * db > c->num_sms) db = 1;
@@ -327,7 +327,6 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.step, 4));
     CUDA_TRY(c->alloc(&s.act_pos, 2 * BT * 4));
     CUDA_TRY(c->alloc(&s.act_len, 2 * (size_t)s.B * 4));
-    CUDA_TRY(c->alloc(&s.dticket, (size_t)s.B * 4));
     CUDA_TRY(c->alloc(&s.dagg, (size_t)s.B * 32 * 8));
     CUDA_TRY(c->alloc(&s.redo, 4));
     CUDA_TRY(c->alloc(&s.pre_done, 4));
@@ -361,7 +360,6 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(cudaMemsetAsync(s.err, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.ticket, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.pre_ticket, 0, (size_t)s.B * 4, st));
-    CUDA_TRY(cudaMemsetAsync(s.dticket, 0, (size_t)s.B * 4, st));
     CUDA_TRY(cudaMemsetAsync(s.dagg, 0, (size_t)s.B * 32 * 8, st));
     CUDA_TRY(cudaMemsetAsync(s.redo, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.pre_done, 0, 4, st));

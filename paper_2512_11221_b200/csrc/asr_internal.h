@@ -119,7 +119,6 @@ struct DevState {
   uint32_t* err;              // [1]
   int32_t* ticket;            // [1]
   int32_t* pre_ticket;        // [B] last phase-A unit of a sequence runs its phase B (unit_finish)
-  int32_t* dticket;           // [B] arrivals of the decide blocks of a sequence, over all steps
   unsigned long long* dagg;   // [B][32] per decide block: (step + 1) << 32 | its count of A_{i+1}
   int32_t* redo;              // [1] recovery changed some A_i after the attention started (pre_in_attn)
   int32_t* pre_done;          // [1] = step + 1 once phase B of the step is done (pre_in_attn)

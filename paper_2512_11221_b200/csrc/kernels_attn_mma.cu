@@ -100,6 +100,47 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// The same with an L2 cache policy (the KV stream is read once per step: evict_first keeps it from
+// displacing the ledger, partials and q that the next kernels read).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Near the end of its last tile each CTA prefetches into L2 its share (4 KiB chunks, round robin) of
+// the ledger rows the decide kernel reads next: residency, timer and count of positions [0, n) and
+// the A_i list — otherwise each of the decide's dependent loads would go to DRAM.
+__device__ void prefetch_ledger(const DevState& s, int p, const int* __restrict__ alen) {
+  constexpr int kChunk = 4096;
+  int k = 0;   // running chunk index over all (sequence, array) rows
+  for (int b = 0; b < s.B; ++b) {
+    const int n = s.prompt_len[b] + *s.step + 1;
+    const long row = (long)b * s.max_ctx;
+    const char* base[4] = {reinterpret_cast<const char*>(s.res + row), reinterpret_cast<const char*>(s.timer + row),
+                           reinterpret_cast<const char*>(s.count + row),
+                           reinterpret_cast<const char*>(s.act_pos + act_off(s, p) + row)};
+    const int bytes[4] = {n, 4 * n, 4 * n, 4 * alen[b]};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int len = (bytes[a] + 15) & ~15;
+      for (int off = 0; off < len; off += kChunk, ++k)
+        if (k % (int)gridDim.x == (int)blockIdx.x) prefetch_l2(base[a] + off, (uint32_t)min(kChunk, len - off));
+    }
+  }
+}
+
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -236,6 +277,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
+    const uint64_t kv_policy = policy_evict_first();
     while (cur.t < t_end) {
       Cursor nxt = cur;
       nxt.next(s, alen);
@@ -279,14 +321,15 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
           bulk_g2s(&sm.kv[stage][lane * kTokPad + kRowBytes], v_new + r, kRowBytes, &sm.full[stage]);
         } else {
           const long slot = j_cur;
-          bulk_g2s(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
-                   &sm.full[stage]);
+          bulk_g2s_hint(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
+                        &sm.full[stage], kv_policy);
         }
       }
       j_cur = j_next;
       cur = nxt;
       ++g;
     }
+    if (lane == 0) prefetch_ledger(s, p, alen);
     // drain: the last (up to) kStagesRing tiles still owe their score epilogue
     for (int k = 0; k < kStagesRing; ++k) {
       const int gg = g + k;  // waiting for the release of tile gg - kStagesRing

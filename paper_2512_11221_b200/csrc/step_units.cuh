@@ -37,6 +37,7 @@ struct UnitShm {
   int level;
   int total;
   int last;
+  int lo, hi;   // decide: this block's position range
 };
 
 __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
@@ -164,39 +165,41 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
 // counts gives every lane its output offset, so the writes of a group are contiguous too.
 // Residency (and slots) are read through L2 (ld.global.cg): other blocks of the same kernel wrote
 // them (decide slices, recovery), and this block's L1 may hold older lines.
-__device__ __forceinline__ uint32_t active_bits4(const uint32_t* res4, int q, int n) {
-  // bit k set iff position 4q + k < n is Active (residency byte == 1)
-  if (4 * q >= n) return 0u;
+__device__ __forceinline__ uint32_t active_bits4(const uint32_t* res4, int q, int lo, int n) {
+  // bit k set iff position 4q + k in [lo, n) is Active (residency byte == 1)
+  if (4 * q >= n || 4 * q + 4 <= lo) return 0u;
   const uint32_t e = __vcmpeq4(__ldcg(res4 + q), 0x01010101u);   // 0xff per byte equal to 1
   uint32_t m = ((e >> 7) & 1u) | ((e >> 14) & 2u) | ((e >> 21) & 4u) | ((e >> 28) & 8u);
   const int left = n - 4 * q;
   if (left < 4) m &= (1u << left) - 1u;
+  if (lo > 4 * q) m &= ~((1u << (lo - 4 * q)) - 1u);
   return m;
 }
 
 struct Compactor {
   static constexpr int kKeep = 8;   // masks of a warp's first kKeep groups stay in registers
   const uint32_t* res4;
-  int lo, hi, g0, g1;
+  int lo, hi, g0, g1, lo_al;
   uint32_t keep[kKeep];
-  // count pass: returns the team's total; u.wsum[w] = exclusive offset of warp w within the team
+  // count pass over [lo_, hi_): returns the team's total; u.wsum[w] = exclusive offset of warp w
   __device__ int count(const DevState& s, int b, int lo_, int hi_, UnitShm& u) {
     res4 = reinterpret_cast<const uint32_t*>(s.res + (long)b * s.max_ctx);   // rows are 64-byte aligned
     lo = lo_;
     hi = hi_;
+    lo_al = lo & ~127;   // groups are 128-position aligned; positions below lo are masked
     const int tid = (int)ASR_UNIT_TID(), lane = tid & 31, w = tid >> 5, nw = (int)ASR_UNIT_THREADS() >> 5;
-    const int ngrp = hi > lo ? (hi - lo + 127) >> 7 : 0;
+    const int ngrp = hi > lo ? (hi - lo_al + 127) >> 7 : 0;
     const int per = (ngrp + nw - 1) / nw;
     g0 = min(ngrp, w * per);
     g1 = min(ngrp, g0 + per);
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kKeep; ++k) {
-      keep[k] = g0 + k < g1 ? active_bits4(res4, (lo >> 2) + (g0 + k) * 32 + lane, hi) : 0u;
+      keep[k] = g0 + k < g1 ? active_bits4(res4, (lo_al >> 2) + (g0 + k) * 32 + lane, lo, hi) : 0u;
       cnt += __popc(keep[k]);
     }
 #pragma unroll 4
-    for (int g = g0 + kKeep; g < g1; ++g) cnt += __popc(active_bits4(res4, (lo >> 2) + g * 32 + lane, hi));
+    for (int g = g0 + kKeep; g < g1; ++g) cnt += __popc(active_bits4(res4, (lo_al >> 2) + g * 32 + lane, lo, hi));
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) u.wsum[w] = cnt;
     ASR_UNIT_SYNC();
@@ -222,14 +225,14 @@ struct Compactor {
     const int32_t* slot_of = s.slot_of + row;
     int off = base_idx + u.wsum[w];
     for (int g = g0; g < g1; ++g) {
-      const int q = (lo >> 2) + g * 32 + lane;
+      const int q = (lo_al >> 2) + g * 32 + lane;
       uint32_t m = 0u;
       if (g - g0 < kKeep) {
 #pragma unroll
         for (int k = 0; k < kKeep; ++k)
           if (g - g0 == k) m = keep[k];
       } else {
-        m = active_bits4(res4, q, hi);
+        m = active_bits4(res4, q, lo, hi);
       }
       const int c = __popc(m);
       int incl = c;
@@ -544,8 +547,17 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
   // loop: tokens of A_i read Active here and are skipped by the tick below)
   constexpr int kPF = 8;
-  const int per_n = (n + X - 1) / X;
-  const int n0 = x * per_n, n_end = min(n, n0 + per_n);
+  // this block: A-slice [a0, a_end) (x-th of X equal parts) and the positions [pos(a0), pos(a_end))
+  // with pos(0) = 0, pos(A) = n — exactly its A-tokens and the frozen tokens between them, so the
+  // block alone settles the final residency of its positions (unit_next_list compacts them)
+  const int per_a = max(1, (A + X - 1) / X);
+  const int a0 = min(A, x * per_a), a_end = min(A, (x + 1) * per_a);
+  const int n0 = x == 0 ? 0 : a0 >= A ? n : act_pos[a0];
+  const int n_end = a_end >= A ? n : act_pos[a_end];
+  if (ASR_UNIT_TID() == 0) {
+    u.lo = n0;
+    u.hi = n_end;
+  }
   uint8_t pr[kPF];
   int pt[kPF];
 #pragma unroll
@@ -556,9 +568,7 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   }
   int frozen_now = 0, restored = 0, evicted = 0;
   const int pf_row = (i & 1) * s.B + b;   // prefetch list written by this step
-  const int per_a = (A + X - 1) / X;
-  const int a_end = min(A, (x + 1) * per_a);
-  for (int a = x * per_a + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS()) {
+  for (int a = a0 + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS()) {
     const int j = act_pos[a];
     const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
     float sj = sum / heads;             // mean over the L*Hq (layer, head) pairs (correctly rounded)
@@ -635,38 +645,22 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   }
 }
 
-// After unit_decide of step i (whole ledger of sequence b final for this step): A_{i+1} into parity
-// (i+1) & 1, by the X decide blocks of b together — block x compacts positions [x*P, (x+1)*P)
-// (P = ceil(n/X) rounded up to 128; the last block also appends position n, the token step i+1
-// appends).  The blocks first meet at a per-sequence barrier (dticket counts arrivals over all steps;
-// the host only uses X > 1 when every decide block is co-resident), then each publishes its count
-// in dagg[b][x] tagged with the step and adds up its predecessors' counts (decoupled look-back
-// without a chain) to place its part.
+// After unit_decide of step i: A_{i+1} into parity (i+1) & 1.  Decide block x owns the positions
+// [u.lo, u.hi) and has settled their final residency itself, so it compacts them without waiting for
+// the other blocks; the block holding index A-1 also appends position n (the token step i+1 appends).
+// Each block publishes its count in dagg[b][x] tagged with the step and adds up its predecessors'
+// counts (look-back without a chain: lane k of warp 0 waits for block k) to place its part.  The
+// host uses X > 1 only when every decide block is co-resident.
 __device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
   const int n = s.prompt_len[b] + i + 1;    // tokens held after step i
   const bool next = n + 1 <= s.cap;         // step i+1 can run
   const int tid = (int)ASR_UNIT_TID();
-  if (X > 1) {
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&s.dticket[b], 1);
-      const volatile int* c = s.dticket + b;
-      const int want = (i + 1) * X;
-      const unsigned long long t0 = gtimer();
-      while (*c < want) {
-        __nanosleep(32);
-        if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
-          atomicOr(s.err, kErrStall);
-          break;
-        }
-      }
-      __threadfence();
-    }
-  }
-  const int per = (((n + X - 1) / X) + 127) & ~127;
-  const int lo = min(n, x * per);
-  int hi = x == X - 1 ? n : min(n, lo + per);
-  if (x == X - 1 && next) {
+  const int A = s.act_len[(i & 1) * s.B + b];
+  const int per_a = max(1, (A + X - 1) / X);
+  const bool tail = x == max(0, A - 1) / per_a;   // holds index A-1 (the last position of A_i)
+  const int lo = u.lo;
+  int hi = u.hi;
+  if (tail && next) {
     if (tid == 0) ledger_entry_new(s, b, n);
     hi = n + 1;
   }
@@ -675,11 +669,8 @@ __device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, Un
   const int cnt = c.count(s, b, lo, hi, u);
   const unsigned long long tag = (unsigned long long)(unsigned)(i + 1) << 32;
   if (X > 1) {
-    if (tid == 0) {
-      __threadfence();
-      atomicExch(&s.dagg[(long)b * 32 + x], tag | (unsigned)cnt);
-    }
-    if (tid < 32) {   // warp 0: lane k waits for predecessor k's count
+    if (tid == 0) atomicExch(&s.dagg[(long)b * 32 + x], tag | (unsigned)cnt);
+    if (tid < 32) {   // warp 0: lane k waits for block k < x
       int pre = 0;
       if (tid < x) {
         const volatile unsigned long long* a = s.dagg + (long)b * 32 + tid;
@@ -688,7 +679,7 @@ __device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, Un
         while ((v & 0xffffffff00000000ull) != tag) {
           __nanosleep(32);
           v = *a;
-          if (gtimer() - t0 > 2000000000ull) {
+          if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
             atomicOr(s.err, kErrStall);
             break;
           }
@@ -698,14 +689,13 @@ __device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, Un
       for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
       if (tid == 0) u.level = pre;
     }
-    ASR_UNIT_SYNC();
   } else if (tid == 0) {
     u.level = 0;
   }
-  if (X == 1) ASR_UNIT_SYNC();
+  ASR_UNIT_SYNC();
   const int base = u.level;
   if (next) c.write(s, b, (i + 1) & 1, base, u);
-  if (tid == 0 && x == X - 1 && next) {
+  if (tid == 0 && tail && next) {
     s.act_len[((i + 1) & 1) * s.B + b] = base + cnt;
     if (base + cnt == 0) atomicOr(s.err, kErrEmptyActive);
   }
