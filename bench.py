@@ -255,9 +255,13 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     flush_r = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flush_acc = torch.empty((), dtype=torch.float32, device=dev)
 
+    no_flush = os.environ.get("ASR_BENCH_NO_FLUSH") == "1"   # diagnostics only (never a bench value)
+
     class _Flush:
         @staticmethod
         def zero_():
+            if no_flush:
+                return
             flush_w.zero_()
             torch.sum(flush_r, dim=0, out=flush_acc)
     flush = _Flush()
@@ -312,7 +316,9 @@ def run_asr(a, rank: int, world: int, local_rank: int):
             tls.append(ctx.timeline())
         med = [round(statistics.median(x), 3) for x in zip(*tls)]
         timeline = {"pre_start_end_attn_start_end_post_start_end_us": med[:6],
-                    "post_decide_end_next_list_end_combine_end_released_us": med[6:10]}
+                    "post_decide_end_next_list_end_combine_end_us": med[6:9],
+                    "pre_entropy_end_append_end_phaseB_start_end_us": med[9:13],
+                    "post_released_us": med[13:14]}
         print("timeline (us):", json.dumps(tls), file=sys.stderr)
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below

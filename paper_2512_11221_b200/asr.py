@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libasr.so")
+LIB_PATH = os.environ.get("ASR_LIB_PATH") or os.path.join(_HERE, "libasr.so")   # override: A/B of two builds
 
 ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, ASR_E_STATE = 0, 1, 2, 3, 4, 5, 7
 KV_BF16, KV_F32 = 0, 1
@@ -280,9 +280,9 @@ def asr_stage_times(ctx):
 
 def asr_timeline(ctx) -> list:
     """[pre start, end, attention start, end, post start, end, decide end, next-A end, combine end,
-    post released] (us)."""
-    us = (ctypes.c_double * 10)()
-    _check(lib().asr_timeline(ctx, us, 10))
+    entropy units end, append units end, phase B start, phase B end, post released] (us)."""
+    us = (ctypes.c_double * 14)()
+    _check(lib().asr_timeline(ctx, us, 14))
     return list(us)
 
 

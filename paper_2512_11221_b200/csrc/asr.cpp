@@ -117,10 +117,31 @@ struct asr_ctx {
       for (auto e : a) cudaEventDestroy(e);
   }
 
+  // Device memory.  Arrays up to kArenaMax bytes are carved (256-byte aligned) out of one arena, so
+  // the ledger, lists, detector state and counters that each step's latency chains touch share a
+  // few large pages instead of one allocation (and TLB entry) each; bigger arrays (KV pool,
+  // partials) get their own allocation.
+  static constexpr size_t kArena = 32u << 20, kArenaMax = 4u << 20;
+  char* arena = nullptr;
+  size_t arena_used = 0;
   template <typename P>
   cudaError_t alloc(P** p, size_t bytes) {
+    bytes = bytes ? (bytes + 255) & ~(size_t)255 : 256;
+    static const bool no_arena = [] { const char* e = getenv("ASR_NO_ARENA"); return e && e[0] == '1'; }();
+    if (bytes <= kArenaMax && !no_arena) {
+      if (!arena) {
+        cudaError_t e = cudaMalloc(&arena, kArena);
+        if (e != cudaSuccess) return e;
+        allocs.push_back(arena);
+      }
+      if (arena_used + bytes <= kArena) {
+        *p = reinterpret_cast<P*>(arena + arena_used);
+        arena_used += bytes;
+        return cudaSuccess;
+      }
+    }
     void* v = nullptr;
-    cudaError_t e = cudaMalloc(&v, bytes ? bytes : 16);
+    cudaError_t e = cudaMalloc(&v, bytes);
     if (e == cudaSuccess) {
       allocs.push_back(v);
       *p = reinterpret_cast<P*>(v);
@@ -394,6 +415,22 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       }
     }
     CUDA_TRY(cudaStreamSynchronize(st));
+    // batch 1 on the tensor-core path: phase A (+B) inside the attention kernel, on an extra warp of
+    // CTAs 0..95, one unit each (not with the slot pool, whose prefetch copies must follow phase B)
+    {
+      const char* pa = getenv("ASR_PRE_KERNEL");
+      const bool force_kernel = pa && pa[0] == '1';
+      s.pre_in_attn = asr::attention_mma_supported(s) && !s.pool_mode && !force_kernel &&
+                      asr::kEntSplits * s.B + s.L * s.B <= c->num_sms;
+      // phase-A unit grouping: one unit per warp-sized piece inside the attention kernel; otherwise
+      // one entropy split per warp (8 per 256-thread unit) and appends grouped to ~one unit per SM
+      auto pow2ceil = [](long v) { int p = 1; while (p < v) p <<= 1; return p; };
+      s.ent_per_unit = s.pre_in_attn ? 1 : 8;
+      const int l = s.pre_in_attn ? 1 : pow2ceil(((long)s.L * s.B + c->num_sms - 1) / c->num_sms);
+      s.layers_per_unit = l > s.L ? s.L : l;
+      // small batch: the combine rides in the phase-D kernel (one launch fewer on the critical path)
+      s.combine_in_decide = (long)s.B * s.L * s.Hq <= 64L * c->num_sms;
+    }
     c->attn_grid = asr::attention_grid(s, c->num_sms);
     if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
     const char* ng = getenv("ASR_NO_GRAPH");
@@ -405,13 +442,6 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     c->timeline_on = tlenv && tlenv[0] == '1';
     s.tl = nullptr;
     s.sk_grid = asr::attention_mma_supported(s) ? c->attn_grid : 0;
-    {   // batch 1: phase A inside the attention kernel (one unit per CTA; not with the slot pool,
-        // whose prefetch copies must follow phase B)
-      const char* pa = getenv("ASR_PRE_KERNEL");
-      const bool force_kernel = pa && pa[0] == '1';
-      s.pre_in_attn = s.sk_grid && !s.pool_mode && !force_kernel &&
-                      asr::kEntSplits * s.B + s.L * s.B <= c->attn_grid;
-    }
     // A_0 of every sequence (the ledger entry of the first appended position + compaction)
     {
       asr::KNode pn;
@@ -419,6 +449,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       CUDA_TRY(pn.launch(st));
       CUDA_TRY(cudaStreamSynchronize(st));
     }
+    const char* ke = getenv("ASR_KV_EVICT_FIRST");
+    s.kv_evict_first = !(ke && ke[0] == '0');
     const char* np = getenv("ASR_NO_PDL");
     c->use_pdl = !(np && np[0] == '1');
     c->last_stream = st;
@@ -554,12 +586,14 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
 }
 
 // The step's kernels and their dependencies (A_i was compacted by the previous step's phase D).
-//  batch 1, tensor-core path (DevState::pre_in_attn): 2 kernels
+//  batch 1, tensor-core path (DevState::pre_in_attn):
 //     attention (phase A + B on an extra warp of CTAs 0..95; a second pass inside the kernel only if
-//     recovery recompacted A_i) --full edge--> phase D   (--PDL--> scoresum --PDL--> in head-shard mode)
+//     recovery recompacted A_i) --> { combine, [scoresum -->] phase D }
 //  otherwise:
-//     phase A (+B) --PDL--> attention --PDL--> [scoresum] --PDL--> phase D, and in pressure mode the
+//     phase A (+B) --PDL--> attention --> { combine, [scoresum -->] phase D }, and in pressure mode the
 //     prefetch copy kernel as a branch after phase A (nothing waits on it within the step).
+//  (--> = full edge: a dependent launched early beside the attention waits for whole SMs and then ran
+//  its latency chain slower than a fresh launch.)
 // A profiled step (event nodes between the stages) runs the same kernels as a chain.
 static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st) {
   const DevState& s = c->s;
@@ -570,6 +604,7 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
   int nk = 0;
   const void* lgp = a.has_logits ? a.lg : nullptr;
   float* entp = a.has_logits ? a.ent : nullptr;
+  int kT = -1;
   if (part != kPartDecide) {
     if (s.pre_in_attn) {
       asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, lgp, a.logits_dtype, entp);
@@ -587,20 +622,23 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
       kn_list[nk].dep_prog = kA;
       stage_of[nk++] = 1;
     }
+    kT = nk - 1;
     if (s.sharded) {
       asr::node_scoresum(kn_list[nk], sd);
-      kn_list[nk].dep_prog = nk - 1;
+      kn_list[nk].dep_prog = kT;
       stage_of[nk++] = 2;
     }
   }
-  if (part != kPartAttend) {
+  if (part != kPartAttend) {   // decide (after scoresum in head-shard mode) — on the critical path
     asr::node_phaseD(kn_list[nk], sd, a.o);
-    if (part == kPartFull) {   // after the last attention-side kernel
-      // batch-1 path: a full edge — phase D launched early beside the attention measured slower
-      // (its blocks wait for whole SMs and then run its latency chain slower than a fresh launch)
-      if (s.pre_in_attn && nk == 1) kn_list[nk].dep_full[0] = nk - 1;
-      else kn_list[nk].dep_prog = nk - 1;
-    }
+    if (part == kPartFull) kn_list[nk].dep_full[0] = nk - 1;
+    stage_of[nk++] = 2;
+  }
+  if (part != kPartDecide && !s.combine_in_decide) {
+    // combine: a branch after the attention (full edges: kernels launched early beside the
+    // attention wait for whole SMs and measured slower)
+    asr::node_combine(kn_list[nk], sd, a.o);
+    kn_list[nk].dep_full[0] = kT;
     stage_of[nk++] = 2;
   }
   const bool last_part = part != kPartAttend;

@@ -9,9 +9,10 @@ namespace asr {
 
 constexpr int kStages = 3;          // pre (entropy+append+recovery), attention, post (combine+decide+next A)
 // diagnostic timeline slots: [2k], [2k+1] = start / end of stage k; then phase D detail: end of the
-// decide blocks, end of the next-step preparation (A_{i+1}), end of the combine, release of phase D
-// (its first block past griddepcontrol.wait)
-constexpr int kTimelineSlots = 2 * kStages + 4;
+// decide blocks, end of the next-step preparation (A_{i+1}), end of the combine; then phase A detail:
+// end of the entropy units, end of the append units, start and end of phase B; last: release of
+// phase D (its first block past griddepcontrol.wait)
+constexpr int kTimelineSlots = 2 * kStages + 8;
 constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
 constexpr int kLedgerThreads = 1024;
 constexpr int kDecideThreads = 512;
@@ -74,6 +75,10 @@ struct DevState {
   int decide_blocks;          // blocks per sequence of the decide kernel
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
+  int combine_in_decide;      // 1: the combine runs as extra blocks of the phase-D kernel (small batch)
+  int kv_evict_first;         // 1: the attention's KV bulk copies carry an L2 evict_first policy
+  int ent_per_unit;           // entropy splits per phase-A unit (divides kEntSplits)
+  int layers_per_unit;        // layers per phase-A append unit
   // pressure mode (pool_tokens > 0)
   int pool_mode;              // 0 full residency (slot = b*max_ctx + pos), 1 slot pool
   int evict_min;              // evict at freeze when the remaining absence >= evict_min
@@ -121,7 +126,7 @@ struct DevState {
   int32_t* pre_ticket;        // [B] last phase-A unit of a sequence runs its phase B (unit_finish)
   unsigned long long* dagg;   // [B][32] per decide block: (step + 1) << 32 | its count of A_{i+1}
   int32_t* redo;              // [1] recovery changed some A_i after the attention started (pre_in_attn)
-  int32_t* pre_done;          // [1] = step + 1 once phase B of the step is done (pre_in_attn)
+  int32_t* pre_done;          // [1] = step + 1 once phase B of the step is done
   unsigned* gbar;             // [2] grid barrier of the attention kernel's redo pass
   unsigned long long* tl;     // [kTimelineSlots] diagnostic timeline (globaltimer ns), NULL = off
 };
@@ -226,6 +231,7 @@ void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dty
 void node_attention(KNode& n, const DevState& s, const void* q, const void* k_new, const void* v_new, int grid,
                     const void* pre_logits, int logits_dtype, float* entropy_out);
 void node_phaseD(KNode& n, const DevState& s, float* o);
+void node_combine(KNode& n, const DevState& s, float* o);
 void node_prepare(KNode& n, const DevState& s);            // A_0 at asr_create
 void node_restore(KNode& n, const DevState& s, int seq, int level);
 void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies

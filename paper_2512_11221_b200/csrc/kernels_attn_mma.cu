@@ -115,28 +115,42 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Near the end of its last tile each CTA prefetches into L2 its share (4 KiB chunks, round robin) of
-// the ledger rows the decide kernel reads next: residency, timer and count of positions [0, n) and
-// the A_i list — otherwise each of the decide's dependent loads would go to DRAM.
-__device__ void prefetch_ledger(const DevState& s, int p, const int* __restrict__ alen) {
+// Near the end of its last tile each CTA prefetches into L2 its share (4 KiB chunks, round robin in
+// sequence / array order) of the ledger rows the decide kernel reads next: residency, timer and count
+// of positions [0, n) and the A_i list (otherwise each of the decide's dependent loads would go to
+// DRAM).  Called by the whole producer warp: the per-sequence sizes are loaded 32 at a time by the
+// lanes, lane 0 issues the prefetches.
+__device__ void prefetch_ledger(const DevState& s, int p, const int* __restrict__ alen, int step, int lane) {
   constexpr int kChunk = 4096;
   int k = 0;   // running chunk index over all (sequence, array) rows
-  for (int b = 0; b < s.B; ++b) {
-    const int n = s.prompt_len[b] + *s.step + 1;
-    const long row = (long)b * s.max_ctx;
-    const char* base[4] = {reinterpret_cast<const char*>(s.res + row), reinterpret_cast<const char*>(s.timer + row),
-                           reinterpret_cast<const char*>(s.count + row),
-                           reinterpret_cast<const char*>(s.act_pos + act_off(s, p) + row)};
-    const int bytes[4] = {n, 4 * n, 4 * n, 4 * alen[b]};
+  for (int b0 = 0; b0 < s.B; b0 += 32) {
+    const int bl = b0 + lane;
+    const int n_l = bl < s.B ? s.prompt_len[bl] + step + 1 : 0;
+    const int a_l = bl < s.B ? alen[bl] : 0;
+    for (int q = 0; q < 32 && b0 + q < s.B; ++q) {
+      const int n = __shfl_sync(0xffffffffu, n_l, q), A = __shfl_sync(0xffffffffu, a_l, q);
+      if (lane != 0) continue;
+      const int b = b0 + q;
+      const long row = (long)b * s.max_ctx;
+      const char* base[4] = {reinterpret_cast<const char*>(s.res + row), reinterpret_cast<const char*>(s.timer + row),
+                             reinterpret_cast<const char*>(s.count + row),
+                             reinterpret_cast<const char*>(s.act_pos + act_off(s, p) + row)};
+      const int bytes[4] = {n, 4 * n, 4 * n, 4 * A};
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int len = (bytes[a] + 15) & ~15;
-      for (int off = 0; off < len; off += kChunk, ++k)
-        if (k % (int)gridDim.x == (int)blockIdx.x) prefetch_l2(base[a] + off, (uint32_t)min(kChunk, len - off));
+      for (int a = 0; a < 4; ++a) {
+        const int len = (bytes[a] + 15) & ~15;
+        for (int off = 0; off < len; off += kChunk, ++k)
+          if (k % (int)gridDim.x == (int)blockIdx.x) prefetch_l2(base[a] + off, (uint32_t)min(kChunk, len - off));
+      }
     }
   }
 }
@@ -277,7 +291,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
-    const uint64_t kv_policy = policy_evict_first();
+    // L2 policy of the KV stream: evict_first (ASR_KV_EVICT_FIRST=0: evict_normal, for comparison)
+    const uint64_t kv_policy = s.kv_evict_first ? policy_evict_first() : policy_evict_normal();
     while (cur.t < t_end) {
       Cursor nxt = cur;
       nxt.next(s, alen);
@@ -329,7 +344,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       cur = nxt;
       ++g;
     }
-    if (lane == 0) prefetch_ledger(s, p, alen);
+    if (s.B <= 8) prefetch_ledger(s, p, alen, step, lane);   // large batches: phase D is not latency-bound
     // drain: the last (up to) kStagesRing tiles still owe their score epilogue
     for (int k = 0; k < kStagesRing; ++k) {
       const int gg = g + k;  // waiting for the release of tile gg - kStagesRing

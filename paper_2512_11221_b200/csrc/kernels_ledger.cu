@@ -23,16 +23,26 @@ __global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, cons
   units::phaseA_block<TL, TK>(s, blockIdx.x, *s.step, logits, k_new, v_new, entropy_out, u);
 }
 
-// Blocks [0, decide_blocks * B): decide + tick (unit x of sequence b), then together A_{i+1} into the
-// other parity (unit_next_list); the last decide block overall advances the step counter and clears
-// the redo flag.  The remaining blocks: combine, one warp per (b, l, h).
+// decide_blocks blocks per sequence: decide + tick (unit x of sequence b), then together A_{i+1} into
+// the other parity (unit_next_list); the last decide block overall advances the step counter and
+// clears the redo flag.  With combine_in_decide (small batch) further blocks combine O (one warp
+// per (b, l, h)), saving the separate combine launch.
 __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float* __restrict__ o) {
   Stamp stamp(s.tl, 2);
   pdl_wait();      // every input comes from the attention kernel(s) and phase A
   if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[kTimelineSlots - 1], gtimer());
   __shared__ units::UnitShm u;
   const int nd = s.decide_blocks * s.B;
-  if ((int)blockIdx.x < nd) {
+  if ((int)blockIdx.x >= nd) {   // combine_in_decide: blocks after the decide blocks combine O
+    const int wid = ((int)blockIdx.x - nd) * (kUnitThreads / 32) + (threadIdx.x >> 5);
+    if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
+    if (s.tl) {
+      __syncthreads();
+      if (threadIdx.x == 0) atomicMax(&s.tl[2 * kStages + 2], gtimer());
+    }
+    return;
+  }
+  {
     const int i = *s.step;
     const int b = blockIdx.x / s.decide_blocks;
     units::unit_decide(s, b, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
@@ -48,9 +58,14 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
         *s.step = i + 1;
       }
     }
-    return;
   }
-  const int wid = ((int)blockIdx.x - nd) * (kUnitThreads / 32) + (threadIdx.x >> 5);
+}
+
+// (a4') combine of the split-KV partials -> O, one warp per (b, l, h); a graph branch beside phase D.
+constexpr int kCombineThreads = 256;
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(DevState s, float* __restrict__ o) {
+  pdl_wait();
+  const int wid = (int)blockIdx.x * (kCombineThreads / 32) + (threadIdx.x >> 5);
   if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
   if (s.tl) {
     __syncthreads();
@@ -119,7 +134,16 @@ void node_phaseD(KNode& n, const DevState& s, float* o) {
   n.set(0, o);
   const int warps = s.B * s.L * s.Hq;
   const int wpb = kUnitThreads / 32;
-  n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + (warps + wpb - 1) / wpb), dim3(kUnitThreads), 0);
+  const int nc = s.combine_in_decide ? (warps + wpb - 1) / wpb : 0;
+  n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + nc), dim3(kUnitThreads), 0);
+}
+
+void node_combine(KNode& n, const DevState& s, float* o) {
+  n.s = s;
+  n.set(0, o);
+  const int warps = s.B * s.L * s.Hq;
+  const int wpb = kCombineThreads / 32;
+  n.finalize((const void*)combine_kernel, dim3((warps + wpb - 1) / wpb), dim3(kCombineThreads), 0);
 }
 
 void node_prepare(KNode& n, const DevState& s) {

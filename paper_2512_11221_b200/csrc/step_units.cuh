@@ -4,7 +4,7 @@
 // dedicated warp of the attention CTA in kernels_attn_mma.cu (where phase A of a batch-1 step runs
 // inside the attention kernel, beside the producer and consumer warps).
 //
-//   phase A  unit_entropy_split   (a6) partial (m, Z, S) of one split of a logits row
+//   phase A  warp_entropy_split   (a6) partial (m, Z, S) of one split of a logits row (one warp)
 //            unit_append          (a0) the new token's K/V rows of (b, l) -> its slot
 //            unit_finish          (a6) H = ln Z - S/Z, detector (R-det), ladder (R-ladder) and, when
 //                                 a level fires (rare), the level (Sec 3.6) + recompaction of A_i;
@@ -112,8 +112,9 @@ __device__ __forceinline__ void tri_merge(float& m, float& z, float& sx, float o
   m = M; z = nz; sx = ns;
 }
 
+// Partial (m, Z, S) of split `split` of row b's logits, computed by one warp (lane = lane index).
 template <typename TL>
-__device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ logits, int b, int split, UnitShm& u) {
+__device__ void warp_entropy_split(const DevState& s, const TL* __restrict__ logits, int b, int split, int lane) {
   const int V = s.vocab;
   const int seg = (((V + kEntSplits - 1) / kEntSplits) + 7) & ~7;   // multiple of 8 elements
   const int e0 = min(V, split * seg), e1 = min(V, e0 + seg);
@@ -121,14 +122,7 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
   const bool vecok = (reinterpret_cast<uintptr_t>(row) & 31) == 0;
   const float invT = 1.0f / s.ent_temp;
   float m = -INFINITY, z = 0.f, sx = 0.f;
-  for (int v = e0 + (int)ASR_UNIT_TID() * 8; v < e1; v += (int)ASR_UNIT_THREADS() * 8) {
-    float x[8];
-    if (vecok && v + 8 <= e1) {
-      load8<TL>(row + v, x);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = (v + e < e1) ? tof(row[v + e]) : -INFINITY;
-    }
+  auto accum = [&](float* x) {   // fold 8 logits into the running (m, Z, S)
     float mx = -INFINITY;
 #pragma unroll
     for (int e = 0; e < 8; ++e) { x[e] *= invT; mx = fmaxf(mx, x[e]); }
@@ -143,18 +137,61 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
       z += ex;
       sx += ex > 0.f ? ex * d : 0.f;
     }
+  };
+  if (!vecok) {
+    for (int v = e0 + lane * 8; v < e1; v += 32 * 8) {
+      float x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = (v + e < e1) ? tof(row[v + e]) : -INFINITY;
+      accum(x);
+    }
+  } else {
+    // all kIn 16-byte loads of a batch are issued before any is consumed (unconditional, clamped
+    // addresses): a branch between them would make each wait for the previous one
+    constexpr int kIn = 8;
+    constexpr int kW = sizeof(TL) == 2 ? 1 : 2;   // 16-byte words per 8 logits
+    for (int v0 = e0 + lane * 8; v0 < e1; v0 += kIn * 32 * 8) {
+      uint4 raw[kIn][kW];
+#pragma unroll
+      for (int k = 0; k < kIn; ++k) {
+        const int v = v0 + k * 32 * 8;
+        const uint4* src = reinterpret_cast<const uint4*>(row + (v + 8 <= e1 ? v : e0));
+#pragma unroll
+        for (int w = 0; w < kW; ++w) raw[k][w] = __ldg(src + w);
+      }
+#pragma unroll 1
+      for (int k = 0; k < kIn; ++k) {
+        const int v = v0 + k * 32 * 8;
+        if (v >= e1) break;
+        float x[8];
+        if (v + 8 <= e1) {
+          if constexpr (sizeof(TL) == 2) {
+            const uint32_t w4[4] = {raw[k][0].x, raw[k][0].y, raw[k][0].z, raw[k][0].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              x[2 * q] = __uint_as_float(w4[q] << 16);
+              x[2 * q + 1] = __uint_as_float(w4[q] & 0xffff0000u);
+            }
+          } else {
+            const uint32_t w8[8] = {raw[k][0].x, raw[k][0].y, raw[k][0].z, raw[k][0].w,
+                                    raw[k][kW - 1].x, raw[k][kW - 1].y, raw[k][kW - 1].z, raw[k][kW - 1].w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = __uint_as_float(w8[q]);
+          }
+        } else {   // the row's last, partial group of 8
+#pragma unroll
+          for (int e = 0; e < 8; ++e) x[e] = (v + e < e1) ? tof(row[v + e]) : -INFINITY;
+        }
+        accum(x);
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1)
     tri_merge(m, z, sx, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, z, o),
               __shfl_xor_sync(0xffffffffu, sx, o));
-  const int w = ASR_UNIT_TID() >> 5, lane = ASR_UNIT_TID() & 31;
-  if (lane == 0) { u.wm[w] = m; u.wz[w] = z; u.ws[w] = sx; }
-  ASR_UNIT_SYNC();
-  if (ASR_UNIT_TID() == 0) {
-    float M = -INFINITY, Z = 0.f, S = 0.f;
-    for (int k = 0; k < (int)(ASR_UNIT_THREADS() >> 5); ++k) tri_merge(M, Z, S, u.wm[k], u.wz[k], u.ws[k]);
+  if (lane == 0) {
     float* ep = s.ent_part + ((long)b * kEntSplits + split) * 3;
-    ep[0] = M; ep[1] = Z; ep[2] = S;
+    ep[0] = m; ep[1] = z; ep[2] = sx;
   }
 }
 
@@ -166,9 +203,11 @@ __device__ void unit_entropy_split(const DevState& s, const TL* __restrict__ log
 // Residency (and slots) are read through L2 (ld.global.cg): other blocks of the same kernel wrote
 // them (decide slices, recovery), and this block's L1 may hold older lines.
 __device__ __forceinline__ uint32_t active_bits4(const uint32_t* res4, int q, int lo, int n) {
-  // bit k set iff position 4q + k in [lo, n) is Active (residency byte == 1)
-  if (4 * q >= n || 4 * q + 4 <= lo) return 0u;
-  const uint32_t e = __vcmpeq4(__ldcg(res4 + q), 0x01010101u);   // 0xff per byte equal to 1
+  // bit k set iff position 4q + k in [lo, n) is Active (residency byte == 1); the load is
+  // unconditional (clamped address) so a caller's batch of these issues all loads back to back
+  const bool in = 4 * q < n && 4 * q + 4 > lo;
+  const uint32_t e = __vcmpeq4(__ldcg(res4 + (in ? q : (lo >> 2))), 0x01010101u);   // 0xff per byte == 1
+  if (!in) return 0u;
   uint32_t m = ((e >> 7) & 1u) | ((e >> 14) & 2u) | ((e >> 21) & 4u) | ((e >> 28) & 8u);
   const int left = n - 4 * q;
   if (left < 4) m &= (1u << left) - 1u;
@@ -301,10 +340,22 @@ __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __
   const int vec = (int)(16 / sizeof(TK));
   if (row % vec == 0) {
     const int nv = row / vec;
-    for (int t = ASR_UNIT_TID(); t < 2 * nv; t += ASR_UNIT_THREADS()) {
-      const uint4 x = *(reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv));
-      reinterpret_cast<uint4*>(dst)[t] = x;
-      if (mir) reinterpret_cast<uint4*>(mir)[t] = x;
+    const int T = (int)ASR_UNIT_THREADS();
+    for (int t0 = ASR_UNIT_TID(); t0 < 2 * nv; t0 += 8 * T) {   // 8 vectors in flight per thread
+      uint4 x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = t0 + k * T;
+        if (t < 2 * nv) x[k] = __ldg(reinterpret_cast<const uint4*>(t < nv ? ks : vs) + (t < nv ? t : t - nv));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int t = t0 + k * T;
+        if (t < 2 * nv) {
+          reinterpret_cast<uint4*>(dst)[t] = x[k];
+          if (mir) reinterpret_cast<uint4*>(mir)[t] = x[k];
+        }
+      }
     }
   } else {
     for (int t = ASR_UNIT_TID(); t < 2 * row; t += ASR_UNIT_THREADS()) {
@@ -392,11 +443,13 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
       // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
       const float* ep = s.ent_part + (long)b * kEntSplits * 3;   // written by other blocks: via L2
       float M = -INFINITY, Zl = 0.f, Sl = 0.f;
+      float pv[kEntSplits / 32][3];   // all loads first, then the merges
 #pragma unroll
-      for (int k = 0; k < kEntSplits / 32; ++k) {
-        const int sp = k * 32 + lane;
-        tri_merge(M, Zl, Sl, __ldcg(ep + sp * 3), __ldcg(ep + sp * 3 + 1), __ldcg(ep + sp * 3 + 2));
-      }
+      for (int k = 0; k < kEntSplits / 32; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pv[k][c] = __ldcg(ep + (k * 32 + lane) * 3 + c);
+#pragma unroll
+      for (int k = 0; k < kEntSplits / 32; ++k) tri_merge(M, Zl, Sl, pv[k][0], pv[k][1], pv[k][2]);
       for (int o = 16; o > 0; o >>= 1)
         tri_merge(M, Zl, Sl, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Zl, o),
                   __shfl_xor_sync(0xffffffffu, Sl, o));
@@ -800,27 +853,38 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   }
 }
 
-// Work units of phase A: entropy splits (with logits), then one append unit per (b, l).
+// Work units of phase A: per sequence kEntSplits / ent_per_unit entropy units (with logits), then
+// ceil(L / layers_per_unit) append units (the host picks the grouping so a large batch does not
+// launch thousands of tiny blocks).
+__host__ __device__ inline int ent_units_per_seq(const DevState& s) { return kEntSplits / s.ent_per_unit; }
+__host__ __device__ inline int app_units_per_seq(const DevState& s) {
+  return (s.L + s.layers_per_unit - 1) / s.layers_per_unit;
+}
 __host__ __device__ inline int phaseA_units(const DevState& s, bool has_logits) {
-  return (has_logits ? s.B * kEntSplits : 0) + s.B * s.L;
+  return s.B * ((has_logits ? ent_units_per_seq(s) : 0) + app_units_per_seq(s));
 }
 // Sequence of phase-A unit `unit`, and how many units each sequence has.
 __host__ __device__ inline int phaseA_seq(const DevState& s, bool has_logits, int unit) {
-  const int ne = has_logits ? s.B * kEntSplits : 0;
-  return unit < ne ? unit / kEntSplits : (unit - ne) / s.L;
+  const int ne = has_logits ? s.B * ent_units_per_seq(s) : 0;
+  return unit < ne ? unit / ent_units_per_seq(s) : (unit - ne) / app_units_per_seq(s);
 }
 __host__ __device__ inline int phaseA_units_per_seq(const DevState& s, bool has_logits) {
-  return (has_logits ? kEntSplits : 0) + s.L;
+  return (has_logits ? ent_units_per_seq(s) : 0) + app_units_per_seq(s);
 }
 template <typename TL, typename TK>
 __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* logits, const TK* k_new,
                                 const TK* v_new, UnitShm& u) {
-  const int ne = logits ? s.B * kEntSplits : 0;
+  const int eu = ent_units_per_seq(s), au = app_units_per_seq(s);
+  const int ne = logits ? s.B * eu : 0;
   if (unit < ne) {
-    unit_entropy_split<TL>(s, logits, unit / kEntSplits, unit % kEntSplits, u);
+    const int b = unit / eu, k = unit % eu;
+    const int w = (int)ASR_UNIT_TID() >> 5, nw = (int)ASR_UNIT_THREADS() >> 5;
+    for (int sp = k * s.ent_per_unit + w; sp < (k + 1) * s.ent_per_unit; sp += nw)   // one split per warp
+      warp_entropy_split<TL>(s, logits, b, sp, (int)ASR_UNIT_TID() & 31);
   } else {
     const int a = unit - ne;
-    unit_append<TK>(s, a / s.L, a % s.L, i, k_new, v_new);
+    const int b = a / au, k = a % au;
+    for (int l = k * s.layers_per_unit; l < min(s.L, (k + 1) * s.layers_per_unit); ++l) unit_append<TK>(s, b, l, i, k_new, v_new);
   }
 }
 
@@ -831,6 +895,8 @@ __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logit
                              float* entropy_out, UnitShm& u) {
   const bool has_logits = logits != nullptr;
   run_phaseA_unit<TL, TK>(s, unit, i, logits, k_new, v_new, u);
+  if (s.tl && ASR_UNIT_TID() == 0)
+    atomicMax(&s.tl[2 * kStages + 3 + ((has_logits && unit < s.B * ent_units_per_seq(s)) ? 0 : 1)], gtimer());
   const int b = phaseA_seq(s, has_logits, unit);
   ASR_UNIT_SYNC();
   if (ASR_UNIT_TID() == 0) {
@@ -843,7 +909,9 @@ __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logit
   }
   ASR_UNIT_SYNC();
   if (u.last) {
+    if (s.tl && ASR_UNIT_TID() == 0) atomicMax(&s.tl[2 * kStages + 5], gtimer());
     unit_finish(s, b, i, has_logits, entropy_out, u);
+    if (s.tl && ASR_UNIT_TID() == 0) atomicMax(&s.tl[2 * kStages + 6], gtimer());
     ASR_UNIT_SYNC();
     if (ASR_UNIT_TID() == 0) {
       __threadfence();
