@@ -55,6 +55,7 @@ class Case:
     pool_tokens: int = 0           # > 0: pressure mode (device slot pool, eviction / prefetch / demand)
     evict_min: int = 2
     nccl_world1: bool = False      # attach a one-rank NCCL communicator (attend -> all-reduce -> decide)
+    logits_dtype: str = "bf16"     # "f32": the same (bf16-exact) logits passed as fp32
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -121,6 +122,7 @@ def run(c: Case, check_o: bool = True) -> dict:
     orc = [oracle.OracleSeq(orc_cfg(c), cap, P[b]) for b in range(c.B)]
     worst_o, worst_h, frozen_total, restored_total = 0.0, 0.0, 0, 0
     evicted_total = prefetched_total = demand_total = 0
+    recoveries = 0
     for i in range(c.steps):
         if i in c.restore_at:
             seq, level = c.restore_at[i]
@@ -131,7 +133,7 @@ def run(c: Case, check_o: bool = True) -> dict:
         q = np.stack([gen.q(p, b, i, c.dtype) for b in range(c.B)])
         kn = np.stack([KV[b][0][P[b] + i] for b in range(c.B)])
         vn = np.stack([KV[b][1][P[b] + i] for b in range(c.B)])
-        lg = np.stack([gen.logits(p, b, i - 1) for b in range(c.B)]) if (c.vocab and i > 0) else None
+        lg = np.stack([gen.logits(p, b, i - 1, c.logits_dtype) for b in range(c.B)]) if (c.vocab and i > 0) else None
         if c.host_io:
             o = np.zeros((c.B, c.L, c.Hq, c.d), np.float32)
             ent = np.zeros(c.B, np.float32)
@@ -162,6 +164,7 @@ def run(c: Case, check_o: bool = True) -> dict:
             assert g["frozen_this_step"] == out["frozen_this_step"], where
             assert g["restored_this_step"] == out["restored_this_step"], (where, g, out)
             assert g["recovery_action"] == out["recovery_action"], where
+            recoveries += out["recovery_action"] > 0
             assert g["rewalk_requested"] == out["rewalk_requested"], where
             assert g["device_error"] == 0
             if out["entropy_valid"]:
@@ -201,6 +204,7 @@ def run(c: Case, check_o: bool = True) -> dict:
             np.testing.assert_array_equal(kd, KV[b][0][j], err_msg=f"device K seq {b} pos {j}")
             np.testing.assert_array_equal(vd, KV[b][1][j], err_msg=f"device V seq {b} pos {j}")
     summary = {"worst_o": worst_o, "worst_h": worst_h, "frozen": frozen_total, "restored": restored_total,
+               "recoveries": recoveries,
                "evicted": evicted_total, "prefetched": prefetched_total, "demand": demand_total,
                "final": [ctx.stats(b) for b in range(c.B)]}
     ctx.close()

@@ -119,3 +119,23 @@ def test_mma_path_gqa_layouts(hq, hkv):
     # heads per KV head: Qwen2-7B-like (28 q / 4 KV), head shards of LLaMA-3-8B (16/4, 8/2 ...), G = 8
     run(Case(L=2, Hq=hq, Hkv=hkv, d=128, B=2, prompt=(90, 37), steps=20, window=16, hot_permille=300, a_hot=64,
              seed=3000 + hq + hkv, vocab=2048))
+
+
+@pytest.mark.parametrize("logits_dtype", ["bf16", "f32"])
+def test_batch1_phase_a_inside_attention_with_recovery(logits_dtype):
+    # batch 1 on the tensor-core path runs phase A/B on an extra warp of the attention kernel while
+    # the attention already streams A_i as the previous step compacted it; planted entropy spikes make
+    # recovery recompact A_i mid-kernel, which forces the in-kernel second pass (grid barrier + redo);
+    # explicit restores between steps recompact the precomputed A_i in place
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=1, prompt=(60,), steps=150, window=8, vocab=128256, seed=91,
+             spike_first=50, spike_period=16, spike_count=4, hot_permille=300, a_hot=64,
+             restore_at={30: (0, 1), 120: (0, 3)}, logits_dtype=logits_dtype)
+    s = run(c)
+    assert s["restored"] > 0 and s["recoveries"] >= 3   # SR, WR, FR fired (each forced a redo pass)
+
+
+def test_large_batch_grouped_phase_a_units():
+    # batch > 1 on the tensor-core path with phase A as its own kernel (units grouped per warp / layer
+    # range) and the combine as a separate kernel (batch * L * Hq > 64 warps per SM)
+    run(Case(L=4, Hq=32, Hkv=8, d=128, B=80, prompt=tuple(20 + (7 * b) % 50 for b in range(80)), steps=12,
+             window=8, vocab=1024, seed=93, hot_permille=300, a_hot=64))
