@@ -607,7 +607,7 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
   int kT = -1;
   if (part != kPartDecide) {
     if (s.pre_in_attn) {
-      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, lgp, a.logits_dtype, entp);
+      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, lgp, a.logits_dtype, entp, a.o);
       stage_of[nk++] = 1;
     } else {
       const int kA = nk;
@@ -618,7 +618,7 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
         kn_list[nk].dep_full[0] = kA;
         stage_of[nk++] = 1;
       }
-      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, nullptr, 0, nullptr);
+      asr::node_attention(kn_list[nk], sd, a.q, a.kn, a.vn, c->attn_grid, nullptr, 0, nullptr, a.o);
       kn_list[nk].dep_prog = kA;
       stage_of[nk++] = 1;
     }

@@ -229,7 +229,7 @@ NcclApi& nccl_api();
 void node_phaseA(KNode& n, const DevState& s, const void* logits, int logits_dtype, const void* k_new,
                  const void* v_new, float* entropy_out);
 void node_attention(KNode& n, const DevState& s, const void* q, const void* k_new, const void* v_new, int grid,
-                    const void* pre_logits, int logits_dtype, float* entropy_out);
+                    const void* pre_logits, int logits_dtype, float* entropy_out, float* o);
 void node_phaseD(KNode& n, const DevState& s, float* o);
 void node_combine(KNode& n, const DevState& s, float* o);
 void node_prepare(KNode& n, const DevState& s);            // A_0 at asr_create

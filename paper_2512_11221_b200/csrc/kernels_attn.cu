@@ -194,7 +194,7 @@ int attention_grid(const DevState& s, int num_sms) {
 }
 
 void node_attention(KNode& n, const DevState& s, const void* q, const void* k_new, const void* v_new, int grid,
-                    const void* pre_logits, int logits_dtype, float* entropy_out) {
+                    const void* pre_logits, int logits_dtype, float* entropy_out, float* o) {
   n.s = s;
   n.set(0, q);
   if (attention_mma_supported(s)) {
@@ -202,6 +202,7 @@ void node_attention(KNode& n, const DevState& s, const void* q, const void* k_ne
     n.set(2, v_new);
     n.set(3, pre_logits);
     n.set(4, entropy_out);
+    n.set(5, o);
     const void* f;
     int threads;
     unsigned smem;

@@ -241,7 +241,7 @@ template <int HK, typename TL>
 __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q,
                                 const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
                                 typename Geo<HK>::Smem& sm, bool do_pre, const TL* pre_logits, float* entropy_out,
-                                units::UnitShm& u) {
+                                units::UnitShm& u, float* __restrict__ o) {
   ASR_GEO(HK);
   const int step = *s.step;
   const int p = step & 1;                    // A_i lists of this step
@@ -380,6 +380,9 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
   else cur.t = t_end;
   while (cur.t < t_end) {   // one piece (the part of one (b, l) item in this CTA's range) per pass
     const long piece = (long)cur.b * s.L + cur.l + blockIdx.x;
+    const int pb = cur.b, pl = cur.l;
+    const bool from_item_start = cur.ti == 0;
+    bool to_item_end = false;
     // q fragments from the q ring (rows 0..3 = the 4 query heads of this KV head, rows 4..15 zero)
     ++it_local;
     const int qs = it_local & 1;
@@ -406,6 +409,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
       const int cnt = cur.cnt();
       more = cur.ti + 1 < cur.tiles;   // the piece ends with its item's last tile or the range's end
+      to_item_end = !more;
       cur.next(s, alen);
       more = more && cur.t < t_end;
       mbar_wait(&sm.full[stage], ph);
@@ -478,7 +482,13 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     // ---- partial outputs of this item: rows 0..3 (lanes 0..15)
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    if (r < G) {
+    if (r < G && o && from_item_start && to_item_end) {
+      // the whole item lies in this CTA's range: O directly (the combine skips single-piece items)
+      const float inv = 1.0f / l_run;
+      float* dst = o + (((long)pb * s.L + pl) * s.Hq + warp * G + r) * kD + 2 * qd;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) *reinterpret_cast<float2*>(dst + i * 8) = make_float2(acc[i][0] * inv, acc[i][1] * inv);
+    } else if (r < G) {
       const long pi = piece * s.Hq + warp * G + r;
       if (qd == 0) {
         s.part_ml[pi * 2] = m_run;
@@ -526,7 +536,7 @@ __device__ void grid_sync(unsigned* bar, uint32_t* err) {
 template <int HK, typename TL>
 __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
     attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_new,
-                    const __nv_bfloat16* __restrict__ v_new, const TL* logits, float* entropy_out) {
+                    const __nv_bfloat16* __restrict__ v_new, const TL* logits, float* entropy_out, float* o) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   auto& sm = *reinterpret_cast<typename Geo<HK>::Smem*>(smem_raw);
   __shared__ units::UnitShm u;
@@ -538,7 +548,7 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
   const int step = *s.step;
   {
     Stamp stamp(s.tl, 1);
-    attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u);
+    attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
   }
   if (!do_pre) return;
   __syncthreads();
@@ -561,7 +571,7 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
   if (!redo) return;
   grid_sync(s.gbar, s.err);    // every CTA is past its first pass
   attention_prologue<HK>(sm);  // fresh ring barriers
-  attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u);
+  attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
 }
 
 }  // namespace

@@ -799,6 +799,7 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
     const int cf = tiles ? sk_cta_of(S, T, G) : 0;
     nch = tiles ? sk_cta_of(S + tiles - 1, T, G) - cf + 1 : 0;
     it0 = (long)b * s.L + l + cf;
+    if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   } else {
     nch = per_seq;
     it0 = s.item_start[b] + (long)l * nch;

@@ -10,9 +10,9 @@ TAG=${1:-r1}; shift || true
 ARGS="--steps 5 --warmup 3 --no-cpu-baseline --no-e2e --points= --nvtx $*"
 timeout 600 python bench.py $ARGS > gpurun_out/plain_${TAG}.log 2>&1 || { echo "plain run failed"; exit 1; }
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" \
-    -k regex:"attn|phase|copy_kernel" --csv --log-file gpurun_out/launches_${TAG}.csv \
+    -k regex:"attn|phase|copy_kernel|combine" --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py $ARGS > gpurun_out/ncu_launch_${TAG}.log 2>&1 || echo "ncu launch list failed"
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" \
-    -k regex:"attn|phase" -c 4 -o gpurun_out/attn_${TAG} \
+    -k regex:"attn|phase|combine" -c 4 -o gpurun_out/attn_${TAG} \
     python bench.py $ARGS > gpurun_out/ncu_full_${TAG}.log 2>&1 || echo "ncu full failed"
 echo profile-done
