@@ -371,14 +371,18 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);
     # per (sequence, layer): q (Hq*d*2 B).  |A_i| per step ~ att_last (drifts < 0.5 % over the window).
     bytes_per_step = L * att_prof * (2 * hkv_r * D * 2 + 8) + B * L * hq_r * D * 2
+    # batch 1: phase A runs inside the attention kernel (logits row read, k_new/v_new read + slot write)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    if a.pool_frac == 0 and B * (64 + L) <= n_sms:
+        bytes_per_step += B * (VOCAB * 2 + 2 * (2 * L * hkv_r * D * 2))
     achieved = bytes_per_step * K / (attn_ms / 1000.0) / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
-            tr = json.load(f)
-            if tr.get("context") == a.context and tr.get("family") == a.family and tr.get("batch") == B:
-                traffic = tr["dram_bytes_per_launch"]
+            for tr in json.load(f)["entries"]:
+                if tr.get("context") == a.context and tr.get("family") == a.family and tr.get("batch") == B:
+                    traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
     # sequence sharding: every rank decodes its own batch; head sharding: all ranks decode one batch

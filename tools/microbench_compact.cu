@@ -36,7 +36,7 @@ __global__ void k_parts(DevState s, int n, unsigned long long* t) {
   int cnt = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    keep[k] = g0 + k < g1 ? units::active_bits4(res4, (g0 + k) * 32 + lane, n) : 0u;
+    keep[k] = g0 + k < g1 ? units::active_bits4(res4, (g0 + k) * 32 + lane, 0, n) : 0u;
     cnt += __popc(keep[k]);
   }
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
