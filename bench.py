@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="sequences per GPU")
     ap.add_argument("--window", type=int, default=512)
     ap.add_argument("--family", default="w0", choices=["w0", "w1"])
+    ap.add_argument("--tau", type=float, default=0.5, help="tau; <= 0 freezes nothing (the full-KV baseline)")
     ap.add_argument("--seed", type=int, default=2001)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -51,7 +52,7 @@ def parse():
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
-    ap.add_argument("--points", default="cfg3", help="comma list of extra workloads (POINTS) or '' for none")
+    ap.add_argument("--points", default="cfg3,w1,full", help="comma list of extra workloads (POINTS) or '' for none")
     ap.add_argument("--head-shard", action="store_true",
                     help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
     return ap.parse_args()
@@ -198,7 +199,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     g.Hq, g.Hkv = hq_r, hkv_r
     pool = int(a.pool_frac * B * a.context) + 4 * B if a.pool_frac > 0 else 0
     cfg = Config(n_layers=L, n_q_heads=hq_r, n_kv_heads=hkv_r, head_dim=D, batch=B, max_context=max_ctx,
-                 kv_dtype=KV_BF16, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB, profile_stages=0,
+                 kv_dtype=KV_BF16, window=a.window, tau=a.tau, softness=2.0, vocab=VOCAB, profile_stages=0,
                  device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min,
                  score_heads=HQ if a.head_shard else 0)
     bf = torch.bfloat16
@@ -403,8 +404,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
-                               + (f" pool{a.pool_frac:g}" if pool else ""),
-                   "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": 0.5, "k": 2,
+                               + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else ""),
+                   "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": a.tau, "k": 2,
                    "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
                    "parallelism": (f"head-sharded x{world} (NCCL all-reduce of per-token partial scores)" if a.head_shard
                                    else f"sequence-sharded x{world} (no hot-path collective)")},
@@ -436,8 +437,11 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     return line
 
 
-POINTS = {   # extra workloads measured after the headline (BASELINE.json configs[2]: 8K, batch 64)
-    "cfg3": dict(batch=64, steps=16, warmup=4, pool_frac=0.0),
+POINTS = {   # extra workloads measured after the headline
+    "cfg3": dict(batch=64, steps=16, warmup=4, pool_frac=0.0),    # BASELINE.json configs[2]: 8K, batch 64
+    "w1": dict(family="w1"),                                        # 30 % hot tokens (SURVEY W1 family)
+    "full": dict(tau=0.0),                                          # full-KV baseline: nothing freezes
+    "ctx32k": dict(context=32768, steps=32),                        # configs[3]-like length, grown state
 }
 
 
@@ -466,10 +470,14 @@ def main():
             points[name] = {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
                             "ms_per_step": r["ms_per_step"], "steps": r["steps"], "warmup": r["warmup"],
                             "roofline": {k: r["roofline"][k] for k in ("achieved", "peak", "frac", "unit")},
-                            "offload": r["offload"], "clocks": r["clocks"]}
+                            "offload": r["offload"], "clocks": r["clocks"],
+                            "attended_per_step": r["detail"]["attended_per_step"],
+                            "compression": r["detail"]["compression"]}
     if line is not None:
         if points:
             line["points"] = points
+            if "full" in points and points["full"]["value"] > 0:   # ASR-KF-EGR vs attending the whole cache
+                line["detail"]["speedup_vs_full_kv"] = line["value"] / points["full"]["value"]
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
