@@ -190,13 +190,20 @@ asr_status asr_read_kv(asr_ctx* ctx, int32_t seq, int32_t pos, int32_t from_mirr
 /* Accumulated device time since the last call (needs profiling on: profile_stages or
  * asr_set_profile): ms[0] entropy + detector + ladder + append + recovery + compaction, ms[1]
  * attention + fused score, ms[2] combine + decide + tick, ms[3] whole steps (CUDA events around the
- * step's kernels).  With the fused single-kernel step, ms[0..2] are its phases (%globaltimer).
+ * step's kernels).  At batch 1 phase A/B run inside the attention kernel, so ms[0] is ~0 there.
  * *launches = kernel launches of the library in that period.  n >= 4.  Synchronises. */
 asr_status asr_stage_times(asr_ctx* ctx, double* ms, int32_t n, int64_t* launches);
 
 /* Make cuda_stream wait (without blocking the host) until the host-memory outputs of every step
  * issued so far have landed (ASR_MEM_HOST).  No-op otherwise. */
 asr_status asr_flush(asr_ctx* ctx, void* cuda_stream);
+
+/* Measurement: enqueue `reps` back-to-back launches of the attention kernel ((a4) + (a1)) over the
+ * A_i the next asr_step will attend, without phase A/B and without the decide, on cuda_stream (no
+ * host sync).  Inputs (q, the appended token) and O come from internal scratch; the score and split
+ * partials it writes are recomputed by the next step, so the context's state is unchanged.  Bracket
+ * it with CUDA events to time the kernel alone (bench.py's roofline).  reps >= 1. */
+asr_status asr_time_attention(asr_ctx* ctx, int32_t reps, void* cuda_stream);
 
 /* Switch stage profiling (the events asr_stage_times reads) on or off for the following steps.
  * While it is on, stages are separated by event nodes, so the kernels of one step do not overlap

@@ -70,7 +70,8 @@ class asr_ledger_view(ctypes.Structure):
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
            "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
-           "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl")
+           "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
+           "asr_time_attention")
 
 _lib = None
 
@@ -100,9 +101,11 @@ def lib() -> ctypes.CDLL:
         L.asr_score_partials.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64)]
         L.asr_nccl_unique_id.argtypes = [vp, i32]
         L.asr_attach_nccl.argtypes = [vp, vp, i32, i32]
+        L.asr_time_attention.argtypes = [vp, i32, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
                   "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
-                  "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl"):
+                  "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
+                  "asr_time_attention"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -294,6 +297,10 @@ def asr_set_profile(ctx, on: bool) -> None:
     _check(lib().asr_set_profile(ctx, int(bool(on))))
 
 
+def asr_time_attention(ctx, reps: int, stream=None) -> None:
+    _check(lib().asr_time_attention(ctx, int(reps), _stream(stream)))
+
+
 def asr_destroy(ctx) -> None:
     _check(lib().asr_destroy(ctx))
 
@@ -340,6 +347,9 @@ class Context:
 
     def set_profile(self, on: bool):
         asr_set_profile(self._h, on)
+
+    def time_attention(self, reps: int, stream=None):
+        asr_time_attention(self._h, reps, stream)
 
     def close(self):
         if self._h:

@@ -87,6 +87,8 @@ struct asr_ctx {
   bool use_graph = true;
   bool use_pdl = true;
   bool timeline_on = false;     // ASR_TIMELINE=1
+  void *scratch_q = nullptr, *scratch_k = nullptr, *scratch_v = nullptr;   // asr_time_attention
+  float* scratch_o = nullptr;
   unsigned long long* tl_buf = nullptr;
   // stage profiling
   std::vector<std::array<cudaEvent_t, asr::kStages + 1>> prof_pending;
@@ -1017,6 +1019,34 @@ asr_status asr_timeline(asr_ctx* c, double* us, int32_t n) {
   CUDA_TRY(cudaMemcpy(t, c->tl_buf, sizeof(t), cudaMemcpyDeviceToHost));
   const int m = n < asr::kTimelineSlots ? n : asr::kTimelineSlots;
   for (int k = 0; k < m; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
+  return ASR_OK;
+}
+
+asr_status asr_time_attention(asr_ctx* c, int32_t reps, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (reps < 1) return fail(ASR_E_INVALID, "reps must be >= 1");
+  if (c->attend_pending) return fail(ASR_E_STATE, "between asr_step_attend and asr_step_decide");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  const DevState& s = c->s;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  if (!c->scratch_o) {
+    const size_t qb = (size_t)s.B * s.L * s.Hq * s.d * c->kv_elem, kb = (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem;
+    CUDA_TRY(c->alloc(&c->scratch_q, qb));
+    CUDA_TRY(c->alloc(&c->scratch_k, kb));
+    CUDA_TRY(c->alloc(&c->scratch_v, kb));
+    CUDA_TRY(c->alloc(&c->scratch_o, (size_t)s.B * s.L * s.Hq * s.d * 4));
+    CUDA_TRY(cudaMemsetAsync(c->scratch_q, 0, qb, st));
+    CUDA_TRY(cudaMemsetAsync(c->scratch_k, 0, kb, st));
+    CUDA_TRY(cudaMemsetAsync(c->scratch_v, 0, kb, st));
+  }
+  DevState sd = s;
+  sd.pre_in_attn = 0;   // the attention alone
+  sd.tl = nullptr;
+  asr::KNode n;
+  asr::node_attention(n, sd, c->scratch_q, c->scratch_k, c->scratch_v, c->attn_grid, nullptr, 0, nullptr,
+                      c->scratch_o);
+  for (int r = 0; r < reps; ++r) CUDA_TRY(n.launch(st));
+  c->last_stream = st;
   return ASR_OK;
 }
 
