@@ -334,7 +334,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         timeline = {"pre_start_end_attn_start_end_post_start_end_us": med[:6],
                     "post_decide_end_next_list_end_combine_end_us": med[6:9],
                     "pre_entropy_end_append_end_phaseB_start_end_us": med[9:13],
-                    "post_released_us": med[13:14]}
+                    "attn_first_cta_end_us": med[13:14], "post_released_us": med[14:15]}
         print("timeline (us):", json.dumps(tls), file=sys.stderr)
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below

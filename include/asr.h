@@ -212,10 +212,10 @@ asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
 
 /* Diagnostic: device timeline of the last step (needs ASR_TIMELINE=1 in the environment at
  * asr_create): us[2k], us[2k+1] = first-block start and last-block end of stage k (pre, attention,
- * post) in microseconds relative to the pre stage's start (%globaltimer); with n >= 14 also us[6..13] =
+ * post) in microseconds relative to the pre stage's start (%globaltimer); with n >= 15 also us[6..14] =
  * end of the decide blocks, of the next step's A_{i+1} compaction and of the combine; end of the
- * entropy units, of the append units, start and end of phase B; the time the post stage passed its
- * wait for the attention.  n >= 6.
+ * entropy units, of the append units, start and end of phase B; the first attention CTA's end; the
+ * time the post stage passed its wait for the attention.  n >= 6.
  * Synchronises. */
 asr_status asr_timeline(asr_ctx* ctx, double* us, int32_t n);
 

@@ -283,9 +283,10 @@ def asr_stage_times(ctx):
 
 def asr_timeline(ctx) -> list:
     """[pre start, end, attention start, end, post start, end, decide end, next-A end, combine end,
-    entropy units end, append units end, phase B start, phase B end, post released] (us)."""
-    us = (ctypes.c_double * 14)()
-    _check(lib().asr_timeline(ctx, us, 14))
+    entropy units end, append units end, phase B start, phase B end, first attention CTA end,
+    post released] (us)."""
+    us = (ctypes.c_double * 15)()
+    _check(lib().asr_timeline(ctx, us, 15))
     return list(us)
 
 

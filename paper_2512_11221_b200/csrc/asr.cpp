@@ -581,7 +581,7 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
   if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0 (+ phase D detail)
     unsigned long long init[asr::kTimelineSlots];
     for (int k = 0; k < asr::kTimelineSlots; ++k)
-      init[k] = ((k < 2 * asr::kStages && !(k & 1)) || k == asr::kTimelineSlots - 1) ? ~0ull : 0ull;
+      init[k] = ((k < 2 * asr::kStages && !(k & 1)) || k >= asr::kTimelineSlots - 2) ? ~0ull : 0ull;
     CUDA_TRY(cudaMemcpyAsync(a.sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
   }
   return ASR_OK;

@@ -10,9 +10,10 @@ namespace asr {
 constexpr int kStages = 3;          // pre (entropy+append+recovery), attention, post (combine+decide+next A)
 // diagnostic timeline slots: [2k], [2k+1] = start / end of stage k; then phase D detail: end of the
 // decide blocks, end of the next-step preparation (A_{i+1}), end of the combine; then phase A detail:
-// end of the entropy units, end of the append units, start and end of phase B; last: release of
-// phase D (its first block past griddepcontrol.wait)
-constexpr int kTimelineSlots = 2 * kStages + 8;
+// end of the entropy units, end of the append units, start and end of phase B; the first attention
+// CTA's end (with the stage end: the spread of the CTAs' ends); last: release of phase D (its first
+// block past griddepcontrol.wait)
+constexpr int kTimelineSlots = 2 * kStages + 9;
 constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
 constexpr int kLedgerThreads = 1024;
 constexpr int kDecideThreads = 512;

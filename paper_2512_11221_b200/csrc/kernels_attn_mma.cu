@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
   {
     Stamp stamp(s.tl, 1);
     attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
+    if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 7], gtimer());   // first CTA done
   }
   if (!do_pre) return;
   __syncthreads();
