@@ -219,6 +219,17 @@ asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
  * Synchronises. */
 asr_status asr_timeline(asr_ctx* ctx, double* us, int32_t n);
 
+/* NEXT-1 (Alg. 1 "Generate next token"): one draw per row of
+ * logits[batch][vocab] (device; logits_dtype ASR_KV_BF16 or ASR_KV_F32) — greedy if temperature <= 0
+ * or top_k == 1; otherwise p = softmax(x / temperature), keep the top_k largest logits (top_k <= 0:
+ * all; ties to lower indices), then the shortest prefix of those (logit desc, index asc) holding
+ * >= top_p of their mass (top_p >= 1: all), and return the smallest vocab index j of the kept set whose
+ * cumulative kept mass (in vocab order) exceeds uniforms[b] * the kept mass; uniforms[batch] in [0, 1)
+ * (device, the caller's random numbers); token_out[batch] (device, int32).  Stateless (no context),
+ * asynchronous on cuda_stream, bitwise deterministic.  Rules and pins: oracle/sample.py. */
+asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab, float temperature,
+                      int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream);
+
 /* Synchronise and free everything the context owns. */
 asr_status asr_destroy(asr_ctx* ctx);
 

@@ -71,7 +71,7 @@ class asr_ledger_view(ctypes.Structure):
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
            "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
            "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-           "asr_time_attention")
+           "asr_time_attention", "asr_sample")
 
 _lib = None
 
@@ -102,10 +102,11 @@ def lib() -> ctypes.CDLL:
         L.asr_nccl_unique_id.argtypes = [vp, i32]
         L.asr_attach_nccl.argtypes = [vp, vp, i32, i32]
         L.asr_time_attention.argtypes = [vp, i32, vp]
+        L.asr_sample.argtypes = [vp, i32, i32, i32, ctypes.c_float, i32, ctypes.c_float, vp, vp, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
                   "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
                   "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-                  "asr_time_attention"):
+                  "asr_time_attention", "asr_sample"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -296,6 +297,18 @@ def asr_flush(ctx, stream=None) -> None:
 
 def asr_set_profile(ctx, on: bool) -> None:
     _check(lib().asr_set_profile(ctx, int(bool(on))))
+
+
+def asr_sample(logits, uniforms, token_out, temperature: float = 1.0, top_k: int = 0, top_p: float = 1.0,
+               stream=None) -> None:
+    """NEXT-1 next-token draw (include/asr.h asr_sample): logits [B][V] bf16/fp32, uniforms [B] fp32,
+    token_out [B] int32 — CUDA tensors (torch) of the caller."""
+    import torch
+    B, V = logits.shape
+    dt = KV_BF16 if logits.dtype == torch.bfloat16 else KV_F32
+    _check(lib().asr_sample(ctypes.c_void_p(logits.data_ptr()), dt, B, V, float(temperature), int(top_k),
+                            float(top_p), ctypes.c_void_p(uniforms.data_ptr()), ctypes.c_void_p(token_out.data_ptr()),
+                            _stream(stream)))
 
 
 def asr_time_attention(ctx, reps: int, stream=None) -> None:

@@ -1,0 +1,99 @@
+"""NEXT-1 parity: asr_sample (the next-token draw) against oracle/sample.py.
+
+Draws are compared exactly where the answer is unique: u is placed in the middle of the oracle's
+interval of a kept token (u +- half the interval cannot reach a neighbour's), and top-p values sit
+halfway between two consecutive cumulative masses of the sorted kept set (the GPU sums fp32
+probabilities, the oracle fp64).  Random u are checked for validity: the drawn token is kept and its
+oracle interval contains u up to 1e-6.
+"""
+import numpy as np
+import pytest
+
+import gen
+from oracle.sample import interval, kept_set, sample
+
+pytestmark = pytest.mark.gpu
+
+
+def _rows(kind, B, V, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "gen":   # the generator's logits rows (bf16 lattice normal with one peak)
+        p = gen.GenParams(seed=seed, L=1, Hq=2, Hkv=2, d=16, vocab=V)
+        return np.stack([gen.logits(p, b, b) for b in range(B)])
+    if kind == "ties":  # few distinct values: many ties at every boundary
+        x = rng.integers(-3, 4, size=(B, V)).astype(np.float32) * 0.5
+        return x
+    return (rng.normal(scale=2.0, size=(B, V))).astype(np.float32)
+
+
+def _p_between(x, T, k):
+    # a top-p value halfway between two consecutive normalised cumulative masses of the top-k set
+    keep, p = kept_set(x, T, k, 1.0)
+    order = np.lexsort((np.arange(x.size), -(x.astype(np.float64) if x.dtype != np.uint16 else
+                                             (x.astype(np.uint32) << 16).view(np.float32))))
+    kk = order if not (0 < k < x.size) else order[:k]
+    c = np.cumsum(p[kk]) / p[kk].sum()
+    i = min(len(c) - 2, max(0, int(np.searchsorted(c, 0.7))))
+    return float(0.5 * (c[i] + c[i + 1])) if len(c) > 1 else 1.0
+
+
+@pytest.mark.parametrize("kind,V,dtype", [("gen", 128256, "bf16"), ("normal", 5000, "f32"), ("ties", 3000, "f32"),
+                                          ("normal", 131, "bf16")])
+def test_sample_matches_oracle(kind, V, dtype):
+    import torch
+    from paper_2512_11221_b200 import asr_sample
+    B = 6
+    X = _rows(kind, B, V, 11 + V)
+    if dtype == "bf16" and X.dtype != np.uint16:
+        X = (X.view(np.uint32) >> 16).astype(np.uint16)   # truncate to bf16 bits
+    xt = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).cuda() if X.dtype == np.uint16 else \
+        torch.from_numpy(X).cuda()
+    rng = np.random.default_rng(V)
+    settings = [(0.0, 0, 1.0), (1.0, 1, 1.0), (1.0, 0, 1.0), (0.7, 50, 1.0), (1.0, 0, None), (0.8, 100, None),
+                (1.3, 7, None)]
+    for T, k, P in settings:
+        Ps = [(_p_between(X[b], T, k) if P is None else P) for b in range(B)]
+        # exact draws: u in the middle of a kept token's interval
+        us, want = [], []
+        for b in range(B):
+            # a token drawn by the oracle (so it carries real mass) whose interval is wide enough for
+            # fp32 u and fp32 probabilities (>= 1e-4 of the kept mass)
+            for _ in range(50):
+                tok = sample(X[b], T, k, Ps[b], float(rng.random()))
+                lo, hi = interval(X[b], T, k, Ps[b], tok)
+                if hi - lo >= 1e-4:
+                    break
+            us.append(0.5 * (lo + hi))
+            want.append(tok)
+        for b in range(B):   # one row per call when top-p differs per row
+            if not interval(X[b], T, k, Ps[b], want[b])[1] - interval(X[b], T, k, Ps[b], want[b])[0] >= 1e-4:
+                continue
+            u = torch.tensor([us[b]], dtype=torch.float32, device="cuda")
+            out = torch.empty(1, dtype=torch.int32, device="cuda")
+            asr_sample(xt[b:b + 1], u, out, temperature=T, top_k=k, top_p=Ps[b])
+            got = int(out.item())
+            assert got == want[b], (kind, T, k, Ps[b], b, got, want[b], sample(X[b], T, k, Ps[b], us[b]))
+        # random u, whole batch in one call (same top-p for all rows): validity
+        if P is not None:
+            u = rng.random(B).astype(np.float32)
+            ut = torch.from_numpy(u).cuda()
+            out = torch.empty(B, dtype=torch.int32, device="cuda")
+            asr_sample(xt, ut, out, temperature=T, top_k=k, top_p=P)
+            got = out.cpu().numpy()
+            for b in range(B):
+                lo, hi = interval(X[b], T, k, P, int(got[b]))
+                assert lo == lo, (kind, T, k, b, int(got[b]), "not in the kept set")
+                assert lo - 2e-6 <= float(u[b]) <= hi + 2e-6, (kind, T, k, b, lo, float(u[b]), hi)
+
+
+def test_sample_deterministic():
+    import torch
+    from paper_2512_11221_b200 import asr_sample
+    X = _rows("normal", 32, 20000, 3)
+    xt = torch.from_numpy(X).cuda()
+    u = torch.rand(32, device="cuda")
+    a = torch.empty(32, dtype=torch.int32, device="cuda")
+    b = torch.empty_like(a)
+    asr_sample(xt, u, a, temperature=0.9, top_k=200, top_p=0.9)
+    asr_sample(xt, u, b, temperature=0.9, top_k=200, top_p=0.9)
+    assert torch.equal(a, b)
