@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
-    ap.add_argument("--points", default="cfg3,w1,full", help="comma list of extra workloads (POINTS) or '' for none")
+    ap.add_argument("--points", default="cfg3,w1,full,sample",
+                    help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
     ap.add_argument("--head-shard", action="store_true",
                     help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
     return ap.parse_args()
@@ -469,6 +470,39 @@ POINTS = {   # extra workloads measured after the headline
 }
 
 
+def sample_point(local_rank: int) -> dict:
+    """NEXT-1: the next-token draw (asr_sample) at the LLaMA-3 vocabulary, batch 1 and 64, timed with
+    CUDA events over 20 calls (logits resident in HBM; algorithmic bytes = one read of each row)."""
+    import torch
+
+    import gen
+    from paper_2512_11221_b200 import asr_sample
+    dev = torch.device("cuda", local_rank)
+    out = {}
+    for B in (1, 64):
+        g = gen.GenParams(seed=7, L=1, Hq=2, Hkv=2, d=16, vocab=VOCAB)
+        lg = torch.empty((B, VOCAB), dtype=torch.bfloat16, device=dev)
+        gen.dev_logits(g, B, 5, lg)
+        u = torch.rand(B, device=dev)
+        tok = torch.empty(B, dtype=torch.int32, device=dev)
+        res = {}
+        for name, (T, k, P) in {"greedy": (0.0, 0, 1.0), "T0.8_k50_p0.9": (0.8, 50, 0.9), "T1_p0.95": (1.0, 0, 0.95)}.items():
+            for _ in range(3):
+                asr_sample(lg, u, tok, temperature=T, top_k=k, top_p=P)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                asr_sample(lg, u, tok, temperature=T, top_k=k, top_p=P)
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1000 / 20
+            res[name] = {"us_per_call": round(us, 2), "rows_per_s": round(B / us * 1e6),
+                         "gbs_one_read": round(B * VOCAB * 2 / us / 1e3, 1)}
+        out[f"batch{B}"] = res
+    return out
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -484,7 +518,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_asr(a, rank, world, local_rank)
     points = {}
-    for name in [x for x in a.points.split(",") if x]:
+    for name in [x for x in a.points.split(",") if x and x != "sample"]:
         b = argparse.Namespace(**vars(a))
         for k, v in POINTS[name].items():
             setattr(b, k, v)
@@ -497,6 +531,8 @@ def main():
                             "offload": r["offload"], "clocks": r["clocks"],
                             "attended_per_step": r["detail"]["attended_per_step"],
                             "compression": r["detail"]["compression"]}
+    if line is not None and world == 1 and "sample" in [x for x in a.points.split(",") if x]:
+        line["detail"]["next_token_draw"] = sample_point(local_rank)
     if line is not None:
         if points:
             line["points"] = points

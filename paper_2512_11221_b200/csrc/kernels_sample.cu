@@ -7,22 +7,30 @@
 //   (logit desc, index asc) order holding >= P of their probability mass;
 //   draw: the smallest index j in the kept set with  sum_{i kept, i <= j} p_i  >  u * sum_{kept} p_i.
 //
-// One CTA (1024 threads) per row.  The boundaries are found by radix selection on an order-preserving
-// 32-bit key of the logit (digits of 12, 12 and 8 bits, one pass over the row each, histograms of
-// counts and of fixed-point probability mass in shared memory).  Masses are exp((x - max) / T) in
-// fp32, summed as 2^-36 fixed point in 64-bit integers: every sum is exact and order-independent, so
-// a draw is bitwise deterministic.
+// One thread-block cluster of CS CTAs per row (8 for small batches, 4, or 1 for large ones); CTA r
+// owns the contiguous slice r of the row.  Every
+// quantity the decisions need (max, counts and masses above the split points of the boundary search,
+// tie counts, kept masses) is reduced within each CTA and exchanged through distributed shared memory
+// (DSMEM) after a cluster barrier; every CTA then takes the same decision in the same fixed order.
+// The boundaries are found by an 8-ary search on an order-preserving 32-bit key of the logit (bf16
+// keys have 16 significant bits: 6 passes; fp32: 11), counting for top-k and summing mass for top-p.  Masses are exp((x - max) / T) in fp32, summed
+// as 2^-36 fixed point in 64-bit integers: every sum is exact and order-independent, so a draw is
+// bitwise deterministic.
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 
 #include "asr_internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace asr {
 namespace {
 
-constexpr int kSampleThreads = 1024;
-constexpr int kBins = 4096;
-constexpr double kFix = 68719476736.0;   // 2^36
+constexpr int kST = 512;             // threads per CTA
+constexpr int kSW = kST / 32;        // warps per CTA
+constexpr int kWays = 8;             // split points per search pass: kWays - 1
+constexpr float kFix = 68719476736.0f;   // 2^36
 
 __device__ __forceinline__ float lg(const __nv_bfloat16* p, int j) { return __bfloat162float(p[j]); }
 __device__ __forceinline__ float lg(const float* p, int j) { return p[j]; }
@@ -32,262 +40,384 @@ __device__ __forceinline__ uint32_t fkey(float x) {
   uint32_t b = __float_as_uint(x == 0.f ? 0.f : x);
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
+__device__ __forceinline__ float unkey(uint32_t k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
 
 __device__ __forceinline__ unsigned long long wfix(float x, float m, float invT) {
-  return (unsigned long long)((double)__expf((x - m) * invT) * kFix);
+  return (unsigned long long)(__expf((x - m) * invT) * kFix);   // exact power-of-two scale
 }
 
 struct SampleShm {
-  uint32_t cnt[kBins];
-  unsigned long long mass[kBins];
-  unsigned long long wsum[32];
-  uint32_t wcnt[32];
-  float fred[32];
-  int ired[32];
-  uint32_t digit;
-  unsigned long long scan_total, tie_take;
-  uint32_t above_cnt;
-  int token;
+  unsigned long long wq[kSW][2 * kWays];   // per-warp partials (reused by every reduction)
+  unsigned long long out[2][2 * kWays];    // this CTA's totals by call parity, read by the cluster (DSMEM)
+  unsigned long long res[2 * kWays];       // cluster totals of the last reduction
+  float fout;
+  int iout;
 };
 
-// block-wide exclusive scan (thread order) of a 64-bit value; also returns the total
-__device__ unsigned long long block_excl_scan(unsigned long long v, SampleShm& sh, unsigned long long* total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned long long incl = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) sh.wsum[w] = incl;
-  __syncthreads();
-  if (w == 0) {
-    const unsigned long long x = sh.wsum[lane];
-    unsigned long long xi = x;
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, xi, o);
-      if (lane >= o) xi += y;
+// Visit elements j = first, first + stride, ... < end: kU loads are issued before any is used (the
+// loops are latency-bound otherwise: one L2 round trip per element), then f(value, j) runs on each.
+constexpr int kU = 8;
+template <typename TL, typename Fn>
+__device__ __forceinline__ void visit(const TL* __restrict__ x, int first, int end, int stride, Fn&& f) {
+  for (int j0 = first; j0 < end; j0 += kU * stride) {
+    float v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * stride;
+      v[u] = lg(x, j < end ? j : first);
     }
-    sh.wsum[lane] = xi - x;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * stride;
+      if (j < end) f(v[u], j);
+    }
   }
-  __syncthreads();
-  const unsigned long long res = sh.wsum[w] + incl - v;
-  if (threadIdx.x == kSampleThreads - 1) sh.scan_total = res + v;
-  __syncthreads();
-  *total = sh.scan_total;
-  __syncthreads();
-  return res;
 }
 
-// Find the digit d whose bin crosses `target` counting from the top bin down: above(d) < target <=
-// above(d) + bin(d), where bin = counts (by_mass false) or masses.  Sets sh.digit, sh.above_cnt,
-// sh.above_mass (the totals of the bins above d).  nbins <= kBins (a power of two >= 1024... or 256).
-__device__ void find_digit(SampleShm& sh, int nbins, bool by_mass, unsigned long long target) {
-  const int per = nbins / kSampleThreads > 0 ? nbins / kSampleThreads : 1;
-  const int active = nbins / per;
-  // thread t owns bins hi_t, hi_t - 1, ..., hi_t - per + 1 with hi_t = nbins - 1 - t * per
-  const int hi = nbins - 1 - (int)threadIdx.x * per;
-  unsigned long long sv = 0, sc = 0;
-  if ((int)threadIdx.x < active)
-    for (int k = 0; k < per; ++k) {
-      sv += by_mass ? sh.mass[hi - k] : sh.cnt[hi - k];
-      sc += sh.cnt[hi - k];
+// The same over [s0, s1) split among the CTA's threads in runs of 8 consecutive elements (16-byte
+// loads, two for fp32), two runs per thread in flight; needs s0 % 8 == 0 and a 16-byte aligned row,
+// else it falls back to visit().  Each thread sees its elements in increasing index order.
+template <typename TL, typename Fn>
+__device__ __forceinline__ void visit8(const TL* __restrict__ x, int s0, int s1, bool aligned, Fn&& f) {
+  if (!aligned) {
+    visit(x, s0 + (int)threadIdx.x, s1, kST, f);
+    return;
+  }
+  constexpr int kW = sizeof(TL) == 2 ? 1 : 2;   // 16-byte words per run of 8
+  constexpr int kR = 2;                          // runs in flight per thread
+  for (int b0 = s0 + (int)threadIdx.x * 8; b0 < s1; b0 += kR * kST * 8) {
+    uint4 r[kR][kW];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      const int b = b0 + u * kST * 8;
+      const uint4* src = reinterpret_cast<const uint4*>(x + (b + 8 <= s1 ? b : s0));
+#pragma unroll
+      for (int w = 0; w < kW; ++w) r[u][w] = __ldg(src + w);
     }
-  unsigned long long tot;
-  const unsigned long long before = block_excl_scan(sv, sh, &tot);
-  const unsigned long long before_c = block_excl_scan(sc, sh, &tot);
-  const unsigned long long before_m = by_mass ? before : 0;   // mass above, when selecting by mass
-  if ((int)threadIdx.x < active && before < target && target <= before + sv) {
-    unsigned long long a = before, ac = before_c;
-    for (int k = 0; k < per; ++k) {
-      const unsigned long long v = by_mass ? sh.mass[hi - k] : sh.cnt[hi - k];
-      if (a < target && target <= a + v) {
-        sh.digit = (uint32_t)(hi - k);
-        sh.above_cnt = (uint32_t)ac;
-        sh.tie_take = a;   // the selected quantity above the digit (count or mass)
-        break;
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      const int b = b0 + u * kST * 8;
+      if (b >= s1) break;
+      float v[8];
+      if (b + 8 <= s1) {
+        if constexpr (sizeof(TL) == 2) {
+          const uint32_t q[4] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) { v[2 * e] = __uint_as_float(q[e] << 16); v[2 * e + 1] = __uint_as_float(q[e] & 0xffff0000u); }
+        } else {
+          const uint32_t q[8] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w,
+                                 r[u][kW - 1].x, r[u][kW - 1].y, r[u][kW - 1].z, r[u][kW - 1].w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(q[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f(v[e], b + e);
+      } else {
+        for (int e = 0; b + e < s1; ++e) f(lg(x, b + e), b + e);
       }
-      a += v;
-      ac += sh.cnt[hi - k];
     }
   }
-  (void)before_m;
-  __syncthreads();
 }
 
-template <typename TL>
-__global__ void __launch_bounds__(kSampleThreads) sample_kernel(const TL* __restrict__ logits, int V, float temperature,
-                                                                int top_k, float top_p, const float* __restrict__ uniforms,
-                                                                int32_t* __restrict__ token_out) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SampleShm& sh = *reinterpret_cast<SampleShm*>(smem_raw);
-  const TL* x = logits + (long)blockIdx.x * V;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+template <typename F>
+__device__ __forceinline__ F warp_sum(F v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
-  // ---- max (and its first index, for greedy)
+// Sum n (<= 2*kWays) per-thread integers over the cluster: warps, then the CTA's warps, then lane r of
+// warp 0 reads CTA r's total through DSMEM (integer sums: exact in any order).  One cluster barrier:
+// the CTA totals alternate between two slots by call parity `par`, so a slot is rewritten only after
+// every CTA has passed the next call's barrier.  Every thread gets the totals in res[0..n).
+template <int CS>
+__device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned long long* v, int n,
+                            unsigned long long* res, int& par) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    const unsigned long long s = warp_sum(v[k]);
+    if (lane == 0) sh.wq[w][k] = s;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < n) {
+    unsigned long long t = 0;
+    for (int q = 0; q < kSW; ++q) t += sh.wq[q][threadIdx.x];
+    sh.out[par][threadIdx.x] = t;
+  }
+  cl.sync();
+  if (w == 0)
+    for (int k = 0; k < n; ++k) {
+      const unsigned long long t = warp_sum(lane < CS ? cl.map_shared_rank(&sh, lane)->out[par][k] : 0ull);
+      if (lane == 0) sh.res[k] = t;
+    }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) res[k] = sh.res[k];
+  par ^= 1;
+}
+
+// CS CTAs (one cluster) per row
+template <typename TL, int CS>
+__global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logits, int V, float temperature, int top_k,
+                                                     float top_p, const float* __restrict__ uniforms,
+                                                     int32_t* __restrict__ token_out) {
+  __shared__ SampleShm sh;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int row = blockIdx.y;
+  const TL* x = logits + (long)row * V;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int S = ((V + CS - 1) / CS + 31) & ~31;   // slice of this CTA: [s0, s1)
+  int par = 0;                                     // cluster_sum slot parity
+  const int s0 = min(V, rank * S), s1 = min(V, s0 + S);
+
+  // ---- max and its first index (greedy)
   float mx = -INFINITY;
   int mi = 0x7fffffff;
-  for (int j = tid; j < V; j += kSampleThreads) {
-    const float v = lg(x, j);
-    if (v > mx) { mx = v; mi = j; }   // j grows per thread: the first maximum of the thread
-  }
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;   // s0 is a multiple of 32
+  visit8(x, s0, s1, aligned, [&](float v, int j) {
+    if (v > mx) { mx = v; mi = j; }
+  });
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
     const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
     if (om > mx || (om == mx && oi < mi)) { mx = om; mi = oi; }
   }
-  if (lane == 0) { sh.fred[w] = mx; sh.ired[w] = mi; }
+  if (lane == 0) { sh.wq[w][0] = __float_as_uint(mx); sh.wq[w][1] = (unsigned)mi; }
   __syncthreads();
-  if (w == 0) {
-    mx = sh.fred[lane];
-    mi = sh.ired[lane];
-    for (int o = 16; o > 0; o >>= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, mx, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+  if (tid == 0) {
+    for (int q = 0; q < kSW; ++q) {
+      const float om = __uint_as_float((uint32_t)sh.wq[q][0]);
+      const int oi = (int)sh.wq[q][1];
       if (om > mx || (om == mx && oi < mi)) { mx = om; mi = oi; }
     }
-    if (lane == 0) { sh.fred[0] = mx; sh.ired[0] = mi; }
+    sh.fout = mx;
+    sh.iout = mi;
   }
-  __syncthreads();
-  const float m = sh.fred[0];
+  cl.sync();
+  for (int r = 0; r < CS; ++r) {
+    const SampleShm* o = cl.map_shared_rank(&sh, r);
+    const float om = o->fout;
+    const int oi = o->iout;
+    if (om > mx || (om == mx && oi < mi)) { mx = om; mi = oi; }
+  }
+  cl.sync();
+  const float m = mx;
   if (!(temperature > 0.f) || top_k == 1 || V == 1) {
-    if (tid == 0) token_out[blockIdx.x] = sh.ired[0];
+    if (rank == 0 && tid == 0) token_out[row] = mi;
     return;
   }
   const float invT = 1.0f / temperature;
   const bool use_k = top_k > 0 && top_k < V;
   const bool use_p = top_p > 0.f && top_p < 1.f;
 
-  // ---- boundary of the kept set: key fk and how many of the tokens with key == fk (in index order)
-  //      are kept (n_tie); the mass of everything above fk
-  uint32_t fk = 0;               // all keys >= 0: keep everything
-  unsigned long long n_tie = 0xffffffffffffffffull;
-  unsigned long long above_fk_mass = 0;
-  auto radix = [&](bool by_mass, unsigned long long target) {
-    // 3 levels: digits [31:20], [19:8], [7:0]; returns via fk / counts / masses above
-    uint32_t prefix = 0, pmask = 0;
-    unsigned long long above_m = 0, above_c = 0;
-    const int shifts[3] = {20, 8, 0}, bits[3] = {12, 12, 8};
-    for (int lv = 0; lv < 3; ++lv) {
-      const int nb = 1 << bits[lv];
-      for (int k = tid; k < nb; k += kSampleThreads) { sh.cnt[k] = 0; sh.mass[k] = 0; }
-      __syncthreads();
-      for (int j = tid; j < V; j += kSampleThreads) {
-        const float v = lg(x, j);
-        const uint32_t key = fkey(v);
-        if ((key & pmask) == prefix) {
-          const uint32_t d = (key >> shifts[lv]) & (uint32_t)(nb - 1);
-          atomicAdd(&sh.cnt[d], 1u);
-          atomicAdd(&sh.mass[d], wfix(v, m, invT));
+  // ---- the kept set's boundary: key fk, and n_tie of the tokens with key == fk (in index order)
+  uint32_t fk = 0;
+  unsigned long long n_tie = ~0ull;
+  const int kshift = sizeof(TL) == 2 ? 16 : 0;
+  // largest key t with Q(key >= t) >= target, Q = count (by_mass false) or fixed-point mass; an 8-ary
+  // search (the key ranges stay powers of two); returns Q(key > t)
+  auto search = [&](bool by_mass, unsigned long long target) -> unsigned long long {
+    unsigned long long lo = 0, hi = 1ull << (32 - kshift);   // Q(>= lo) >= target > Q(>= hi)
+    unsigned long long q_hi = 0;
+    while (hi - lo > 1) {
+      const unsigned long long step = (hi - lo + kWays - 1) / kWays;
+      // split points as 32-bit keys (clamped: a point at or above hi holds nothing new)
+      uint32_t tk[kWays - 1];
+#pragma unroll
+      for (int k = 0; k < kWays - 1; ++k) {
+        const unsigned long long t = lo + (k + 1) * step;
+        tk[k] = t >= (1ull << (32 - kshift)) ? 0xffffffffu : (uint32_t)t;
+      }
+      unsigned long long q[kWays];
+      uint32_t qc[kWays];
+#pragma unroll
+      for (int k = 0; k < kWays - 1; ++k) { q[k] = 0; qc[k] = 0; }
+      visit8(x, s0, s1, aligned, [&](float v, int) {
+        const uint32_t kk = fkey(v) >> kshift;
+        if (kk < tk[0]) return;
+        if (by_mass) {
+          const unsigned long long wv = wfix(v, m, invT);
+#pragma unroll
+          for (int k = 0; k < kWays - 1; ++k)
+            if (kk >= tk[k]) q[k] += wv;
+        } else {
+#pragma unroll
+          for (int k = 0; k < kWays - 1; ++k) qc[k] += kk >= tk[k];
         }
+      });
+      if (!by_mass)
+#pragma unroll
+        for (int k = 0; k < kWays - 1; ++k) q[k] = qc[k];
+      unsigned long long tot[kWays];
+      cluster_sum<CS>(cl, sh, q, kWays - 1, tot, par);
+      unsigned long long nlo = lo, nhi = hi, nq = q_hi;
+      for (int k = kWays - 2; k >= 0; --k) {
+        const unsigned long long t = lo + (k + 1) * step;
+        if (t >= hi) continue;
+        if (tot[k] >= target) { nlo = t; break; }
+        nhi = t;
+        nq = tot[k];
       }
-      __syncthreads();
-      find_digit(sh, nb, by_mass, target - (by_mass ? above_m : above_c));
-      const uint32_t d = sh.digit;
-      const unsigned long long a_sel = sh.tie_take;   // selected quantity above d within this level
-      // counts / masses of the bins above d (this level)
-      unsigned long long am = 0, ac = 0;
-      {
-        unsigned long long tot;
-        unsigned long long vm = 0, vc = 0;
-        for (int k = tid; k < nb; k += kSampleThreads)
-          if ((uint32_t)k > d) { vm += sh.mass[k]; vc += sh.cnt[k]; }
-        block_excl_scan(vm, sh, &tot);
-        am = tot;
-        block_excl_scan(vc, sh, &tot);
-        ac = tot;
-      }
-      (void)a_sel;
-      above_m += am;
-      above_c += ac;
-      prefix |= d << shifts[lv];
-      pmask |= (uint32_t)(nb - 1) << shifts[lv];
-      __syncthreads();
+      lo = nlo;
+      hi = nhi;
+      q_hi = nq;
     }
-    // the boundary key, tokens strictly above it, and the mass strictly above it
-    fk = prefix;
-    return make_ulonglong2(above_c, above_m);
+    fk = (uint32_t)(lo << kshift);
+    return q_hi;
   };
-  unsigned long long mass_kept_total = 0;
-  if (use_k) {
-    const ulonglong2 r = radix(false, (unsigned long long)top_k);
-    const unsigned long long wk = 0;   // mass of one token at fk (recomputed below)
-    (void)wk;
-    n_tie = (unsigned long long)top_k - r.x;
-    above_fk_mass = r.y;
-    mass_kept_total = above_fk_mass + n_tie * wfix(__uint_as_float((fk & 0x80000000u) ? (fk & 0x7fffffffu) : ~fk), m, invT);
-  } else {
-    // total mass of the row
+  // the mass of the tokens with key > fk (one pass)
+  auto mass_above = [&]() -> unsigned long long {
     unsigned long long v = 0, tot;
-    for (int j = tid; j < V; j += kSampleThreads) v += wfix(lg(x, j), m, invT);
-    block_excl_scan(v, sh, &tot);
-    mass_kept_total = tot;
+    visit8(x, s0, s1, aligned, [&](float x1, int) {
+      if (fkey(x1) > fk) v += wfix(x1, m, invT);
+    });
+    cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
+    return tot;
+  };
+  unsigned long long kept_mass = 0;
+  if (use_k) {
+    const unsigned long long ca = search(false, (unsigned long long)top_k);
+    n_tie = (unsigned long long)top_k - ca;
+    kept_mass = mass_above() + n_tie * wfix(unkey(fk), m, invT);
+  } else {
+    unsigned long long v = 0, tot;
+    visit8(x, s0, s1, aligned, [&](float x1, int) { v += wfix(x1, m, invT); });
+    cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
+    kept_mass = tot;
   }
   if (use_p) {
-    // the shortest prefix (key desc, index asc) of the kept set with mass >= P * M: the boundary key
-    // pk with mass(key > pk) < target <= mass(key >= pk); tokens at pk needed: ceil((target -
-    // mass(key > pk)) / w(pk)) (all equal keys carry equal mass)
-    const unsigned long long target = (unsigned long long)ceil((double)top_p * (double)mass_kept_total);
+    // the boundary key of the shortest mass prefix: mass(key > pk) < target <= mass(key >= pk); it
+    // lies at or above the top-k boundary, and the tokens at pk it needs are the fewest whose equal
+    // masses reach the target
+    const unsigned long long target = (unsigned long long)ceil((double)top_p * (double)kept_mass);
     const uint32_t fk_k = fk;
     const unsigned long long n_tie_k = n_tie;
-    const ulonglong2 r = radix(true, target);
-    const float xb = __uint_as_float((fk & 0x80000000u) ? (fk & 0x7fffffffu) : ~fk);
-    const unsigned long long wb = wfix(xb, m, invT);
-    const unsigned long long need = wb ? (target - r.y + wb - 1) / wb : 1;
-    if (use_k && fk == fk_k) n_tie = need < n_tie_k ? need : n_tie_k;   // same boundary: the stricter
-    else n_tie = need;
-    above_fk_mass = r.y;
+    const unsigned long long ma = search(true, target);
+    const unsigned long long wb = wfix(unkey(fk), m, invT);
+    const unsigned long long need = wb ? (target - ma + wb - 1) / wb : 1;
+    n_tie = (use_k && fk == fk_k && n_tie_k < need) ? n_tie_k : need;
   }
 
-  // ---- the draw: per-thread contiguous chunks, tie ranks and kept masses scanned across the block
-  const int per = (V + kSampleThreads - 1) / kSampleThreads;
-  const int j0 = min(V, tid * per), j1 = min(V, j0 + per);
-  unsigned long long ties = 0;
-  for (int j = j0; j < j1; ++j) ties += fkey(lg(x, j)) == fk;
-  unsigned long long tot;
-  const unsigned long long tie0 = block_excl_scan(ties, sh, &tot);
-  unsigned long long km = 0, rank = tie0;
-  for (int j = j0; j < j1; ++j) {
-    const float v = lg(x, j);
-    const uint32_t key = fkey(v);
-    if (key > fk || (key == fk && rank++ < n_tie)) km += wfix(v, m, invT);
-  }
-  const unsigned long long km0 = block_excl_scan(km, sh, &tot);
-  const unsigned long long target = (unsigned long long)((double)uniforms[blockIdx.x] * (double)tot);
-  if (tid == 0) sh.token = -1;
+  // ---- the draw: ties (key == fk) are ranked in index order; warp q of CTA r owns the contiguous
+  //      chunk q of slice r, read in coalesced groups of 32 lanes
+  const int per = ((s1 - s0 + kSW - 1) / kSW + 31) & ~31;
+  const int c0 = min(s1, s0 + w * per), c1 = min(s1, c0 + per);
+  unsigned long long tw = 0;
+  visit(x, c0 + lane, c1, 32, [&](float x1, int) { tw += fkey(x1) == fk; });
+  tw = warp_sum(tw);
+  if (lane == 0) sh.wq[w][0] = tw;
   __syncthreads();
-  if (km > 0 && km0 <= target && target < km0 + km) {
-    unsigned long long acc = km0, r2 = tie0;
-    for (int j = j0; j < j1; ++j) {
-      const float v = lg(x, j);
-      const uint32_t key = fkey(v);
-      if (key > fk || (key == fk && r2++ < n_tie)) {
-        acc += wfix(v, m, invT);
-        if (acc > target) {
-          sh.token = j;
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int q = 0; q < kSW; ++q) t += sh.wq[q][0];
+    sh.out[par][0] = t;
+  }
+  cl.sync();
+  unsigned long long tie_base = 0;   // ties before this warp's chunk
+  for (int r = 0; r < rank; ++r) tie_base += cl.map_shared_rank(&sh, r)->out[par][0];
+  for (int q = 0; q < w; ++q) tie_base += sh.wq[q][0];
+  par ^= 1;
+  __syncthreads();   // wq[.][0] read by every warp before it is reused
+  auto group = [&](int j, float v, unsigned long long& rk) -> unsigned long long {   // this lane's kept mass
+    const bool in = j < c1;
+    const uint32_t key = in ? fkey(v) : 0u;
+    const bool tie = in && key == fk;
+    const unsigned tm = __ballot_sync(0xffffffffu, tie);
+    const unsigned long long my = rk + __popc(tm & ((1u << lane) - 1u));
+    rk += __popc(tm);
+    return (in && (key > fk || (tie && my < n_tie))) ? wfix(v, m, invT) : 0ull;
+  };
+  // groups of 32 (one element per lane), kU groups' loads in flight per lane
+  auto load_groups = [&](int g0, float* v) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = g0 + u * 32 + lane;
+      v[u] = lg(x, j < c1 ? j : c0);
+    }
+  };
+  unsigned long long wk = 0, rk = tie_base;
+  for (int g0 = c0; g0 < c1; g0 += kU * 32) {
+    float v[kU];
+    load_groups(g0, v);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) wk += group(g0 + u * 32 + lane, v[u], rk);
+  }
+  wk = warp_sum(wk);
+  if (lane == 0) sh.wq[w][1] = wk;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int q = 0; q < kSW; ++q) t += sh.wq[q][1];
+    sh.out[par][1] = t;
+  }
+  cl.sync();
+  unsigned long long before = 0, total = 0;
+  for (int r = 0; r < CS; ++r) {
+    const unsigned long long t = cl.map_shared_rank(&sh, r)->out[par][1];
+    if (r < rank) before += t;
+    total += t;
+  }
+  for (int q = 0; q < w; ++q) before += sh.wq[q][1];
+  const unsigned long long target = (unsigned long long)((double)uniforms[row] * (double)total);
+  if (wk > 0 && before <= target && target < before + wk) {   // warp-uniform: the warp holding the draw
+    unsigned long long acc = before, r2 = tie_base;
+    bool found = false;
+    for (int g0 = c0; g0 < c1 && !found; g0 += kU * 32) {
+      float v[kU];
+      load_groups(g0, v);
+      for (int u = 0; u < kU; ++u) {
+        const int gj = g0 + u * 32;
+        const unsigned long long wv = group(gj + lane, v[u], r2);
+        unsigned long long incl = wv;   // inclusive scan over the group (lane order = index order)
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, wv > 0 && acc + incl > target);
+        if (hit) {
+          if (lane == __ffs(hit) - 1) token_out[row] = gj + lane;
+          found = true;
           break;
         }
+        acc += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
   }
-  __syncthreads();
-  if (tid == 0) {
-    int t = sh.token;
-    if (t < 0) t = sh.ired[0];   // u * M rounded onto the very end: the kept set's maximum
-    token_out[blockIdx.x] = t;
-  }
+  cl.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+template <int CS>
+cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
+                      float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, batch);
+  cfg.blockDim = dim3(kST);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (logits_dtype == 1)
+    return cudaLaunchKernelEx(&cfg, sample_kernel<float, CS>, (const float*)logits, vocab, temperature, top_k, top_p,
+                              uniforms, token_out);
+  return cudaLaunchKernelEx(&cfg, sample_kernel<__nv_bfloat16, CS>, (const __nv_bfloat16*)logits, vocab, temperature,
+                            top_k, top_p, uniforms, token_out);
 }
 
 }  // namespace
 
+// Small batches spread each row over a cluster of 8 CTAs; large ones use one CTA per row (the rows
+// alone fill the GPU).
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
                           float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
-  const unsigned smem = sizeof(SampleShm);
-  const void* f = logits_dtype == 1 ? (const void*)sample_kernel<float> : (const void*)sample_kernel<__nv_bfloat16>;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  void* args[] = {const_cast<void**>(&logits), &vocab, &temperature, &top_k, &top_p, const_cast<float**>(&uniforms),
-                  &token_out};
-  return cudaLaunchKernel(f, dim3(batch), dim3(kSampleThreads), args, smem, st);
+  if (batch >= 32)
+    return launch_cs<1>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
+  if (batch >= 8)
+    return launch_cs<4>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
+  return launch_cs<8>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
 }
 
 }  // namespace asr
