@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--window", type=int, default=512)
     ap.add_argument("--family", default="w0", choices=["w0", "w1"])
     ap.add_argument("--tau", type=float, default=0.5, help="tau; <= 0 freezes nothing (the full-KV baseline)")
+    ap.add_argument("--history-window", type=int, default=0, help="W of Eq. 3's count (0 = lifetime, R-W)")
     ap.add_argument("--seed", type=int, default=2001)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -201,7 +202,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     pool = int(a.pool_frac * B * a.context) + 4 * B if a.pool_frac > 0 else 0
     cfg = Config(n_layers=L, n_q_heads=hq_r, n_kv_heads=hkv_r, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=a.tau, softness=2.0, vocab=VOCAB, profile_stages=0,
-                 device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min,
+                 device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min, history_window=a.history_window,
                  score_heads=HQ if a.head_shard else 0)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, hkv_r, D), dtype=bf, device=dev)
@@ -424,7 +425,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
-                               + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else ""),
+                               + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else "")
+                               + (f" W{a.history_window}" if a.history_window else ""),
                    "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": a.tau, "k": 2,
                    "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
                    "parallelism": (f"head-sharded x{world} (NCCL all-reduce of per-token partial scores)" if a.head_shard
@@ -467,6 +469,7 @@ POINTS = {   # extra workloads measured after the headline
     "w1": dict(family="w1"),                                        # 30 % hot tokens (SURVEY W1 family)
     "full": dict(tau=0.0),                                          # full-KV baseline: nothing freezes
     "ctx32k": dict(context=32768, steps=32),                        # configs[3]-like length, grown state
+    "w128": dict(history_window=128),                               # NEXT-3: finite history window W
 }
 
 

@@ -55,7 +55,8 @@ typedef struct {
   int32_t window;         /* K >= 1: positions >= n-K are never frozen (R-win) */
   float tau;              /* threshold, strict s_j < tau */
   float softness;         /* k > 0 of Eq. 3 */
-  int32_t history_window; /* W: 0 = infinite (R-W, the only value this build accepts) */
+  int32_t history_window; /* W of Eq. 3's count c_j: 0 = lifetime (R-W, default, Table-pinned);
+                             1..128 = detections within the last W steps (a per-token bitmask) */
   int32_t pinned_prefix;  /* positions < pinned_prefix are never frozen (R-sink, default 0) */
   int32_t score_mode;     /* asr_score_mode */
   int32_t tick_order;     /* asr_tick */

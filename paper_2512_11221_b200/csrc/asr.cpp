@@ -209,8 +209,8 @@ static asr_status validate(const asr_config* c) {
   if (c->window < 1) return fail(ASR_E_INVALID, "window (K) must be >= 1");
   if (!(c->softness > 0.f) || !isfinite(c->softness)) return fail(ASR_E_INVALID, "softness k must be > 0");
   if (!isfinite(c->tau)) return fail(ASR_E_INVALID, "tau must be finite");
-  if (c->history_window != 0)
-    return fail(ASR_E_INVALID, "history_window: only W = 0 (infinite, R-W) is supported");
+  if (c->history_window < 0 || c->history_window > 128)
+    return fail(ASR_E_INVALID, "history_window: W = 0 (infinite, R-W) or 1..128");
   if (c->pinned_prefix < 0) return fail(ASR_E_INVALID, "pinned_prefix < 0");
   if (c->score_mode != ASR_SCORE_RAW && c->score_mode != ASR_SCORE_SCALED) return fail(ASR_E_INVALID, "score_mode");
   if (c->tick_order != ASR_TICK_LITERAL && c->tick_order != ASR_TICK_SKIP_NEW) return fail(ASR_E_INVALID, "tick_order");
@@ -346,6 +346,13 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.timer, BT * 4));
     CUDA_TRY(c->alloc(&s.count, BT * 4));
     CUDA_TRY(c->alloc(&s.fstep, BT * 4));
+    s.hist_w = cfg->history_window;
+    if (s.hist_w > 0) {   // finite W: per-token detection history (NEXT-3)
+      CUDA_TRY(c->alloc(&s.hmask, BT * 16));
+      CUDA_TRY(c->alloc(&s.hstep, BT * 4));
+      CUDA_TRY(cudaMemsetAsync(s.hmask, 0, BT * 16, st));
+      CUDA_TRY(cudaMemsetAsync(s.hstep, 0xc0, BT * 4, st));   // 0xc0c0c0c0: never detected
+    }
     CUDA_TRY(c->alloc(&s.prompt_len, (size_t)s.B * 4));
     CUDA_TRY(c->alloc(&s.step, 4));
     CUDA_TRY(c->alloc(&s.act_pos, 2 * BT * 4));
@@ -939,7 +946,26 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
       for (int64_t j = 0; j < n; ++j) detail->residency[j] = asr::res_active(detail->residency[j]) ? 1 : 0;
     }
     if (detail->timer) CUDA_TRY(cudaMemcpy(detail->timer, s.timer + base, n * 4, cudaMemcpyDeviceToHost));
-    if (detail->count) CUDA_TRY(cudaMemcpy(detail->count, s.count + base, n * 4, cudaMemcpyDeviceToHost));
+    if (detail->count && s.hist_w > 0) {
+      // detections within the window that ends at the last completed step
+      std::vector<unsigned long long> hm(2 * (size_t)n);
+      std::vector<int32_t> hs(n);
+      if (n) {
+        CUDA_TRY(cudaMemcpy(hm.data(), s.hmask + 2 * base, 16 * (size_t)n, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(hs.data(), s.hstep + base, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+      }
+      const int64_t last = c->step - 1;
+      for (int64_t j = 0; j < n; ++j) {
+        int c2 = 0;
+        for (int t = 0; t < 128; ++t) {
+          const bool bit = (hm[2 * j + (t >> 6)] >> (t & 63)) & 1ull;
+          if (bit && (int64_t)hs[j] - t > last - s.hist_w) ++c2;
+        }
+        detail->count[j] = (uint32_t)c2;
+      }
+    } else if (detail->count) {
+      CUDA_TRY(cudaMemcpy(detail->count, s.count + base, n * 4, cudaMemcpyDeviceToHost));
+    }
     if (detail->freeze_step) CUDA_TRY(cudaMemcpy(detail->freeze_step, s.fstep + base, n * 4, cudaMemcpyDeviceToHost));
     int32_t A = 0;
     const int p = (int)((c->step - 1) & 1);   // parity of the last step's A_i

@@ -76,6 +76,9 @@ struct DevState {
   int decide_blocks;          // blocks per sequence of the decide kernel
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
+  int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
+  unsigned long long* hmask;  // [B][max_ctx][2] finite W: bit t = detection at step hstep - t
+  int32_t* hstep;             // [B][max_ctx]    finite W: step of bit 0 (never: a large negative)
   int combine_in_decide;      // 1: the combine runs as extra blocks of the phase-D kernel (small batch)
   int kv_evict_first;         // 1: the attention's KV bulk copies carry an L2 evict_first policy
   int ent_per_unit;           // entropy splits per phase-A unit (divides kEntSplits)

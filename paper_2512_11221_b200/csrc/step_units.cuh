@@ -388,7 +388,13 @@ __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
   }
   if (level >= 3 && s.fr_clear_counts) {
     uint32_t* cnt = s.count + (long)b * s.max_ctx;
-    for (int j = ASR_UNIT_TID(); j < n; j += ASR_UNIT_THREADS()) cnt[j] = 0;
+    for (int j = ASR_UNIT_TID(); j < n; j += ASR_UNIT_THREADS()) {
+      cnt[j] = 0;
+      if (s.hist_w > 0) {
+        s.hmask[((long)b * s.max_ctx + j) * 2] = 0;
+        s.hmask[((long)b * s.max_ctx + j) * 2 + 1] = 0;
+      }
+    }
   }
   return restored;
 }
@@ -628,8 +634,38 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     if (s.score_scaled) sj = sj / sqrt_d;
     s.score[base + a] = sj;
     if (j < n - s.window && j >= s.pinned && sj < s.tau) {
-      const uint32_t c = cnt[j] + 1;    // line 4
-      cnt[j] = c;
+      uint32_t c;                       // line 4: c_j <- c_j + 1 (lifetime, or within the window W)
+      if (s.hist_w > 0) {
+        // finite W: a 128-bit history of detections, bit t = step hstep - t; shift it to step
+        // i, record this detection, keep the bits of (i - W, i] and count them
+        unsigned long long* hm = s.hmask + (base + j) * 2;
+        const int sh = i - s.hstep[base + j];
+        unsigned long long lo = hm[0], hi = hm[1];
+        if (sh >= 128) {
+          lo = hi = 0;
+        } else if (sh >= 64) {
+          hi = lo << (sh - 64);
+          lo = 0;
+        } else if (sh > 0) {
+          hi = (hi << sh) | (lo >> (64 - sh));
+          lo <<= sh;
+        }
+        lo |= 1ull;
+        if (s.hist_w < 64) {
+          lo &= (1ull << s.hist_w) - 1ull;
+          hi = 0;
+        } else if (s.hist_w < 128) {
+          hi &= (1ull << (s.hist_w - 64)) - 1ull;
+        }
+        hm[0] = lo;
+        hm[1] = hi;
+        s.hstep[base + j] = i;
+        c = (uint32_t)(__popcll(lo) + __popcll(hi));
+        cnt[j] = c;
+      } else {
+        c = cnt[j] + 1;
+        cnt[j] = c;
+      }
       const int dd = duration(c, s.softness, s.softness_int);  // line 5
       if (dd > 0) {                     // lines 6-7
         frozen_now++;

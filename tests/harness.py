@@ -56,6 +56,7 @@ class Case:
     evict_min: int = 2
     nccl_world1: bool = False      # attach a one-rank NCCL communicator (attend -> all-reduce -> decide)
     logits_dtype: str = "bf16"     # "f32": the same (bf16-exact) logits passed as fp32
+    history_window: int = 0        # W (NEXT-3): 0 = lifetime counts
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -71,7 +72,7 @@ class Case:
 def orc_cfg(c: Case) -> oracle.OrcCfg:
     return oracle.OrcCfg(L=c.L, Hq=c.Hq, Hkv=c.Hkv, d=c.d, window=c.window, tau=c.tau, softness=c.softness,
                          pinned_prefix=c.pinned_prefix, score_scaled=c.score_mode, tick_skip_new=c.tick_order,
-                         vocab=c.vocab, wr_window=c.wr_window)
+                         vocab=c.vocab, wr_window=c.wr_window, history_window=c.history_window)
 
 
 def asr_cfg(c: Case):
@@ -80,7 +81,7 @@ def asr_cfg(c: Case):
                   max_context=c.capacity(), kv_dtype=KV_BF16 if c.dtype == "bf16" else KV_F32,
                   window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
                   score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window,
-                  pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min)
+                  pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min, history_window=c.history_window)
 
 
 def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:

@@ -64,7 +64,7 @@ def test_defaults_are_the_papers():
 
 
 @pytest.mark.parametrize("bad", [dict(n_layers=0), dict(n_q_heads=6, n_kv_heads=4), dict(head_dim=48),
-                                 dict(window=0), dict(softness=0.0), dict(history_window=128),
+                                 dict(window=0), dict(softness=0.0), dict(history_window=129), dict(history_window=-1),
                                  dict(kv_dtype=7), dict(batch=0), dict(det_baseline=1000)])
 def test_invalid_config_is_rejected_synchronously(bad):
     cfg = asr.Config(**bad)

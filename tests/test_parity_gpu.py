@@ -139,3 +139,14 @@ def test_large_batch_grouped_phase_a_units():
     # range) and the combine as a separate kernel (batch * L * Hq > 64 warps per SM)
     run(Case(L=4, Hq=32, Hkv=8, d=128, B=80, prompt=tuple(20 + (7 * b) % 50 for b in range(80)), steps=12,
              window=8, vocab=1024, seed=93, hot_permille=300, a_hot=64))
+
+
+@pytest.mark.parametrize("W", [8, 64, 100, 128])
+def test_finite_history_window(W):
+    # NEXT-3: Eq. 3's count c_j over the last W steps only — a per-token 128-bit detection
+    # history on the device; ledgers (counts within the window), lists and O bitwise against the
+    # oracle's detection log.  W < run length makes counts fall back and durations shrink.
+    s = run(Case(prompt=(40,), steps=160, window=8, seed=300 + W, history_window=W))
+    assert s["frozen"] > 0
+    run(Case(L=2, Hq=32, Hkv=8, d=128, B=1, prompt=(60,), steps=90, window=8, hot_permille=300, a_hot=64,
+             vocab=4096, seed=400 + W, history_window=W))
