@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
-    ap.add_argument("--points", default="cfg3,w1,full,sample",
+    ap.add_argument("--points", default="cfg3,w1,full,sample,replay",
                     help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
     ap.add_argument("--head-shard", action="store_true",
                     help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
@@ -506,6 +506,37 @@ def sample_point(local_rank: int) -> dict:
     return out
 
 
+def replay_point(local_rank: int) -> dict:
+    """NEXT-2: policy replay (asr_step_policy) of the all-cold trace for 1024 sequences at 8K context,
+    K = 512 — Alg. 1 lines 3-15 + compaction for every sequence, no attention; sequence-steps per second
+    (CUDA events over 32 steps, after the sequences have grown to 8K)."""
+    import torch
+
+    from paper_2512_11221_b200 import Config, Context
+    dev = torch.device("cuda", local_rank)
+    B, ctxlen, P, K = 1024, 8192, 512, 32
+    cfg = Config(n_layers=1, n_q_heads=2, n_kv_heads=2, head_dim=16, batch=B, max_context=ctxlen + K + 8, window=512,
+                 tau=0.5, softness=2.0, vocab=0, host_mirror=0, device=local_rank)
+    pk = torch.zeros((B, P, 1, 2, 16), dtype=torch.bfloat16, device=dev)
+    ctx = Context(cfg, pk, pk.clone(), [P] * B)
+    scores = torch.full((B, cfg.max_context), 0.25, dtype=torch.float32, device=dev)   # every token below tau
+    for _ in range(ctxlen - P):
+        ctx.step_policy(scores)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        ctx.step_policy(scores)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    st = ctx.stats(0)
+    ctx.close()
+    return {"workload": f"policy replay, all-cold trace, {B} sequences at {ctxlen} tokens, K=512",
+            "ms_per_step": ms, "sequence_steps_per_s": B / (ms / 1000.0), "active_post": st["active"],
+            "total": st["total"]}
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -521,7 +552,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_asr(a, rank, world, local_rank)
     points = {}
-    for name in [x for x in a.points.split(",") if x and x != "sample"]:
+    for name in [x for x in a.points.split(",") if x and x not in ("sample", "replay")]:
         b = argparse.Namespace(**vars(a))
         for k, v in POINTS[name].items():
             setattr(b, k, v)
@@ -536,6 +567,8 @@ def main():
                             "compression": r["detail"]["compression"]}
     if line is not None and world == 1 and "sample" in [x for x in a.points.split(",") if x]:
         line["detail"]["next_token_draw"] = sample_point(local_rank)
+    if line is not None and world == 1 and "replay" in [x for x in a.points.split(",") if x]:
+        line["detail"]["policy_replay"] = replay_point(local_rank)
     if line is not None:
         if points:
             line["points"] = points

@@ -220,6 +220,17 @@ asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
  * Synchronises. */
 asr_status asr_timeline(asr_ctx* ctx, double* us, int32_t n);
 
+/* NEXT-2: one policy-replay step — Alg. 1 lines 3-15 and the step-
+ * boundary recovery (§3.6) with the per-token scores given instead of computed: scores is a
+ * device array [batch][max_context] fp32 holding s_j of every position (only the step's attended
+ * positions are read; compared with tau as in Eq. 2's decision); logits_prev (device, optional) feeds
+ * the entropy detector as in asr_step.  No attention runs and no K/V is appended (the positions this
+ * call appends have no K/V: use a context for replay only).  Not with a slot pool.  Asynchronous;
+ * asr_stats reports the step as for asr_step.  Many (tau, K, k, W) settings can be swept at once by
+ * replaying one score trace through several contexts. */
+asr_status asr_step_policy(asr_ctx* ctx, const float* scores, const void* logits_prev, int32_t logits_dtype,
+                           float* entropy, void* cuda_stream);
+
 /* NEXT-1 (Alg. 1 "Generate next token"): one draw per row of
  * logits[batch][vocab] (device; logits_dtype ASR_KV_BF16 or ASR_KV_F32) — greedy if temperature <= 0
  * or top_k == 1; otherwise p = softmax(x / temperature), keep the top_k largest logits (top_k <= 0:

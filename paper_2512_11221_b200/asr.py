@@ -71,7 +71,7 @@ class asr_ledger_view(ctypes.Structure):
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
            "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
            "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-           "asr_time_attention", "asr_sample")
+           "asr_time_attention", "asr_sample", "asr_step_policy")
 
 _lib = None
 
@@ -103,10 +103,11 @@ def lib() -> ctypes.CDLL:
         L.asr_attach_nccl.argtypes = [vp, vp, i32, i32]
         L.asr_time_attention.argtypes = [vp, i32, vp]
         L.asr_sample.argtypes = [vp, i32, i32, i32, ctypes.c_float, i32, ctypes.c_float, vp, vp, vp]
+        L.asr_step_policy.argtypes = [vp, vp, vp, i32, vp, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
                   "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
                   "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-                  "asr_time_attention", "asr_sample"):
+                  "asr_time_attention", "asr_sample", "asr_step_policy"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -361,6 +362,16 @@ class Context:
 
     def set_profile(self, on: bool):
         asr_set_profile(self._h, on)
+
+    def step_policy(self, scores, logits_prev=None, entropy=None, stream=None):
+        """NEXT-2 policy replay step: scores [B][max_context] fp32 (CUDA tensor) instead of attention."""
+        import torch
+        lg = None if logits_prev is None else logits_prev
+        dt = 0 if lg is None or lg.dtype == torch.bfloat16 else 1
+        _check(lib().asr_step_policy(self._h, ctypes.c_void_p(scores.data_ptr()),
+                                     None if lg is None else ctypes.c_void_p(lg.data_ptr()), dt,
+                                     None if entropy is None else ctypes.c_void_p(entropy.data_ptr()),
+                                     _stream(stream)))
 
     def time_attention(self, reps: int, stream=None):
         asr_time_attention(self._h, reps, stream)

@@ -1076,6 +1076,37 @@ asr_status asr_time_attention(asr_ctx* c, int32_t reps, void* cuda_stream) {
   return ASR_OK;
 }
 
+asr_status asr_step_policy(asr_ctx* c, const float* scores, const void* logits_prev, int32_t logits_dtype,
+                           float* entropy, void* cuda_stream) {
+  if (!c) return fail(ASR_E_STATE, "context is NULL");
+  if (!scores) return fail(ASR_E_INVALID, "asr_step_policy: scores is NULL");
+  if (c->attend_pending) return fail(ASR_E_STATE, "between asr_step_attend and asr_step_decide");
+  const DevState& s = c->s;
+  if (s.pool_mode) return fail(ASR_E_STATE, "asr_step_policy: not with a slot pool (pool_tokens > 0)");
+  const bool has_logits = logits_prev != nullptr && s.vocab > 0;
+  if (has_logits && logits_dtype != ASR_KV_BF16 && logits_dtype != ASR_KV_F32)
+    return fail(ASR_E_INVALID, "logits_dtype");
+  for (int b = 0; b < s.B; ++b)
+    if (c->prompt_len[b] + c->step + 1 > c->cfg.max_context)
+      return fail(ASR_E_CAPACITY, "sequence " + std::to_string(b) + " is at max_context");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  DevState sd = s;
+  sd.ext_score = scores;
+  sd.pre_in_attn = 0;
+  sd.tl = nullptr;
+  asr::KNode na, nd;
+  asr::node_phaseA(na, sd, has_logits ? logits_prev : nullptr, logits_dtype, nullptr, nullptr,
+                   has_logits ? entropy : nullptr);
+  asr::node_phaseD(nd, sd, nullptr);
+  CUDA_TRY(na.launch(st));
+  CUDA_TRY(nd.launch(st));
+  c->launches += 2;
+  c->step++;
+  c->last_stream = st;
+  return ASR_OK;
+}
+
 asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab, float temperature,
                       int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream) {
   if (!logits || !uniforms || !token_out) return fail(ASR_E_INVALID, "asr_sample: NULL pointer");

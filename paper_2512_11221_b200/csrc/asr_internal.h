@@ -77,6 +77,7 @@ struct DevState {
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
   int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
+  const float* ext_score;     // policy replay (NEXT-2): s_j given per position [B][max_ctx]; NULL = Eq. 2
   unsigned long long* hmask;  // [B][max_ctx][2] finite W: bit t = detection at step hstep - t
   int32_t* hstep;             // [B][max_ctx]    finite W: step of bit 0 (never: a large negative)
   int combine_in_decide;      // 1: the combine runs as extra blocks of the phase-D kernel (small batch)

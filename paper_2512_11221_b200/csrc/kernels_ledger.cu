@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
   __shared__ units::UnitShm u;
   const int nd = s.decide_blocks * s.B;
   if ((int)blockIdx.x >= nd) {   // combine_in_decide: blocks after the decide blocks combine O
+    if (!o) return;                // policy replay: no attention, nothing to combine
     const int wid = ((int)blockIdx.x - nd) * (kUnitThreads / 32) + (threadIdx.x >> 5);
     if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
     if (s.tl) {

@@ -629,9 +629,14 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   const int pf_row = (i & 1) * s.B + b;   // prefetch list written by this step
   for (int a = a0 + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS()) {
     const int j = act_pos[a];
-    const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
-    float sj = sum / heads;             // mean over the L*Hq (layer, head) pairs (correctly rounded)
-    if (s.score_scaled) sj = sj / sqrt_d;
+    float sj;
+    if (s.ext_score) {
+      sj = s.ext_score[(long)b * s.cap + j];   // policy replay: the caller's s_j, rows of max_context
+    } else {
+      const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
+      sj = sum / heads;                 // mean over the L*Hq (layer, head) pairs (correctly rounded)
+      if (s.score_scaled) sj = sj / sqrt_d;
+    }
     s.score[base + a] = sj;
     if (j < n - s.window && j >= s.pinned && sj < s.tau) {
       uint32_t c;                       // line 4: c_j <- c_j + 1 (lifetime, or within the window W)
@@ -918,7 +923,7 @@ __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* lo
     const int w = (int)ASR_UNIT_TID() >> 5, nw = (int)ASR_UNIT_THREADS() >> 5;
     for (int sp = k * s.ent_per_unit + w; sp < (k + 1) * s.ent_per_unit; sp += nw)   // one split per warp
       warp_entropy_split<TL>(s, logits, b, sp, (int)ASR_UNIT_TID() & 31);
-  } else {
+  } else if (k_new) {   // (policy replay appends no K/V)
     const int a = unit - ne;
     const int b = a / au, k = a % au;
     for (int l = k * s.layers_per_unit; l < min(s.L, (k + 1) * s.layers_per_unit); ++l) unit_append<TK>(s, b, l, i, k_new, v_new);
