@@ -7,8 +7,8 @@
 //   (logit desc, index asc) order holding >= P of their probability mass;
 //   draw: the smallest index j in the kept set with  sum_{i kept, i <= j} p_i  >  u * sum_{kept} p_i.
 //
-// One thread-block cluster of CS CTAs per row (8 for small batches, 4, or 1 for large ones); CTA r
-// owns the contiguous slice r of the row.  Every
+// One thread-block cluster of CS CTAs per row (8 for small batches, else 4); CTA r owns the contiguous
+// slice r of the row and, when it fits, keeps it in shared memory for all passes.  Every
 // quantity the decisions need (max, counts and masses above the split points of the boundary search,
 // tie counts, kept masses) is reduced within each CTA and exchanged through distributed shared memory
 // (DSMEM) after a cluster barrier; every CTA then takes the same decision in the same fixed order.
@@ -92,7 +92,7 @@ __device__ __forceinline__ void visit8(const TL* __restrict__ x, int s0, int s1,
       const int b = b0 + u * kST * 8;
       const uint4* src = reinterpret_cast<const uint4*>(x + (b + 8 <= s1 ? b : s0));
 #pragma unroll
-      for (int w = 0; w < kW; ++w) r[u][w] = __ldg(src + w);
+      for (int w = 0; w < kW; ++w) r[u][w] = src[w];   // global or the shared-memory copy of the slice
     }
 #pragma unroll
     for (int u = 0; u < kR; ++u) {
@@ -158,21 +158,39 @@ __device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned
 template <typename TL, int CS>
 __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logits, int V, float temperature, int top_k,
                                                      float top_p, const float* __restrict__ uniforms,
-                                                     int32_t* __restrict__ token_out) {
+                                                     int32_t* __restrict__ token_out, int cache) {
   __shared__ SampleShm sh;
+  extern __shared__ __align__(16) uint8_t slice_smem[];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int row = blockIdx.y;
-  const TL* x = logits + (long)row * V;
+  const TL* xg = logits + (long)row * V;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int S = ((V + CS - 1) / CS + 31) & ~31;   // slice of this CTA: [s0, s1)
   int par = 0;                                     // cluster_sum slot parity
   const int s0 = min(V, rank * S), s1 = min(V, s0 + S);
+  const bool galigned = (reinterpret_cast<uintptr_t>(xg) & 15) == 0;   // s0 is a multiple of 32
+  // the slice is read by every pass: with `cache`, once from global into shared memory
+  const TL* x = xg;
+  if (cache) {
+    TL* c = reinterpret_cast<TL*>(slice_smem);
+    if (galigned) {
+      const int n16 = (s1 - s0) * (int)sizeof(TL) / 16;
+      const uint4* src = reinterpret_cast<const uint4*>(xg + s0);
+      uint4* dst = reinterpret_cast<uint4*>(c);
+      for (int k = tid; k < n16; k += kST) dst[k] = __ldg(src + k);
+      for (int j = s0 + n16 * 16 / (int)sizeof(TL) + tid; j < s1; j += kST) c[j - s0] = xg[j];
+    } else {
+      for (int j = s0 + tid; j < s1; j += kST) c[j - s0] = xg[j];
+    }
+    __syncthreads();
+    x = c - s0;   // x[j] for j in [s0, s1) now reads shared memory
+  }
+  const bool aligned = cache || galigned;
 
   // ---- max and its first index (greedy)
   float mx = -INFINITY;
   int mi = 0x7fffffff;
-  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;   // s0 is a multiple of 32
   visit8(x, s0, s1, aligned, [&](float v, int j) {
     if (v > mx) { mx = v; mi = j; }
   });
@@ -388,10 +406,13 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
 template <int CS>
 cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
                       float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
+  const size_t esz = logits_dtype == 1 ? 4 : 2;
+  const size_t slice = (size_t)(((vocab + CS - 1) / CS + 31) & ~31) * esz;
+  int cache = slice <= 96 * 1024 ? 1 : 0;   // the slice in shared memory (two CTAs per SM still fit)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS, batch);
   cfg.blockDim = dim3(kST);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = cache ? (unsigned)slice : 0u;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -400,22 +421,26 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (logits_dtype == 1)
+  if (logits_dtype == 1) {
+    cudaError_t e = cudaFuncSetAttribute(sample_kernel<float, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, sample_kernel<float, CS>, (const float*)logits, vocab, temperature, top_k, top_p,
-                              uniforms, token_out);
+                              uniforms, token_out, cache);
+  }
+  cudaError_t e = cudaFuncSetAttribute(sample_kernel<__nv_bfloat16, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       96 * 1024);
+  if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, sample_kernel<__nv_bfloat16, CS>, (const __nv_bfloat16*)logits, vocab, temperature,
-                            top_k, top_p, uniforms, token_out);
+                            top_k, top_p, uniforms, token_out, cache);
 }
 
 }  // namespace
 
-// Small batches spread each row over a cluster of 8 CTAs; large ones use one CTA per row (the rows
-// alone fill the GPU).
+// A cluster of 8 CTAs per row for small batches (and fp32 logits), 4 otherwise; each CTA keeps its
+// slice of the row in shared memory when it fits (all passes then read shared memory).
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
                           float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
-  if (batch >= 32)
-    return launch_cs<1>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
-  if (batch >= 8)
+  if (batch >= 8 && logits_dtype != 1)
     return launch_cs<4>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
   return launch_cs<8>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
 }
