@@ -294,9 +294,11 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.max_splits = (int)(want < 1 ? 1 : want > cap ? cap : want);
     if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
     {
-      // decide blocks per sequence: ~2K positions each; X > 1 only if all B*X blocks are co-resident
+      // decide blocks per sequence: ~1K positions each (measured best at 8K); X > 1 only if all B*X blocks are co-resident
       // (one per SM), since a block waits for its predecessors' counts to place its part of A_{i+1}
-      int db = (s.max_ctx + 2047) / 2048;
+      const char* dbe = getenv("ASR_DECIDE_POSITIONS");   // positions per decide block (tuning)
+      const int per_block = dbe ? atoi(dbe) : 1024;
+      int db = (s.max_ctx + per_block - 1) / (per_block > 0 ? per_block : 2048);
       db = db < 1 ? 1 : db > 32 ? 32 : db;
       if ((long)s.B * db > c->num_sms) db = 1;
       s.decide_blocks = db;
