@@ -57,6 +57,7 @@ class Case:
     nccl_world1: bool = False      # attach a one-rank NCCL communicator (attend -> all-reduce -> decide)
     logits_dtype: str = "bf16"     # "f32": the same (bf16-exact) logits passed as fp32
     history_window: int = 0        # W (NEXT-3): 0 = lifetime counts
+    time_attention_at: tuple = ()  # steps before which asr_time_attention runs (must leave no trace)
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -125,6 +126,8 @@ def run(c: Case, check_o: bool = True) -> dict:
     evicted_total = prefetched_total = demand_total = 0
     recoveries = 0
     for i in range(c.steps):
+        if i in c.time_attention_at:
+            ctx.time_attention(2)
         if i in c.restore_at:
             seq, level = c.restore_at[i]
             ctx.restore(seq, level)

@@ -150,3 +150,12 @@ def test_finite_history_window(W):
     assert s["frozen"] > 0
     run(Case(L=2, Hq=32, Hkv=8, d=128, B=1, prompt=(60,), steps=90, window=8, hot_permille=300, a_hot=64,
              vocab=4096, seed=400 + W, history_window=W))
+
+
+def test_time_attention_leaves_no_trace():
+    # bench.py times the attention kernel alone between steps (asr_time_attention); the steps after it
+    # must stay bitwise on the oracle (batch 1: phase A/B inside the attention kernel; batch 3: not)
+    run(Case(L=2, Hq=32, Hkv=8, d=128, B=1, prompt=(70,), steps=30, window=8, hot_permille=300, a_hot=64,
+             vocab=4096, seed=501, time_attention_at=(5, 6, 17)))
+    run(Case(L=2, Hq=32, Hkv=8, d=128, B=3, prompt=(70, 20, 45), steps=30, window=8, hot_permille=300,
+             a_hot=64, vocab=4096, seed=502, time_attention_at=(5, 17)))
