@@ -125,7 +125,10 @@ typedef struct {
   int32_t recovery_action;    /* 0 none, 1 SR, 2 WR, 3 FR, 4 RR */
   int32_t rewalk_requested;   /* RR: the caller should regenerate (needs the model; out of scope) */
   int64_t bytes_h2d, bytes_d2h; /* host-link bytes moved by the library for this context so far */
-  uint32_t device_error;      /* latched invariant flags (0 = none) */
+  uint32_t device_error;      /* latched invariant flags (0 = none): 1 a frozen token inside the
+                               * protected window, 2 an empty active set, 8 pressure mode found no free
+                               * device slot, 16 an active token without a device slot, 32 a wait inside
+                               * the batch-1 attention kernel timed out */
   int64_t resident;           /* tokens of this sequence holding a device slot (pressure mode; else total) */
   int64_t evicted_this_step;  /* device slots released by this step's freezes (pressure mode) */
   int64_t prefetched_this_step; /* tokens copied host -> device ahead of their timer expiry */

@@ -371,11 +371,9 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.part_ml, max_items * s.Hq * 2 * 4));
     CUDA_TRY(c->alloc(&s.part_acc, max_items * s.Hq * s.d * 4));
     CUDA_TRY(c->alloc(&s.ent_part, (size_t)s.B * asr::kEntSplits * 3 * 4));
-    CUDA_TRY(c->alloc(&s.ent_ticket, (size_t)s.B * 4));
-    CUDA_TRY(c->alloc(&s.hist, (size_t)s.B * s.det_baseline * 8));
+      CUDA_TRY(c->alloc(&s.hist, (size_t)s.B * s.det_baseline * 8));
     CUDA_TRY(c->alloc(&s.det, (size_t)s.B * sizeof(asr::DetState)));
-    CUDA_TRY(c->alloc(&s.rec_action, (size_t)s.B * 4));
-    CUDA_TRY(c->alloc(&s.stats, (size_t)s.B * sizeof(asr::SeqStats)));
+      CUDA_TRY(c->alloc(&s.stats, (size_t)s.B * sizeof(asr::SeqStats)));
     CUDA_TRY(c->alloc(&s.err, 4));
     CUDA_TRY(c->alloc(&s.ticket, 4));
     CUDA_TRY(c->alloc(&s.pre_ticket, (size_t)s.B * 4));
@@ -385,10 +383,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(cudaMemsetAsync(s.count, 0, BT * 4, st));
     CUDA_TRY(cudaMemsetAsync(s.fstep, 0xff, BT * 4, st));
     CUDA_TRY(cudaMemsetAsync(s.step, 0, 4, st));
-    CUDA_TRY(cudaMemsetAsync(s.ent_ticket, 0, (size_t)s.B * 4, st));
-    CUDA_TRY(cudaMemsetAsync(s.det, 0, (size_t)s.B * sizeof(asr::DetState), st));
-    CUDA_TRY(cudaMemsetAsync(s.rec_action, 0, (size_t)s.B * 4, st));
-    CUDA_TRY(cudaMemsetAsync(s.stats, 0, (size_t)s.B * sizeof(asr::SeqStats), st));
+      CUDA_TRY(cudaMemsetAsync(s.det, 0, (size_t)s.B * sizeof(asr::DetState), st));
+      CUDA_TRY(cudaMemsetAsync(s.stats, 0, (size_t)s.B * sizeof(asr::SeqStats), st));
     CUDA_TRY(cudaMemsetAsync(s.err, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.ticket, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(s.pre_ticket, 0, (size_t)s.B * 4, st));

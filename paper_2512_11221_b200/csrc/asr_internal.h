@@ -15,8 +15,6 @@ constexpr int kStages = 3;          // pre (entropy+append+recovery), attention,
 // block past griddepcontrol.wait)
 constexpr int kTimelineSlots = 2 * kStages + 9;
 constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
-constexpr int kLedgerThreads = 1024;
-constexpr int kDecideThreads = 512;
 
 // Residency byte: 1 = Active; 0 = Frozen; 2 / 3 = Frozen during a step of even / odd index (tag used
 // by the multi-block decide kernel to tell this step's freezes from older ones without ordering).
@@ -54,7 +52,6 @@ struct DetState {
 enum : uint32_t {
   kErrFrozenInWindow = 1u,   // a frozen token inside the protected window
   kErrEmptyActive = 2u,      // |A_i| == 0 (the current token is always active)
-  kErrTimer = 4u,            // Active token with timer != 0 or Frozen with timer < 1
   kErrPoolEmpty = 8u,        // pressure mode: no free device slot (pool_tokens too small)
   kErrNotResident = 16u,     // pressure mode: an Active token without a device slot
   kErrStall = 32u,           // a wait inside the attention kernel timed out (phase B never finished)
@@ -121,10 +118,8 @@ struct DevState {
   float* part_ml;             // [max_items][Hq][2] (m in log2 domain, l)
   float* part_acc;            // [max_items][Hq][d]
   float* ent_part;            // [B][kEntSplits][3]
-  int32_t* ent_ticket;        // [B]
   double* hist;               // [B][det_baseline]
   DetState* det;              // [B]
-  int32_t* rec_action;        // [B]
   SeqStats* stats;            // [B]
   uint32_t* err;              // [1]
   int32_t* ticket;            // [1]

@@ -540,7 +540,6 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
     st.rewalk_requested = level == 4;
     st.entropy_valid = has_logits ? 1 : 0;
     st.attended = s.act_len[(i & 1) * s.B + b];
-    s.rec_action[b] = level;
   }
 }
 
