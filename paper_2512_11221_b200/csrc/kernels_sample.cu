@@ -7,8 +7,10 @@
 //   (logit desc, index asc) order holding >= P of their probability mass;
 //   draw: the smallest index j in the kept set with  sum_{i kept, i <= j} p_i  >  u * sum_{kept} p_i.
 //
-// One thread-block cluster of CS CTAs per row (8 for small batches, else 4); CTA r owns the contiguous
-// slice r of the row and, when it fits, keeps it in shared memory for all passes.  Every
+// One thread-block cluster of CS CTAs per row (16 for batches up to 4, 8 up to 7, else 4); CTA r owns
+// the contiguous slice r of the row and, when it fits, keeps it in shared memory for all passes.  After
+// a top-k boundary is found, each CTA compacts its elements at or above it (index order) into shared
+// memory and every later pass reads only those.  Every
 // quantity the decisions need (max, counts and masses above the split points of the boundary search,
 // tie counts, kept masses) is reduced within each CTA and exchanged through distributed shared memory
 // (DSMEM) after a cluster barrier; every CTA then takes the same decision in the same fixed order.
@@ -31,6 +33,7 @@ constexpr int kST = 512;             // threads per CTA
 constexpr int kSW = kST / 32;        // warps per CTA
 constexpr int kWays = 8;             // split points per search pass: kWays - 1
 constexpr float kFix = 68719476736.0f;   // 2^36
+constexpr int kCand = 1024;          // top-k candidates kept per CTA in shared memory (value + index)
 
 __device__ __forceinline__ float lg(const __nv_bfloat16* p, int j) { return __bfloat162float(p[j]); }
 __device__ __forceinline__ float lg(const float* p, int j) { return p[j]; }
@@ -119,6 +122,39 @@ __device__ __forceinline__ void visit8(const TL* __restrict__ x, int s0, int s1,
   }
 }
 
+// What a pass reads: this CTA's slice of the row, or its compacted top-k candidates.  each(f) runs
+// f(value, position) on every element (split among the CTA's threads); each_strided visits positions
+// first, first + stride, ... < end; val / idx read one element and its vocabulary index.
+template <typename TL>
+struct SliceSrc {
+  const TL* x;   // the row (global memory or the shared-memory copy, indexed by vocabulary index)
+  int s0, n;
+  bool aligned;
+  template <typename Fn>
+  __device__ __forceinline__ void each(Fn&& f) const { visit8(x, s0, s0 + n, aligned, f); }
+  template <typename Fn>
+  __device__ __forceinline__ void each_strided(int first, int end, int stride, Fn&& f) const {
+    visit(x, s0 + first, s0 + end, stride, f);
+  }
+  __device__ __forceinline__ float val(int p) const { return lg(x, s0 + p); }
+  __device__ __forceinline__ int idx(int p) const { return s0 + p; }
+};
+struct CandSrc {
+  const float* v;   // shared memory, index order
+  const int* ix;
+  int n;
+  template <typename Fn>
+  __device__ __forceinline__ void each(Fn&& f) const {
+    for (int p = threadIdx.x; p < n; p += kST) f(v[p], p);
+  }
+  template <typename Fn>
+  __device__ __forceinline__ void each_strided(int first, int end, int stride, Fn&& f) const {
+    for (int p = first; p < end; p += stride) f(v[p], p);
+  }
+  __device__ __forceinline__ float val(int p) const { return v[p]; }
+  __device__ __forceinline__ int idx(int p) const { return ix[p]; }
+};
+
 template <typename F>
 __device__ __forceinline__ F warp_sum(F v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -133,10 +169,12 @@ template <int CS>
 __device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned long long* v, int n,
                             unsigned long long* res, int& par) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int k = 0; k < n; ++k) {
-    const unsigned long long s = warp_sum(v[k]);
-    if (lane == 0) sh.wq[w][k] = s;
-  }
+#pragma unroll
+  for (int k = 0; k < 2 * kWays; ++k)
+    if (k < n) {
+      const unsigned long long s = warp_sum(v[k]);
+      if (lane == 0) sh.wq[w][k] = s;
+    }
   __syncthreads();
   if ((int)threadIdx.x < n) {
     unsigned long long t = 0;
@@ -144,11 +182,19 @@ __device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned
     sh.out[par][threadIdx.x] = t;
   }
   cl.sync();
-  if (w == 0)
-    for (int k = 0; k < n; ++k) {
-      const unsigned long long t = warp_sum(lane < CS ? cl.map_shared_rank(&sh, lane)->out[par][k] : 0ull);
-      if (lane == 0) sh.res[k] = t;
-    }
+  if (w == 0) {
+    // all n remote loads in flight before the first is used (one DSMEM round trip, not n)
+    unsigned long long r[2 * kWays];
+    const SampleShm* o = cl.map_shared_rank(&sh, lane < CS ? lane : 0);
+#pragma unroll
+    for (int k = 0; k < 2 * kWays; ++k) r[k] = (k < n && lane < CS) ? o->out[par][k] : 0ull;
+#pragma unroll
+    for (int k = 0; k < 2 * kWays; ++k)
+      if (k < n) {
+        const unsigned long long t = warp_sum(r[k]);
+        if (lane == 0) sh.res[k] = t;
+      }
+  }
   __syncthreads();
   for (int k = 0; k < n; ++k) res[k] = sh.res[k];
   par ^= 1;
@@ -231,10 +277,11 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
   uint32_t fk = 0;
   unsigned long long n_tie = ~0ull;
   const int kshift = sizeof(TL) == 2 ? 16 : 0;
-  // largest key t with Q(key >= t) >= target, Q = count (by_mass false) or fixed-point mass; an 8-ary
-  // search (the key ranges stay powers of two); returns Q(key > t)
-  auto search = [&](bool by_mass, unsigned long long target) -> unsigned long long {
-    unsigned long long lo = 0, hi = 1ull << (32 - kshift);   // Q(>= lo) >= target > Q(>= hi)
+  // largest key t in [lo, hi) with Q(key >= t) >= target, Q = count (by_mass false) or fixed-point mass
+  // over the elements `src` holds; needs Q(>= lo) >= target > Q(>= hi); an 8-ary search (the key ranges
+  // stay powers of two); returns Q(key > t)
+  auto search = [&](const auto& src, bool by_mass, unsigned long long target, unsigned long long lo,
+                    unsigned long long hi) -> unsigned long long {
     unsigned long long q_hi = 0;
     while (hi - lo > 1) {
       const unsigned long long step = (hi - lo + kWays - 1) / kWays;
@@ -249,7 +296,7 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
       uint32_t qc[kWays];
 #pragma unroll
       for (int k = 0; k < kWays - 1; ++k) { q[k] = 0; qc[k] = 0; }
-      visit8(x, s0, s1, aligned, [&](float v, int) {
+      src.each([&](float v, int) {
         const uint32_t kk = fkey(v) >> kshift;
         if (kk < tk[0]) return;
         if (by_mass) {
@@ -282,122 +329,166 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
     fk = (uint32_t)(lo << kshift);
     return q_hi;
   };
-  // the mass of the tokens with key > fk (one pass)
-  auto mass_above = [&]() -> unsigned long long {
-    unsigned long long v = 0, tot;
-    visit8(x, s0, s1, aligned, [&](float x1, int) {
-      if (fkey(x1) > fk) v += wfix(x1, m, invT);
-    });
-    cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
-    return tot;
-  };
-  unsigned long long kept_mass = 0;
-  if (use_k) {
-    const unsigned long long ca = search(false, (unsigned long long)top_k);
-    n_tie = (unsigned long long)top_k - ca;
-    kept_mass = mass_above() + n_tie * wfix(unkey(fk), m, invT);
-  } else {
-    unsigned long long v = 0, tot;
-    visit8(x, s0, s1, aligned, [&](float x1, int) { v += wfix(x1, m, invT); });
-    cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
-    kept_mass = tot;
-  }
-  if (use_p) {
-    // the boundary key of the shortest mass prefix: mass(key > pk) < target <= mass(key >= pk); it
-    // lies at or above the top-k boundary, and the tokens at pk it needs are the fewest whose equal
-    // masses reach the target
-    const unsigned long long target = (unsigned long long)ceil((double)top_p * (double)kept_mass);
-    const uint32_t fk_k = fk;
-    const unsigned long long n_tie_k = n_tie;
-    const unsigned long long ma = search(true, target);
-    const unsigned long long wb = wfix(unkey(fk), m, invT);
-    const unsigned long long need = wb ? (target - ma + wb - 1) / wb : 1;
-    n_tie = (use_k && fk == fk_k && n_tie_k < need) ? n_tie_k : need;
-  }
+  const unsigned long long key_hi = (unsigned long long)(fkey(m) >> kshift) + 1;   // Q(>= key_hi) = 0
 
-  // ---- the draw: ties (key == fk) are ranked in index order; warp q of CTA r owns the contiguous
-  //      chunk q of slice r, read in coalesced groups of 32 lanes
-  const int per = ((s1 - s0 + kSW - 1) / kSW + 31) & ~31;
-  const int c0 = min(s1, s0 + w * per), c1 = min(s1, c0 + per);
-  unsigned long long tw = 0;
-  visit(x, c0 + lane, c1, 32, [&](float x1, int) { tw += fkey(x1) == fk; });
-  tw = warp_sum(tw);
-  if (lane == 0) sh.wq[w][0] = tw;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long t = 0;
-    for (int q = 0; q < kSW; ++q) t += sh.wq[q][0];
-    sh.out[par][0] = t;
-  }
-  cl.sync();
-  unsigned long long tie_base = 0;   // ties before this warp's chunk
-  for (int r = 0; r < rank; ++r) tie_base += cl.map_shared_rank(&sh, r)->out[par][0];
-  for (int q = 0; q < w; ++q) tie_base += sh.wq[q][0];
-  par ^= 1;
-  __syncthreads();   // wq[.][0] read by every warp before it is reused
-  auto group = [&](int j, float v, unsigned long long& rk) -> unsigned long long {   // this lane's kept mass
-    const bool in = j < c1;
-    const uint32_t key = in ? fkey(v) : 0u;
-    const bool tie = in && key == fk;
-    const unsigned tm = __ballot_sync(0xffffffffu, tie);
-    const unsigned long long my = rk + __popc(tm & ((1u << lane) - 1u));
-    rk += __popc(tm);
-    return (in && (key > fk || (tie && my < n_tie))) ? wfix(v, m, invT) : 0ull;
-  };
-  // groups of 32 (one element per lane), kU groups' loads in flight per lane
-  auto load_groups = [&](int g0, float* v) {
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int j = g0 + u * 32 + lane;
-      v[u] = lg(x, j < c1 ? j : c0);
+  // the top-p boundary (if any), then the draw, over the elements `src` holds (all of this CTA's
+  // elements with key >= fk, in index order)
+  auto finish = [&](const auto& src, unsigned long long kept_mass) {
+    if (use_p) {
+      // the boundary key of the shortest mass prefix: mass(key > pk) < target <= mass(key >= pk); it
+      // lies at or above the top-k boundary (mass(key >= fk) >= kept_mass >= target), and the tokens
+      // at pk it needs are the fewest whose equal masses reach the target
+      const unsigned long long target = (unsigned long long)ceil((double)top_p * (double)kept_mass);
+      const uint32_t fk_k = fk;
+      const unsigned long long n_tie_k = n_tie;
+      const unsigned long long ma = search(src, true, target, fk >> kshift, use_k ? key_hi : (1ull << (32 - kshift)));
+      const unsigned long long wb = wfix(unkey(fk), m, invT);
+      const unsigned long long need = wb ? (target - ma + wb - 1) / wb : 1;
+      n_tie = (use_k && fk == fk_k && n_tie_k < need) ? n_tie_k : need;
     }
-  };
-  unsigned long long wk = 0, rk = tie_base;
-  for (int g0 = c0; g0 < c1; g0 += kU * 32) {
-    float v[kU];
-    load_groups(g0, v);
+
+    // ---- the draw: ties (key == fk) are ranked in index order; warp q owns the contiguous chunk q of
+    //      this CTA's elements, read in coalesced groups of 32 lanes
+    const int per = ((src.n + kSW - 1) / kSW + 31) & ~31;
+    const int c0 = min(src.n, w * per), c1 = min(src.n, c0 + per);
+    unsigned long long tw = 0;
+    src.each_strided(c0 + lane, c1, 32, [&](float x1, int) { tw += fkey(x1) == fk; });
+    tw = warp_sum(tw);
+    if (lane == 0) sh.wq[w][0] = tw;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int q = 0; q < kSW; ++q) t += sh.wq[q][0];
+      sh.out[par][0] = t;
+    }
+    cl.sync();
+    unsigned long long tie_base = 0;   // ties before this warp's chunk
+    for (int r = 0; r < rank; ++r) tie_base += cl.map_shared_rank(&sh, r)->out[par][0];
+    for (int q = 0; q < w; ++q) tie_base += sh.wq[q][0];
+    par ^= 1;
+    __syncthreads();   // wq[.][0] read by every warp before it is reused
+    auto group = [&](int p, float v, unsigned long long& rk) -> unsigned long long {   // this lane's kept mass
+      const bool in = p < c1;
+      const uint32_t key = in ? fkey(v) : 0u;
+      const bool tie = in && key == fk;
+      const unsigned tm = __ballot_sync(0xffffffffu, tie);
+      const unsigned long long my = rk + __popc(tm & ((1u << lane) - 1u));
+      rk += __popc(tm);
+      return (in && (key > fk || (tie && my < n_tie))) ? wfix(v, m, invT) : 0ull;
+    };
+    // groups of 32 (one element per lane), kU groups' loads in flight per lane
+    auto load_groups = [&](int g0, float* v) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) wk += group(g0 + u * 32 + lane, v[u], rk);
-  }
-  wk = warp_sum(wk);
-  if (lane == 0) sh.wq[w][1] = wk;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long t = 0;
-    for (int q = 0; q < kSW; ++q) t += sh.wq[q][1];
-    sh.out[par][1] = t;
-  }
-  cl.sync();
-  unsigned long long before = 0, total = 0;
-  for (int r = 0; r < CS; ++r) {
-    const unsigned long long t = cl.map_shared_rank(&sh, r)->out[par][1];
-    if (r < rank) before += t;
-    total += t;
-  }
-  for (int q = 0; q < w; ++q) before += sh.wq[q][1];
-  const unsigned long long target = (unsigned long long)((double)uniforms[row] * (double)total);
-  if (wk > 0 && before <= target && target < before + wk) {   // warp-uniform: the warp holding the draw
-    unsigned long long acc = before, r2 = tie_base;
-    bool found = false;
-    for (int g0 = c0; g0 < c1 && !found; g0 += kU * 32) {
+      for (int u = 0; u < kU; ++u) {
+        const int p = g0 + u * 32 + lane;
+        v[u] = src.val(p < c1 ? p : c0);
+      }
+    };
+    unsigned long long wk = 0, rk = tie_base;
+    for (int g0 = c0; g0 < c1; g0 += kU * 32) {
       float v[kU];
       load_groups(g0, v);
-      for (int u = 0; u < kU; ++u) {
-        const int gj = g0 + u * 32;
-        const unsigned long long wv = group(gj + lane, v[u], r2);
-        unsigned long long incl = wv;   // inclusive scan over the group (lane order = index order)
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) wk += group(g0 + u * 32 + lane, v[u], rk);
+    }
+    wk = warp_sum(wk);
+    if (lane == 0) sh.wq[w][1] = wk;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int q = 0; q < kSW; ++q) t += sh.wq[q][1];
+      sh.out[par][1] = t;
+    }
+    cl.sync();
+    unsigned long long before = 0, total = 0;
+    for (int r = 0; r < CS; ++r) {
+      const unsigned long long t = cl.map_shared_rank(&sh, r)->out[par][1];
+      if (r < rank) before += t;
+      total += t;
+    }
+    for (int q = 0; q < w; ++q) before += sh.wq[q][1];
+    const unsigned long long target = (unsigned long long)((double)uniforms[row] * (double)total);
+    if (wk > 0 && before <= target && target < before + wk) {   // warp-uniform: the warp holding the draw
+      unsigned long long acc = before, r2 = tie_base;
+      bool found = false;
+      for (int g0 = c0; g0 < c1 && !found; g0 += kU * 32) {
+        float v[kU];
+        load_groups(g0, v);
+        for (int u = 0; u < kU; ++u) {
+          const int gp = g0 + u * 32;
+          const unsigned long long wv = group(gp + lane, v[u], r2);
+          unsigned long long incl = wv;   // inclusive scan over the group (lane order = index order)
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, wv > 0 && acc + incl > target);
+          if (hit) {
+            if (lane == __ffs(hit) - 1) token_out[row] = src.idx(gp + lane);
+            found = true;
+            break;
+          }
+          acc += __shfl_sync(0xffffffffu, incl, 31);
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, wv > 0 && acc + incl > target);
-        if (hit) {
-          if (lane == __ffs(hit) - 1) token_out[row] = gj + lane;
-          found = true;
-          break;
-        }
-        acc += __shfl_sync(0xffffffffu, incl, 31);
       }
+    }
+  };
+
+  const SliceSrc<TL> slice{x, s0, s1 - s0, aligned};
+  if (!use_k) {
+    unsigned long long v = 0, tot;
+    slice.each([&](float x1, int) { v += wfix(x1, m, invT); });
+    cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
+    finish(slice, tot);
+  } else {
+    const unsigned long long ca = search(slice, false, (unsigned long long)top_k, 0, key_hi);
+    n_tie = (unsigned long long)top_k - ca;
+    // ---- compaction: this CTA's elements with key >= fk (top_k plus any further ties, so few) in
+    //      index order into shared memory, when they fit; every later pass then reads only them.  The
+    //      choice is per CTA: every later quantity is a sum over the elements with key >= fk.
+    const int per = ((s1 - s0 + kSW - 1) / kSW + 31) & ~31;
+    const int c0 = s0 + min(s1 - s0, w * per), c1 = min(s1, c0 + per);
+    const int cend = c0 + ((c1 - c0 + 31) & ~31);   // whole groups of 32: every lane reaches the ballots
+    unsigned cnt = 0;
+    for (int j = c0 + lane; j < cend; j += 32) {
+      const bool in = j < c1 && fkey(lg(x, j < c1 ? j : c0)) >= fk;
+      cnt += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    if (lane == 0) sh.wq[w][2] = cnt;
+    __syncthreads();
+    unsigned long long base = 0, ncand = 0;
+    for (int q = 0; q < kSW; ++q) {
+      if (q < w) base += sh.wq[q][2];
+      ncand += sh.wq[q][2];
+    }
+    float* cv = reinterpret_cast<float*>(slice_smem + (cache ? (S * (int)sizeof(TL) + 15) / 16 * 16 : 0));
+    int* ci = reinterpret_cast<int*>(cv + kCand);
+    const bool compact = ncand <= (unsigned long long)kCand;   // CTA-uniform
+    if (compact) {
+      for (int j = c0 + lane; j < cend; j += 32) {
+        const float v = lg(x, j < c1 ? j : c0);
+        const bool in = j < c1 && fkey(v) >= fk;
+        const unsigned msk = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int p = (int)base + __popc(msk & ((1u << lane) - 1u));
+          cv[p] = v;
+          ci[p] = j;
+        }
+        base += __popc(msk);
+      }
+    }
+    __syncthreads();
+    if (compact) {
+      const CandSrc cand{cv, ci, (int)ncand};
+      unsigned long long v = 0, tot;
+      cand.each([&](float x1, int) { if (fkey(x1) > fk) v += wfix(x1, m, invT); });
+      cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
+      finish(cand, tot + n_tie * wfix(unkey(fk), m, invT));
+    } else {
+      unsigned long long v = 0, tot;
+      slice.each([&](float x1, int) { if (fkey(x1) > fk) v += wfix(x1, m, invT); });
+      cluster_sum<CS>(cl, sh, &v, 1, &tot, par);
+      finish(slice, tot + n_tie * wfix(unkey(fk), m, invT));
     }
   }
   cl.sync();   // no CTA leaves while another may still read its shared memory
@@ -409,11 +500,19 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
   const size_t esz = logits_dtype == 1 ? 4 : 2;
   const size_t slice = (size_t)(((vocab + CS - 1) / CS + 31) & ~31) * esz;
   int cache = slice <= 96 * 1024 ? 1 : 0;   // the slice in shared memory (two CTAs per SM still fit)
+  const size_t smem = (cache ? (slice + 15) / 16 * 16 : 0) + (size_t)kCand * 8;   // + the top-k candidates
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS, batch);
   cfg.blockDim = dim3(kST);
-  cfg.dynamicSmemBytes = cache ? (unsigned)slice : 0u;
+  cfg.dynamicSmemBytes = (unsigned)smem;
   cfg.stream = st;
+  if (CS > 8) {   // non-portable cluster size
+    cudaError_t e = logits_dtype == 1
+                        ? cudaFuncSetAttribute(sample_kernel<float, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)
+                        : cudaFuncSetAttribute(sample_kernel<__nv_bfloat16, CS>,
+                                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
@@ -422,13 +521,13 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (logits_dtype == 1) {
-    cudaError_t e = cudaFuncSetAttribute(sample_kernel<float, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(sample_kernel<float, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024 + kCand * 8);
     if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, sample_kernel<float, CS>, (const float*)logits, vocab, temperature, top_k, top_p,
                               uniforms, token_out, cache);
   }
   cudaError_t e = cudaFuncSetAttribute(sample_kernel<__nv_bfloat16, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       96 * 1024);
+                                       96 * 1024 + kCand * 8);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, sample_kernel<__nv_bfloat16, CS>, (const __nv_bfloat16*)logits, vocab, temperature,
                             top_k, top_p, uniforms, token_out, cache);
@@ -436,10 +535,14 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
 
 }  // namespace
 
-// A cluster of 8 CTAs per row for small batches (and fp32 logits), 4 otherwise; each CTA keeps its
-// slice of the row in shared memory when it fits (all passes then read shared memory).
+// A cluster of 16 CTAs per row for batches up to 4 (not greedy), 8 up to 7 (and for fp32 logits), 4
+// otherwise; each CTA keeps its slice of the row in shared memory when it fits (all passes then read
+// shared memory).
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
                           float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
+  const bool greedy = !(temperature > 0.f) || top_k == 1;   // one pass: the larger cluster's launch costs more
+  if (batch <= 4 && !greedy)   // few rows: 16-CTA clusters (non-portable size; one per GPC) halve every pass
+    return launch_cs<16>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
   if (batch >= 8 && logits_dtype != 1)
     return launch_cs<4>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
   return launch_cs<8>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);

@@ -50,7 +50,10 @@ def test_sample_matches_oracle(kind, V, dtype):
         torch.from_numpy(X).cuda()
     rng = np.random.default_rng(V)
     settings = [(0.0, 0, 1.0), (1.0, 1, 1.0), (1.0, 0, 1.0), (0.7, 50, 1.0), (1.0, 0, None), (0.8, 100, None),
-                (1.3, 7, None)]
+                (1.3, 7, None),
+                # large k: the kept candidates overflow a CTA's shared-memory list (kCand) on some or all
+                # CTAs, which then keep reading their slice
+                (0.9, 2000, 1.0), (1.0, 20000, None)]
     for T, k, P in settings:
         Ps = [(_p_between(X[b], T, k) if P is None else P) for b in range(B)]
         # exact draws: u in the middle of a kept token's interval
