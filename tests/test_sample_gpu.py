@@ -100,3 +100,34 @@ def test_sample_deterministic():
     asr_sample(xt, u, a, temperature=0.9, top_k=200, top_p=0.9)
     asr_sample(xt, u, b, temperature=0.9, top_k=200, top_p=0.9)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("B", [3, 16])
+def test_sample_batched_rows(B):
+    """Several rows per call: 16-CTA clusters (batch <= 4) and 4-CTA clusters (bf16, batch >= 8), one
+    grid row per logits row; each row's u sits mid-interval of an oracle-drawn token."""
+    import torch
+    from paper_2512_11221_b200 import asr_sample
+    V = 128256
+    X = _rows("gen", B, V, 500 + B)
+    xt = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).cuda()
+    rng = np.random.default_rng(B)
+    for T, k, P in [(0.8, 50, 0.9), (1.0, 0, 0.95), (0.7, 20000, 1.0)]:
+        us, want = [], []
+        for b in range(B):
+            for _ in range(50):
+                tok = sample(X[b], T, k, P, float(rng.random()))
+                lo, hi = interval(X[b], T, k, P, tok)
+                if hi - lo >= 1e-4:
+                    break
+            us.append(0.5 * (lo + hi) if hi - lo >= 1e-4 else float(rng.random()))
+            want.append(tok if hi - lo >= 1e-4 else -1)
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        asr_sample(xt, torch.tensor(us, dtype=torch.float32, device="cuda"), out, temperature=T, top_k=k, top_p=P)
+        got = out.cpu().numpy()
+        for b in range(B):
+            if want[b] >= 0:
+                assert int(got[b]) == want[b], (B, T, k, P, b, int(got[b]), want[b])
+            else:
+                lo, hi = interval(X[b], T, k, P, int(got[b]))
+                assert lo - 2e-6 <= us[b] <= hi + 2e-6, (B, T, k, P, b, lo, us[b], hi)
