@@ -98,6 +98,9 @@ def lib() -> ctypes.CDLL:
         _lib.orc_duration.restype = ci
         _lib.orc_entropy.argtypes = [vp, ci, ci, ctypes.c_double]
         _lib.orc_entropy.restype = ctypes.c_double
+        _lib.orc_attend_head.argtypes = [vp, ci, vp, vp, ci, ci, ci, vp]
+        _lib.orc_score_token.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, ci]
+        _lib.orc_score_token.restype = ctypes.c_double
     return _lib
 
 
@@ -117,6 +120,24 @@ def duration(c: int, k: float) -> int:
 def entropy(logits: np.ndarray, temp: float = 1.0) -> float:
     a = np.ascontiguousarray(logits)
     return lib().orc_entropy(a.ctypes.data, _code(a), a.size, temp)
+
+
+def attend_head(q: np.ndarray, K: np.ndarray, V: np.ndarray) -> np.ndarray:
+    """Eq. 1 for one (layer, head): q [d], K, V [n][d] (bf16 bits or f32) -> out [d] fp64."""
+    q, K, V = (np.ascontiguousarray(x) for x in (q, K, V))
+    n, d = K.shape
+    assert q.shape == (d,) and V.shape == (n, d) and K.dtype == V.dtype
+    out = np.empty(d, np.float64)
+    lib().orc_attend_head(q.ctypes.data, _code(q), K.ctypes.data, V.ctypes.data, _code(K), n, d, out.ctypes.data)
+    return out
+
+
+def score_token(q: np.ndarray, k: np.ndarray, scaled: bool = False) -> float:
+    """Eq. 2 for one token: q [L][Hq][d], k [L][Hkv][d]."""
+    q, k = np.ascontiguousarray(q), np.ascontiguousarray(k)
+    L, Hq, d = q.shape
+    assert k.shape[0] == L and k.shape[2] == d
+    return lib().orc_score_token(q.ctypes.data, _code(q), k.ctypes.data, _code(k), L, Hq, k.shape[1], d, int(scaled))
 
 
 class OracleSeq:

@@ -383,3 +383,45 @@ int orc_step_policy(orc_seq* s, const unsigned char* below_pos, double H, int H_
   s->step++;
   return 0;
 }
+
+/* ---------------------------------------------------------------- single outputs */
+
+/* Eq. 1 for one (layer, head), in the same order as orc_step: logits q.k_a / sqrt(d),
+ * their maximum, Z = sum exp(logit - max), out[e] = sum_a exp(logit_a - max) / Z * v_a[e]. */
+void orc_attend_head(const void* q, int q_dtype, const void* K, const void* V, int kv_dtype, int n, int d,
+                     double* out) {
+  double* logit = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double mx = -DBL_MAX;
+  for (int a = 0; a < n; ++a) {
+    double dot = 0.0;
+    for (int e = 0; e < d; ++e) dot += val(q, e, q_dtype) * val(K, (long)a * d + e, kv_dtype);
+    logit[a] = dot / sqrt((double)d);
+    if (logit[a] > mx) mx = logit[a];
+  }
+  double Z = 0.0;
+  for (int a = 0; a < n; ++a) Z += exp(logit[a] - mx);
+  for (int e = 0; e < d; ++e) {
+    double acc = 0.0;
+    for (int a = 0; a < n; ++a) acc += exp(logit[a] - mx) / Z * val(V, (long)a * d + e, kv_dtype);
+    out[e] = acc;
+  }
+  free(logit);
+}
+
+/* Eq. 2 for one token, H = L*Hq (R-layer, R-gqa), raw unless scaled (R-scale). */
+double orc_score_token(const void* q, int q_dtype, const void* k, int kv_dtype, int L, int Hq, int Hkv, int d,
+                       int scaled) {
+  const int group = Hq / Hkv;
+  double sum = 0.0;
+  for (int l = 0; l < L; ++l)
+    for (int h = 0; h < Hq; ++h) {
+      const long qo = ((long)l * Hq + h) * d;
+      const long ko = ((long)l * Hkv + h / group) * d;
+      double dot = 0.0;
+      for (int e = 0; e < d; ++e) dot += val(q, qo + e, q_dtype) * val(k, ko + e, kv_dtype);
+      sum += fabs(dot);
+    }
+  double sj = sum / (double)(L * Hq);
+  if (scaled) sj = sj / sqrt((double)d);
+  return sj;
+}

@@ -86,4 +86,14 @@ void orc_ledger(const orc_seq* s, unsigned char* res, int* timer, uint32_t* coun
 int orc_duration(uint32_t c, double k);                                       /* Eq. 3 */
 double orc_entropy(const void* logits, int dtype, int vocab, double temp);     /* -sum p ln p */
 
+/* Single outputs, for sampled parity checks at full size (where a whole orc_step is too slow):
+ * Eq. 1 for one (layer, head): out[d] = softmax(q K^T / sqrt(d)) V over n rows K, V [n][d] (the
+ * head's KV rows of the attended tokens, in attended order); q [d]. */
+void orc_attend_head(const void* q, int q_dtype, const void* K, const void* V, int kv_dtype, int n, int d,
+                     double* out);
+/* Eq. 2 for one token: s_j = (1/(L*Hq)) sum over (layer, head) of |q_{l,h} . k_{j,l,h/(Hq/Hkv)}|,
+ * q [L][Hq][d], k_j [L][Hkv][d]; x 1/sqrt(d) when scaled (R-scale). */
+double orc_score_token(const void* q, int q_dtype, const void* k, int kv_dtype, int L, int Hq, int Hkv, int d,
+                       int scaled);
+
 #endif

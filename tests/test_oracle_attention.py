@@ -194,3 +194,51 @@ def test_full_step_matches_policy_replay_on_lat():
         assert o1 == o2
         for key in ("residency", "timer", "count", "freeze_step"):
             np.testing.assert_array_equal(s_full.ledger()[key], s_pol.ledger()[key])
+
+
+# ---- the single-output functions (orc_attend_head, orc_score_token) used by the full-size sampled
+#      parity test: pinned by the same special cases and closed values, then shown to agree with
+#      orc_step's outputs on a random case
+
+def test_attend_head_special_cases():
+    rng = np.random.default_rng(5)
+    d = 8
+    q = f32(rng.normal(size=d))
+    K1, V1 = f32(rng.normal(size=(1, d))), f32(rng.normal(size=(1, d)))
+    assert np.array_equal(oracle.attend_head(q, K1, V1), V1[0].astype(np.float64))   # singleton softmax = 1
+    K = f32(rng.normal(size=(5, d)))
+    V = f32(rng.normal(size=(5, d)))
+    np.testing.assert_allclose(oracle.attend_head(f32(np.zeros(d)), K, V), V.astype(np.float64).mean(0),
+                               rtol=0, atol=1e-15)   # equal logits: the mean
+    K2, V2 = K[:2], V[:2]
+    gap = float(np.dot(q.astype(np.float64), K2[0].astype(np.float64) - K2[1].astype(np.float64))) / math.sqrt(d)
+    w = 1.0 / (1.0 + math.exp(-gap))    # two tokens: the logistic of the scaled logit gap
+    np.testing.assert_allclose(oracle.attend_head(q, K2, V2), w * V2[0].astype(np.float64) + (1 - w) * V2[1].astype(np.float64),
+                               rtol=0, atol=1e-14)
+
+
+def test_score_token_closed_values():
+    # L=1, Hq=2, Hkv=1, d=2: |1*0.5 + 2*(-1)| + |-3*0.5 + 0.5*(-1)| = 1.5 + 2 = 3.5, over H = 2
+    q = f32([[[1, 2], [-3, 0.5]]])
+    k = f32([[[0.5, -1]]])
+    assert oracle.score_token(q, k) == 1.75
+    assert oracle.score_token(q, k, scaled=True) == 1.75 / math.sqrt(2)
+    # GQA: heads 0, 1 read KV head 0 and heads 2, 3 KV head 1 (h // (Hq/Hkv)): (2+4+9+12)/4; the
+    # interleaved map h % Hkv would give 26/4
+    assert oracle.score_token(f32([[[1], [2], [3], [4]]]), f32([[[2], [3]]])) == 6.75
+
+
+def test_single_outputs_agree_with_step():
+    rng = np.random.default_rng(9)
+    L, Hq, Hkv, d, P = 2, 4, 2, 16, 12
+    cfg = oracle.OrcCfg(L=L, Hq=Hq, Hkv=Hkv, d=d, window=4, tau=0.3)
+    K = f32(rng.normal(size=(P + 1, L, Hkv, d)))
+    V = f32(rng.normal(size=(P + 1, L, Hkv, d)))
+    q = f32(rng.normal(size=(L, Hq, d)))
+    O, act, scores, _ = one_step(cfg, K, V, q, P)
+    for l in range(L):
+        for h in range(Hq):
+            g = h // (Hq // Hkv)
+            np.testing.assert_array_equal(oracle.attend_head(q[l, h], K[act, l, g], V[act, l, g]), O[l, h])
+    for a, j in enumerate(act):
+        assert oracle.score_token(q, K[j]) == scores[a]
