@@ -1,0 +1,114 @@
+"""Parity at BASELINE.json's full sizes, in bench.py's launch configuration: configs[1] (8K context,
+batch 1, the headline) and configs[2] (8K context, batch 64).  LLaMA-3-8B shape (L=32, Hq=32, Hkv=8,
+d=128, V=128256), window K=512, tau=0.5, k=2, the W0 trace, grown from a 512-token prompt to n = 8192
+by 7680 steps with the device generator — the workload, Config (max_context included) and schedule
+bench.py times (tensor-core attention; phase A inside the attention kernel at batch 1).
+
+The oracle cannot run 7680 full steps of 32 layers, so the sampled sequences are checked against:
+- the oracle's policy replay of every step (orc_step_policy): on W0 every out-of-window token scores
+  < tau, which the LAT construction guarantees (cold |q.k| <= 7/16 per head); the
+  entropy of each step's logits row comes from the oracle too.  Ledgers (residency, timer, count,
+  freeze step), the attended list and the counters of the final step: bit-exact;
+- Eq. 2 scores of sampled attended tokens of the final step: equal to oracle.score_token (exact on
+  LAT inputs, one correctly rounded fp32 division);
+- O of sampled (layer, head) pairs of the final step: oracle.attend_head over the attended tokens'
+  K/V rows, max_e|o - o*| / max_e|o*| <= 2e-3 (the north_star's bf16 bar).
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+L, HQ, HKV, D, VOCAB = 32, 32, 8, 128, 128256
+CONTEXT, WINDOW, TAU, SOFT, SEED = 8192, 512, 0.5, 2.0, 2001
+# bench.py's defaults: --steps 64 --warmup 8, e2e on: max_context = context + W + 2K + K + 16
+MAX_CTX = CONTEXT + 8 + 2 * 64 + 64 + 16
+
+
+def _oracle_replay(g, b, steps):
+    """The oracle's policy replay of steps 0..steps-1 for sequence b; returns (seq, act, out) of the
+    last step."""
+    def H(i):
+        return oracle.entropy(gen.logits(g, b, i - 1))
+    with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:   # ctypes calls drop the GIL
+        Hs = [None] + list(ex.map(H, range(1, steps)))
+    cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=TAU, softness=SOFT)
+    s = oracle.OracleSeq(cfg, MAX_CTX, WINDOW)
+    act = out = None
+    for i in range(steps):
+        act, out = s.step_policy(np.ones(s.n + 1, np.uint8), Hs[i])
+    return s, act, out, Hs[-1]
+
+
+@pytest.mark.parametrize("B,sampled", [(1, (0,)), (64, (0, 63))])
+def test_full_size_sampled(B, sampled):
+    import torch
+    from paper_2512_11221_b200 import Config, Context, KV_BF16
+
+    g = gen.GenParams(seed=SEED, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D, hot_permille=0, a_hot=4, vocab=VOCAB)
+    P = WINDOW
+    steps = CONTEXT - P   # the last one appends position 8191
+    cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=MAX_CTX,
+                 kv_dtype=KV_BF16, window=WINDOW, tau=TAU, softness=SOFT, vocab=VOCAB, profile_stages=0)
+    bf = torch.bfloat16
+    pk = torch.empty((B, P, L, HKV, D), dtype=bf, device="cuda")
+    pv = torch.empty_like(pk)
+    gen.dev_kv(g, B, 0, P, pk, pv)
+    torch.cuda.synchronize()
+    ctx = Context(cfg, pk, pv, [P] * B)
+    del pk, pv
+    q = torch.empty((B, L, HQ, D), dtype=bf, device="cuda")
+    kn = torch.empty((B, L, HKV, D), dtype=bf, device="cuda")
+    vn = torch.empty_like(kn)
+    lg = torch.empty((B, VOCAB), dtype=bf, device="cuda")
+    o = torch.empty((B, L, HQ, D), dtype=torch.float32, device="cuda")
+    ent = torch.empty((B,), dtype=torch.float32, device="cuda")
+    pos = torch.full((B,), P, dtype=torch.int32, device="cuda")
+    for i in range(steps):
+        gen.dev_q(g, B, i, q)
+        gen.dev_kv(g, B, 0, 1, kn, vn, pos0_dev=pos + i)
+        gen.dev_logits(g, B, i - 1, lg)
+        ctx.step(q, kn, vn, o, logits_prev=lg if i > 0 else None, entropy=ent)
+    torch.cuda.synchronize()
+    O = o.cpu().numpy()
+    E = ent.cpu().numpy()
+    rng = np.random.default_rng(B)
+    for b in sampled:
+        s, act, out, H_last = _oracle_replay(g, b, steps)
+        st = ctx.stats(b, detail=True)
+        where = f"B={B} seq {b}"
+        assert st["device_error"] == 0, where
+        np.testing.assert_array_equal(st["active_list"], act, err_msg=where)
+        led = s.ledger()
+        for key in ("residency", "timer", "count", "freeze_step"):
+            np.testing.assert_array_equal(st["ledger"][key], led[key], err_msg=f"{where} {key}")
+        assert st["total"] == out["n"] == CONTEXT and st["attended"] == out["attended"], where
+        assert st["active"] == out["active_post"] and st["frozen"] == out["frozen_post"], where
+        assert st["frozen_this_step"] == out["frozen_this_step"], where
+        assert st["restored_this_step"] == out["restored_this_step"], where
+        assert st["recovery_action"] == out["recovery_action"], where
+        assert abs(float(E[b]) - H_last) <= 1e-4, (where, float(E[b]), H_last)
+        # the final step's inputs, from the host build of the generator
+        qb = gen.q(g, b, steps - 1)
+        rows = [gen.kv(g, b, int(j), 1) for j in act]
+        Kb = np.stack([r[0][0] for r in rows])   # [A][L][Hkv][d] bf16 bits
+        Vb = np.stack([r[1][0] for r in rows])
+        # Eq. 2 scores of sampled attended tokens (first, last, random)
+        pick = sorted({0, len(act) - 1, *rng.integers(0, len(act), 30).tolist()})
+        for a in pick:
+            want = np.float32(oracle.score_token(qb, Kb[a]))
+            assert st["scores"][a] == want, (where, a, int(act[a]), float(st["scores"][a]), float(want))
+        # O of sampled (layer, head) pairs (first, last, random)
+        pairs = {(0, 0), (L - 1, HQ - 1), *[(int(x), int(y)) for x, y in rng.integers(0, [L, HQ], (6, 2))]}
+        for l, h in sorted(pairs):
+            kvh = h // (HQ // HKV)
+            ref = oracle.attend_head(qb[l, h], Kb[:, l, kvh], Vb[:, l, kvh])
+            err = float(np.max(np.abs(O[b, l, h] - ref)) / np.max(np.abs(ref)))
+            assert err <= 2e-3, (where, l, h, err)
+    ctx.close()
