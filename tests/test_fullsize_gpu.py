@@ -1,13 +1,14 @@
 """Parity at BASELINE.json's full sizes, in bench.py's launch configuration: configs[1] (8K context,
 batch 1, the headline) and configs[2] (8K context, batch 64).  LLaMA-3-8B shape (L=32, Hq=32, Hkv=8,
-d=128, V=128256), window K=512, tau=0.5, k=2, the W0 trace, grown from a 512-token prompt to n = 8192
+d=128, V=128256), window K=512, tau=0.5, k=2, the W0 trace (and W1), grown from a 512-token prompt to n = 8192
 by 7680 steps with the device generator — the workload, Config (max_context included) and schedule
 bench.py times (tensor-core attention; phase A inside the attention kernel at batch 1).
 
 The oracle cannot run 7680 full steps of 32 layers, so the sampled sequences are checked against:
 - the oracle's policy replay of every step (orc_step_policy): on W0 every out-of-window token scores
-  < tau, which the LAT construction guarantees (cold |q.k| <= 7/16 per head); the
-  entropy of each step's logits row comes from the oracle too.  Ledgers (residency, timer, count,
+  < tau, on W1 (bench.py's "w1" point, 30 % hot tokens) the cold ones do and the hot ones score
+  >= 1.3125 — classes the LAT construction guarantees (cold |q.k| <= 7/16 per head);
+  the entropy of each step's logits row comes from the oracle too.  Ledgers (residency, timer, count,
   freeze step), the attended list and the counters of the final step: bit-exact;
 - Eq. 2 scores of sampled attended tokens of the final step: equal to oracle.score_token (exact on
   LAT inputs, one correctly rounded fp32 division);
@@ -33,7 +34,8 @@ MAX_CTX = CONTEXT + 8 + 2 * 64 + 64 + 16
 
 def _oracle_replay(g, b, steps):
     """The oracle's policy replay of steps 0..steps-1 for sequence b; returns (seq, act, out) of the
-    last step."""
+    last step.  below[pos] = the position's LAT class (cold: s < tau; hot, W1 only: s >= 1.3125)."""
+    cold = np.array([0 if gen.is_hot(g, b, j) else 1 for j in range(MAX_CTX)], np.uint8)
     def H(i):
         return oracle.entropy(gen.logits(g, b, i - 1))
     with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:   # ctypes calls drop the GIL
@@ -42,16 +44,17 @@ def _oracle_replay(g, b, steps):
     s = oracle.OracleSeq(cfg, MAX_CTX, WINDOW)
     act = out = None
     for i in range(steps):
-        act, out = s.step_policy(np.ones(s.n + 1, np.uint8), Hs[i])
+        act, out = s.step_policy(cold[:s.n + 1], Hs[i])
     return s, act, out, Hs[-1]
 
 
-@pytest.mark.parametrize("B,sampled", [(1, (0,)), (64, (0, 63))])
-def test_full_size_sampled(B, sampled):
+@pytest.mark.parametrize("B,sampled,family", [(1, (0,), "w0"), (64, (0, 63), "w0"), (1, (0,), "w1")])
+def test_full_size_sampled(B, sampled, family):
     import torch
     from paper_2512_11221_b200 import Config, Context, KV_BF16
 
-    g = gen.GenParams(seed=SEED, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D, hot_permille=0, a_hot=4, vocab=VOCAB)
+    g = gen.GenParams(seed=SEED, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D,
+                      hot_permille=300 if family == "w1" else 0, a_hot=4, vocab=VOCAB)   # bench.gen_params
     P = WINDOW
     steps = CONTEXT - P   # the last one appends position 8191
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=MAX_CTX,
