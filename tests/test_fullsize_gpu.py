@@ -29,36 +29,45 @@ pytestmark = pytest.mark.gpu
 L, HQ, HKV, D, VOCAB = 32, 32, 8, 128, 128256
 CONTEXT, WINDOW, TAU, SOFT, SEED = 8192, 512, 0.5, 2.0, 2001
 # bench.py's defaults: --steps 64 --warmup 8, e2e on: max_context = context + W + 2K + K + 16
-MAX_CTX = CONTEXT + 8 + 2 * 64 + 64 + 16
+SLACK = 8 + 2 * 64 + 64 + 16
 
 
-def _oracle_replay(g, b, steps):
+def _oracle_replay(g, b, steps, tau, max_ctx):
     """The oracle's policy replay of steps 0..steps-1 for sequence b; returns (seq, act, out) of the
     last step.  below[pos] = the position's LAT class (cold: s < tau; hot, W1 only: s >= 1.3125)."""
-    cold = np.array([0 if gen.is_hot(g, b, j) else 1 for j in range(MAX_CTX)], np.uint8)
+    cold = np.array([0 if gen.is_hot(g, b, j) else 1 for j in range(max_ctx)], np.uint8)
+    assert tau <= 0 or 0.4375 < tau < 1.3125   # the classes decide s < tau
+    below = cold if tau > 0 else np.zeros_like(cold)   # scores are >= 0: nothing is below tau <= 0
     def H(i):
         return oracle.entropy(gen.logits(g, b, i - 1))
     with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:   # ctypes calls drop the GIL
         Hs = [None] + list(ex.map(H, range(1, steps)))
-    cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=TAU, softness=SOFT)
-    s = oracle.OracleSeq(cfg, MAX_CTX, WINDOW)
+    cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=tau, softness=SOFT)
+    s = oracle.OracleSeq(cfg, max_ctx, WINDOW)
     act = out = None
     for i in range(steps):
-        act, out = s.step_policy(cold[:s.n + 1], Hs[i])
+        act, out = s.step_policy(below[:s.n + 1], Hs[i])
     return s, act, out, Hs[-1]
 
 
-@pytest.mark.parametrize("B,sampled,family", [(1, (0,), "w0"), (64, (0, 63), "w0"), (1, (0,), "w1")])
-def test_full_size_sampled(B, sampled, family):
+@pytest.mark.parametrize("B,sampled,family,context,tau", [
+    (1, (0,), "w0", CONTEXT, TAU),       # configs[1], the headline
+    (64, (0, 63), "w0", CONTEXT, TAU),   # configs[2]
+    (1, (0,), "w1", CONTEXT, TAU),       # bench point "w1"
+    (1, (0,), "w0", 32768, TAU),         # bench point "ctx32k"
+    (1, (0,), "w0", CONTEXT, 0.0),       # bench point "full": tau <= 0 freezes nothing
+])
+def test_full_size_sampled(B, sampled, family, context, tau):
     import torch
     from paper_2512_11221_b200 import Config, Context, KV_BF16
 
     g = gen.GenParams(seed=SEED, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D,
                       hot_permille=300 if family == "w1" else 0, a_hot=4, vocab=VOCAB)   # bench.gen_params
     P = WINDOW
-    steps = CONTEXT - P   # the last one appends position 8191
-    cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=MAX_CTX,
-                 kv_dtype=KV_BF16, window=WINDOW, tau=TAU, softness=SOFT, vocab=VOCAB, profile_stages=0)
+    steps = context - P   # the last one appends position context - 1
+    max_ctx = context + SLACK
+    cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
+                 kv_dtype=KV_BF16, window=WINDOW, tau=tau, softness=SOFT, vocab=VOCAB, profile_stages=0)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, HKV, D), dtype=bf, device="cuda")
     pv = torch.empty_like(pk)
@@ -83,7 +92,7 @@ def test_full_size_sampled(B, sampled, family):
     E = ent.cpu().numpy()
     rng = np.random.default_rng(B)
     for b in sampled:
-        s, act, out, H_last = _oracle_replay(g, b, steps)
+        s, act, out, H_last = _oracle_replay(g, b, steps, tau, max_ctx)
         st = ctx.stats(b, detail=True)
         where = f"B={B} seq {b}"
         assert st["device_error"] == 0, where
@@ -91,7 +100,7 @@ def test_full_size_sampled(B, sampled, family):
         led = s.ledger()
         for key in ("residency", "timer", "count", "freeze_step"):
             np.testing.assert_array_equal(st["ledger"][key], led[key], err_msg=f"{where} {key}")
-        assert st["total"] == out["n"] == CONTEXT and st["attended"] == out["attended"], where
+        assert st["total"] == out["n"] == context and st["attended"] == out["attended"], where
         assert st["active"] == out["active_post"] and st["frozen"] == out["frozen_post"], where
         assert st["frozen_this_step"] == out["frozen_this_step"], where
         assert st["restored_this_step"] == out["restored_this_step"], where
