@@ -32,7 +32,7 @@ CONTEXT, WINDOW, TAU, SOFT, SEED = 8192, 512, 0.5, 2.0, 2001
 SLACK = 8 + 2 * 64 + 64 + 16
 
 
-def _oracle_replay(g, b, steps, tau, max_ctx):
+def _oracle_replay(g, b, steps, tau, max_ctx, W):
     """The oracle's policy replay of steps 0..steps-1 for sequence b; returns (seq, act, out) of the
     last step.  below[pos] = the position's LAT class (cold: s < tau; hot, W1 only: s >= 1.3125)."""
     cold = np.array([0 if gen.is_hot(g, b, j) else 1 for j in range(max_ctx)], np.uint8)
@@ -42,7 +42,7 @@ def _oracle_replay(g, b, steps, tau, max_ctx):
         return oracle.entropy(gen.logits(g, b, i - 1))
     with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:   # ctypes calls drop the GIL
         Hs = [None] + list(ex.map(H, range(1, steps)))
-    cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=tau, softness=SOFT)
+    cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=tau, softness=SOFT, history_window=W)
     s = oracle.OracleSeq(cfg, max_ctx, WINDOW)
     act = out = None
     for i in range(steps):
@@ -50,14 +50,15 @@ def _oracle_replay(g, b, steps, tau, max_ctx):
     return s, act, out, Hs[-1]
 
 
-@pytest.mark.parametrize("B,sampled,family,context,tau", [
-    (1, (0,), "w0", CONTEXT, TAU),       # configs[1], the headline
-    (64, (0, 63), "w0", CONTEXT, TAU),   # configs[2]
-    (1, (0,), "w1", CONTEXT, TAU),       # bench point "w1"
-    (1, (0,), "w0", 32768, TAU),         # bench point "ctx32k"
-    (1, (0,), "w0", CONTEXT, 0.0),       # bench point "full": tau <= 0 freezes nothing
+@pytest.mark.parametrize("B,sampled,family,context,tau,W", [
+    (1, (0,), "w0", CONTEXT, TAU, 0),       # configs[1], the headline
+    (64, (0, 63), "w0", CONTEXT, TAU, 0),   # configs[2]
+    (1, (0,), "w1", CONTEXT, TAU, 0),       # bench point "w1"
+    (1, (0,), "w0", 32768, TAU, 0),         # bench point "ctx32k"
+    (1, (0,), "w0", CONTEXT, 0.0, 0),       # bench point "full": tau <= 0 freezes nothing
+    (1, (0,), "w0", CONTEXT, TAU, 128),     # bench point "w128": finite history window (NEXT-3)
 ])
-def test_full_size_sampled(B, sampled, family, context, tau):
+def test_full_size_sampled(B, sampled, family, context, tau, W):
     import torch
     from paper_2512_11221_b200 import Config, Context, KV_BF16
 
@@ -67,7 +68,8 @@ def test_full_size_sampled(B, sampled, family, context, tau):
     steps = context - P   # the last one appends position context - 1
     max_ctx = context + SLACK
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
-                 kv_dtype=KV_BF16, window=WINDOW, tau=tau, softness=SOFT, vocab=VOCAB, profile_stages=0)
+                 kv_dtype=KV_BF16, window=WINDOW, tau=tau, softness=SOFT, vocab=VOCAB, profile_stages=0,
+                 history_window=W)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, HKV, D), dtype=bf, device="cuda")
     pv = torch.empty_like(pk)
@@ -92,7 +94,7 @@ def test_full_size_sampled(B, sampled, family, context, tau):
     E = ent.cpu().numpy()
     rng = np.random.default_rng(B)
     for b in sampled:
-        s, act, out, H_last = _oracle_replay(g, b, steps, tau, max_ctx)
+        s, act, out, H_last = _oracle_replay(g, b, steps, tau, max_ctx, W)
         st = ctx.stats(b, detail=True)
         where = f"B={B} seq {b}"
         assert st["device_error"] == 0, where
