@@ -50,15 +50,16 @@ def _oracle_replay(g, b, steps, tau, max_ctx, W):
     return s, act, out, Hs[-1]
 
 
-@pytest.mark.parametrize("B,sampled,family,context,tau,W", [
-    (1, (0,), "w0", CONTEXT, TAU, 0),       # configs[1], the headline
-    (64, (0, 63), "w0", CONTEXT, TAU, 0),   # configs[2]
-    (1, (0,), "w1", CONTEXT, TAU, 0),       # bench point "w1"
-    (1, (0,), "w0", 32768, TAU, 0),         # bench point "ctx32k"
-    (1, (0,), "w0", CONTEXT, 0.0, 0),       # bench point "full": tau <= 0 freezes nothing
-    (1, (0,), "w0", CONTEXT, TAU, 128),     # bench point "w128": finite history window (NEXT-3)
+@pytest.mark.parametrize("B,sampled,family,context,tau,W,pool_frac", [
+    (1, (0,), "w0", CONTEXT, TAU, 0, 0.0),       # configs[1], the headline
+    (64, (0, 63), "w0", CONTEXT, TAU, 0, 0.0),   # configs[2]
+    (1, (0,), "w1", CONTEXT, TAU, 0, 0.0),       # bench point "w1"
+    (1, (0,), "w0", 32768, TAU, 0, 0.0),         # bench point "ctx32k"
+    (1, (0,), "w0", CONTEXT, 0.0, 0, 0.0),       # bench point "full": tau <= 0 freezes nothing
+    (1, (0,), "w0", CONTEXT, TAU, 128, 0.0),     # bench point "w128": finite history window (NEXT-3)
+    (1, (0,), "w0", CONTEXT, TAU, 0, 0.5),       # bench --pool-frac 0.5: frozen KV leaves the GPU
 ])
-def test_full_size_sampled(B, sampled, family, context, tau, W):
+def test_full_size_sampled(B, sampled, family, context, tau, W, pool_frac):
     import torch
     from paper_2512_11221_b200 import Config, Context, KV_BF16
 
@@ -69,7 +70,8 @@ def test_full_size_sampled(B, sampled, family, context, tau, W):
     max_ctx = context + SLACK
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=WINDOW, tau=tau, softness=SOFT, vocab=VOCAB, profile_stages=0,
-                 history_window=W)
+                 history_window=W, pool_tokens=int(pool_frac * B * context) + 4 * B if pool_frac > 0 else 0,
+                 evict_min_absence=2)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, HKV, D), dtype=bf, device="cuda")
     pv = torch.empty_like(pk)
@@ -98,6 +100,8 @@ def test_full_size_sampled(B, sampled, family, context, tau, W):
         st = ctx.stats(b, detail=True)
         where = f"B={B} seq {b}"
         assert st["device_error"] == 0, where
+        if pool_frac > 0:   # pressure mode: within the pool, every attended token on the device
+            assert st["active"] <= st["resident"] <= cfg.pool_tokens, (where, st["resident"])
         np.testing.assert_array_equal(st["active_list"], act, err_msg=where)
         led = s.ledger()
         for key in ("residency", "timer", "count", "freeze_step"):
