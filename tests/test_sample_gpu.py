@@ -131,3 +131,26 @@ def test_sample_batched_rows(B):
             else:
                 lo, hi = interval(X[b], T, k, P, int(got[b]))
                 assert lo - 2e-6 <= us[b] <= hi + 2e-6, (B, T, k, P, b, lo, us[b], hi)
+
+
+def test_sample_uncached_slice():
+    """A vocabulary whose per-CTA slice exceeds the shared-memory cache (fp32, V = 400000, one row:
+    16 CTAs of 100 KB): every pass reads global memory; exact draws as above."""
+    import torch
+    from paper_2512_11221_b200 import asr_sample
+    V = 400000
+    x = _rows("normal", 1, V, 77)[0]
+    xt = torch.from_numpy(x[None]).cuda()
+    rng = np.random.default_rng(3)
+    for T, k, P in [(0.8, 50, 0.9), (1.0, 0, 0.95), (0.7, 3000, 1.0)]:
+        for _ in range(50):
+            tok = sample(x, T, k, P, float(rng.random()))
+            lo, hi = interval(x, T, k, P, tok)
+            if hi - lo >= 1e-4:
+                break
+        if hi - lo < 1e-4:
+            continue
+        out = torch.empty(1, dtype=torch.int32, device="cuda")
+        asr_sample(xt, torch.tensor([0.5 * (lo + hi)], dtype=torch.float32, device="cuda"), out,
+                   temperature=T, top_k=k, top_p=P)
+        assert int(out.item()) == tok, (T, k, P, int(out.item()), tok)
