@@ -241,7 +241,9 @@ asr_status asr_step_policy(asr_ctx* ctx, const float* scores, const void* logits
  * >= top_p of their mass (top_p >= 1: all), and return the smallest vocab index j of the kept set whose
  * cumulative kept mass (in vocab order) exceeds uniforms[b] * the kept mass; uniforms[batch] in [0, 1)
  * (device, the caller's random numbers); token_out[batch] (device, int32).  Stateless (no context),
- * asynchronous on cuda_stream, bitwise deterministic.  Rules and pins: oracle/sample.py. */
+ * asynchronous on cuda_stream, bitwise deterministic.  Rules and pins: oracle/sample.py.
+ * Errors: ASR_E_INVALID for a NULL pointer, an unknown dtype, batch outside 1..65535, vocab outside
+ * 1..2^24-1, or a non-finite temperature / top_p; launch failures as ASR_E_CUDA. */
 asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab, float temperature,
                       int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream);
 

@@ -1109,7 +1109,8 @@ asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, i
                       int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream) {
   if (!logits || !uniforms || !token_out) return fail(ASR_E_INVALID, "asr_sample: NULL pointer");
   if (logits_dtype != ASR_KV_BF16 && logits_dtype != ASR_KV_F32) return fail(ASR_E_INVALID, "asr_sample: logits_dtype");
-  if (batch < 1 || vocab < 1 || vocab >= (1 << 24)) return fail(ASR_E_INVALID, "asr_sample: batch / vocab out of range");
+  if (batch < 1 || batch > 65535 || vocab < 1 || vocab >= (1 << 24))   // grid.y = batch
+    return fail(ASR_E_INVALID, "asr_sample: batch / vocab out of range");
   if (!isfinite(temperature) || !isfinite(top_p)) return fail(ASR_E_INVALID, "asr_sample: temperature / top_p");
   CUDA_TRY(asr::launch_sample(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out,
                               (cudaStream_t)cuda_stream));

@@ -94,3 +94,18 @@ def test_oracle_and_product_share_no_code():
             deps = re.findall(r"(?:#include\s+[\"<]([\w./]+)|^\s*(?:import|from)\s+([\w.]+))", txt, flags=re.M)
             deps = {a or b for a, b in deps}
             assert not any("asr" in x or "paper_2512" in x or "gen" == x.split(".")[0] for x in deps), (f, deps)
+
+
+@pytest.mark.parametrize("args", [
+    dict(logits=None), dict(dtype=5), dict(batch=0), dict(batch=65536), dict(vocab=0), dict(vocab=1 << 24),
+    dict(temperature=float("nan")), dict(top_p=float("inf")), dict(uniforms=None), dict(token_out=None)])
+def test_sample_invalid_arguments_rejected(args):
+    """asr_sample validates before touching the device (include/asr.h): ASR_E_INVALID, no launch."""
+    p = ctypes.c_void_p(16)   # never dereferenced: validation fails first
+    a = dict(logits=p, dtype=asr.KV_BF16, batch=1, vocab=128256, temperature=1.0, top_k=0, top_p=1.0,
+             uniforms=p, token_out=p)
+    a.update(args)
+    rc = asr.lib().asr_sample(a["logits"], a["dtype"], a["batch"], a["vocab"], a["temperature"], a["top_k"],
+                              a["top_p"], a["uniforms"], a["token_out"], None)
+    assert rc == asr.ASR_E_INVALID
+    assert asr.lib().asr_last_error()
