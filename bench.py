@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
-    ap.add_argument("--points", default="cfg3,w1,full,sample,replay",
+    ap.add_argument("--points", default="cfg3,w1,full,sample,replay,quant",
                     help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
     ap.add_argument("--head-shard", action="store_true",
                     help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
@@ -506,6 +506,71 @@ def sample_point(local_rank: int) -> dict:
     return out
 
 
+def quant_point(local_rank: int) -> dict:
+    """NEXT-4: the quantised frozen tier (asr_kv_quantize / asr_kv_dequantize).  Tier = the frozen
+    KV of the configs[1] point (6900 tokens x 32 layers x K,V x 8 heads = 3.53M rows of 128 bf16, 904 MB;
+    larger than L2, so every call streams HBM).  Kernel GB/s = algorithmic bytes (bf16 read + codes and
+    scales written, or the reverse) / CUDA-event time over 10 calls.  Restore over the host link: the
+    pressure-mode H2D volume per step at 8K (105 MB of bf16) copied from pinned memory as
+    bf16, vs its INT8/INT4 codes + scales copied and dequantised on the device."""
+    import torch
+
+    from paper_2512_11221_b200 import asr_kv_dequantize, asr_kv_quantize
+    dev = torch.device("cuda", local_rank)
+    peak, kind = measured_peak_hbm()
+    rows, n = 6900 * 512, 128
+    g = torch.Generator(device=dev).manual_seed(5)
+    kv = torch.randn((rows, n), device=dev, generator=g).to(torch.bfloat16)
+    back = torch.empty_like(kv)
+    scales = torch.empty(rows, dtype=torch.float32, device=dev)
+    out = {"rows": rows, "row_elems": n, "peak_gbs": peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({kind})"}
+
+    def timed(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps   # ms
+
+    for bits in (8, 4):
+        cb = n if bits == 8 else n // 2
+        codes = torch.empty((rows, cb), dtype=torch.int8, device=dev)
+        moved = rows * (2 * n + cb + 4)
+        tq = timed(lambda: asr_kv_quantize(kv, codes, scales, bits=bits))
+        td = timed(lambda: asr_kv_dequantize(codes, scales, back, bits=bits))
+        # host-link restore of 105 MB of bf16 KV (the pressure-mode H2D per step at 8K): 420K rows of 256 B
+        rr = 105 * 1024 * 1024 // (2 * n)
+        h_bf16 = torch.empty((rr, n), dtype=torch.bfloat16, pin_memory=True)
+        h_codes = torch.empty((rr, cb), dtype=torch.int8, pin_memory=True)
+        h_sc = torch.empty(rr, dtype=torch.float32, pin_memory=True)
+        d_codes = torch.empty((rr, cb), dtype=torch.int8, device=dev)
+        d_sc = torch.empty(rr, dtype=torch.float32, device=dev)
+        d_kv = torch.empty((rr, n), dtype=torch.bfloat16, device=dev)
+        t_bf16 = timed(lambda: d_kv.copy_(h_bf16, non_blocking=True), reps=5)
+
+        def q_restore():
+            d_codes.copy_(h_codes, non_blocking=True)
+            d_sc.copy_(h_sc, non_blocking=True)
+            asr_kv_dequantize(d_codes, d_sc, d_kv, bits=bits)
+        t_q = timed(q_restore, reps=5)
+        out[f"int{bits}"] = {
+            "quantize_us": round(tq * 1e3, 1), "quantize_gbs": round(moved / tq / 1e6, 1),
+            "quantize_frac": round(moved / tq / 1e6 / peak, 3),
+            "dequantize_us": round(td * 1e3, 1), "dequantize_gbs": round(moved / td / 1e6, 1),
+            "dequantize_frac": round(moved / td / 1e6 / peak, 3),
+            "bytes_per_row": {"bf16": 2 * n, "codes": cb, "scale": 4},
+            "restore_105MB": {"bf16_h2d_us": round(t_bf16 * 1e3, 1), "quant_h2d_plus_dequant_us": round(t_q * 1e3, 1),
+                              "h2d_bytes_bf16": rr * 2 * n, "h2d_bytes_quant": rr * (cb + 4),
+                              "speedup": round(t_bf16 / t_q, 2)}}
+        del codes, h_bf16, h_codes, h_sc, d_codes, d_sc, d_kv
+    return out
+
+
 def replay_point(local_rank: int) -> dict:
     """NEXT-2: policy replay (asr_step_policy) of the all-cold trace for 1024 sequences at 8K context,
     K = 512 — Alg. 1 lines 3-15 + compaction for every sequence, no attention; sequence-steps per second
@@ -552,7 +617,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_asr(a, rank, world, local_rank)
     points = {}
-    for name in [x for x in a.points.split(",") if x and x not in ("sample", "replay")]:
+    for name in [x for x in a.points.split(",") if x and x not in ("sample", "replay", "quant")]:
         b = argparse.Namespace(**vars(a))
         for k, v in POINTS[name].items():
             setattr(b, k, v)
@@ -569,6 +634,8 @@ def main():
         line["detail"]["next_token_draw"] = sample_point(local_rank)
     if line is not None and world == 1 and "replay" in [x for x in a.points.split(",") if x]:
         line["detail"]["policy_replay"] = replay_point(local_rank)
+    if line is not None and world == 1 and "quant" in [x for x in a.points.split(",") if x]:
+        line["detail"]["frozen_tier_quant"] = quant_point(local_rank)
     if line is not None:
         if points:
             line["points"] = points

@@ -247,6 +247,29 @@ asr_status asr_step_policy(asr_ctx* ctx, const float* scores, const void* logits
 asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab, float temperature,
                       int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream);
 
+/* NEXT-4 (§Future Work, "hybrid compression combining ASR-KF-EGR with
+ * quantization methods"): the frozen tier stored quantised so a restore moves fewer bytes over the host
+ * link (row a5).  The paper fixes no scheme; the reading R-quant (oracle/quant.py):
+ *   a row = one head vector (token, layer, K|V, KV head) of row_elems = head_dim bf16 values, i.e. the
+ *   frozen tier [token][L][2][Hkv][d] is rows = tokens * L * 2 * Hkv rows of d;
+ *   qmax = 2^(bits-1) - 1 (127 or 7); scale = max|x| / qmax (IEEE fp32 division, round to nearest);
+ *   code = clamp(rint(x / scale), -qmax, qmax) (x / scale an IEEE fp32 division, rint half-to-even),
+ *   all codes 0 when scale = 0;  dequantised x' = bf16_rn(fp32(code) * scale).
+ * asr_kv_quantize: kv [rows][row_elems] bf16 (device, 16-byte aligned) -> codes (device) [rows][row_elems]
+ *   int8 for bits = 8 (8-byte aligned), or [rows][row_elems / 2] bytes for bits = 4 (4-byte aligned;
+ *   element 2i in the low nibble, 2i+1 in the high nibble, 4-bit two's complement), and scales[rows]
+ *   fp32 (device).
+ * asr_kv_dequantize: the inverse map, codes + scales -> kv [rows][row_elems] bf16 (device).
+ * row_elems in {8, 16, 32, 64, 128, 256}; bits in {8, 4}; rows in [0, 2^40] (0: no-op).  Stateless,
+ * asynchronous on cuda_stream, bitwise deterministic.  Buffers are the caller's (ranges must not
+ * overlap).  Rows holding non-finite values get unspecified codes (the KV cache is finite).
+ * Errors: ASR_E_INVALID for a NULL or misaligned pointer or an argument out of range (nothing is
+ * launched); launch failures as ASR_E_CUDA. */
+asr_status asr_kv_quantize(const void* kv, int64_t rows, int32_t row_elems, int32_t bits, void* codes, float* scales,
+                           void* cuda_stream);
+asr_status asr_kv_dequantize(const void* codes, const float* scales, int64_t rows, int32_t row_elems, int32_t bits,
+                             void* kv, void* cuda_stream);
+
 /* Synchronise and free everything the context owns. */
 asr_status asr_destroy(asr_ctx* ctx);
 

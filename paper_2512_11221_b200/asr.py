@@ -71,7 +71,7 @@ class asr_ledger_view(ctypes.Structure):
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
            "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
            "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-           "asr_time_attention", "asr_sample", "asr_step_policy")
+           "asr_time_attention", "asr_sample", "asr_step_policy", "asr_kv_quantize", "asr_kv_dequantize")
 
 _lib = None
 
@@ -104,10 +104,13 @@ def lib() -> ctypes.CDLL:
         L.asr_time_attention.argtypes = [vp, i32, vp]
         L.asr_sample.argtypes = [vp, i32, i32, i32, ctypes.c_float, i32, ctypes.c_float, vp, vp, vp]
         L.asr_step_policy.argtypes = [vp, vp, vp, i32, vp, vp]
+        L.asr_kv_quantize.argtypes = [vp, ctypes.c_int64, i32, i32, vp, vp, vp]
+        L.asr_kv_dequantize.argtypes = [vp, vp, ctypes.c_int64, i32, i32, vp, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
                   "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
                   "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-                  "asr_time_attention", "asr_sample", "asr_step_policy"):
+                  "asr_time_attention", "asr_sample", "asr_step_policy", "asr_kv_quantize",
+                  "asr_kv_dequantize"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
         L.asr_last_error.restype = ctypes.c_char_p
@@ -310,6 +313,26 @@ def asr_sample(logits, uniforms, token_out, temperature: float = 1.0, top_k: int
     _check(lib().asr_sample(ctypes.c_void_p(logits.data_ptr()), dt, B, V, float(temperature), int(top_k),
                             float(top_p), ctypes.c_void_p(uniforms.data_ptr()), ctypes.c_void_p(token_out.data_ptr()),
                             _stream(stream)))
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def asr_kv_quantize(kv, codes, scales, bits: int = 8, stream=None) -> None:
+    """NEXT-4 frozen-tier quantisation (include/asr.h asr_kv_quantize): kv [..., n] bf16 (rows = all
+    leading dims), codes [rows][n] int8 (bits 8) or [rows][n/2] uint8 (bits 4), scales [rows] fp32 —
+    CUDA tensors (torch) of the caller."""
+    n = kv.shape[-1]
+    rows = kv.numel() // n if n else 0
+    _check(lib().asr_kv_quantize(_ptr(kv), rows, n, int(bits), _ptr(codes), _ptr(scales), _stream(stream)))
+
+
+def asr_kv_dequantize(codes, scales, kv, bits: int = 8, stream=None) -> None:
+    """NEXT-4 inverse map (include/asr.h asr_kv_dequantize): codes + scales -> kv [..., n] bf16."""
+    n = kv.shape[-1]
+    rows = kv.numel() // n if n else 0
+    _check(lib().asr_kv_dequantize(_ptr(codes), _ptr(scales), rows, n, int(bits), _ptr(kv), _stream(stream)))
 
 
 def asr_time_attention(ctx, reps: int, stream=None) -> None:

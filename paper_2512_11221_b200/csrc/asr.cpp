@@ -1117,6 +1117,38 @@ asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, i
   return ASR_OK;
 }
 
+static bool aligned(const void* p, uintptr_t a) { return ((uintptr_t)p & (a - 1)) == 0; }
+
+static asr_status kvq_check(const char* fn, const void* kv, int64_t rows, int32_t n, int32_t bits, const void* codes,
+                            const void* scales) {
+  const std::string f(fn);
+  if (!kv || !codes || !scales) return fail(ASR_E_INVALID, f + ": NULL pointer");
+  if (rows < 0 || rows > ((int64_t)1 << 40)) return fail(ASR_E_INVALID, f + ": rows out of range [0, 2^40]");
+  if (n != 8 && n != 16 && n != 32 && n != 64 && n != 128 && n != 256)
+    return fail(ASR_E_INVALID, f + ": row_elems must be one of 8, 16, 32, 64, 128, 256");
+  if (bits != 8 && bits != 4) return fail(ASR_E_INVALID, f + ": bits must be 8 or 4");
+  if (!aligned(kv, 16) || !aligned(codes, bits == 8 ? 8 : 4) || !aligned(scales, 4))
+    return fail(ASR_E_INVALID, f + ": misaligned pointer (kv 16 B, codes 8 B (INT8) / 4 B (INT4), scales 4 B)");
+  return ASR_OK;
+}
+
+asr_status asr_kv_quantize(const void* kv, int64_t rows, int32_t row_elems, int32_t bits, void* codes, float* scales,
+                           void* cuda_stream) {
+  const asr_status st = kvq_check("asr_kv_quantize", kv, rows, row_elems, bits, codes, scales);
+  if (st != ASR_OK) return st;
+  CUDA_TRY(asr::launch_kv_quantize(kv, (long)rows, row_elems, bits, (int8_t*)codes, scales, (cudaStream_t)cuda_stream));
+  return ASR_OK;
+}
+
+asr_status asr_kv_dequantize(const void* codes, const float* scales, int64_t rows, int32_t row_elems, int32_t bits,
+                             void* kv, void* cuda_stream) {
+  const asr_status st = kvq_check("asr_kv_dequantize", kv, rows, row_elems, bits, codes, scales);
+  if (st != ASR_OK) return st;
+  CUDA_TRY(asr::launch_kv_dequantize((const int8_t*)codes, scales, (long)rows, row_elems, bits, kv,
+                                     (cudaStream_t)cuda_stream));
+  return ASR_OK;
+}
+
 asr_status asr_set_profile(asr_ctx* c, int32_t on) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
   c->cfg.profile_stages = on ? 1 : 0;

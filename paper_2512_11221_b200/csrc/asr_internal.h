@@ -239,6 +239,10 @@ void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: 
 int attention_grid(const DevState& s, int num_sms);
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
                           float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st);   // NEXT-1
+cudaError_t launch_kv_quantize(const void* kv, long rows, int n, int bits, int8_t* codes, float* scales,
+                               cudaStream_t st);   // NEXT-4
+cudaError_t launch_kv_dequantize(const int8_t* codes, const float* scales, long rows, int n, int bits, void* kv,
+                                 cudaStream_t st);  // NEXT-4
 bool attention_mma_supported(const DevState& s);   // bf16, d=128, 1/2/4/8 KV heads, <= 4 (8) q heads per KV head
 cudaError_t attention_mma_prepare();               // opt-in to > 48 KiB dynamic shared memory
 void attention_mma_launch_shape(const DevState& s, bool logits_f32, const void** func, int* threads, unsigned* smem);

@@ -109,3 +109,27 @@ def test_sample_invalid_arguments_rejected(args):
                               a["top_p"], a["uniforms"], a["token_out"], None)
     assert rc == asr.ASR_E_INVALID
     assert asr.lib().asr_last_error()
+
+
+@pytest.mark.parametrize("fn,args", [
+    (f, a) for f in ("asr_kv_quantize", "asr_kv_dequantize") for a in (
+        dict(kv=None), dict(codes=None), dict(scales=None), dict(rows=-1), dict(rows=(1 << 40) + 1), dict(n=0),
+        dict(n=48), dict(n=512), dict(bits=2), dict(bits=16), dict(kv=ctypes.c_void_p(24)),
+        dict(codes=ctypes.c_void_p(20)), dict(bits=4, codes=ctypes.c_void_p(18)), dict(scales=ctypes.c_void_p(18)))])
+def test_kv_quant_invalid_arguments_rejected(fn, args):
+    """asr_kv_quantize / asr_kv_dequantize (NEXT-4) validate before touching the device: ASR_E_INVALID."""
+    p = ctypes.c_void_p(256)   # never dereferenced: validation fails first
+    a = dict(kv=p, rows=1024, n=128, bits=8, codes=p, scales=p)
+    a.update(args)
+    if fn == "asr_kv_quantize":
+        rc = asr.lib().asr_kv_quantize(a["kv"], a["rows"], a["n"], a["bits"], a["codes"], a["scales"], None)
+    else:
+        rc = asr.lib().asr_kv_dequantize(a["codes"], a["scales"], a["rows"], a["n"], a["bits"], a["kv"], None)
+    assert rc == asr.ASR_E_INVALID
+    assert asr.lib().asr_last_error()
+
+
+def test_kv_quant_zero_rows_is_a_noop():
+    p = ctypes.c_void_p(256)
+    assert asr.lib().asr_kv_quantize(p, 0, 128, 8, p, p, None) == 0
+    assert asr.lib().asr_kv_dequantize(p, p, 0, 128, 4, p, None) == 0
