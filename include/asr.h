@@ -256,7 +256,7 @@ asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, i
  *   code = clamp(rint(x / scale), -qmax, qmax) (x / scale an IEEE fp32 division, rint half-to-even),
  *   all codes 0 when scale = 0;  dequantised x' = bf16_rn(fp32(code) * scale).
  * asr_kv_quantize: kv [rows][row_elems] bf16 (device, 16-byte aligned) -> codes (device) [rows][row_elems]
- *   int8 for bits = 8 (8-byte aligned), or [rows][row_elems / 2] bytes for bits = 4 (4-byte aligned;
+ *   int8 for bits = 8, or [rows][row_elems / 2] bytes for bits = 4 (16-byte aligned either way;
  *   element 2i in the low nibble, 2i+1 in the high nibble, 4-bit two's complement), and scales[rows]
  *   fp32 (device).
  * asr_kv_dequantize: the inverse map, codes + scales -> kv [rows][row_elems] bf16 (device).

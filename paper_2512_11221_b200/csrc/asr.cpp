@@ -1127,8 +1127,8 @@ static asr_status kvq_check(const char* fn, const void* kv, int64_t rows, int32_
   if (n != 8 && n != 16 && n != 32 && n != 64 && n != 128 && n != 256)
     return fail(ASR_E_INVALID, f + ": row_elems must be one of 8, 16, 32, 64, 128, 256");
   if (bits != 8 && bits != 4) return fail(ASR_E_INVALID, f + ": bits must be 8 or 4");
-  if (!aligned(kv, 16) || !aligned(codes, bits == 8 ? 8 : 4) || !aligned(scales, 4))
-    return fail(ASR_E_INVALID, f + ": misaligned pointer (kv 16 B, codes 8 B (INT8) / 4 B (INT4), scales 4 B)");
+  if (!aligned(kv, 16) || !aligned(codes, 16) || !aligned(scales, 4))
+    return fail(ASR_E_INVALID, f + ": misaligned pointer (kv and codes 16 B, scales 4 B)");
   return ASR_OK;
 }
 
