@@ -315,24 +315,24 @@ def asr_sample(logits, uniforms, token_out, temperature: float = 1.0, top_k: int
                             _stream(stream)))
 
 
-def _ptr(t):
-    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
-
-
 def asr_kv_quantize(kv, codes, scales, bits: int = 8, stream=None) -> None:
     """NEXT-4 frozen-tier quantisation (include/asr.h asr_kv_quantize): kv [..., n] bf16 (rows = all
     leading dims), codes [rows][n] int8 (bits 8) or [rows][n/2] uint8 (bits 4), scales [rows] fp32 —
     CUDA tensors (torch) of the caller."""
     n = kv.shape[-1]
     rows = kv.numel() // n if n else 0
-    _check(lib().asr_kv_quantize(_ptr(kv), rows, n, int(bits), _ptr(codes), _ptr(scales), _stream(stream)))
+    _check(lib().asr_kv_quantize(_vp(kv), rows, n, int(bits), _vp(codes), _vp(scales), _stream(stream)))
 
 
 def asr_kv_dequantize(codes, scales, kv, bits: int = 8, stream=None) -> None:
     """NEXT-4 inverse map (include/asr.h asr_kv_dequantize): codes + scales -> kv [..., n] bf16."""
     n = kv.shape[-1]
     rows = kv.numel() // n if n else 0
-    _check(lib().asr_kv_dequantize(_ptr(codes), _ptr(scales), rows, n, int(bits), _ptr(kv), _stream(stream)))
+    _check(lib().asr_kv_dequantize(_vp(codes), _vp(scales), rows, n, int(bits), _vp(kv), _stream(stream)))
+
+
+def _vp(x) -> ctypes.c_void_p:
+    return ctypes.c_void_p(_ptr(x))
 
 
 def asr_time_attention(ctx, reps: int, stream=None) -> None:
