@@ -133,3 +133,12 @@ def test_kv_quant_zero_rows_is_a_noop():
     p = ctypes.c_void_p(256)
     assert asr.lib().asr_kv_quantize(p, 0, 128, 8, p, p, None) == 0
     assert asr.lib().asr_kv_dequantize(p, p, 0, 128, 4, p, None) == 0
+
+
+def test_binding_has_no_shadowed_definitions():
+    """Every top-level name of the ctypes binding is defined once (a second helper of the same name once
+    silently replaced the first and broke numpy host-memory I/O)."""
+    import ast
+    tree = ast.parse(open(asr.__file__).read())
+    names = [n.name for n in tree.body if isinstance(n, (ast.FunctionDef, ast.ClassDef))]
+    assert len(names) == len(set(names)), sorted({n for n in names if names.count(n) > 1})
