@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import os
+import threading
 
 import numpy as np
 
@@ -55,31 +56,38 @@ class GenParams:
 
 _host = None
 _dev = None
+_lock = threading.Lock()
 
 
 def host_lib() -> ctypes.CDLL:
+    """Thread-safe loader: configured on a local, published last (under a lock)."""
     global _host
-    if _host is None:
+    if _host is not None:
+        return _host
+    with _lock:
+        if _host is not None:
+            return _host
         path = os.path.join(_HERE, "libasrgen_host.so")
-        if not os.path.exists(path):
-            import sys
+        import sys
+        if os.path.dirname(_HERE) not in sys.path:
             sys.path.insert(0, os.path.dirname(_HERE))
-            from tools.build import build_gen_host
-            build_gen_host()
-        _host = ctypes.CDLL(path)
+        from tools.build import build_gen_host
+        build_gen_host()
+        L = ctypes.CDLL(path)
         P = ctypes.POINTER(_Params)
         vp, ci = ctypes.c_void_p, ctypes.c_int
-        _host.asrgen_host_kv.argtypes = [P, ci, ci, ci, vp, vp, ci]
-        _host.asrgen_host_q.argtypes = [P, ci, ci, vp, ci]
-        _host.asrgen_host_logits.argtypes = [P, ci, ci, vp, ci]
+        L.asrgen_host_kv.argtypes = [P, ci, ci, ci, vp, vp, ci]
+        L.asrgen_host_q.argtypes = [P, ci, ci, vp, ci]
+        L.asrgen_host_logits.argtypes = [P, ci, ci, vp, ci]
         for f in ("asrgen_host_is_hot", "asrgen_host_is_needle", "asrgen_host_peak_index"):
-            getattr(_host, f).argtypes = [P, ci, ci]
-            getattr(_host, f).restype = ci
+            getattr(L, f).argtypes = [P, ci, ci]
+            getattr(L, f).restype = ci
         for f in ("asrgen_host_is_query_step", "asrgen_host_is_spike_step"):
-            getattr(_host, f).argtypes = [P, ci]
-            getattr(_host, f).restype = ci
-        _host.asrgen_host_mix.argtypes = [ctypes.c_uint64]
-        _host.asrgen_host_mix.restype = ctypes.c_uint64
+            getattr(L, f).argtypes = [P, ci]
+            getattr(L, f).restype = ci
+        L.asrgen_host_mix.argtypes = [ctypes.c_uint64]
+        L.asrgen_host_mix.restype = ctypes.c_uint64
+        _host = L
     return _host
 
 
@@ -144,18 +152,23 @@ def bf16_to_f32(a: np.ndarray) -> np.ndarray:
 
 def dev_lib() -> ctypes.CDLL:
     global _dev
-    if _dev is None:
+    if _dev is not None:
+        return _dev
+    with _lock:
+        if _dev is not None:
+            return _dev
         path = os.path.join(_HERE, "libasrgen_dev.so")
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run `python tools/build.py` (needs nvcc)")
-        _dev = ctypes.CDLL(path)
+        L = ctypes.CDLL(path)
         P = ctypes.POINTER(_Params)
         vp, ci = ctypes.c_void_p, ctypes.c_int
-        _dev.asrgen_dev_kv.argtypes = [P, ci, vp, ci, ci, vp, vp, ci, vp]
-        _dev.asrgen_dev_q.argtypes = [P, ci, ci, vp, ci, vp]
-        _dev.asrgen_dev_logits.argtypes = [P, ci, ci, vp, ci, vp]
+        L.asrgen_dev_kv.argtypes = [P, ci, vp, ci, ci, vp, vp, ci, vp]
+        L.asrgen_dev_q.argtypes = [P, ci, ci, vp, ci, vp]
+        L.asrgen_dev_logits.argtypes = [P, ci, ci, vp, ci, vp]
         for f in ("asrgen_dev_kv", "asrgen_dev_q", "asrgen_dev_logits"):
-            getattr(_dev, f).restype = ci
+            getattr(L, f).restype = ci
+        _dev = L
     return _dev
 
 

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import os
+import threading
 
 import numpy as np
 
@@ -69,38 +70,47 @@ class OrcCfg:
 
 
 _lib = None
+_lib_lock = threading.Lock()
 
 
 def lib() -> ctypes.CDLL:
+    """Load (building first if stale) liborc.so.  Thread-safe: the CDLL is fully configured on a
+    local and published last, under a lock, so no caller ever sees it without its argtypes."""
     global _lib
-    if _lib is None:
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
         path = os.path.join(_HERE, "liborc.so")
         import sys
-        sys.path.insert(0, os.path.dirname(_HERE))
+        if os.path.dirname(_HERE) not in sys.path:
+            sys.path.insert(0, os.path.dirname(_HERE))
         from tools.build import build_oracle
         build_oracle()
-        _lib = ctypes.CDLL(path)
+        L = ctypes.CDLL(path)
         vp, ci = ctypes.c_void_p, ctypes.c_int
         C, O = ctypes.POINTER(_Cfg), ctypes.POINTER(_Out)
-        _lib.orc_seq_new.argtypes = [C, ci, ci]
-        _lib.orc_seq_new.restype = vp
-        _lib.orc_seq_free.argtypes = [vp]
-        _lib.orc_step.argtypes = [vp, vp, ci, vp, vp, ci, vp, ci, vp, vp, vp, O]
-        _lib.orc_step.restype = ci
-        _lib.orc_step_policy.argtypes = [vp, vp, ctypes.c_double, ci, vp, O]
-        _lib.orc_step_policy.restype = ci
-        _lib.orc_restore.argtypes = [vp, ci]
-        _lib.orc_restore.restype = ci
-        _lib.orc_n.argtypes = [vp]
-        _lib.orc_n.restype = ci
-        _lib.orc_ledger.argtypes = [vp, vp, vp, vp, vp]
-        _lib.orc_duration.argtypes = [ctypes.c_uint32, ctypes.c_double]
-        _lib.orc_duration.restype = ci
-        _lib.orc_entropy.argtypes = [vp, ci, ci, ctypes.c_double]
-        _lib.orc_entropy.restype = ctypes.c_double
-        _lib.orc_attend_head.argtypes = [vp, ci, vp, vp, ci, ci, ci, vp]
-        _lib.orc_score_token.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, ci]
-        _lib.orc_score_token.restype = ctypes.c_double
+        L.orc_seq_new.argtypes = [C, ci, ci]
+        L.orc_seq_new.restype = vp
+        L.orc_seq_free.argtypes = [vp]
+        L.orc_step.argtypes = [vp, vp, ci, vp, vp, ci, vp, ci, vp, vp, vp, O]
+        L.orc_step.restype = ci
+        L.orc_step_policy.argtypes = [vp, vp, ctypes.c_double, ci, vp, O]
+        L.orc_step_policy.restype = ci
+        L.orc_restore.argtypes = [vp, ci]
+        L.orc_restore.restype = ci
+        L.orc_n.argtypes = [vp]
+        L.orc_n.restype = ci
+        L.orc_ledger.argtypes = [vp, vp, vp, vp, vp]
+        L.orc_duration.argtypes = [ctypes.c_uint32, ctypes.c_double]
+        L.orc_duration.restype = ci
+        L.orc_entropy.argtypes = [vp, ci, ci, ctypes.c_double]
+        L.orc_entropy.restype = ctypes.c_double
+        L.orc_attend_head.argtypes = [vp, ci, vp, vp, ci, ci, ci, vp]
+        L.orc_score_token.argtypes = [vp, ci, vp, ci, ci, ci, ci, ci, ci]
+        L.orc_score_token.restype = ctypes.c_double
+        _lib = L
     return _lib
 
 

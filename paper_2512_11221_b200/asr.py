@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import os
+import threading
 
 import numpy as np
 
@@ -74,12 +75,18 @@ EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_
            "asr_time_attention", "asr_sample", "asr_step_policy", "asr_kv_quantize", "asr_kv_dequantize")
 
 _lib = None
+_lib_lock = threading.Lock()
 
 
 def lib() -> ctypes.CDLL:
-    """Load libasr.so (raises if it was not built: there is no fallback)."""
+    """Load libasr.so (raises if it was not built: there is no fallback).  Thread-safe: configured on
+    a local, published last."""
     global _lib
-    if _lib is None:
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} not built: run `python tools/build.py` (needs nvcc, sm_100a)")
         L = ctypes.CDLL(LIB_PATH)
@@ -169,10 +176,43 @@ def _ptr(x) -> int | None:
     if x is None:
         return None
     if isinstance(x, np.ndarray):
-        assert x.flags["C_CONTIGUOUS"]
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
         return x.ctypes.data
-    assert x.is_contiguous(), "tensors must be contiguous"
+    if not x.is_contiguous():
+        raise ValueError("tensors must be contiguous")
     return x.data_ptr()
+
+
+_KIND = {"bf16": ("bfloat16", (np.uint16,)), "f32": ("float32", (np.float32,)), "i32": ("int32", (np.int32,)),
+         "i8": ("int8", (np.int8, np.uint8)), "u8": ("uint8", (np.uint8, np.int8))}
+
+
+def _arg(name: str, x, kinds, shape=None, host: bool | None = None, device: int | None = None):
+    """Validate one caller buffer before its pointer crosses the C ABI (no asserts: survives -O).
+    kinds: allowed element kinds (keys of _KIND); shape: exact shape, or a leading-dims prefix given as
+    (..., n) tuples of ints where None matches anything; host: None = either memory kind."""
+    if x is None:
+        raise ValueError(f"{name}: missing")
+    if isinstance(x, np.ndarray):
+        ok = any(x.dtype == np.dtype(t) for k in kinds for t in _KIND[k][1])
+        is_host = True
+    else:
+        import torch
+        ok = any(x.dtype == getattr(torch, _KIND[k][0]) for k in kinds)
+        is_host = not x.is_cuda
+        if not is_host and device is not None and x.device.index != device:
+            raise ValueError(f"{name}: on cuda:{x.device.index}, the context is on cuda:{device}")
+    if not ok:
+        raise ValueError(f"{name}: dtype {x.dtype} not in {kinds}")
+    if host is not None and is_host != host:
+        raise ValueError(f"{name}: expected {'host' if host else 'device'} memory")
+    if shape is not None:
+        xs = tuple(x.shape)
+        if len(xs) != len(shape) or any(w is not None and w != h for w, h in zip(shape, xs)):
+            raise ValueError(f"{name}: shape {xs}, expected {tuple('*' if w is None else w for w in shape)}")
+    _ptr(x)
+    return x
 
 
 def _is_host(x) -> bool:
@@ -202,24 +242,40 @@ def asr_create(cfg: Config, prompt_k, prompt_v, prompt_len, stream=None) -> ctyp
     out = ctypes.c_void_p()
     _check(lib().asr_create(ctypes.byref(c), _ptr(prompt_k), _ptr(prompt_v), pl.ctypes.data, stride, mem,
                             _stream(stream), ctypes.byref(out)))
+    _CFGS[out.value] = cfg
     return out
 
 
+_CFGS: dict = {}   # ctx handle value -> Config (for argument validation)
+
+
+def _io(ctx, q, k_new, v_new, o, logits_prev, entropy):
+    cfg = _CFGS.get(ctx.value if isinstance(ctx, ctypes.c_void_p) else ctx)
+    host = _is_host(q)
+    if cfg is not None:
+        B, L, Hq, Hkv, d = cfg.batch, cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+        kv = ["bf16"] if cfg.kv_dtype == KV_BF16 else ["f32"]
+        dev = None if host else cfg.device
+        _arg("q", q, kv, (B, L, Hq, d), host, dev)
+        _arg("k_new", k_new, kv, (B, L, Hkv, d), host, dev)
+        _arg("v_new", v_new, kv, (B, L, Hkv, d), host, dev)
+        _arg("o", o, ["f32"], (B, L, Hq, d), host, dev)
+        if logits_prev is not None:
+            _arg("logits_prev", logits_prev, ["bf16", "f32"], (B, cfg.vocab), host, dev)
+        if entropy is not None:
+            _arg("entropy", entropy, ["f32"], (B,), host, dev)
+    return asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
+                       _dtype_code(logits_prev) if logits_prev is not None else 0,
+                       MEM_HOST if host else MEM_DEVICE, _ptr(o), _ptr(entropy))
+
+
 def asr_step(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None) -> None:
-    io = asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
-                     _dtype_code(logits_prev) if logits_prev is not None else 0,
-                     MEM_HOST if _is_host(q) else MEM_DEVICE, _ptr(o), _ptr(entropy))
+    io = _io(ctx, q, k_new, v_new, o, logits_prev, entropy)
     _check(lib().asr_step(ctx, ctypes.byref(io), _stream(stream)))
 
 
-def _io(q, k_new, v_new, o, logits_prev, entropy):
-    return asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
-                       _dtype_code(logits_prev) if logits_prev is not None else 0,
-                       MEM_HOST if _is_host(q) else MEM_DEVICE, _ptr(o), _ptr(entropy))
-
-
 def asr_step_attend(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None) -> None:
-    io = _io(q, k_new, v_new, o, logits_prev, entropy)
+    io = _io(ctx, q, k_new, v_new, o, logits_prev, entropy)
     _check(lib().asr_step_attend(ctx, ctypes.byref(io), _stream(stream)))
 
 
@@ -308,7 +364,10 @@ def asr_sample(logits, uniforms, token_out, temperature: float = 1.0, top_k: int
     """NEXT-1 next-token draw (include/asr.h asr_sample): logits [B][V] bf16/fp32, uniforms [B] fp32,
     token_out [B] int32 — CUDA tensors (torch) of the caller."""
     import torch
+    _arg("logits", logits, ["bf16", "f32"], (None, None), False)
     B, V = logits.shape
+    _arg("uniforms", uniforms, ["f32"], (B,), False, logits.device.index)
+    _arg("token_out", token_out, ["i32"], (B,), False, logits.device.index)
     dt = KV_BF16 if logits.dtype == torch.bfloat16 else KV_F32
     _check(lib().asr_sample(ctypes.c_void_p(logits.data_ptr()), dt, B, V, float(temperature), int(top_k),
                             float(top_p), ctypes.c_void_p(uniforms.data_ptr()), ctypes.c_void_p(token_out.data_ptr()),
@@ -321,6 +380,9 @@ def asr_kv_quantize(kv, codes, scales, bits: int = 8, stream=None) -> None:
     CUDA tensors (torch) of the caller."""
     n = kv.shape[-1]
     rows = kv.numel() // n if n else 0
+    _arg("kv", kv, ["bf16"], None, False)
+    _arg("codes", codes, ["i8", "u8"], (rows, n if bits == 8 else n // 2), False, kv.device.index)
+    _arg("scales", scales, ["f32"], (rows,), False, kv.device.index)
     _check(lib().asr_kv_quantize(_vp(kv), rows, n, int(bits), _vp(codes), _vp(scales), _stream(stream)))
 
 
@@ -328,6 +390,9 @@ def asr_kv_dequantize(codes, scales, kv, bits: int = 8, stream=None) -> None:
     """NEXT-4 inverse map (include/asr.h asr_kv_dequantize): codes + scales -> kv [..., n] bf16."""
     n = kv.shape[-1]
     rows = kv.numel() // n if n else 0
+    _arg("kv", kv, ["bf16"], None, False)
+    _arg("codes", codes, ["i8", "u8"], (rows, n if bits == 8 else n // 2), False, kv.device.index)
+    _arg("scales", scales, ["f32"], (rows,), False, kv.device.index)
     _check(lib().asr_kv_dequantize(_vp(codes), _vp(scales), rows, n, int(bits), _vp(kv), _stream(stream)))
 
 
@@ -340,6 +405,7 @@ def asr_time_attention(ctx, reps: int, stream=None) -> None:
 
 
 def asr_destroy(ctx) -> None:
+    _CFGS.pop(ctx.value if isinstance(ctx, ctypes.c_void_p) else ctx, None)
     _check(lib().asr_destroy(ctx))
 
 
@@ -389,7 +455,12 @@ class Context:
     def step_policy(self, scores, logits_prev=None, entropy=None, stream=None):
         """NEXT-2 policy replay step: scores [B][max_context] fp32 (CUDA tensor) instead of attention."""
         import torch
-        lg = None if logits_prev is None else logits_prev
+        c = self.cfg
+        _arg("scores", scores, ["f32"], (c.batch, c.max_context), False, c.device)
+        lg = None if logits_prev is None else _arg("logits_prev", logits_prev, ["bf16", "f32"],
+                                                   (c.batch, c.vocab), False, c.device)
+        if entropy is not None:
+            _arg("entropy", entropy, ["f32"], (c.batch,), False, c.device)
         dt = 0 if lg is None or lg.dtype == torch.bfloat16 else 1
         _check(lib().asr_step_policy(self._h, ctypes.c_void_p(scores.data_ptr()),
                                      None if lg is None else ctypes.c_void_p(lg.data_ptr()), dt,

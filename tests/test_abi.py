@@ -142,3 +142,47 @@ def test_binding_has_no_shadowed_definitions():
     tree = ast.parse(open(asr.__file__).read())
     names = [n.name for n in tree.body if isinstance(n, (ast.FunctionDef, ast.ClassDef))]
     assert len(names) == len(set(names)), sorted({n for n in names if names.count(n) > 1})
+
+
+def test_binding_validates_buffers_before_the_abi():
+    """The binding rejects wrong dtypes / shapes / memory kinds with ValueError (not assert: it must
+    survive python -O) before any pointer reaches the library (an fp16 logits row or a
+    bf16 `o` would otherwise be read / written out of bounds)."""
+    import numpy as np
+    import torch
+    cfg = asr.Config(n_layers=2, n_q_heads=4, n_kv_heads=2, head_dim=16, batch=3, max_context=64, vocab=100)
+    h = ctypes.c_void_p(0xDEAD0)
+    asr._CFGS[h.value] = cfg
+    try:
+        bf, f32 = torch.bfloat16, torch.float32
+        q = torch.zeros(3, 2, 4, 16, dtype=bf)
+        kn = torch.zeros(3, 2, 2, 16, dtype=bf)
+        o = torch.zeros(3, 2, 4, 16, dtype=f32)
+        lg = torch.zeros(3, 100, dtype=bf)
+        ent = torch.zeros(3, dtype=f32)
+        io = asr._io(h, q, kn, kn, o, lg, ent)          # all valid (host memory)
+        assert io.memory == asr.MEM_HOST and io.logits_dtype == asr.KV_BF16
+        bad = [
+            dict(q=q.to(torch.float16)),                  # wrong KV dtype
+            dict(o=o.to(bf)),                             # bf16 o would be written as fp32
+            dict(o=torch.zeros(3, 2, 4, 8, dtype=f32)),   # undersized o
+            dict(logits_prev=lg.to(torch.float16)),       # fp16 logits read as fp32
+            dict(logits_prev=torch.zeros(3, 99, dtype=bf)),
+            dict(entropy=torch.zeros(2, dtype=f32)),
+            dict(k_new=torch.zeros(3, 2, 4, 16, dtype=bf)),   # Hq heads instead of Hkv
+            dict(q=torch.zeros(3, 2, 16, 4, dtype=bf).transpose(2, 3)),   # non-contiguous
+        ]
+        for kw in bad:
+            a = dict(q=q, k_new=kn, v_new=kn, o=o, logits_prev=lg, entropy=ent)
+            a.update(kw)
+            with pytest.raises(ValueError):
+                asr._io(h, **a)
+        # numpy host buffers: bf16 as uint16 bits
+        qn = np.zeros((3, 2, 4, 16), np.uint16)
+        asr._io(h, qn, np.zeros((3, 2, 2, 16), np.uint16), np.zeros((3, 2, 2, 16), np.uint16),
+                np.zeros((3, 2, 4, 16), np.float32), None, None)
+        with pytest.raises(ValueError):
+            asr._io(h, qn, np.zeros((3, 2, 2, 16), np.uint16), np.zeros((3, 2, 2, 16), np.uint16),
+                    np.zeros((3, 2, 4, 16), np.float64), None, None)
+    finally:
+        asr._CFGS.pop(h.value, None)

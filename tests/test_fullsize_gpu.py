@@ -40,6 +40,7 @@ def _oracle_replay(g, b, steps, tau, max_ctx, W):
     below = cold if tau > 0 else np.zeros_like(cold)   # scores are >= 0: nothing is below tau <= 0
     def H(i):
         return oracle.entropy(gen.logits(g, b, i - 1))
+    oracle.lib(), gen.host_lib()   # load both libraries in this thread, before the pool
     with ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:   # ctypes calls drop the GIL
         Hs = [None] + list(ex.map(H, range(1, steps)))
     cfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=WINDOW, tau=tau, softness=SOFT, history_window=W)

@@ -9,14 +9,39 @@ Each target is rebuilt only when one of its sources is newer than the .so.
 """
 from __future__ import annotations
 
+import contextlib
+import fcntl
 import glob
 import os
 import subprocess
 import sys
+import threading
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+_TLOCK = threading.Lock()
+
+
+@contextlib.contextmanager
+def _locked():
+    """Serialise builds across threads (pytest workers) and processes (torchrun ranks)."""
+    with _TLOCK:
+        os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+        with open(os.path.join(ROOT, "build", ".lock"), "w") as f:
+            fcntl.flock(f, fcntl.LOCK_EX)
+            try:
+                yield
+            finally:
+                fcntl.flock(f, fcntl.LOCK_UN)
+
+
+def _tmp(out: str) -> str:
+    """Every target is linked to a private temp path and os.replace()d into place, so a concurrent
+    dlopen never sees a half-written file."""
+    return f"{out}.tmp.{os.getpid()}.{threading.get_ident()}"
 
 
 def _stale(out: str, srcs: list[str]) -> bool:
@@ -36,26 +61,32 @@ def _run(cmd: list[str]) -> None:
 def build_gen_host(force: bool = False) -> str:
     out = os.path.join(ROOT, "gen", "libasrgen_host.so")
     srcs = [os.path.join(ROOT, "gen", f) for f in ("asrgen.h", "asrgen_host.c")]
-    if force or _stale(out, srcs):
-        _run(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", out, srcs[1]])
+    with _locked():
+        if force or _stale(out, srcs):
+            _run(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", _tmp(out), srcs[1]])
+            os.replace(_tmp(out), out)
     return out
 
 
 def build_oracle(force: bool = False) -> str:
     out = os.path.join(ROOT, "oracle", "liborc.so")
     srcs = [os.path.join(ROOT, "oracle", f) for f in ("orc.h", "orc.c")]
-    if force or _stale(out, srcs):
-        _run(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
-              "-o", out, srcs[1], "-lm"])
+    with _locked():
+        if force or _stale(out, srcs):
+            _run(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-ffp-contract=off", "-shared", "-fPIC",
+                  "-o", _tmp(out), srcs[1], "-lm"])
+            os.replace(_tmp(out), out)
     return out
 
 
 def build_gen_dev(force: bool = False) -> str:
     out = os.path.join(ROOT, "gen", "libasrgen_dev.so")
     srcs = [os.path.join(ROOT, "gen", f) for f in ("asrgen.h", "asrgen_dev.cu")]
-    if force or _stale(out, srcs):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-cudart", "shared", "-Xcompiler", "-fPIC",
-              "-o", out, srcs[1]])
+    with _locked():
+        if force or _stale(out, srcs):
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-shared", "-cudart", "shared", "-Xcompiler", "-fPIC",
+                  "-o", _tmp(out), srcs[1]])
+            os.replace(_tmp(out), out)
     return out
 
 
@@ -71,6 +102,11 @@ def _nccl_include() -> str:
 
 
 def build_asr(force: bool = False) -> str:
+    with _locked():
+        return _build_asr(force)
+
+
+def _build_asr(force: bool) -> str:
     pkg = os.path.join(ROOT, "paper_2512_11221_b200")
     out = os.path.join(pkg, "libasr.so")
     csrc = os.path.join(pkg, "csrc")
@@ -94,7 +130,8 @@ def build_asr(force: bool = False) -> str:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         _run([NVCC, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", *common, "-I", nccl_inc, "-c", s, "-o", o])
         objs.append(o)
-    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", out, *objs, "-ldl"])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", _tmp(out), *objs, "-ldl"])
+    os.replace(_tmp(out), out)
     return out
 
 
