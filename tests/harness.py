@@ -58,6 +58,7 @@ class Case:
     logits_dtype: str = "bf16"     # "f32": the same (bf16-exact) logits passed as fp32
     history_window: int = 0        # W (NEXT-3): 0 = lifetime counts
     time_attention_at: tuple = ()  # steps before which asr_time_attention runs (must leave no trace)
+    fr_clear_counts: int = 0       # FR also clears the detection counts (SPEC S:391 reading)
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -73,7 +74,8 @@ class Case:
 def orc_cfg(c: Case) -> oracle.OrcCfg:
     return oracle.OrcCfg(L=c.L, Hq=c.Hq, Hkv=c.Hkv, d=c.d, window=c.window, tau=c.tau, softness=c.softness,
                          pinned_prefix=c.pinned_prefix, score_scaled=c.score_mode, tick_skip_new=c.tick_order,
-                         vocab=c.vocab, wr_window=c.wr_window, history_window=c.history_window)
+                         vocab=c.vocab, wr_window=c.wr_window, history_window=c.history_window,
+                         fr_clear_counts=c.fr_clear_counts)
 
 
 def asr_cfg(c: Case):
@@ -82,7 +84,8 @@ def asr_cfg(c: Case):
                   max_context=c.capacity(), kv_dtype=KV_BF16 if c.dtype == "bf16" else KV_F32,
                   window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
                   score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window,
-                  pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min, history_window=c.history_window)
+                  pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min, history_window=c.history_window,
+                  fr_clear_counts=c.fr_clear_counts)
 
 
 def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:

@@ -159,3 +159,13 @@ def test_time_attention_leaves_no_trace():
              vocab=4096, seed=501, time_attention_at=(5, 6, 17)))
     run(Case(L=2, Hq=32, Hkv=8, d=128, B=3, prompt=(70, 20, 45), steps=30, window=8, hot_permille=300,
              a_hot=64, vocab=4096, seed=502, time_attention_at=(5, 17)))
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_fr_clear_counts(B):
+    # NEXT-3 option: FR also clears the detection counts (oracle pinned in test_oracle_variants.py);
+    # planted spikes drive the ladder through SR, WR, FR, RR; counts compared bitwise every step
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=B, prompt=(60, 41)[:B], steps=150, window=8, vocab=128256, seed=95,
+             spike_first=50, spike_period=16, spike_count=4, fr_clear_counts=1)
+    s = run(c)
+    assert s["recoveries"] >= 3 * B
