@@ -328,15 +328,34 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     timeline = None
     if a.timeline:
         tls = []
+        from paper_2512_11221_b200.asr import asr_tail_trace
+        traces = []
         for t in range(8):
             flush.zero_()
             ctx.step(Q[W + t], KN[W + t], VN[W + t], o, logits_prev=LG[W + t], entropy=ent)
             tls.append(ctx.timeline())
+            traces.append(asr_tail_trace(ctx._h))
+        tr = traces[-1]
+        settle = tr[[c * 32 + w for c in range(148) for w in range(10)]]
+        settle = settle[settle[:, 0] >= 0]
+        comb = tr[[c * 32 + 16 + w for c in range(148) for w in range(10)]]
+        comb = comb[comb[:, 0] >= 0]
+        if len(settle):
+            d = np.diff(settle, axis=1)
+            print("tail trace settle warps:", len(settle), "start med/max", np.median(settle[:, 0]), settle[:, 0].max(),
+                  "stage durations med", np.round(np.median(d, axis=0), 3).tolist(), "max", np.round(d.max(axis=0), 3).tolist(),
+                  "end max", settle[:, 7].max(), file=sys.stderr)
+        if len(comb):
+            print("tail trace combine warps:", len(comb), "start med/max", np.median(comb[:, 0]), comb[:, 0].max(),
+                  "dur med/max", np.median(comb[:, 7] - comb[:, 0]), (comb[:, 7] - comb[:, 0]).max(),
+                  "end max", comb[:, 7].max(), file=sys.stderr)
         med = [round(statistics.median(x), 3) for x in zip(*tls)]
         timeline = {"pre_start_end_attn_start_end_post_start_end_us": med[:6],
                     "post_decide_end_next_list_end_combine_end_us": med[6:9],
                     "pre_entropy_end_append_end_phaseB_start_end_us": med[9:13],
-                    "attn_first_cta_end_us": med[13:14], "post_released_us": med[14:15]}
+                    "attn_first_cta_end_us": med[13:14], "post_released_us": med[14:15],
+                    "tail_barrier_arrive_release_decide_tick_count_lookback_write_first_us": med[15:23],
+                    "cta_past_attention_past_phaseB_wait_us": med[23:25], "tail_dry_pass_end_us": med[25:26]}
         print("timeline (us):", json.dumps(tls), file=sys.stderr)
     # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
     # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below

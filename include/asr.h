@@ -219,7 +219,9 @@ asr_status asr_set_profile(asr_ctx* ctx, int32_t on);
  * post) in microseconds relative to the pre stage's start (%globaltimer); with n >= 15 also us[6..14] =
  * end of the decide blocks, of the next step's A_{i+1} compaction and of the combine; end of the
  * entropy units, of the append units, start and end of phase B; the first attention CTA's end; the
- * time the post stage passed its wait for the attention.  n >= 6.
+ * time the post stage passed its wait for the attention; with the fused tail (one kernel per step)
+ * eight more: grid-barrier arrival (last CTA) and release, the ends of the tile warps' decide,
+ * tick, count, look-back and write, and the first tile warp done.  n >= 6.
  * Synchronises. */
 asr_status asr_timeline(asr_ctx* ctx, double* us, int32_t n);
 

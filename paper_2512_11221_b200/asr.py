@@ -342,12 +342,23 @@ def asr_stage_times(ctx):
     return list(ms), int(n.value)
 
 
+def asr_tail_trace(ctx, n_slots: int = 26):
+    """Diagnostics (ASR_TIMELINE=1): per-warp stamps of the fused tail of the last step, us relative
+    to the step start, -1 = not stamped: array [148 * 32][8] (row = CTA * 32 + slot)."""
+    rows, cols = 148 * 32, 8
+    total = n_slots + rows * cols
+    us = (ctypes.c_double * total)()
+    _check(lib().asr_timeline(ctx, us, total))
+    return np.frombuffer(us, dtype=np.float64)[n_slots:].reshape(rows, cols).copy()
+
+
 def asr_timeline(ctx) -> list:
     """[pre start, end, attention start, end, post start, end, decide end, next-A end, combine end,
     entropy units end, append units end, phase B start, phase B end, first attention CTA end,
-    post released] (us)."""
-    us = (ctypes.c_double * 15)()
-    _check(lib().asr_timeline(ctx, us, 15))
+    post released, fused tail: barrier arrival, barrier release, tile warps' decide / tick / count /
+    look-back / write ends, first tile warp done, CTA past the attention, past the phase-B wait] (us)."""
+    us = (ctypes.c_double * 26)()
+    _check(lib().asr_timeline(ctx, us, 26))
     return list(us)
 
 

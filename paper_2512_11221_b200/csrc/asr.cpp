@@ -439,12 +439,25 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       s.combine_in_decide = (long)s.B * s.L * s.Hq <= 64L * c->num_sms;
     }
     c->attn_grid = asr::attention_grid(s, c->num_sms);
+    // fused tail (opt-in, ASR_FUSE_TAIL=1): the attention kernel settles the step itself (decide + tick
+    // + A_{i+1} + combine after a grid barrier) — tensor-core path, full residency, unsharded.  Off by
+    // default: measured 56.1 vs 53.2 us per batch-1 8K step
+    {
+      const char* ft = getenv("ASR_FUSE_TAIL");
+      s.max_tiles = (s.max_ctx + 15) / 16;
+      s.fuse_tail = asr::attention_mma_supported(s) && !s.pool_mode && !s.sharded && ft && ft[0] == '1';
+      const char* te = getenv("ASR_TAIL_EXP");
+      s.tail_exp = te ? atoi(te) : 0;
+      CUDA_TRY(c->alloc(&s.seg_flag, (size_t)s.B * s.max_tiles * 8));
+      CUDA_TRY(cudaMemsetAsync(s.seg_flag, 0, (size_t)s.B * s.max_tiles * 8, st));
+    }
     if (asr::attention_mma_supported(s)) CUDA_TRY(asr::attention_mma_prepare());
     const char* ng = getenv("ASR_NO_GRAPH");
     c->use_graph = !(ng && ng[0] == '1');
     // device timeline: [2*kStages] stamps + [kStages] accumulated phase ns + [1] step count
-    CUDA_TRY(c->alloc(&c->tl_buf, sizeof(unsigned long long) * asr::kTimelineSlots));
-    CUDA_TRY(cudaMemsetAsync(c->tl_buf, 0, sizeof(unsigned long long) * asr::kTimelineSlots, st));
+    const size_t tl_words = asr::kTimelineSlots + (size_t)asr::kTraceRows * asr::kTraceCols;
+    CUDA_TRY(c->alloc(&c->tl_buf, sizeof(unsigned long long) * tl_words));
+    CUDA_TRY(cudaMemsetAsync(c->tl_buf, 0, sizeof(unsigned long long) * tl_words, st));
     const char* tlenv = getenv("ASR_TIMELINE");
     c->timeline_on = tlenv && tlenv[0] == '1';
     s.tl = nullptr;
@@ -586,8 +599,10 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
   if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0 (+ phase D detail)
     unsigned long long init[asr::kTimelineSlots];
     for (int k = 0; k < asr::kTimelineSlots; ++k)
-      init[k] = ((k < 2 * asr::kStages && !(k & 1)) || k >= asr::kTimelineSlots - 2) ? ~0ull : 0ull;
+      init[k] = asr::tl_is_min(k) ? ~0ull : 0ull;
     CUDA_TRY(cudaMemcpyAsync(a.sd.tl, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(a.sd.tl + asr::kTimelineSlots, 0,
+                             sizeof(unsigned long long) * asr::kTraceRows * asr::kTraceCols, st));
   }
   return ASR_OK;
 }
@@ -636,12 +651,12 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
       stage_of[nk++] = 2;
     }
   }
-  if (part != kPartAttend) {   // decide (after scoresum in head-shard mode) — on the critical path
+  if (part != kPartAttend && !s.fuse_tail) {   // decide (after scoresum in head-shard mode) — on the critical path
     asr::node_phaseD(kn_list[nk], sd, a.o);
     if (part == kPartFull) kn_list[nk].dep_full[0] = nk - 1;
     stage_of[nk++] = 2;
   }
-  if (part != kPartDecide && !s.combine_in_decide) {
+  if (part != kPartDecide && !s.combine_in_decide && !s.fuse_tail) {
     // combine: a branch after the attention (full edges: kernels launched early beside the
     // attention wait for whole SMs and measured slower)
     asr::node_combine(kn_list[nk], sd, a.o);
@@ -871,6 +886,7 @@ asr_status asr_attach_nccl(asr_ctx* c, const void* unique_id, int32_t nranks, in
   // from now on every step runs attend -> all-reduce -> decide; cached graphs captured the
   // unsharded kernel arguments
   c->s.sharded = 1;
+  c->s.fuse_tail = 0;   // the all-reduce sits between the attention and the decide
   for (auto& g : c->graphs) {
     if (g.x) cudaGraphExecDestroy(g.x);
     if (g.g) cudaGraphDestroy(g.g);
@@ -1039,10 +1055,12 @@ asr_status asr_timeline(asr_ctx* c, double* us, int32_t n) {
   if (!us || n < 2 * asr::kStages) return fail(ASR_E_INVALID, "us must hold 6 values");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
-  unsigned long long t[asr::kTimelineSlots];
-  CUDA_TRY(cudaMemcpy(t, c->tl_buf, sizeof(t), cudaMemcpyDeviceToHost));
-  const int m = n < asr::kTimelineSlots ? n : asr::kTimelineSlots;
-  for (int k = 0; k < m; ++k) us[k] = ((double)t[k] - (double)t[0]) * 1e-3;
+  const int total = asr::kTimelineSlots + asr::kTraceRows * asr::kTraceCols;
+  std::vector<unsigned long long> t(total);
+  CUDA_TRY(cudaMemcpy(t.data(), c->tl_buf, sizeof(unsigned long long) * total, cudaMemcpyDeviceToHost));
+  const int m = n < total ? n : total;
+  for (int k = 0; k < m; ++k)
+    us[k] = (k >= asr::kTimelineSlots && t[k] == 0) ? -1.0 : ((double)t[k] - (double)t[0]) * 1e-3;
   return ASR_OK;
 }
 
@@ -1065,6 +1083,7 @@ asr_status asr_time_attention(asr_ctx* c, int32_t reps, void* cuda_stream) {
   }
   DevState sd = s;
   sd.pre_in_attn = 0;   // the attention alone
+  sd.fuse_tail = 0;
   sd.tl = nullptr;
   asr::KNode n;
   asr::node_attention(n, sd, c->scratch_q, c->scratch_k, c->scratch_v, c->attn_grid, nullptr, 0, nullptr,

@@ -13,7 +13,17 @@ constexpr int kStages = 3;          // pre (entropy+append+recovery), attention,
 // end of the entropy units, end of the append units, start and end of phase B; the first attention
 // CTA's end (with the stage end: the spread of the CTAs' ends); last: release of phase D (its first
 // block past griddepcontrol.wait)
-constexpr int kTimelineSlots = 2 * kStages + 9;
+constexpr int kTimelineSlots = 2 * kStages + 9 + 11;
+// fused-tail detail (max stamps): grid-barrier arrival, release, then per tile-decide warp: decide,
+// tick, count, look-back, write; the first tile warp done (min); batch 1: the CTA past the
+// attention (all warps), past its wait for phase B
+constexpr int kTlTail = 2 * kStages + 9;
+// per-warp trace of the fused tail (diagnostics, with the timeline): [CTA * 32 + slot][8] stamps,
+// slot = warp (segment settle) or 16 + warp (combine)
+constexpr int kTraceRows = 148 * 32, kTraceCols = 8;
+__host__ __device__ constexpr bool tl_is_min(int k) {
+  return (k < 2 * kStages && !(k & 1)) || k == 2 * kStages + 7 || k == 2 * kStages + 8 || k == kTlTail + 7;
+}
 constexpr int kEntSplits = 64;      // logits row splits for the entropy reduction
 
 // Residency byte: 1 = Active; 0 = Frozen; 2 / 3 = Frozen during a step of even / odd index (tag used
@@ -127,7 +137,15 @@ struct DevState {
   unsigned long long* dagg;   // [B][32] per decide block: (step + 1) << 32 | its count of A_{i+1}
   int32_t* redo;              // [1] recovery changed some A_i after the attention started (pre_in_attn)
   int32_t* pre_done;          // [1] = step + 1 once phase B of the step is done
-  unsigned* gbar;             // [2] grid barrier of the attention kernel's redo pass
+  unsigned* gbar;             // [2] grid barrier of the attention kernel (redo pass, fused tail)
+  // fused tail (fuse_tail = 1): the attention kernel itself combines O, decides + ticks and compacts
+  // A_{i+1} after a grid barrier (one kernel per step; no phase-D launch).  A_{i+1} is compacted per
+  // segment: segment t of sequence b = the positions from A_i[16t] up to A_i[16t+16] (the first from
+  // 0, the last through the appended position), placed by a decoupled look-back over seg_flag.
+  int fuse_tail;
+  int tail_exp;               // diagnostics (ASR_TAIL_EXP): bit 0 no combine, bit 1 dry decide pass first
+  int max_tiles;              // ceil(max_ctx / 16): seg_flag row length
+  unsigned long long* seg_flag;   // [B][max_tiles] (step+1) << 34 | state << 32 | value
   unsigned long long* tl;     // [kTimelineSlots] diagnostic timeline (globaltimer ns), NULL = off
 };
 
@@ -140,6 +158,40 @@ __host__ __device__ inline long act_off(const DevState& s, int p) { return (long
 // without a programmatic edge (direct launches, profiled graphs).
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// A value the compiler cannot see through (keeps a non-inlined function from being cloned and
+// specialised for a constant argument, so a dry run executes the very code of the real run).
+__device__ __forceinline__ int opaque(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// Release / acquire synchronisation at GPU scope (cheaper than __threadfence(), which is a
+// sequentially consistent fence: MEMBAR.SC.GPU + an L1 invalidation on sm_100).
+__device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_acqrel_u64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Diagnostic timeline: thread 0 of every block stamps %globaltimer at entry (atomicMin) and exit
 // (atomicMax) into tl[2*stage], tl[2*stage+1].  Only when DevState::tl is set (ASR_TIMELINE=1).

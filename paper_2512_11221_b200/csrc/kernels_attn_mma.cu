@@ -196,7 +196,7 @@ struct Cursor {
       else hi = mid - 1;
     }
     b = lo;
-    A = alen[b];
+    A = __ldcg(alen + b);
     tiles = (A + kTM - 1) / kTM;
     const int r = tt - start[b];
     l = r / tiles;
@@ -209,7 +209,7 @@ struct Cursor {
     if (++l < s.L) return;
     l = 0;
     for (++b; b < s.B; ++b) {
-      A = alen[b];
+      A = __ldcg(alen + b);
       tiles = (A + kTM - 1) / kTM;
       if (tiles) break;
     }
@@ -254,7 +254,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       sm.start[b] = acc;
-      acc += s.L * ((alen[b] + kTM - 1) / kTM);
+      acc += s.L * ((__ldcg(alen + b) + kTM - 1) / kTM);
     }
     sm.start[s.B] = acc;
     if (blockIdx.x == 0)
@@ -287,7 +287,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     else cur.t = t_end;
     auto load_idx = [&](const Cursor& c) -> int {
       if (c.t >= t_end || lane >= c.cnt()) return 0;
-      return max(0, __ldg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));   // device slot
+      // device slot; through L2: recovery may recompact A_i while the kernel runs (redo pass)
+      return max(0, __ldcg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));
     };
     int j_cur = load_idx(cur);
     int g = 0, it_local = -1;
@@ -344,7 +345,8 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       cur = nxt;
       ++g;
     }
-    if (s.B <= 8) prefetch_ledger(s, p, alen, step, lane);   // large batches: phase D is not latency-bound
+    // large batches: phase D is not latency-bound; fused tail: the aux warp prefetched at the start
+    if (s.B <= 8 && !s.fuse_tail) prefetch_ledger(s, p, alen, step, lane);
     // drain: the last (up to) kStagesRing tiles still owe their score epilogue
     for (int k = 0; k < kStagesRing; ++k) {
       const int gg = g + k;  // waiting for the release of tile gg - kStagesRing
@@ -362,6 +364,20 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       if (s.tl && lane == 0) atomicMin(&s.tl[0], gtimer());
       units::phaseA_block<TL, __nv_bfloat16>(s, blockIdx.x, step, pre_logits, k_new, v_new, entropy_out, u);
       if (s.tl && lane == 0) atomicMax(&s.tl[1], gtimer());
+    }
+    if (s.fuse_tail && s.B <= 8) prefetch_ledger(s, step & 1, s.act_len + (step & 1) * s.B, step, lane);
+    if (s.fuse_tail && !(s.tail_exp & 2)) {
+      // instruction prefetch: a dry run (loads and arithmetic only, no stores, no waits) of the fused
+      // tail's two functions while the attention streams, so their code is on chip when the tail runs
+      // (it runs once per SM per step, right on the critical path); the arguments are opaque to the
+      // compiler so both runs execute the one non-inlined copy
+      const int D = sm.start[s.B] / s.L;
+      const bool dry = opaque(0) != 0;
+      uint32_t* no_scratch = reinterpret_cast<uint32_t*>((uintptr_t)opaque(0));
+      if (D > 0)
+        units::warp_settle_segment(s, 0, min((int)blockIdx.x, (sm.start[1] / s.L) - 1), step, no_scratch, opaque(0),
+                                   dry);
+      if (o) units::combine_warp_tail(s, (int)blockIdx.x % (s.B * s.L * s.Hq), o, dry);
     }
     return;
   }
@@ -502,40 +518,85 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 }
 
 
-// Sense-reversing barrier over the CTAs of the attention grid (one CTA per SM, all resident once
-// the kernel has triggered its dependents); used only when recovery forces a second pass.
-__device__ void grid_sync(unsigned* bar, uint32_t* err) {
+// Barrier over the CTAs of the attention grid (one CTA per SM, all resident: persistent grid of
+// num_SMs CTAs at one CTA per SM); used when recovery forces a second pass and before the fused
+// tail.  bar is a monotonic 64-bit arrival counter (never reset): barrier instance k completes when
+// it reaches (k+1) * gridDim.x.  Release on arrival, acquire on the wait (bar.sync makes them
+// cumulative over the CTA's threads).
+__device__ void grid_sync(unsigned* bar32, uint32_t* err) {
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(bar32);
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
+    const unsigned long long G = gridDim.x;
+    const unsigned long long old = atom_add_acqrel_u64(bar, 1ull);
+    const unsigned long long target = old - old % G + G;
+    if (ld_acquire_u64(bar) < target) {
       const unsigned long long t0 = gtimer();
-      while (*vgen == gen) {
-        __nanosleep(64);
+      while (ld_acquire_u64(bar) < target) {
+        __nanosleep(32);
         if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
           atomicOr(err, kErrStall);
           break;
         }
       }
     }
-    __threadfence();
   }
   __syncthreads();
+}
+
+// Fused tail of a step (DevState::fuse_tail): after a grid barrier (every partial and score of the
+// step is in memory), the warps of the grid settle the step — Alg. 1 lines 3-15 + A_{i+1} per token
+// tile (units::warp_decide_tile, placed by a decoupled look-back) and the fixed-order combine of the
+// items split across CTAs (units::combine_warp) — then the last CTA out advances the step.  Replaces
+// the phase-D kernel (its launch gap and one-block latency chains) at small batch.
+template <int HK>
+__device__ void fused_tail(const DevState& s, typename Geo<HK>::Smem& sm, int step, float* o) {
+  if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[kTlTail], gtimer());
+  grid_sync(s.gbar, s.err);
+  if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[kTlTail + 1], gtimer());
+  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * 2], gtimer());
+  const int nw = (int)(blockDim.x >> 5), warp = (int)(threadIdx.x >> 5);
+  const int G = (int)gridDim.x, NW = G * nw;
+  const int r = warp * G + (int)blockIdx.x;   // consecutive ranks sit on different CTAs
+  const int D = sm.start[s.B] / s.L;         // token tiles of all sequences (start[] counts L per tile)
+  for (int k = r; k < D; k += NW) {
+    int lo = 0, hi = s.B - 1;                // last sequence whose first token tile is <= k
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sm.start[mid] / s.L <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    // the KV ring is idle now: a slice of it per warp holds the segment's final residency words
+    constexpr int kScap = (int)(sizeof(sm.kv) / 4) / (Geo<HK>::kThreads / 32);
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(&sm.kv[0][0]) + warp * kScap;
+    units::warp_settle_segment(s, lo, k - sm.start[lo] / s.L, step, scratch, kScap, opaque(1) != 0);
+  }
+  if (s.tl && (threadIdx.x & 31) == 0) atomicMax(&s.tl[2 * kStages], gtimer());
+  // combine tasks (one warp per (b, l, h)), first on the warps without a tile
+  const int C = s.B * s.L * s.Hq;
+  if (o && !(s.tail_exp & 1))   // (ASR_TAIL_EXP bit 0: no combine — timing diagnostics only)
+    for (int k = ((r - D) % NW + NW) % NW; k < C; k += NW) units::combine_warp_tail(s, k, o, opaque(1) != 0);
+  if (s.tl && (threadIdx.x & 31) == 0) atomicMax(&s.tl[2 * kStages + 2], gtimer());
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s.tl) atomicMax(&s.tl[2 * 2 + 1], gtimer());
+    // every CTA read *s.step at its start; the next kernel sees all writes of this one
+    if (atomicAdd(s.ticket, 1) == gridDim.x - 1) {   // the last CTA out: the step is done
+      *s.ticket = 0;
+      *s.redo = 0;
+      *s.step = step + 1;
+    }
+  }
 }
 
 // The attention kernel over A_i as phase D of the previous step compacted it.  With pre_in_attn
 // (batch 1) the CTAs' extra warps also run phase A and B of the step; since recovery (phase B) may
 // recompact A_i while the attention runs, every CTA then waits for phase B (*pre_done) and, only if
 // recovery fired (*redo, rare), all CTAs pass a grid barrier and redo the attention over the new A_i.
+// With fuse_tail the kernel then settles the step itself (fused_tail).
 template <int HK, typename TL>
 __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
-    attn_mma_kernel(DevState s, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_new,
+    attn_mma_kernel(const __grid_constant__ DevState s, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_new,
                     const __nv_bfloat16* __restrict__ v_new, const TL* logits, float* entropy_out, float* o) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   auto& sm = *reinterpret_cast<typename Geo<HK>::Smem*>(smem_raw);
@@ -551,28 +612,31 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
     attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
     if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 7], gtimer());   // first CTA done
   }
-  if (!do_pre) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const volatile int* done = s.pre_done;
-    const unsigned long long t0 = gtimer();
-    bool ok = true;
-    while (*done != step + 1) {
-      __nanosleep(64);
-      if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
-        atomicOr(s.err, kErrStall);
-        ok = false;
-        break;
+  if (do_pre) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s.tl) atomicMax(&s.tl[kTlTail + 8], gtimer());   // every warp of the CTA is past the attention
+      const unsigned long long t0 = gtimer();
+      bool ok = true;
+      while (ld_acquire(s.pre_done) != step + 1) {   // acquire: phase B's ledger / A_i writes
+        __nanosleep(64);
+        if (gtimer() - t0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
+          atomicOr(s.err, kErrStall);
+          ok = false;
+          break;
+        }
       }
+      redo = ok ? *reinterpret_cast<const volatile int*>(s.redo) : 0;
+      if (s.tl) atomicMax(&s.tl[kTlTail + 9], gtimer());
     }
-    __threadfence();
-    redo = ok ? *reinterpret_cast<const volatile int*>(s.redo) : 0;
+    __syncthreads();
+    if (redo) {
+      grid_sync(s.gbar, s.err);    // every CTA is past its first pass
+      attention_prologue<HK>(sm);  // fresh ring barriers
+      attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
+    }
   }
-  __syncthreads();
-  if (!redo) return;
-  grid_sync(s.gbar, s.err);    // every CTA is past its first pass
-  attention_prologue<HK>(sm);  // fresh ring barriers
-  attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
+  if (s.fuse_tail) fused_tail<HK>(s, sm, step, o);
 }
 
 }  // namespace

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, cons
 __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float* __restrict__ o) {
   Stamp stamp(s.tl, 2);
   pdl_wait();      // every input comes from the attention kernel(s) and phase A
-  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[kTimelineSlots - 1], gtimer());
+  if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 8], gtimer());
   __shared__ units::UnitShm u;
   const int nd = s.decide_blocks * s.B;
   if ((int)blockIdx.x >= nd) {   // combine_in_decide: blocks after the decide blocks combine O
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
     units::unit_next_list(s, b, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
     if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[2 * kStages + 1], gtimer());
     if (threadIdx.x == 0) {
-      __threadfence();
+      // every block read *s.step at its start; the next kernel sees all writes of this one
       if (atomicAdd(s.ticket, 1) == nd - 1) {   // the last decide block of the step
         *s.ticket = 0;
         *s.redo = 0;

@@ -569,7 +569,7 @@ __device__ __forceinline__ float layer_sum(const DevState& s, int b, int a) {
   for (int l0 = 0; l0 < s.L; l0 += 32) {
     float v[32];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = l0 + q < s.L ? sp[(long)(l0 + q) * s.max_ctx] : 0.f;
+    for (int q = 0; q < 32; ++q) v[q] = l0 + q < s.L ? __ldcg(sp + (long)(l0 + q) * s.max_ctx) : 0.f;
 #pragma unroll
     for (int q = 0; q < 32; ++q)
       if (l0 + q < s.L) sum += v[q];
@@ -586,22 +586,125 @@ __device__ void unit_score_sum(const DevState& s, int b, int x, int X, int i) {
     s.tok_score[(long)b * s.max_ctx + a] = layer_sum(s, b, a);
 }
 
+// Alg. 1 lines 3-9 (+ the R0 tick of a token frozen now) for attended index a (position j) of
+// sequence b at step i; returns through the counters.  Shared by the decide block (unit_decide) and
+// the fused tail's tile decide (warp_decide_tile).
+struct DecideCtx {
+  long base;
+  uint8_t tag_now;
+  float heads, sqrt_d;
+  int n, pf_row;
+};
+__device__ __forceinline__ DecideCtx decide_ctx(const DevState& s, int b, int i) {
+  DecideCtx c;
+  c.base = (long)b * s.max_ctx;
+  c.tag_now = res_tag(i);
+  c.heads = (float)(s.L * s.score_heads);   // Eq. 2's H over all layers (R-layer)
+  c.sqrt_d = sqrtf((float)s.d);
+  c.n = s.prompt_len[b] + i + 1;
+  c.pf_row = (i & 1) * s.B + b;            // prefetch list written by this step (pressure mode)
+  return c;
+}
+
+__device__ __forceinline__ void decide_token(const DevState& s, const DecideCtx& c, int b, int a, int j, int i,
+                                             int& frozen_now, int& restored, int& evicted) {
+  const long base = c.base;
+  float sj;
+  if (s.ext_score) {
+    sj = s.ext_score[(long)b * s.cap + j];   // policy replay: the caller's s_j, rows of max_context
+  } else {
+    const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
+    sj = sum / c.heads;               // mean over the L*Hq (layer, head) pairs (correctly rounded)
+    if (s.score_scaled) sj = sj / c.sqrt_d;
+  }
+  s.score[base + a] = sj;
+  if (!(j < c.n - s.window && j >= s.pinned && sj < s.tau)) return;
+  uint32_t cc;                        // line 4: c_j <- c_j + 1 (lifetime, or within the window W)
+  if (s.hist_w > 0) {
+    // finite W: a 128-bit history of detections, bit t = step hstep - t; shift it to step
+    // i, record this detection, keep the bits of (i - W, i] and count them
+    unsigned long long* hm = s.hmask + (base + j) * 2;
+    const int sh = i - s.hstep[base + j];
+    unsigned long long lo = hm[0], hi = hm[1];
+    if (sh >= 128) {
+      lo = hi = 0;
+    } else if (sh >= 64) {
+      hi = lo << (sh - 64);
+      lo = 0;
+    } else if (sh > 0) {
+      hi = (hi << sh) | (lo >> (64 - sh));
+      lo <<= sh;
+    }
+    lo |= 1ull;
+    if (s.hist_w < 64) {
+      lo &= (1ull << s.hist_w) - 1ull;
+      hi = 0;
+    } else if (s.hist_w < 128) {
+      hi &= (1ull << (s.hist_w - 64)) - 1ull;
+    }
+    hm[0] = lo;
+    hm[1] = hi;
+    s.hstep[base + j] = i;
+    cc = (uint32_t)(__popcll(lo) + __popcll(hi));
+    s.count[base + j] = cc;
+  } else {
+    cc = s.count[base + j] + 1;
+    s.count[base + j] = cc;
+  }
+  const int dd = duration(cc, s.softness, s.softness_int);  // line 5
+  if (dd <= 0) return;
+  frozen_now++;                       // lines 6-7
+  s.fstep[base + j] = i;
+  const int t = s.tick_skip_new ? dd : dd - 1;   // R0: this step's tick applies too
+  if (t <= 0) {
+    s.timer[base + j] = 0;            // frozen and restored by the same tick (no absence)
+    restored++;
+    return;
+  }
+  s.timer[base + j] = t;
+  s.res[base + j] = c.tag_now;
+  if (s.pool_mode && t >= s.evict_min && s.slot_of[base + j] >= 0) {   // (a5) offload
+    pool_push(s, s.slot_of[base + j]);
+    s.slot_of[base + j] = -1;
+    evicted++;
+  }
+  if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)
+    s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
+}
+
+// Alg. 1 lines 10-15 for position j, frozen before this step (residency r, timer tm at step start);
+// tokens of A_i (r == 1, or this step's tag) are skipped.
+__device__ __forceinline__ void tick_position(const DevState& s, const DecideCtx& c, int j, uint8_t r, int tm,
+                                              int& restored, uint32_t& err) {
+  if (r == 1 || r == c.tag_now) return;
+  const long base = c.base;
+  const int t = tm - 1;
+  if (t <= 0) {
+    s.res[base + j] = 1;
+    s.timer[base + j] = 0;
+    restored++;
+    if (s.pool_mode && s.slot_of[base + j] < 0) err |= kErrNotResident;
+  } else {
+    s.timer[base + j] = t;
+    if (r != 0) s.res[base + j] = 0;           // drop the previous step's tag
+    if (j >= c.n - s.window) err |= kErrFrozenInWindow;
+    if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)   // back next step: prefetch it
+      s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
+  }
+}
+
 // Unit x of X for sequence b: a slice of the attended list (Alg. 1 lines 3-9 + the R0 tick of the
 // tokens it freezes) and a slice of the positions (lines 10-15 for tokens frozen at earlier steps).
 // The two index sets are disjoint (A_i = the tokens Active at the step start) and tokens frozen in
 // this step carry the step-parity tag res_tag(i), so units need no ordering between them.
 __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
-  const int n = s.prompt_len[b] + i + 1;
-  const long base = (long)b * s.max_ctx;
+  const DecideCtx dc = decide_ctx(s, b, i);
+  const int n = dc.n;
+  const long base = dc.base;
   const int A = s.act_len[(i & 1) * s.B + b];
   const int32_t* act_pos = s.act_pos + act_off(s, i) + base;
-  uint8_t* res = s.res + base;
-  int32_t* timer = s.timer + base;
-  uint32_t* cnt = s.count + base;
-  int32_t* fstep = s.fstep + base;
-  const float heads = (float)(s.L * s.score_heads);   // Eq. 2's H over all layers (R-layer)
-  const float sqrt_d = sqrtf((float)s.d);
-  const uint8_t tag_now = res_tag(i);
+  const uint8_t* res = s.res + base;
+  const int32_t* timer = s.timer + base;
   // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
   // loop: tokens of A_i read Active here and are skipped by the tick below)
   constexpr int kPF = 8;
@@ -625,97 +728,17 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     pt[k] = j < n_end ? timer[j] : 0;
   }
   int frozen_now = 0, restored = 0, evicted = 0;
-  const int pf_row = (i & 1) * s.B + b;   // prefetch list written by this step
-  for (int a = a0 + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS()) {
-    const int j = act_pos[a];
-    float sj;
-    if (s.ext_score) {
-      sj = s.ext_score[(long)b * s.cap + j];   // policy replay: the caller's s_j, rows of max_context
-    } else {
-      const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
-      sj = sum / heads;                 // mean over the L*Hq (layer, head) pairs (correctly rounded)
-      if (s.score_scaled) sj = sj / sqrt_d;
-    }
-    s.score[base + a] = sj;
-    if (j < n - s.window && j >= s.pinned && sj < s.tau) {
-      uint32_t c;                       // line 4: c_j <- c_j + 1 (lifetime, or within the window W)
-      if (s.hist_w > 0) {
-        // finite W: a 128-bit history of detections, bit t = step hstep - t; shift it to step
-        // i, record this detection, keep the bits of (i - W, i] and count them
-        unsigned long long* hm = s.hmask + (base + j) * 2;
-        const int sh = i - s.hstep[base + j];
-        unsigned long long lo = hm[0], hi = hm[1];
-        if (sh >= 128) {
-          lo = hi = 0;
-        } else if (sh >= 64) {
-          hi = lo << (sh - 64);
-          lo = 0;
-        } else if (sh > 0) {
-          hi = (hi << sh) | (lo >> (64 - sh));
-          lo <<= sh;
-        }
-        lo |= 1ull;
-        if (s.hist_w < 64) {
-          lo &= (1ull << s.hist_w) - 1ull;
-          hi = 0;
-        } else if (s.hist_w < 128) {
-          hi &= (1ull << (s.hist_w - 64)) - 1ull;
-        }
-        hm[0] = lo;
-        hm[1] = hi;
-        s.hstep[base + j] = i;
-        c = (uint32_t)(__popcll(lo) + __popcll(hi));
-        cnt[j] = c;
-      } else {
-        c = cnt[j] + 1;
-        cnt[j] = c;
-      }
-      const int dd = duration(c, s.softness, s.softness_int);  // line 5
-      if (dd > 0) {                     // lines 6-7
-        frozen_now++;
-        fstep[j] = i;
-        const int t = s.tick_skip_new ? dd : dd - 1;   // R0: this step's tick applies too
-        if (t <= 0) {
-          timer[j] = 0;                 // frozen and restored by the same tick (no absence)
-          restored++;
-        } else {
-          timer[j] = t;
-          res[j] = tag_now;
-          if (s.pool_mode && t >= s.evict_min && s.slot_of[base + j] >= 0) {   // (a5) offload
-            pool_push(s, s.slot_of[base + j]);
-            s.slot_of[base + j] = -1;
-            evicted++;
-          }
-          if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)
-            s.pf_list[(long)pf_row * s.max_ctx + atomicAdd(&s.pf_count[pf_row], 1)] = j;
-        }
-      }
-    }
-  }
+  for (int a = a0 + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS())
+    decide_token(s, dc, b, a, act_pos[a], i, frozen_now, restored, evicted);
   // lines 10-15 for tokens frozen before this step
   uint32_t err = 0;
-  auto tick = [&](int j, uint8_t r, int tm) {
-    if (r == 1 || r == tag_now) return;
-    const int t = tm - 1;
-    if (t <= 0) {
-      res[j] = 1;
-      timer[j] = 0;
-      restored++;
-      if (s.pool_mode && s.slot_of[base + j] < 0) err |= kErrNotResident;
-    } else {
-      timer[j] = t;
-      if (r != 0) res[j] = 0;           // drop the previous step's tag
-      if (j >= n - s.window) err |= kErrFrozenInWindow;
-      if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)   // back next step: prefetch it
-        s.pf_list[(long)pf_row * s.max_ctx + atomicAdd(&s.pf_count[pf_row], 1)] = j;
-    }
-  };
 #pragma unroll
   for (int k = 0; k < kPF; ++k) {
     const int j = n0 + (int)ASR_UNIT_TID() + k * (int)ASR_UNIT_THREADS();
-    if (j < n_end) tick(j, pr[k], pt[k]);
+    if (j < n_end) tick_position(s, dc, j, pr[k], pt[k], restored, err);
   }
-  for (int j = n0 + (int)ASR_UNIT_TID() + kPF * (int)ASR_UNIT_THREADS(); j < n_end; j += ASR_UNIT_THREADS()) tick(j, res[j], timer[j]);
+  for (int j = n0 + (int)ASR_UNIT_TID() + kPF * (int)ASR_UNIT_THREADS(); j < n_end; j += ASR_UNIT_THREADS())
+    tick_position(s, dc, j, res[j], timer[j], restored, err);
   if (err) atomicOr(s.err, err);
   int f = frozen_now, r = restored;
   for (int o = 16; o > 0; o >>= 1) {
@@ -736,6 +759,355 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     for (int o = 16; o > 0; o >>= 1) evicted += __shfl_xor_sync(0xffffffffu, evicted, o);
     if (lane == 0 && evicted) atomicAdd(&s.stats[b].evicted, evicted);
   }
+}
+
+// ---------------------------------------------------------------------------------- fused tail
+// One warp settles segment t of sequence b at step i (DevState::fuse_tail): the 16 attended tokens
+// A_i[16t .. 16t+15] (Alg. 1 lines 3-9), the frozen positions between them and A_i[16t+16] (lines
+// 10-15; the first segment starts at 0, the last runs through n, where it also writes the ledger
+// entry of the position step i+1 appends), then its part of A_{i+1}: the segment's surviving
+// positions are counted, published in seg_flag and placed by a decoupled look-back over the earlier
+// segments (a warp waits only on smaller segments, whose warps never wait on larger ones: no
+// deadlock, given every warp of the grid is resident).  Full residency only (slot = row + position).
+//
+// Written for latency: this code runs once per SM per step, right after the attention, so its
+// instruction fetches (cold code, L2 or DRAM) are on the critical path — loops stay rolled and the
+// function is small and not inlined, so one copy serves the dry run that pre-fetches it (wr = false:
+// loads and arithmetic only, every store and wait predicated off) and the real run.  Data: three
+// dependent rounds of loads (A_i entries; Eq. 2 partials, counts and the segment's residency /
+// timers; the look-back); the final residency of every position is derived in registers (an Active
+// position is the k-th token of the tile; its freeze decision comes from the deciding lane by
+// ballot) and kept in a shared-memory scratch (fin) for the write pass.
+__device__ __forceinline__ unsigned long long seg_word(int i, unsigned state, unsigned v) {
+  return ((unsigned long long)((unsigned)(i + 1) & 0x3fffffffu) << 34) | ((unsigned long long)state << 32) | v;
+}
+// per-warp stamps of the fused tail: compiled in only with -DASR_TAIL_TRACE (diagnostic builds), since
+// every instruction of this cold, once-per-step code is on the critical path
+__device__ __forceinline__ void trace(const DevState& s, int slot, int k) {
+#ifdef ASR_TAIL_TRACE
+  if (s.tl && (threadIdx.x & 31) == 0)
+    s.tl[kTimelineSlots + ((long)blockIdx.x * 32 + slot) * kTraceCols + k] = gtimer();
+#endif
+}
+__device__ __noinline__ void warp_settle_segment(const DevState& s, int b, int t, int i, uint32_t* fin_scratch,
+                                                 int scap, bool wr) {
+  const int lane = threadIdx.x & 31;
+  const int tslot = wr ? (int)(threadIdx.x >> 5) : 31;
+  trace(s, tslot, 0);
+  const long base = (long)b * s.max_ctx;
+  const int p = i & 1;
+  const uint8_t tag_now = res_tag(i);
+  // ---- round 1: step geometry and the tile's A_i entries (lane 16: the next segment's first position)
+  const int n = s.prompt_len[b] + i + 1;
+  const int A = __ldcg(s.act_len + p * s.B + b);   // A_i may have been recompacted in this kernel
+  const int a0 = t * 16;
+  const int32_t* act_pos = s.act_pos + act_off(s, p) + base;
+  const int j = lane <= 16 ? __ldcg(act_pos + min(a0 + lane, s.max_ctx - 1)) : 0;
+  const int cnt = min(16, A - a0);
+  const bool last = a0 + 16 >= A;
+  const bool next = n + 1 <= s.cap;   // step i+1 can run
+  const int lo = t == 0 ? 0 : __shfl_sync(0xffffffffu, j, 0);
+  const int jn = __shfl_sync(0xffffffffu, j, 16);
+  const int hi = last ? n : jn;
+  const bool dec = lane < cnt;
+  trace(s, tslot, 1);
+  // ---- round 2: the deciding lanes' Eq. 2 partials and counts
+  // (unconditional loads from clamped, always valid addresses: straight-line code, all in flight)
+  float part[32];
+  const int L = s.L;
+  const float* sp = s.score_part + (long)b * L * s.max_ctx + min(a0 + lane, s.max_ctx - 1);
+#pragma unroll
+  for (int q = 0; q < 32; ++q) part[q] = __ldcg(sp + (long)min(q, L - 1) * s.max_ctx);
+  const long jc = base + (dec ? j : 0);
+  const uint32_t cnt_old = __ldcg(s.count + jc);
+  unsigned long long hm_lo = 0, hm_hi = 0;
+  int hst = 0;
+  if (s.hist_w > 0) {
+    hm_lo = __ldcg(s.hmask + jc * 2);
+    hm_hi = __ldcg(s.hmask + jc * 2 + 1);
+    hst = __ldcg(s.hstep + jc);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) sum += q < L ? part[q] : 0.f;   // fixed order l = 0 .. L-1 (as layer_sum)
+#pragma unroll 1
+  for (int l = 32; l < s.L; ++l) sum += dec ? __ldcg(sp + (long)l * s.max_ctx) : 0.f;
+  trace(s, tslot, 2);
+  // ---- decide (lines 3-9) on the deciding lanes
+  int frozen_now = 0, restored = 0;
+  bool absent = false;               // frozen with a remaining absence (leaves A_{i+1})
+  if (dec) {
+    float sj = sum / (float)(s.L * s.score_heads);
+    if (s.score_scaled) sj = sj / sqrtf((float)s.d);
+    if (wr) s.score[base + a0 + lane] = sj;
+    if (j < n - s.window && j >= s.pinned && sj < s.tau) {
+      uint32_t c;
+      if (s.hist_w > 0) {
+        const int sh = i - hst;
+        unsigned long long lo2 = hm_lo, hi2 = hm_hi;
+        if (sh >= 128) {
+          lo2 = hi2 = 0;
+        } else if (sh >= 64) {
+          hi2 = lo2 << (sh - 64);
+          lo2 = 0;
+        } else if (sh > 0) {
+          hi2 = (hi2 << sh) | (lo2 >> (64 - sh));
+          lo2 <<= sh;
+        }
+        lo2 |= 1ull;
+        if (s.hist_w < 64) {
+          lo2 &= (1ull << s.hist_w) - 1ull;
+          hi2 = 0;
+        } else if (s.hist_w < 128) {
+          hi2 &= (1ull << (s.hist_w - 64)) - 1ull;
+        }
+        if (wr) {
+          s.hmask[(base + j) * 2] = lo2;
+          s.hmask[(base + j) * 2 + 1] = hi2;
+          s.hstep[base + j] = i;
+        }
+        c = (uint32_t)(__popcll(lo2) + __popcll(hi2));
+      } else {
+        c = cnt_old + 1;
+      }
+      if (wr) s.count[base + j] = c;
+      const int dd = duration(c, s.softness, s.softness_int);
+      if (dd > 0) {
+        frozen_now = 1;
+        const int tt = s.tick_skip_new ? dd : dd - 1;   // R0: this step's tick applies too
+        restored = tt <= 0;           // frozen and restored by the same tick (no absence)
+        absent = tt > 0;
+        if (wr) {
+          s.fstep[base + j] = i;
+          s.timer[base + j] = tt > 0 ? tt : 0;
+          if (tt > 0) s.res[base + j] = tag_now;
+        }
+      }
+    }
+  }
+  const unsigned absent_mask = __ballot_sync(0xffffffffu, absent);   // bit k: token a0 + k leaves
+  trace(s, tslot, 3);
+  // ---- tick (lines 10-15) of the positions frozen before this step; final residency per word of
+  //      4 positions (bit e = position 4w + e survives), two words per lane per round of loads
+  const uint32_t* res4 = reinterpret_cast<const uint32_t*>(s.res + base);
+  const int4* tim4 = reinterpret_cast<const int4*>(s.timer + base);
+  const int wlo = lo >> 2, whi = (hi + 3) >> 2;
+  uint32_t err = 0;
+  int rank = 0;          // Active positions of the segment seen so far (= tile index of the next one)
+  int c_seg = 0;         // surviving positions of the segment (this lane's words)
+#pragma unroll 1
+  for (int m0 = 0; wlo + m0 < whi; m0 += 64) {
+    uint32_t rw[2];
+    int4 tw[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int w = min(wlo + m0 + 32 * h + lane, whi - 1);   // clamped: masked below by w < whi
+      rw[h] = __ldcg(res4 + w);
+      tw[h] = __ldcg(tim4 + w);
+    }
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int w = wlo + m0 + 32 * h + lane;
+      const uint32_t r4 = h ? rw[1] : rw[0];
+      const int4 t4 = h ? tw[1] : tw[0];
+      uint32_t act0 = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = 4 * w + e;
+        const uint32_t r = (r4 >> (8 * e)) & 0xffu;
+        // Active at the step start (the tag if a deciding lane's store was already visible)
+        if (w < whi && q >= lo && q < hi && (r == 1u || r == tag_now)) act0 |= 1u << e;
+      }
+      const int ca = __popc(act0);
+      int incl = ca;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int rk = rank + incl - ca;
+      rank += __shfl_sync(0xffffffffu, incl, 31);
+      uint32_t fin = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = 4 * w + e;
+        const uint32_t r = (r4 >> (8 * e)) & 0xffu;
+        const int tv = e == 0 ? t4.x : e == 1 ? t4.y : e == 2 ? t4.z : t4.w;
+        if (w >= whi || q < lo || q >= hi) continue;
+        if (act0 & (1u << e)) {
+          if (rk >= 32 || !((absent_mask >> rk) & 1u)) fin |= 1u << e;
+          ++rk;
+        } else if (tv <= 1) {        // timer reaches 0: restored (Active in A_{i+1})
+          fin |= 1u << e;
+          restored++;
+          if (wr) {
+            s.res[base + q] = 1;
+            s.timer[base + q] = 0;
+          }
+        } else {
+          if (wr) {
+            s.timer[base + q] = tv - 1;
+            if (r != 0) s.res[base + q] = 0;        // drop the previous step's tag
+          }
+          if (q >= n - s.window) err |= kErrFrozenInWindow;
+        }
+      }
+      c_seg += __popc(fin);
+      const int widx = m0 + 32 * h + lane;
+      if (widx < scap) fin_scratch[widx] = fin;
+    }
+  }
+  trace(s, tslot, 4);
+  int f = frozen_now, rr = restored;
+  for (int o = 16; o > 0; o >>= 1) {
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+    c_seg += __shfl_xor_sync(0xffffffffu, c_seg, o);
+  }
+  if (wr) {
+    if (err) atomicOr(s.err, err);
+    if (lane == 0 && f) atomicAdd(&s.stats[b].frozen_this_step, f);
+    if (lane == 0 && rr) atomicAdd(&s.stats[b].restored_tick, rr);
+  }
+  if (!next) return;   // no step i+1: A_{i+1} is never read
+  if (wr && last && lane == 0) ledger_entry_new(s, b, n);
+  const int c = c_seg + (last ? 1 : 0);   // + the position step i+1 appends
+  // ---- publish (inclusive at once for the first segment), then look back over the earlier ones
+  unsigned long long* flag = s.seg_flag + (long)b * s.max_tiles;
+  const unsigned long long tag = (unsigned long long)((unsigned)(i + 1) & 0x3fffffffu) << 34;
+  if (wr && lane == 0) atomicExch(&flag[t], seg_word(i, t == 0 ? 2u : 1u, (unsigned)c));
+  trace(s, tslot, 5);
+  int excl = 0;
+#pragma unroll 1
+  for (int k = t - 1; k >= 0; k -= 32) {
+    const int idx = k - lane;
+    unsigned long long v = 0;
+    if (idx >= 0) {
+      const volatile unsigned long long* fp = flag + idx;
+      v = *fp;
+      if (wr && (v & 0xfffffffc00000000ull) != tag) {
+        const unsigned long long tm0 = gtimer();
+        while ((v & 0xfffffffc00000000ull) != tag) {
+          __nanosleep(20);
+          v = *fp;
+          if (gtimer() - tm0 > 2000000000ull) {   // 2 s: never on a healthy device; do not hang it
+            atomicOr(s.err, kErrStall);
+            break;
+          }
+        }
+      }
+    }
+    const unsigned incl = __ballot_sync(0xffffffffu, idx >= 0 && ((v >> 32) & 3u) == 2u);
+    // lanes up to (and including) the nearest inclusive predecessor contribute
+    const int stop = incl ? __ffs(incl) - 1 : 31;
+    int x = (lane <= stop && idx >= 0) ? (int)(v & 0xffffffffu) : 0;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    excl += x;
+    if (incl || !wr) break;
+  }
+  if (wr && lane == 0 && t > 0) atomicExch(&flag[t], seg_word(i, 2u, (unsigned)(excl + c)));
+  trace(s, tslot, 6);
+  // ---- write the segment's surviving positions (and device slots) to A_{i+1}[excl ...]
+  int32_t* out = s.act_pos + act_off(s, p ^ 1) + base;
+  int32_t* out_slot = s.act_slot + act_off(s, p ^ 1) + base;
+  int off = excl;
+  __syncwarp();
+#pragma unroll 1
+  for (int m0 = 0; wlo + m0 < whi; m0 += 32) {
+    const int w = wlo + m0 + lane;
+    uint32_t fin = 0;
+    if (m0 + lane < scap) {
+      fin = fin_scratch[m0 + lane];
+    } else if (w < whi) {   // beyond the scratch: re-read the residency this warp just settled
+      const uint32_t rw = __ldcg(res4 + w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (((rw >> (8 * e)) & 0xffu) == 1u && 4 * w + e >= lo && 4 * w + e < hi) fin |= 1u << e;
+    }
+    const int cm = __popc(fin);
+    int incl = cm;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int o = off + incl - cm;
+    while (fin) {
+      const int jj = 4 * w + __ffs(fin) - 1;
+      if (wr) {
+        out[o] = jj;
+        out_slot[o] = (int)(base + jj);
+      }
+      ++o;
+      fin &= fin - 1;
+    }
+    off += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (wr && last && lane == 0) {
+    out[off] = n;
+    out_slot[off] = (int)(base + n);
+    s.act_len[(p ^ 1) * s.B + b] = off + 1;
+  }
+  trace(s, tslot, 7);
+}
+
+// (a4') combine for the fused tail, one warp per (b, l, h), head_dim 128, stream-K pieces: the same
+// fixed-order merge as combine_warp in compact form (rolled over pieces, 8 piece loads in flight);
+// wr = false: dry run (no store).
+__device__ __noinline__ void combine_warp_tail(const DevState& s, int wid, float* __restrict__ o, bool wr) {
+  const int lane = threadIdx.x & 31;
+  const int tslot = wr ? 16 + (int)(threadIdx.x >> 5) : 31;
+  trace(s, tslot, 0);
+  const int h = wid % s.Hq;
+  const int l = (wid / s.Hq) % s.L;
+  const int b = wid / (s.Hq * s.L);
+  const int is_b = __ldcg(s.item_start + b), is_b1 = __ldcg(s.item_start + b + 1);
+  const long T = __ldcg(s.item_start + s.B);
+  const int tiles = (is_b1 - is_b) / s.L;
+  if (!tiles || T <= 0) return;
+  const long S = is_b + (long)l * tiles;
+  const int G = sk_span(T, s.sk_grid);
+  const int cf = sk_cta_of(S, T, G);
+  int nch = sk_cta_of(S + tiles - 1, T, G) - cf + 1;
+  if (nch == 1) return;   // one CTA held the whole item and wrote O itself
+  if (!wr) nch = min(nch, 8);
+  const long it0 = (long)b * s.L + l + cf;
+  float M = -INFINITY;
+#pragma unroll 1
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(s.part_ml + ((it0 + c) * s.Hq + h) * 2));
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+  float den = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < nch; c0 += 32) {
+    const long pl = (it0 + min(c0 + lane, nch - 1)) * s.Hq + h;   // clamped: weight 0 beyond nch
+    const float m_l = __ldcg(s.part_ml + pl * 2), l_l = __ldcg(s.part_ml + pl * 2 + 1);
+    const float wl = c0 + lane < nch ? exp2f(m_l - M) : 0.f;
+    const float ll = c0 + lane < nch ? l_l : 0.f;
+    const int cn = min(32, nch - c0);
+#pragma unroll 1
+    for (int cb = 0; cb < cn; cb += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        v[q] = __ldcg(reinterpret_cast<const float4*>(s.part_acc + ((it0 + c0 + min(cb + q, cn - 1)) * s.Hq + h) * 128L) +
+                      lane);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {   // chunk order: deterministic (w = 0 adds exact zeros past cn)
+        const float w = cb + q < cn ? __shfl_sync(0xffffffffu, wl, (cb + q) & 31) : 0.f;
+        const float lq = __shfl_sync(0xffffffffu, ll, (cb + q) & 31);
+        if (cb + q < cn) den = fmaf(lq, w, den);
+        num.x = fmaf(v[q].x, w, num.x);
+        num.y = fmaf(v[q].y, w, num.y);
+        num.z = fmaf(v[q].z, w, num.z);
+        num.w = fmaf(v[q].w, w, num.w);
+      }
+    }
+  }
+  trace(s, tslot, 6);
+  const float inv = 1.0f / den;
+  if (wr)
+    *reinterpret_cast<float4*>(o + (((long)b * s.L + l) * s.Hq + h) * 128L + lane * 4) =
+        make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
+  trace(s, tslot, 7);
 }
 
 // After unit_decide of step i: A_{i+1} into parity (i+1) & 1.  Decide block x owns the positions
@@ -831,10 +1203,12 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   const int b = wid / (s.Hq * s.L);
   int nch;
   long it0;
-  const int per_seq = (s.item_start[b + 1] - s.item_start[b]) / s.L;   // tiles (or chunks) per layer
+  // (read through L2: in the fused tail these were written by other CTAs of the same kernel)
+  const int is_b = __ldcg(s.item_start + b), is_b1 = __ldcg(s.item_start + b + 1);
+  const int per_seq = (is_b1 - is_b) / s.L;   // tiles (or chunks) per layer
   if (s.sk_grid) {   // stream-K pieces (asr_internal.h)
     const int tiles = per_seq;
-    const long T = s.item_start[s.B], S = s.item_start[b] + (long)l * tiles;
+    const long T = __ldcg(s.item_start + s.B), S = is_b + (long)l * tiles;
     const int G = sk_span(T, s.sk_grid);
     const int cf = tiles ? sk_cta_of(S, T, G) : 0;
     nch = tiles ? sk_cta_of(S + tiles - 1, T, G) - cf + 1 : 0;
@@ -842,10 +1216,10 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
     if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   } else {
     nch = per_seq;
-    it0 = s.item_start[b] + (long)l * nch;
+    it0 = is_b + (long)l * nch;
   }
   float M = -INFINITY;
-  for (int c = lane; c < nch; c += 32) M = fmaxf(M, s.part_ml[((it0 + c) * s.Hq + h) * 2]);
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(s.part_ml + ((it0 + c) * s.Hq + h) * 2));
   for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
   const int epl = s.d >= 32 ? s.d / 32 : 1;   // elements per lane (d <= 256 -> <= 8)
   const bool on = lane * epl < s.d;
@@ -855,8 +1229,8 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
     float wl = 0.f, ll = 0.f;
     if (c0 + lane < nch) {
       const long pi = (it0 + c0 + lane) * s.Hq + h;
-      wl = exp2f(s.part_ml[pi * 2] - M);
-      ll = s.part_ml[pi * 2 + 1];
+      wl = exp2f(__ldcg(s.part_ml + pi * 2) - M);
+      ll = __ldcg(s.part_ml + pi * 2 + 1);
     }
     const int cn = min(32, nch - c0);
     if (epl == 4) {
@@ -865,8 +1239,8 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (cb + q < cn)
-            v[q] = *reinterpret_cast<const float4*>(s.part_acc + ((it0 + c0 + cb + q) * s.Hq + h) * (long)s.d +
-                                                    lane * 4);
+            v[q] = __ldcg(reinterpret_cast<const float4*>(s.part_acc + ((it0 + c0 + cb + q) * s.Hq + h) * (long)s.d +
+                                                          lane * 4));
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (cb + q >= cn) break;
@@ -882,7 +1256,7 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
         den = fmaf(__shfl_sync(0xffffffffu, ll, c), w, den);
         if (on) {
           const float* src = s.part_acc + ((it0 + c0 + c) * s.Hq + h) * (long)s.d + lane * epl;
-          for (int e = 0; e < epl; ++e) num[e] = fmaf(src[e], w, num[e]);
+          for (int e = 0; e < epl; ++e) num[e] = fmaf(__ldcg(src + e), w, num[e]);
         }
       }
     }
@@ -941,12 +1315,9 @@ __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logit
   const int b = phaseA_seq(s, has_logits, unit);
   ASR_UNIT_SYNC();
   if (ASR_UNIT_TID() == 0) {
-    __threadfence();   // this unit's results before the ticket
-    u.last = atomicAdd(&s.pre_ticket[b], 1) == phaseA_units_per_seq(s, has_logits) - 1;
-    if (u.last) {
-      s.pre_ticket[b] = 0;
-      __threadfence();
-    }
+    // release: this unit's results before the ticket; acquire: the last unit sees every unit's results
+    u.last = atom_add_acqrel(&s.pre_ticket[b], 1) == phaseA_units_per_seq(s, has_logits) - 1;
+    if (u.last) s.pre_ticket[b] = 0;
   }
   ASR_UNIT_SYNC();
   if (u.last) {
@@ -954,10 +1325,8 @@ __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logit
     unit_finish(s, b, i, has_logits, entropy_out, u);
     if (s.tl && ASR_UNIT_TID() == 0) atomicMax(&s.tl[2 * kStages + 6], gtimer());
     ASR_UNIT_SYNC();
-    if (ASR_UNIT_TID() == 0) {
-      __threadfence();
-      *s.pre_done = i + 1;   // the attention kernel's CTAs wait for this when phase A runs inside it
-    }
+    if (ASR_UNIT_TID() == 0)
+      st_release(s.pre_done, i + 1);   // the attention kernel's CTAs wait for this when phase A runs inside it
   }
 }
 

@@ -169,3 +169,19 @@ def test_fr_clear_counts(B):
              spike_first=50, spike_period=16, spike_count=4, fr_clear_counts=1)
     s = run(c)
     assert s["recoveries"] >= 3 * B
+
+
+@pytest.fixture
+def fused_tail(monkeypatch):
+    monkeypatch.setenv("ASR_FUSE_TAIL", "1")   # read at asr_create
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_fused_tail_mode(fused_tail, B):
+    # opt-in one-kernel step (DevState::fuse_tail): decide + tick + A_{i+1} (segment look-back) +
+    # combine inside the attention kernel after a grid barrier; bitwise the same ledgers and lists
+    run(Case(L=2, Hq=32, Hkv=8, d=128, B=B, prompt=(300, 129, 77)[:B], steps=40, window=16, hot_permille=300,
+             a_hot=64, vocab=4096, seed=700 + B))
+    # finite W, planted entropy spikes (recovery recompacts A_i mid-kernel at batch 1: redo pass)
+    run(Case(L=2, Hq=32, Hkv=8, d=128, B=B, prompt=(60, 41, 33)[:B], steps=150, window=8, vocab=128256,
+             seed=710 + B, spike_first=50, spike_period=16, spike_count=4, history_window=64))

@@ -120,6 +120,8 @@ def _build_asr(force: bool) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-I", os.path.join(ROOT, "include"), "-I", csrc]
+    if os.environ.get("ASR_TAIL_TRACE") == "1":   # diagnostic build: per-warp stamps of the fused tail
+        common.append("-DASR_TAIL_TRACE")
     for s in cu:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
