@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--timeline", action="store_true", help="device timeline of 8 extra steps (ASR_TIMELINE)")
     ap.add_argument("--pool-frac", type=float, default=0.0,
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
-    ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: evict freezes absent >= this")
+    ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: never evict tokens returning sooner")
+    ap.add_argument("--evict-policy", type=int, default=0, help="pressure mode: 0 Belady under pressure, 1 at freeze")
     ap.add_argument("--points", default="cfg3,w1,full,sample,replay,quant",
                     help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
     ap.add_argument("--head-shard", action="store_true",
@@ -203,6 +204,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     cfg = Config(n_layers=L, n_q_heads=hq_r, n_kv_heads=hkv_r, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=a.tau, softness=2.0, vocab=VOCAB, profile_stages=0,
                  device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min, history_window=a.history_window,
+                 evict_policy=a.evict_policy,
                  score_heads=HQ if a.head_shard else 0)
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, hkv_r, D), dtype=bf, device=dev)

@@ -72,9 +72,10 @@ typedef struct {
   int32_t host_mirror;    /* 1 = keep the write-once pinned host copy of every token's KV */
   int32_t profile_stages; /* 1 = record CUDA events around every stage (asr_stage_times) */
   int32_t device;         /* CUDA device ordinal */
-  int32_t evict_min_absence; /* pressure mode: a token frozen for >= this many more steps gives up its
-                                device slot at freeze time (default 2) */
-  int32_t reserved0;
+  int32_t evict_min_absence; /* pressure mode: tokens returning in fewer than this many steps are never
+                                evicted (default 2; a token back next step would be copied right back) */
+  int32_t pool_reserve;   /* pressure mode: device slots kept free beyond the next step's appends and
+                           * prefetches, for demand restores (recovery / asr_restore); 0 = batch */
   int64_t pool_tokens;    /* 0: full residency (every token keeps its device slot; freezing only flips
                            * its residency bit).  > 0: pressure mode (Sec 3.3, "moves the token's
                            * KV pair from GPU to CPU"): the device holds pool_tokens token slots; frozen
@@ -85,8 +86,15 @@ typedef struct {
                            * n_q_heads of them); 0 = n_q_heads (unsharded).  The per-token partial sums
                            * must then be summed across shards between asr_step_attend and
                            * asr_step_decide (asr_attach_nccl does it inside asr_step). */
-  int32_t reserved1;
+  int32_t evict_policy;   /* pressure mode (Sec 3.3): ASR_EVICT_BELADY (default): frozen tokens
+                           * keep their device slots until the pool runs short; then, after each step,
+                           * the resident frozen tokens returning LAST (largest remaining timer: the
+                           * return step is known at freeze time, Eq. 3) are evicted until the free
+                           * slots cover the next step's appends + prefetches + pool_reserve.
+                           * ASR_EVICT_AT_FREEZE: every token frozen for >= evict_min_absence steps
+                           * is evicted when it freezes (round-1 policy, kept for comparison). */
 } asr_config;
+typedef enum { ASR_EVICT_BELADY = 0, ASR_EVICT_AT_FREEZE = 1 } asr_evict_policy;
 
 /* Fills *cfg with the paper's defaults (K=32, tau=0.5, k=2: P:112) and LLaMA-3-8B shape. */
 void asr_config_defaults(asr_config* cfg);
@@ -133,6 +141,10 @@ typedef struct {
   int64_t evicted_this_step;  /* device slots released by this step's freezes (pressure mode) */
   int64_t prefetched_this_step; /* tokens copied host -> device ahead of their timer expiry */
   int64_t demand_restored_this_step; /* evicted tokens copied back on demand (recovery / asr_restore) */
+  int64_t h2d_stall_ns;       /* context-wide, cumulative: device time the steps waited on the host link
+                               * (demand copies before compaction + prefetch copies outlasting the
+                               * attention kernel), %globaltimer on the device (pressure mode) */
+  int64_t free_slots;         /* pressure mode: free device slots after the last step (else 0) */
 } asr_stats_t;
 
 /* Host buffers for a full ledger snapshot of one sequence (any pointer may be NULL). */

@@ -23,6 +23,7 @@ ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, A
 KV_BF16, KV_F32 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 SR, WR, FR = 1, 2, 3
+EVICT_BELADY, EVICT_AT_FREEZE = 0, 1
 STAGES = ("entropy_append_recover_compact", "attention_score", "combine_decide_tick", "step_total")
 
 
@@ -42,8 +43,8 @@ class asr_config(ctypes.Structure):
                 ("det_baseline", ctypes.c_int32), ("det_cooldown", ctypes.c_int32), ("wr_window", ctypes.c_int32),
                 ("det_z", ctypes.c_float), ("det_sigma_floor", ctypes.c_float), ("fr_clear_counts", ctypes.c_int32),
                 ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("evict_min_absence", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("pool_tokens", ctypes.c_int64),
-                ("score_heads", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
+                ("evict_min_absence", ctypes.c_int32), ("pool_reserve", ctypes.c_int32), ("pool_tokens", ctypes.c_int64),
+                ("score_heads", ctypes.c_int32), ("evict_policy", ctypes.c_int32)]
 
 
 class asr_step_io(ctypes.Structure):
@@ -60,7 +61,8 @@ class asr_stats_t(ctypes.Structure):
                 ("recovery_action", ctypes.c_int32), ("rewalk_requested", ctypes.c_int32),
                 ("bytes_h2d", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64), ("device_error", ctypes.c_uint32),
                 ("resident", ctypes.c_int64), ("evicted_this_step", ctypes.c_int64),
-                ("prefetched_this_step", ctypes.c_int64), ("demand_restored_this_step", ctypes.c_int64)]
+                ("prefetched_this_step", ctypes.c_int64), ("demand_restored_this_step", ctypes.c_int64),
+                ("h2d_stall_ns", ctypes.c_int64), ("free_slots", ctypes.c_int64)]
 
 
 class asr_ledger_view(ctypes.Structure):
@@ -159,11 +161,11 @@ class Config:
     host_mirror: int = 1
     profile_stages: int = 0
     device: int = 0
-    evict_min_absence: int = 2
-    reserved0: int = 0
+    evict_min_absence: int = 2       # pressure mode: never evict tokens returning in fewer steps
+    pool_reserve: int = 0            # pressure mode: free slots kept for demand restores (0 = batch)
     pool_tokens: int = 0             # 0 = full residency; > 0 = pressure mode (device slot pool)
     score_heads: int = 0             # head-sharded mode: H of Eq. 2 over all shards (0 = n_q_heads)
-    reserved1: int = 0
+    evict_policy: int = 0            # pressure mode: EVICT_BELADY (capacity-driven) or EVICT_AT_FREEZE
 
     def c(self) -> asr_config:
         v = dataclasses.asdict(self)

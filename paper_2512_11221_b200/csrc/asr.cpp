@@ -187,10 +187,10 @@ void asr_config_defaults(asr_config* c) {
   c->profile_stages = 0;
   c->device = 0;
   c->evict_min_absence = 2;
-  c->reserved0 = 0;
+  c->pool_reserve = 0;
   c->pool_tokens = 0;
   c->score_heads = 0;
-  c->reserved1 = 0;
+  c->evict_policy = ASR_EVICT_BELADY;
 }
 
 static asr_status validate(const asr_config* c) {
@@ -222,6 +222,9 @@ static asr_status validate(const asr_config* c) {
   if (c->pool_tokens < 0) return fail(ASR_E_INVALID, "pool_tokens < 0");
   if (c->pool_tokens > 0 && !c->host_mirror) return fail(ASR_E_INVALID, "pool_tokens > 0 needs host_mirror = 1");
   if (c->pool_tokens > ((int64_t)1 << 31) - 1) return fail(ASR_E_INVALID, "pool_tokens too large");
+  if (c->evict_policy != ASR_EVICT_BELADY && c->evict_policy != ASR_EVICT_AT_FREEZE)
+    return fail(ASR_E_INVALID, "evict_policy");
+  if (c->pool_reserve < 0) return fail(ASR_E_INVALID, "pool_reserve < 0");
   if (c->score_heads != 0 && c->score_heads < c->n_q_heads)
     return fail(ASR_E_INVALID, "score_heads must be 0 or >= n_q_heads (the heads of all shards)");
   return ASR_OK;
@@ -310,6 +313,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     const size_t BT = (size_t)s.B * s.max_ctx;
     s.pool_mode = cfg->pool_tokens > 0 ? 1 : 0;
     s.evict_min = cfg->evict_min_absence > 0 ? cfg->evict_min_absence : 2;
+    s.evict_policy = cfg->evict_policy;
+    s.pool_reserve = cfg->pool_reserve;
     const size_t slots = s.pool_mode ? (size_t)cfg->pool_tokens : BT;
     CUDA_TRY(c->alloc(&s.kv, slots * c->tok_bytes));
     CUDA_TRY(c->alloc(&s.act_slot, 2 * BT * 4));
@@ -330,6 +335,12 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       CUDA_TRY(c->alloc(&s.cp_list, BT * 4));
       CUDA_TRY(c->alloc(&s.cp_count, (size_t)s.B * 4));
       CUDA_TRY(c->alloc(&s.h2d, 8));
+      CUDA_TRY(c->alloc(&s.ev_hist, asr::kEvBins * 4));
+      CUDA_TRY(c->alloc(&s.ev_ctrl, 16));
+      CUDA_TRY(c->alloc(&s.stall, 24));
+      CUDA_TRY(cudaMemset(s.ev_hist, 0, asr::kEvBins * 4));
+      CUDA_TRY(cudaMemset(s.ev_ctrl, 0, 16));
+      CUDA_TRY(cudaMemset(s.stall, 0, 24));
       std::vector<int32_t> so(BT, -1), sp(s.B), fs;
       for (int b = 0; b < s.B; ++b)
         for (int p = 0; p < prompt_len[b]; ++p) so[(size_t)b * s.max_ctx + p] = (int32_t)(slot0[b] + p);
@@ -621,8 +632,8 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
   const DevState& s = c->s;
   const DevState& sd = a.sd;
   const bool prof = a.ev != nullptr;
-  asr::KNode kn_list[6];
-  int stage_of[6];   // 0 ledger pre, 1 attention, 2 decide/combine (profiling events)
+  asr::KNode kn_list[8];
+  int stage_of[8];   // 0 ledger pre, 1 attention, 2 decide/combine (profiling events)
   int nk = 0;
   const void* lgp = a.has_logits ? a.lg : nullptr;
   float* entp = a.has_logits ? a.ent : nullptr;
@@ -655,6 +666,11 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
     asr::node_phaseD(kn_list[nk], sd, a.o);
     if (part == kPartFull) kn_list[nk].dep_full[0] = nk - 1;
     stage_of[nk++] = 2;
+    if (s.pool_mode && s.evict_policy == ASR_EVICT_BELADY) {   // the Belady cut phase D computed
+      asr::node_evict(kn_list[nk], sd, c->num_sms);
+      kn_list[nk].dep_full[0] = nk - 1;
+      stage_of[nk++] = 2;
+    }
   }
   if (part != kPartDecide && !s.combine_in_decide && !s.fuse_tail) {
     // combine: a branch after the attention (full edges: kernels launched early beside the
@@ -951,6 +967,12 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
     out->evicted_this_step = st.evicted;
     out->prefetched_this_step = st.prefetched;
     out->demand_restored_this_step = st.demand;
+    unsigned long long stl[3] = {0, 0, 0};
+    int32_t free_top = 0;
+    CUDA_TRY(cudaMemcpy(stl, s.stall, 24, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&free_top, s.free_top, 4, cudaMemcpyDeviceToHost));
+    out->h2d_stall_ns = (int64_t)stl[0] + ((stl[1] && stl[2] > stl[1]) ? (int64_t)(stl[2] - stl[1]) : 0);
+    out->free_slots = free_top;
   }
   if (detail) {
     if (detail->capacity < n) return fail(ASR_E_INVALID, "detail->capacity < total");

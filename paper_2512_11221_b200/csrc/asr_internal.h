@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include "asr.h"
+
 namespace asr {
 
 constexpr int kStages = 3;          // pre (entropy+append+recovery), attention, post (combine+decide+next A)
@@ -31,6 +33,7 @@ constexpr int kEntSplits = 64;      // logits row splits for the entropy reducti
 __host__ __device__ constexpr bool res_active(uint8_t x) { return x == 1; }
 __host__ __device__ constexpr uint8_t res_tag(int step) { return (uint8_t)(2 + (step & 1)); }
 constexpr int kMaxDetBaseline = 256;
+constexpr int kEvBins = 64;         // Belady histogram bins of the remaining timer
 
 // Per-sequence per-step statistics written by the kernels (read by asr_stats).
 struct SeqStats {
@@ -93,7 +96,12 @@ struct DevState {
   int layers_per_unit;        // layers per phase-A append unit
   // pressure mode (pool_tokens > 0)
   int pool_mode;              // 0 full residency (slot = b*max_ctx + pos), 1 slot pool
-  int evict_min;              // evict at freeze when the remaining absence >= evict_min
+  int evict_min;              // never evict tokens returning in fewer steps (at-freeze policy: evict at >=)
+  int evict_policy;           // 0 Belady under pressure (histogram in phase D + evict kernel), 1 at freeze
+  int pool_reserve;           // free slots kept beyond the next step's appends + prefetches
+  int32_t* ev_hist;           // [kEvBins] resident frozen tokens per remaining timer (min(t, kEvBins-1))
+  int32_t* ev_ctrl;           // [4] Belady cut of this step: timer threshold T, quota at T, used, need
+  unsigned long long* stall;  // [3] h2d stall ns (cumulative), attention end, prefetch-copy end (stamps)
   long tok_bytes;             // bytes of one token (all layers, K and V)
   int32_t* slot_of;           // [B][max_ctx] device slot of each position, -1 = evicted (pool mode)
   int32_t* spare;             // [B] slot reserved for the next appended token (pool mode)
@@ -287,6 +295,7 @@ void node_combine(KNode& n, const DevState& s, float* o);
 void node_prepare(KNode& n, const DevState& s);            // A_0 at asr_create
 void node_restore(KNode& n, const DevState& s, int seq, int level);
 void node_copy(KNode& n, const DevState& s, int grid);   // pressure mode: prefetch copies
+void node_evict(KNode& n, const DevState& s, int grid);  // pressure mode: Belady eviction after phase D
 void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: layer sums -> tok_score
 int attention_grid(const DevState& s, int num_sms);
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,

@@ -171,6 +171,10 @@ __global__ void attn_generic_kernel(DevState s, const T* __restrict__ q) {
         for (int e = 0; e < EPL; ++e) s.part_acc[pi * D + lane * EPL + e] = acc[hh][e];
     }
   }
+  if (s.pool_mode) {   // the attention's end, against which the prefetch copies are timed
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&s.stall[1], gtimer());
+  }
 }
 
 template <typename T>

@@ -636,6 +636,10 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
       attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
     }
   }
+  if (s.pool_mode) {   // the attention's end, against which the prefetch copies are timed
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&s.stall[1], gtimer());
+  }
   if (s.fuse_tail) fused_tail<HK>(s, sm, step, o);
 }
 

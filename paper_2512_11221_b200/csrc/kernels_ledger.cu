@@ -20,6 +20,12 @@ __global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, cons
   pdl_trigger();
   Stamp stamp(s.tl, 0);
   __shared__ units::UnitShm u;
+  if (s.pool_mode && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the previous step's prefetch copies that outlasted its attention kernel: a host-link stall
+    const unsigned long long ae = s.stall[1], ce = s.stall[2];
+    if (ae && ce > ae) s.stall[0] += ce - ae;
+    s.stall[1] = s.stall[2] = 0;
+  }
   units::phaseA_block<TL, TK>(s, blockIdx.x, *s.step, logits, k_new, v_new, entropy_out, u);
 }
 
@@ -52,8 +58,10 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
     units::unit_next_list(s, b, blockIdx.x % s.decide_blocks, s.decide_blocks, i, u);
     if (s.tl && threadIdx.x == 0) atomicMax(&s.tl[2 * kStages + 1], gtimer());
     if (threadIdx.x == 0) {
-      // every block read *s.step at its start; the next kernel sees all writes of this one
-      if (atomicAdd(s.ticket, 1) == nd - 1) {   // the last decide block of the step
+      // every block read *s.step at its start; the next kernel sees all writes of this one.  Release /
+      // acquire: the last block sees every block's Belady histogram (pressure mode)
+      if (atom_add_acqrel(s.ticket, 1) == nd - 1) {   // the last decide block of the step
+        if (s.pool_mode && s.evict_policy == ASR_EVICT_BELADY) units::belady_cut(s, i);
         *s.ticket = 0;
         *s.redo = 0;
         *s.step = i + 1;
@@ -96,7 +104,9 @@ __global__ void __launch_bounds__(1024) restore_kernel(DevState s, int seq, int 
   if (s.pool_mode && threadIdx.x == 0) s.cp_count[b] = 0;
   __syncthreads();
   const int r = units::block_sum_int(units::apply_level(s, b, n, level, i), u);
+  const unsigned long long t0 = gtimer();
   const int d = s.pool_mode ? units::demand_copies(s, b) : 0;
+  if (d && threadIdx.x == 0) atomicAdd(&s.stall[0], gtimer() - t0);
   if (threadIdx.x == 0) {
     s.stats[b].pending_restored += r;
     s.stats[b].pending_demand += d;
@@ -110,7 +120,13 @@ constexpr int kCopyThreads = 256;
 __global__ void __launch_bounds__(kCopyThreads) copy_kernel(DevState s) {
   __shared__ int start[4097];
   units::prefetch_copies(s, start);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&s.stall[2], gtimer());   // vs the attention's end: stall if later
 }
+
+// Pressure mode, Belady policy: evict the cut phase D computed (after phase D, in the step graph).
+constexpr int kEvictThreads = 256;
+__global__ void __launch_bounds__(kEvictThreads) evict_kernel(DevState s) { units::evict_positions(s); }
 
 }  // namespace
 
@@ -160,6 +176,11 @@ void node_scoresum(KNode& n, const DevState& s) {
 void node_copy(KNode& n, const DevState& s, int grid) {
   n.s = s;
   n.finalize((const void*)copy_kernel, dim3(grid), dim3(kCopyThreads), 0);
+}
+
+void node_evict(KNode& n, const DevState& s, int grid) {
+  n.s = s;
+  n.finalize((const void*)evict_kernel, dim3(grid), dim3(kEvictThreads), 0);
 }
 
 void node_restore(KNode& n, const DevState& s, int seq, int level) {

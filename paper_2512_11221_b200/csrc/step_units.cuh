@@ -33,6 +33,7 @@ namespace {   // internal linkage: this header is compiled into several translat
 
 struct UnitShm {
   int sh[32], sh2[32], wsum[32];
+  int ev[kEvBins];   // decide: Belady histogram of this block's resident frozen tokens (pressure mode)
   float wm[32], wz[32], ws[32];
   int level;
   int total;
@@ -509,7 +510,11 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
   if (level > 0) {   // rare: apply the level (copy evicted tokens back), then recompact A_i
     const int n = s.prompt_len[b] + i + 1;
     restored = block_sum_int(apply_level(s, b, n - 1, level, i), u);
-    if (s.pool_mode) demand = demand_copies(s, b);
+    if (s.pool_mode) {
+      const unsigned long long t0 = gtimer();
+      demand = demand_copies(s, b);
+      if (ASR_UNIT_TID() == 0 && demand) atomicAdd(&s.stall[0], gtimer() - t0);   // the step waits on these
+    }
     compact_positions(s, b, n, i, u);
     if (ASR_UNIT_TID() == 0) *s.redo = 1;   // a speculative attention pass over the old A_i is void
   }
@@ -606,8 +611,10 @@ __device__ __forceinline__ DecideCtx decide_ctx(const DevState& s, int b, int i)
   return c;
 }
 
+// ev (pressure mode, Belady policy): shared histogram of the remaining timers of resident frozen
+// tokens (the eviction candidates of this step, cut after phase D: asr.cpp / evict_kernel).
 __device__ __forceinline__ void decide_token(const DevState& s, const DecideCtx& c, int b, int a, int j, int i,
-                                             int& frozen_now, int& restored, int& evicted) {
+                                             int& frozen_now, int& restored, int& evicted, int* ev = nullptr) {
   const long base = c.base;
   float sj;
   if (s.ext_score) {
@@ -664,18 +671,22 @@ __device__ __forceinline__ void decide_token(const DevState& s, const DecideCtx&
   s.timer[base + j] = t;
   s.res[base + j] = c.tag_now;
   if (s.pool_mode && t >= s.evict_min && s.slot_of[base + j] >= 0) {   // (a5) offload
-    pool_push(s, s.slot_of[base + j]);
-    s.slot_of[base + j] = -1;
-    evicted++;
+    if (s.evict_policy == ASR_EVICT_AT_FREEZE) {
+      pool_push(s, s.slot_of[base + j]);
+      s.slot_of[base + j] = -1;
+      evicted++;
+      if (t == 1)   // back at the next step's tick (evict_min = 1): prefetch it
+        s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
+    } else if (ev) {
+      atomicAdd(&ev[min(t, kEvBins - 1)], 1);   // a Belady candidate (returns in t + 1 steps)
+    }
   }
-  if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)
-    s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
 }
 
 // Alg. 1 lines 10-15 for position j, frozen before this step (residency r, timer tm at step start);
 // tokens of A_i (r == 1, or this step's tag) are skipped.
 __device__ __forceinline__ void tick_position(const DevState& s, const DecideCtx& c, int j, uint8_t r, int tm,
-                                              int& restored, uint32_t& err) {
+                                              int& restored, uint32_t& err, int* ev = nullptr) {
   if (r == 1 || r == c.tag_now) return;
   const long base = c.base;
   const int t = tm - 1;
@@ -688,8 +699,13 @@ __device__ __forceinline__ void tick_position(const DevState& s, const DecideCtx
     s.timer[base + j] = t;
     if (r != 0) s.res[base + j] = 0;           // drop the previous step's tag
     if (j >= c.n - s.window) err |= kErrFrozenInWindow;
-    if (s.pool_mode && t == 1 && s.slot_of[base + j] < 0)   // back next step: prefetch it
-      s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
+    if (s.pool_mode) {
+      const int so = s.slot_of[base + j];
+      if (t == 1 && so < 0)   // back next step: prefetch it
+        s.pf_list[(long)c.pf_row * s.max_ctx + atomicAdd(&s.pf_count[c.pf_row], 1)] = j;
+      else if (ev && so >= 0 && t >= s.evict_min)
+        atomicAdd(&ev[min(t, kEvBins - 1)], 1);   // a Belady candidate
+    }
   }
 }
 
@@ -727,18 +743,28 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
     pr[k] = j < n_end ? res[j] : (uint8_t)1;
     pt[k] = j < n_end ? timer[j] : 0;
   }
+  int* ev = s.pool_mode && s.evict_policy == ASR_EVICT_BELADY ? u.ev : nullptr;
+  if (ev) {
+    for (int k = (int)ASR_UNIT_TID(); k < kEvBins; k += ASR_UNIT_THREADS()) ev[k] = 0;
+    ASR_UNIT_SYNC();
+  }
   int frozen_now = 0, restored = 0, evicted = 0;
   for (int a = a0 + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS())
-    decide_token(s, dc, b, a, act_pos[a], i, frozen_now, restored, evicted);
+    decide_token(s, dc, b, a, act_pos[a], i, frozen_now, restored, evicted, ev);
   // lines 10-15 for tokens frozen before this step
   uint32_t err = 0;
 #pragma unroll
   for (int k = 0; k < kPF; ++k) {
     const int j = n0 + (int)ASR_UNIT_TID() + k * (int)ASR_UNIT_THREADS();
-    if (j < n_end) tick_position(s, dc, j, pr[k], pt[k], restored, err);
+    if (j < n_end) tick_position(s, dc, j, pr[k], pt[k], restored, err, ev);
   }
   for (int j = n0 + (int)ASR_UNIT_TID() + kPF * (int)ASR_UNIT_THREADS(); j < n_end; j += ASR_UNIT_THREADS())
-    tick_position(s, dc, j, res[j], timer[j], restored, err);
+    tick_position(s, dc, j, res[j], timer[j], restored, err, ev);
+  if (ev) {   // this block's candidates into the step's histogram (cut by the last decide block)
+    ASR_UNIT_SYNC();
+    for (int k = (int)ASR_UNIT_TID(); k < kEvBins; k += ASR_UNIT_THREADS())
+      if (ev[k]) atomicAdd(&s.ev_hist[k], ev[k]);
+  }
   if (err) atomicOr(s.err, err);
   int f = frozen_now, r = restored;
   for (int o = 16; o > 0; o >>= 1) {
@@ -1165,6 +1191,61 @@ __device__ void unit_next_list(const DevState& s, int b, int x, int X, int i, Un
     if (base + cnt == 0) atomicOr(s.err, kErrEmptyActive);
   }
   ASR_UNIT_SYNC();
+}
+
+// ---------------------------------------------------------------------------------- (a5) Belady
+// Pressure mode, Belady policy: after phase D of step i every resident frozen token with remaining
+// timer t >= evict_min is in ev_hist (bin min(t, kEvBins-1)); it is next attended at step i + t + 1,
+// known exactly (Eq. 3 fixes the absence at freeze time).  The slots the next step needs are its B
+// appends, its prefetches (tokens returning then that were evicted) and pool_reserve for demand
+// restores; if the free stack is short by `need`, the candidates returning LAST are evicted first
+// (Belady's MIN with clairvoyant reuse times): every candidate above the cut bin T and `quota` of
+// those in it.  Computed by the last decide block (one thread), applied by evict_kernel.
+__device__ void belady_cut(const DevState& s, int i) {
+  int pf = 0;
+  for (int b = 0; b < s.B; ++b) pf += __ldcg(s.pf_count + (i & 1) * s.B + b);
+  const int reserve = s.pool_reserve > 0 ? s.pool_reserve : s.B;
+  const int need = s.B + pf + reserve - __ldcg(s.free_top);
+  int T = kEvBins, quota = 0;
+  if (need > 0) {
+    int cum = 0;
+    for (int k = kEvBins - 1; k >= s.evict_min && k >= 0; --k) {
+      const int h = __ldcg(s.ev_hist + k);
+      T = k;
+      quota = min(h, need - cum);
+      cum += h;
+      if (cum >= need) break;
+    }
+  }
+  s.ev_ctrl[0] = T;
+  s.ev_ctrl[1] = quota;
+  s.ev_ctrl[2] = 0;
+  s.ev_ctrl[3] = need;
+  for (int k = 0; k < kEvBins; ++k) s.ev_hist[k] = 0;
+}
+
+// Evict the cut (one thread per position, grid-stride over all sequences): a resident frozen token
+// with bin > T, or in bin T while the quota lasts, gives its slot back (its bytes are in the host
+// mirror since its append).  Pushes only: the next pops are in the next step's phase B.
+__device__ void evict_positions(const DevState& s) {
+  const int need = __ldcg(s.ev_ctrl + 3);
+  if (need <= 0) return;
+  const int T = __ldcg(s.ev_ctrl + 0), quota = __ldcg(s.ev_ctrl + 1);
+  const int step = *s.step;   // phase D advanced it: positions held = prompt_len + step
+  for (long g = blockIdx.x * (long)blockDim.x + threadIdx.x; g < (long)s.B * s.max_ctx; g += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(g / s.max_ctx), j = (int)(g % s.max_ctx);
+    if (j >= s.prompt_len[b] + step) continue;
+    const long k = (long)b * s.max_ctx + j;
+    if (res_active(s.res[k])) continue;
+    const int so = s.slot_of[k];
+    const int t = s.timer[k];
+    if (so < 0 || t < s.evict_min) continue;
+    const int bin = min(t, kEvBins - 1);
+    if (bin < T || (bin == T && atomicAdd(s.ev_ctrl + 2, 1) >= quota)) continue;
+    pool_push(s, so);
+    s.slot_of[k] = -1;
+    atomicAdd(&s.stats[b].evicted, 1);
+  }
 }
 
 // Pressure mode: copy the tokens phase B gave slots to (this step's prefetch list) from the host

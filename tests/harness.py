@@ -54,6 +54,8 @@ class Case:
     max_context: int = 0
     pool_tokens: int = 0           # > 0: pressure mode (device slot pool, eviction / prefetch / demand)
     evict_min: int = 2
+    evict_policy: int = 0          # 0 Belady under pressure, 1 evict at freeze (round-1 policy)
+    pool_reserve: int = 0
     nccl_world1: bool = False      # attach a one-rank NCCL communicator (attend -> all-reduce -> decide)
     logits_dtype: str = "bf16"     # "f32": the same (bf16-exact) logits passed as fp32
     history_window: int = 0        # W (NEXT-3): 0 = lifetime counts
@@ -85,7 +87,7 @@ def asr_cfg(c: Case):
                   window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
                   score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window,
                   pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min, history_window=c.history_window,
-                  fr_clear_counts=c.fr_clear_counts)
+                  fr_clear_counts=c.fr_clear_counts, evict_policy=c.evict_policy, pool_reserve=c.pool_reserve)
 
 
 def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:
@@ -191,6 +193,7 @@ def run(c: Case, check_o: bool = True) -> dict:
                 # every attended token held a device slot (else the device would have latched an error)
                 assert g["resident"] >= g["active"], where
                 evicted_total += g["evicted_this_step"]
+                assert g["free_slots"] >= 0, where
                 prefetched_total += g["prefetched_this_step"]
                 demand_total += g["demand_restored_this_step"]
     # exact restoration ("no permanent information loss"): every stored token's bytes, on the

@@ -95,20 +95,21 @@ def test_pressure_mode_tiny(dtype):
     # evict every freeze (evict_min=1): frozen tokens leave the device and are prefetched back one step
     # before they return (early on the sublinear schedule gives 1-2 step absences, so the pool still
     # needs ~n slots here); results identical to the oracle, bytes restored exactly
-    s = run(Case(prompt=(32,), steps=64, window=8, seed=61, dtype=dtype, pool_tokens=100, evict_min=1))
+    s = run(Case(prompt=(32,), steps=64, window=8, seed=61, dtype=dtype, pool_tokens=100, evict_min=1, evict_policy=1))
     assert s["evicted"] > 0 and s["prefetched"] > 0
 
 
 def test_pressure_mode_llama_heads_and_recovery():
     # MMA attention path with slot indirection; planted entropy spikes force demand copies (SR/WR/FR)
     c = Case(L=2, Hq=32, Hkv=8, d=128, B=2, prompt=(40, 25), steps=110, window=8, vocab=128256, seed=71,
-             spike_first=50, spike_period=16, spike_count=4, pool_tokens=300, hot_permille=300, a_hot=64)
+             spike_first=50, spike_period=16, spike_count=4, pool_tokens=300, hot_permille=300, a_hot=64,
+             evict_policy=1)
     s = run(c)
     assert s["evicted"] > 0 and s["prefetched"] > 0 and s["demand"] > 0
 
 
 def test_pressure_mode_explicit_restore_and_evict_threshold():
-    s = run(Case(B=2, prompt=(30, 12), steps=70, window=4, seed=81, pool_tokens=200, evict_min=1,
+    s = run(Case(B=2, prompt=(30, 12), steps=70, window=4, seed=81, pool_tokens=200, evict_min=1, evict_policy=1,
                  restore_at={40: (-1, 3), 55: (0, 1)}))
     assert s["evicted"] > 0 and s["demand"] > 0
 
@@ -185,3 +186,25 @@ def test_fused_tail_mode(fused_tail, B):
     # finite W, planted entropy spikes (recovery recompacts A_i mid-kernel at batch 1: redo pass)
     run(Case(L=2, Hq=32, Hkv=8, d=128, B=B, prompt=(60, 41, 33)[:B], steps=150, window=8, vocab=128256,
              seed=710 + B, spike_first=50, spike_period=16, spike_count=4, history_window=64))
+
+
+# ------------------------------------------------------------------ (a5) capacity-driven Belady eviction
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_pressure_belady_tight_pool(dtype):
+    # a pool smaller than the context: nothing is evicted until the free stack runs short; then the
+    # resident frozen tokens returning last go first.  All-cold prompt of 64 + 200 steps, K = 8:
+    # 264 tokens on a 220-slot pool (the trace needs >= 207 at once: A_{i+1} + the tokens returning
+    # at step i+1's tick + the spare; a smaller pool is infeasible for any policy).  Results bitwise
+    # the oracle's; bytes restored exactly.
+    s = run(Case(prompt=(64,), steps=200, window=8, seed=62, dtype=dtype, pool_tokens=220))
+    assert s["evicted"] > 0 and s["prefetched"] > 0
+
+
+def test_pressure_belady_llama_batch_with_recovery():
+    # MMA path, 2 sequences (410 tokens) sharing one 390-slot pool (the all-cold lockstep cohorts need
+    # up to 360 slots at once near the end), a planted spike (SR); the per-step cut keeps the free
+    # stack above the next step's appends + prefetches + pool_reserve
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=2, prompt=(80, 50), steps=140, window=8, vocab=128256, seed=72,
+             spike_first=60, spike_period=16, spike_count=1, pool_tokens=390, pool_reserve=24)
+    s = run(c)
+    assert s["evicted"] > 0 and s["prefetched"] > 0
