@@ -5,15 +5,21 @@ JSON line on rank 0.  A "step" = one asr_step over the context's batch: append, 
 + recovery, compaction, split-KV attention over the active set with the fused Eq. 2 score,
 combine, decide + tick, and the host-mirror copy — every stage of SURVEY.md §8(a).
 
-Workload (BASELINE.json configs[1]): LLaMA-3-8B shape (32 layers, 32 q / 8 KV heads, d=128,
-vocab 128256), bf16 KV, window K=512, tau=0.5, k=2, batch 1 per GPU, 8K context reached by decoding
-from a 512-token prompt ("grown" state), synthetic LAT inputs (all-cold W0 by default,
---family w1 for the 30 % hot mix).  Metric: decode tokens/s (unit tok/s, whole job = all ranks).
+Workload (BASELINE.json configs[1], the headline): LLaMA-3-8B shape (32 layers, 32 q / 8 KV heads,
+d=128, vocab 128256), bf16 KV, window K=512, tau=0.5, k=2, batch 1 per GPU, 8K context reached by
+decoding from a 512-token prompt ("grown" state), synthetic LAT inputs (all-cold W0 by
+default, --family w1 for the 30 % hot mix).  Metric: decode tokens/s (unit tok/s, whole job = all
+ranks).  Further points (--points, each with its own roofline line): configs[2] (8K, batch 64),
+32K at batch 1 (the north_star's context), configs[3] (32K prefill, batch 16, needle + entropy-
+triggered recovery), the 30 % hot mix, tau = 0 (full KV), pressure mode (50 % device pool, Belady),
+the next-token draw, policy replay and the quantised frozen tier.  --workload c4: configs[4]'s
+per-GPU share (256 sequences at 32K over --gpus ranks, no host mirror).
 
 Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching stream
 with a 256 MiB L2 flush between steps (outside the events); barrier + synchronize on both sides;
 the max over ranks of the summed step times.  Multi-GPU: one process per GPU, each rank owns its own
-batch (sequence sharding, no collective on the hot path) -> "scaling": "weak".
+batch (sequence sharding, no collective on the hot path) -> "scaling": "weak"; `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -54,17 +60,32 @@ def parse():
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: never evict tokens returning sooner")
     ap.add_argument("--evict-policy", type=int, default=0, help="pressure mode: 0 Belady under pressure, 1 at freeze")
-    ap.add_argument("--points", default="cfg3,w1,full,sample,replay,quant",
+    ap.add_argument("--points", default=parse_default_points(),
                     help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
+    ap.add_argument("--workload", default="c1", choices=["c1", "c3", "c4"],
+                    help="c1: grown state (configs[1]/[2] and the context points); c3: configs[3] (32K prefill, "
+                         "needle + entropy spikes); c4: configs[4]'s per-rank share (256/N sequences at 32K)")
+    ap.add_argument("--no-mirror", action="store_true", help="full residency without the pinned host mirror")
     ap.add_argument("--head-shard", action="store_true",
                     help="N>1: split the KV heads across ranks (NCCL score all-reduce) instead of the sequences")
     return ap.parse_args()
 
 
+C3_Q = 55         # configs[3]: first step at which the prefill cohort (and the needle) is frozen with timer
+                  # >= 2 (d = 3 from c = 36; tests/test_needle_gpu.py finds it with the oracle
+                  # and asserts 55)
+C3_NEEDLE = 16384
+
+
 def gen_params(a, rank: int):
     import gen
-    return gen.GenParams(seed=a.seed + 7919 * rank, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D,
-                         hot_permille=300 if a.family == "w1" else 0, a_hot=4, vocab=VOCAB)
+    g = gen.GenParams(seed=a.seed + 7919 * rank, family=gen.LAT, L=L, Hq=HQ, Hkv=HKV, d=D,
+                      hot_permille=300 if a.family == "w1" else 0, a_hot=4, vocab=VOCAB)
+    if a.workload == "c3":   # needle in every sequence, retrieval queries after q, spikes -> SR at q+1, WR at q+17
+        g.needle_pos, g.needle_b = C3_NEEDLE, -1
+        g.query_first, g.query_count = C3_Q + 1, 8
+        g.spike_first, g.spike_period, g.spike_count = C3_Q, 16, 2
+    return g
 
 
 def measured_peak_hbm():
@@ -113,35 +134,36 @@ class Clocks:
 
 # ------------------------------------------------------------------------------------ oracle arm
 
-def oracle_sample(a, seconds_budget: float, steps: int | None = None, warmup: int = 0, layers: int = 2):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the same workload: one sequence at
-    the same context, warm ledger from the policy-only replay (untimed), then full oracle steps over
-    `layers` of the 32 layers.  tokens/s = (layers/32 of a token per step) / time."""
+def _oracle_worker(wid: int, layers: int, context: int, window: int, family: str, seed: int, seconds: float,
+                   steps, warmup: int, q) -> None:
+    """One host core: the fp64 oracle (as it stands) on `layers` of the 32 layers of the workload's
+    sequence, warm ledger from the oracle's own policy replay (untimed, the grown state), then full
+    oracle steps (Alg. 1 lines 1-15 over the explicit A_i) timed one by one."""
     import numpy as np
 
     import gen
     import oracle
-    g = gen_params(a, 0)
-    g.L = layers
-    P = a.window
-    grow = a.context - P - 1
-    total_steps = (steps if steps is not None else 10_000) + warmup
-    cap = a.context + total_steps + 1
-    cfg = oracle.OrcCfg(L=layers, Hq=HQ, Hkv=HKV, d=D, window=a.window, tau=0.5, softness=2.0, vocab=VOCAB)
+    g = gen.GenParams(seed=seed, family=gen.LAT, L=layers, Hq=HQ, Hkv=HKV, d=D,
+                      hot_permille=300 if family == "w1" else 0, a_hot=4, vocab=VOCAB)
+    P = window
+    grow = context - P - 1
+    total_steps = (steps if steps is not None else 100_000) + warmup
+    cap = context + total_steps + 1
+    cfg = oracle.OrcCfg(L=layers, Hq=HQ, Hkv=HKV, d=D, window=window, tau=0.5, softness=2.0, vocab=VOCAB)
     K, V = gen.kv(g, 0, 0, cap)
     s = oracle.OracleSeq(cfg, cap, P)
     below = np.ones(cap, np.uint8)
-    if a.family == "w1":
+    if family == "w1":
         for j in range(cap):
             below[j] = 0 if gen.is_hot(g, 0, j) else 1
-    for i in range(grow):
+    for _ in range(grow):
         s.step_policy(below)
     done, t_total, i = 0, 0.0, grow
     while True:
-        q = gen.q(g, 0, i)
+        qv = gen.q(g, 0, i)
         lg = gen.logits(g, 0, i - 1)
         t0 = time.perf_counter()
-        s.step(q, K, V, lg)
+        s.step(qv, K, V, lg)
         dt = time.perf_counter() - t0
         i += 1
         if warmup > 0:
@@ -151,26 +173,49 @@ def oracle_sample(a, seconds_budget: float, steps: int | None = None, warmup: in
         t_total += dt
         if steps is not None and done >= steps:
             break
-        if steps is None and t_total >= seconds_budget:
+        if steps is None and t_total >= seconds:
             break
-    frac = layers / L
-    return {"value": done * frac / t_total, "steps": done, "seconds": t_total,
-            "sample": f"1 sequence x {done} decode steps at n~{a.context} over {layers} of {L} layers "
-                      f"(policy-replay warm ledger), fp64 C oracle, tokens scaled by {layers}/{L}"}
+    q.put((wid, layers, done, t_total))
+
+
+def oracle_sample(a, seconds_budget: float, steps: int | None = None, warmup: int = 0):
+    """Time the fp64 oracle (as it stands) on the box's host cores over the same workload: the 32
+    layers of one decode step are split over min(32, cores) processes (one C oracle each, running
+    concurrently); a step is done when every process has done its layers, so tokens/s =
+    min over processes of steps/s.  Layer subsets decide identically (LAT classes hold per head:
+    DESIGN.md §4), so every process replays the same ledger."""
+    import multiprocessing as mp
+    cores = max(1, min(L, os.cpu_count() or 1))
+    per = [L // cores + (1 if r < L % cores else 0) for r in range(cores)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_oracle_worker, args=(w, per[w], a.context, a.window, a.family, a.seed,
+                                                      seconds_budget, steps, warmup, q)) for w in range(cores)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=3600) for _ in procs]
+    for pr in procs:
+        pr.join()
+    rate = min(done / t for _, _, done, t in res)             # full steps (tokens) per second
+    done = min(d for _, _, d, _ in res)
+    return {"value": rate, "steps": done, "seconds": done / rate, "cores": cores,
+            "sample": f"1 sequence x {done} decode steps at n~{a.context}, all {L} layers split over {cores} "
+                      f"host processes (one fp64 C oracle each, concurrent), policy-replay warm ledger"}
 
 
 def run_reference(a, rank: int, world: int):
     if rank != 0:
         return
     r = oracle_sample(a, 0, steps=a.steps, warmup=a.warmup)
-    ms = 1000.0 * r["seconds"] / r["steps"]
-    line = {"impl": "reference", "metric": "decode tokens/s at LLaMA-3-8B shape (8K context, window 512)",
+    ms = 1000.0 / r["value"]
+    line = {"impl": "reference", "metric": "decode tokens/sec at LLaMA-3-8B shape vs context; achieved HBM GB/s vs 8 TB/s",
             "value": r["value"], "unit": "tok/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"llama3-8b-shape ctx{a.context} batch1 window{a.window} {a.family}",
                        "context": a.context, "batch_per_gpu": 1, "window": a.window, "family": a.family},
-            "cpu_baseline": {"value": r["value"], "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": r["sample"]},
+            "cpu_baseline": {"value": r["value"], "unit": "tok/s", "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -193,19 +238,31 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     if a.timeline:
         os.environ["ASR_TIMELINE"] = "1"
     B = a.batch
-    P = a.window
-    grow = a.context - P - 1                     # steps before the measured region starts
     W, K = a.warmup, a.steps
+    if a.workload == "c3":
+        # configs[3]: a 32K prompt (prefill: every token Active, R-prefill), decoded until the needle's
+        # cohort is frozen (step C3_Q); the timed steps cover the spike-triggered SR at C3_Q + 1 and the
+        # retrieval queries, the profiled pass the WR at C3_Q + 17
+        P = a.context - 256
+        grow = max(0, C3_Q - 3 - W)
+    else:
+        P = a.window                             # grown state: decoded from a window-sized prompt
+        grow = a.context - P - 1                 # steps before the measured region starts
     e2e_steps = 0 if a.no_e2e else K
-    max_ctx = a.context + W + 2 * K + e2e_steps + 16
+    max_ctx = P + grow + W + 2 * K + e2e_steps + 16
     g = gen_params(a, 0 if a.head_shard else rank)
     g.Hq, g.Hkv = hq_r, hkv_r
     pool = int(a.pool_frac * B * a.context) + 4 * B if a.pool_frac > 0 else 0
     cfg = Config(n_layers=L, n_q_heads=hq_r, n_kv_heads=hkv_r, head_dim=D, batch=B, max_context=max_ctx,
                  kv_dtype=KV_BF16, window=a.window, tau=a.tau, softness=2.0, vocab=VOCAB, profile_stages=0,
                  device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min, history_window=a.history_window,
-                 evict_policy=a.evict_policy,
+                 evict_policy=a.evict_policy, host_mirror=0 if (a.no_mirror and a.pool_frac == 0) else 1,
                  score_heads=HQ if a.head_shard else 0)
+    need = B * max_ctx * TOKEN_KV_BYTES * (2 if a.workload == "c3" else 1) * 1.03 + (2 << 30)
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    if need > free_b:
+        return {"unavailable": f"{a.workload} batch {B} at {a.context} tokens needs {need / 2**30:.0f} GiB of HBM, "
+                               f"{free_b / 2**30:.0f} GiB free on this GPU (run with more ranks)"}
     bf = torch.bfloat16
     pk = torch.empty((B, P, L, hkv_r, D), dtype=bf, device=dev)
     pv = torch.empty_like(pk)
@@ -306,9 +363,17 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     #      programmatic overlap): per-stage device times and the attention kernel's duration (roofline)
     ctx.set_profile(True)
     ctx.stage_times()
+    recov = []      # configs[3]: recovery actions seen (the spike-triggered ladder), per profiled step
+    att_steps = []  # sum over sequences of |A_i| of every profiled step (stage times are device events:
+                    # the host reads between steps do not enter them)
     for t in range(K):
         flush.zero_()
         ctx.step(Q[W + K + t], KN[W + K + t], VN[W + K + t], o, logits_prev=LG[W + K + t], entropy=ent)
+        sts = [ctx.stats(b) for b in range(B)]
+        att_steps.append(sum(x["attended"] for x in sts))
+        if a.workload == "c3" and sts[0]["recovery_action"]:
+            recov.append({"step": int(sts[0]["step"]), "level": int(sts[0]["recovery_action"]),
+                          "restored": int(sts[0]["restored_this_step"])})
     torch.cuda.synchronize()
     stage_ms, launches = ctx.stage_times()
     ctx.set_profile(False)
@@ -359,10 +424,11 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                     "tail_barrier_arrive_release_decide_tick_count_lookback_write_first_us": med[15:23],
                     "cta_past_attention_past_phaseB_wait_us": med[23:25], "tail_dry_pass_end_us": med[25:26]}
         print("timeline (us):", json.dumps(tls), file=sys.stderr)
-    # attended per step: |A_i| drifts by at most a few tokens over K steps; read the last step's
-    # and reconstruct the timed steps' sum from the step statistics recorded by a second pass below
+    # attended per step: the mean over the profiled pass's steps (the K steps right after the timed
+    # ones; |A_i| drifts by a few tokens per step in the grown state and cycles with the cohort in
+    # configs[3]'s prefill state, so the mean over K steps stands for the timed steps)
     att_last = sum(s["attended"] for s in stats)
-    att_prof = sum(s["attended"] for s in stats_p)
+    att_prof = sum(att_steps) / len(att_steps)
     total_t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(total_t, op=dist.ReduceOp.MAX)
@@ -389,14 +455,22 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        # the library's pipelined host I/O (inputs of step t+1 copied while step t computes, outputs of
+        # step t copied while step t+1 computes), with the same L2 flush before every step as the
+        # device-timed loop: the flushes are bracketed by their own events and their time subtracted
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
         e0.record(st)
         for t in range(e2e_steps):
+            fev[t][0].record(st)
+            flush.zero_()
+            fev[t][1].record(st)
             ctx.step(hq_rs[t], HKs[t], HVs[t], ho, logits_prev=HLs[t], entropy=he)
         ctx.flush()   # the stream waits for the last step's outputs to land in host memory
         e1.record(st)
         torch.cuda.synchronize()
-        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        e2e_total = e0.elapsed_time(e1) - sum(f0.elapsed_time(f1) for f0, f1 in fev)
+        e2e_ms = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         h2d = B * (L * hq_r * D * 2 + 2 * L * hkv_r * D * 2 + VOCAB * 2)
@@ -404,7 +478,8 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         e2e = {"value": B * e2e_steps * (1 if a.head_shard else world) / (float(e2e_ms.item()) / 1000.0), "unit": "tok/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "asr_step with pinned host q/k/v/logits in and o/entropy out, copies inside the timed region "
-                       "(the library overlaps them with neighbouring steps on two copy streams)"}
+                       "(the library overlaps them with neighbouring steps on two copy streams); L2 flushed before "
+                       "every step, the flushes' own event-timed durations subtracted"}
     # ---- roofline of the dominant kernel (attention + fused score), measured live via stage events
     attn_ms = stage_ms[1]
     # algorithmic bytes per attended token-layer: K+V rows (2*Hkv*d*2 B) + index (4 B) + score partial (4 B);
@@ -415,8 +490,9 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     if a.pool_frac == 0 and B * (64 + L) <= n_sms:
         bytes_per_step += B * (VOCAB * 2 + 2 * (2 * L * hkv_r * D * 2))
     achieved_prof = bytes_per_step * K / (attn_ms / 1000.0) / 1e9
-    # the kernel alone moves the attention's bytes only (no phase A inside); its A is the next step's
-    att_next = att_prof + B
+    # the kernel alone moves the attention's bytes only (no phase A inside); its A is the next step's:
+    # the post-step Active tokens + the one the next step appends, per sequence
+    att_next = sum(x["active"] + 1 for x in stats_p)
     bytes_alone = L * att_next * (2 * hkv_r * D * 2 + 8) + B * L * hq_r * D * 2
     achieved = bytes_alone / (attn_alone_ms / 1000.0) / 1e9
     peak, peak_kind = measured_peak_hbm()
@@ -430,6 +506,26 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         pass
     # sequence sharding: every rank decodes its own batch; head sharding: all ranks decode one batch
     value = B * K * (1 if a.head_shard else world) / (total_max / 1000.0)
+    # the whole step against the same roofline: the attention's algorithmic bytes of a mean step (the
+    # profiled pass's |A_i|) / the timed step time
+    step_bytes = L * att_prof * (2 * hkv_r * D * 2 + 8) + B * L * hq_r * D * 2
+    step_gbs = step_bytes / (total_max / K / 1000.0) / 1e9
+    stall_ns = (stats[0]["h2d_stall_ns"] - io0["h2d_stall_ns"]) / K if pool else 0.0
+    link_peak = None
+    if pool and rank == 0:   # pinned host -> device cudaMemcpyAsync peak on this box, same run
+        hbuf = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        dbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        for _ in range(2):
+            dbuf.copy_(hbuf, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(5):
+            dbuf.copy_(hbuf, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        link_peak = 5 * (256 << 20) / (e0.elapsed_time(e1) / 1000.0) / 1e9
+        del hbuf, dbuf
     ctx.close()
     del Q, KN, VN, LG, flush_w, flush_r
     torch.cuda.empty_cache()
@@ -438,18 +534,28 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     cpu = None
     if not a.no_cpu_baseline and world == 1:
         r = oracle_sample(a, a.cpu_seconds)
-        cpu = {"value": r["value"], "unit": "tok/s", "cores": 1, "kind": "oracle", "sample": r["sample"]}
+        cpu = {"value": r["value"], "unit": "tok/s", "cores": r["cores"], "kind": "oracle", "sample": r["sample"]}
+    if a.workload == "c3":
+        wl = f"configs[3]: llama3-8b-shape ctx{a.context} prefill batch{B} window{a.window} needle+entropy-spikes"
+        state = f"{P}-token prompt (prefill, every token Active), decoded to step {C3_Q - 3} before timing"
+    elif a.workload == "c4":
+        wl = f"configs[4] share: llama3-8b-shape ctx{a.context} batch{B}/rank of {B * world} window{a.window} {a.family}"
+        state = "grown from a 512-token prompt"
+    else:
+        wl = (f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
+              + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else "")
+              + (f" W{a.history_window}" if a.history_window else ""))
+        state = "grown from a 512-token prompt"
     line = {
-        "metric": "decode tokens/s at LLaMA-3-8B shape (8K context, window 512)",
+        "metric": "decode tokens/sec at LLaMA-3-8B shape vs context; achieved HBM GB/s vs 8 TB/s",
         "value": value, "unit": "tok/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": total_max / K, "higher_is_better": True, "scaling": "strong" if a.head_shard else "weak",
         "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
-                               + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else "")
-                               + (f" W{a.history_window}" if a.history_window else ""),
+        "config": {"workload": wl,
                    "context": a.context, "batch_per_gpu": B, "window": a.window, "tau": a.tau, "k": 2,
-                   "family": a.family, "state": "grown from a 512-token prompt", "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events); active KV 177 MB > 126 MB L2",
+                   "family": a.family, "state": state,
+                   "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)",
                    "parallelism": (f"head-sharded x{world} (NCCL all-reduce of per-token partial scores)" if a.head_shard
                                    else f"sequence-sharded x{world} (no hot-path collective)")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -458,6 +564,9 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                      "bytes_per_launch": bytes_alone, "ms_per_launch": attn_alone_ms,
                      "timing": f"CUDA events around {R} back-to-back launches of the attention kernel over the "
                                "A_i of the measured workload (asr_time_attention, after an L2 flush; median of 3)",
+                     "step_level": {"achieved": step_gbs, "frac": step_gbs / peak, "bytes_per_step": step_bytes,
+                                    "timing": "the attention's algorithmic bytes per step / the timed step time "
+                                              "(every stage of the step in the denominator)"},
                      "profiled_pass": {"achieved": achieved_prof, "frac": achieved_prof / peak,
                                        "bytes_per_launch": bytes_per_step, "ms_per_launch": attn_ms / K,
                                        "timing": "CUDA event nodes around the kernel inside K further steps "
@@ -472,25 +581,37 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                     "total_tokens": sum(s_["total"] for s_ in stats),
                     "h2d_bytes_per_step": h2d_timed / K, "d2h_bytes_per_step": d2h_timed / K,
                     "host_link_gbs": (h2d_timed + d2h_timed) / (total_max / 1000.0) / 1e9,
-                    "note": "H2D = prefetch + demand copies of evicted tokens; D2H = write-once mirror of appended tokens"},
-        "detail": {"attended_per_step": att_last / B, "active_post": stats[0]["active"], "total": stats[0]["total"],
+                    "host_link_peak_gbs": link_peak,
+                    "host_link_frac": ((h2d_timed / (total_max / 1000.0) / 1e9) / link_peak) if link_peak else None,
+                    "evict_policy": ("belady" if a.evict_policy == 0 else "at-freeze") if pool else None,
+                    "h2d_stall_us_per_step": stall_ns / 1000.0,
+                    "note": "H2D = prefetch + demand copies of evicted tokens (device-driven gather over the mapped "
+                            "mirror); D2H = write-once mirror of appended tokens; host_link_peak = pinned "
+                            "cudaMemcpyAsync H2D of 256 MiB in the same run; stall = demand copies + prefetch copies "
+                            "outlasting the attention kernel (device clock)"},
+        "detail": {"attended_per_step": att_prof / B, "attended_per_step_range": [min(att_steps) / B, max(att_steps) / B],
+                   "active_post": stats[0]["active"], "total": stats[0]["total"],
                    "compression": stats[0]["compression"],
                    "stage_ms_per_step_profiled": {n: v / K for n, v in zip(STAGES, stage_ms)},
                    "profiled_launches": launches,
                    "timeline": timeline,
                    "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
                    "wall_s_timed": t_wall, "grow_s": t_grow,
-                   "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES},
+                   "host_link_d2h_mirror_bytes_per_step": B * TOKEN_KV_BYTES if cfg.host_mirror else 0,
+                   "recovery_in_profiled_pass": recov if a.workload == "c3" else None},
     }
     return line
 
 
 POINTS = {   # extra workloads measured after the headline
-    "cfg3": dict(batch=64, steps=16, warmup=4, pool_frac=0.0),    # BASELINE.json configs[2]: 8K, batch 64
+    "c2": dict(batch=64, steps=16, warmup=4, pool_frac=0.0),        # BASELINE.json configs[2]: 8K, batch 64
+    "ctx32k": dict(context=32768, steps=32, no_mirror=True),        # the north_star's 32K context, batch 1
+    "c3": dict(workload="c3", context=32768, batch=16, steps=16, warmup=3, no_mirror=True),   # configs[3]
     "w1": dict(family="w1"),                                        # 30 % hot tokens (SURVEY W1 family)
     "full": dict(tau=0.0),                                          # full-KV baseline: nothing freezes
-    "ctx32k": dict(context=32768, steps=32),                        # configs[3]-like length, grown state
+    "pool": dict(pool_frac=0.5, steps=16, warmup=4),                # pressure mode: 50 % device pool, Belady
     "w128": dict(history_window=128),                               # NEXT-3: finite history window W
+    "c4share": dict(workload="c4", context=32768, batch=32, steps=8, warmup=3, no_mirror=True),  # opt-in
 }
 
 
@@ -623,49 +744,89 @@ def replay_point(local_rank: int) -> dict:
             "total": st["total"]}
 
 
+def spawn_ranks(a) -> int:
+    """`--gpus N` outside torchrun: re-launch this command as N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1 and return its exit code (rank 0 prints the line)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(spawn_ranks(a))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} but WORLD_SIZE={world}: launch one rank per GPU"}), flush=True)
+        sys.exit(2)
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
+    if a.workload == "c4":
+        # configs[4]: 256 sequences at 32K sharded by sequence over the ranks (weak in the per-rank share)
+        a.context, a.batch, a.no_mirror = 32768, max(1, 256 // world), True
+        a.points = a.points if a.points != parse_default_points() else ""
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_asr(a, rank, world, local_rank)
+    if line is not None and "unavailable" in line:
+        print(json.dumps({"metric": "decode tokens/sec at LLaMA-3-8B shape vs context; achieved HBM GB/s vs 8 TB/s",
+                          "unavailable": line["unavailable"], "n_gpus": world}), flush=True)
+        sys.exit(0)
     points = {}
-    for name in [x for x in a.points.split(",") if x and x not in ("sample", "replay", "quant")]:
+    wanted = [x for x in a.points.split(",") if x]
+    for name in [x for x in wanted if x not in ("sample", "replay", "quant")]:
         b = argparse.Namespace(**vars(a))
         for k, v in POINTS[name].items():
             setattr(b, k, v)
         b.no_e2e, b.no_cpu_baseline, b.timeline = True, True, False
         r = run_asr(b, rank, world, local_rank)
-        if r is not None:
-            points[name] = {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
-                            "ms_per_step": r["ms_per_step"], "steps": r["steps"], "warmup": r["warmup"],
-                            "roofline": {k: r["roofline"][k] for k in ("achieved", "peak", "frac", "unit")},
-                            "offload": r["offload"], "clocks": r["clocks"],
-                            "attended_per_step": r["detail"]["attended_per_step"],
-                            "compression": r["detail"]["compression"]}
-    if line is not None and world == 1 and "sample" in [x for x in a.points.split(",") if x]:
+        if r is None:
+            continue
+        if "unavailable" in r:
+            points[name] = {"unavailable": r["unavailable"]}
+            continue
+        points[name] = {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
+                        "ms_per_step": r["ms_per_step"], "steps": r["steps"], "warmup": r["warmup"],
+                        "roofline": {k: r["roofline"][k] for k in ("bound", "achieved", "peak", "frac", "unit",
+                                                                   "bytes_per_launch", "ms_per_launch")},
+                        "step_level": r["roofline"]["step_level"],
+                        "offload": r["offload"], "clocks": r["clocks"], "gpu_launches": r["gpu_launches"],
+                        "attended_per_step": r["detail"]["attended_per_step"],
+                        "compression": r["detail"]["compression"],
+                        "state": r["config"]["state"]}
+        if r["detail"].get("recovery_in_profiled_pass") is not None:
+            points[name]["recovery_in_profiled_pass"] = r["detail"]["recovery_in_profiled_pass"]
+    if line is not None and world == 1 and "sample" in wanted:
         line["detail"]["next_token_draw"] = sample_point(local_rank)
-    if line is not None and world == 1 and "replay" in [x for x in a.points.split(",") if x]:
+    if line is not None and world == 1 and "replay" in wanted:
         line["detail"]["policy_replay"] = replay_point(local_rank)
-    if line is not None and world == 1 and "quant" in [x for x in a.points.split(",") if x]:
+    if line is not None and world == 1 and "quant" in wanted:
         line["detail"]["frozen_tier_quant"] = quant_point(local_rank)
     if line is not None:
         if points:
             line["points"] = points
-            if "full" in points and points["full"]["value"] > 0:   # ASR-KF-EGR vs attending the whole cache
+            if "full" in points and points["full"].get("value", 0) > 0:   # ASR-KF-EGR vs attending the whole cache
                 line["detail"]["speedup_vs_full_kv"] = line["value"] / points["full"]["value"]
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def parse_default_points() -> str:
+    return "c2,ctx32k,c3,w1,full,pool,sample,replay,quant"
 
 
 if __name__ == "__main__":

@@ -137,3 +137,26 @@ def test_sharded_batch_equals_whole_batch_on_oracle():
             np.testing.assert_array_equal(o1, o2)
             np.testing.assert_array_equal(a1, a2)
             assert n1 == n2
+
+
+def test_bench_gpus_n_spawns_ranks_and_checks_world():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run on
+    127.0.0.1); rank 0 alone prints the line.  Exercised on CPU through the reference arm (the
+    oracle), which needs no GPU; a WORLD_SIZE that contradicts --gpus is refused."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    args = [sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+            "--warmup", "0", "--context", "560", "--window", "512"]
+    r = subprocess.run(args, capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["cores"] >= 1
+    env["WORLD_SIZE"] = "1"
+    r = subprocess.run(args, capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stdout

@@ -44,6 +44,7 @@ def test_needle_restore_ladder_32k(pool):
 
     P = CTX - 256
     q = find_q(P)
+    assert q == 55   # SURVEY A.6 (prefill lockstep, d = 3 from c = 36): bench.py's configs[3] point relies on it
     steps = q + 56
     p = gen.GenParams(seed=4001, L=L, Hq=HQ, Hkv=HKV, d=D, needle_pos=NEEDLE, query_first=q + 1, query_count=8,
                       vocab=V, spike_first=q, spike_period=16, spike_count=4)
@@ -53,7 +54,8 @@ def test_needle_restore_ladder_32k(pool):
     pk = torch.stack([to_t(KVs[b][0][:P]) for b in range(B)])
     pv = torch.stack([to_t(KVs[b][1][:P]) for b in range(B)])
     cfg = Config(n_layers=L, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=cap, window=K, vocab=V,
-                 pool_tokens=(B * cap + 4 * B) if pool else 0, evict_min_absence=2)
+                 pool_tokens=(B * cap + 4 * B) if pool else 0, evict_min_absence=2,
+                 evict_policy=1)   # at-freeze eviction: the pool holds everything, Belady would evict nothing
     ctx = Context(cfg, pk, pv, [P] * B)
     del pk, pv
     ocfg = oracle.OrcCfg(L=L, Hq=HQ, Hkv=HKV, d=D, window=K, vocab=V)
