@@ -378,7 +378,10 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(c->alloc(&s.score_part, BT * s.L * 4));
     CUDA_TRY(c->alloc(&s.score, BT * 4));
     size_t max_items = (size_t)s.B * s.L * s.max_splits;
-    if (max_items < (size_t)s.B * s.L + c->num_sms) max_items = (size_t)s.B * s.L + c->num_sms;   // stream-K
+    const size_t sk_slots = (size_t)s.B * s.L + (size_t)c->num_sms * (1 + asr::kSkMaxChunksPerCta);   // units
+    if (max_items < sk_slots) max_items = sk_slots;
+    CUDA_TRY(c->alloc(&s.sk_ctr, 8));
+    CUDA_TRY(cudaMemsetAsync(s.sk_ctr, 0, 8, st));
     CUDA_TRY(c->alloc(&s.part_ml, max_items * s.Hq * 2 * 4));
     CUDA_TRY(c->alloc(&s.part_acc, max_items * s.Hq * s.d * 4));
     CUDA_TRY(c->alloc(&s.ent_part, (size_t)s.B * asr::kEntSplits * 3 * 4));
@@ -479,6 +482,15 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
       asr::node_prepare(pn, s);
       CUDA_TRY(pn.launch(st));
       CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    {   // dynamic tail of the attention's work split (asr_internal.h): 1/sk_dyn of the tiles in chunks
+      const char* sd = getenv("ASR_SK_DYN");
+      const char* sc = getenv("ASR_SK_CHUNK");
+      // measured (profiles/r2): batch 64 at 8K 1890 -> 1810 us per step; batch 1 loses 1-5 us (chunk
+      // overheads and the producer's registers), so batch < 16 keeps the static split
+      s.sk_dyn = sd ? atoi(sd) : (s.B >= 16 ? 8 : 0);
+      s.sk_chunk = sc ? atoi(sc) : 2;
+      if (s.Hkv != 8) s.sk_dyn = 0;   // the dynamic variant is compiled for 8 KV heads only
     }
     const char* ke = getenv("ASR_KV_EVICT_FIRST");
     s.kv_evict_first = !(ke && ke[0] == '0');

@@ -85,6 +85,8 @@ struct DevState {
   int max_splits, chunk_min;
   int decide_blocks;          // blocks per sequence of the decide kernel
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
+  int sk_dyn, sk_chunk;       // 1/sk_dyn of the tiles go out as dynamic chunks of sk_chunk tiles (0: none)
+  int32_t* sk_ctr;            // [2] next dynamic chunk, CTAs done with chunks (the last one resets both)
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
   int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
   const float* ext_score;     // policy replay (NEXT-2): s_j given per position [B][max_ctx]; NULL = Eq. 2
@@ -228,16 +230,42 @@ __host__ __device__ inline void chunking(int A, int max_splits, int chunk_min, i
   *nch = (A + c - 1) / c;
 }
 
-// Stream-K split of the tensor-core attention (DevState::sk_grid = G > 0).  The L * ceil(A_b / 16)
-// 16-token tiles of all (b, l) items, in (b, l, tile) order, T in total, are cut into G contiguous
-// ranges [floor(cT/G), floor((c+1)T/G)), one per CTA, so every CTA streams the same number of tiles
-// (+-1); G = sk_span(T, grid) = min(grid, T) keeps every range non-empty (CTAs >= G idle).  The part of item i = b*L + l that CTA c covers writes its softmax partial to slot i + c
-// (unique: both indices grow along the tile order), so item i's partials are the consecutive slots
-// i + sk_cta_of(S_i) .. i + sk_cta_of(S_i + tiles_b - 1), S_i = item_start[b] + l * tiles_b, and there
-// are at most B*L + G of them.  sk_cta_of(t) = the CTA whose range holds tile t.
+// Work split of the tensor-core attention (DevState::sk_grid = grid > 0).  The L * ceil(A_b / 16)
+// 16-token tiles of all (b, l) items, in (b, l, tile) order, T in total, are handed out as *units*:
+// the first Ts tiles are cut into G = min(grid, Ts) contiguous static ranges [floor(cTs/G),
+// floor((c+1)Ts/G)), one per CTA (units 0..G-1) — stream-K; the last T/sk_dyn tiles (nchunks chunks
+// of C tiles) are taken dynamically (units G + k, chunk k drawn from an atomic ticket) by the CTAs
+// that finish their range first: SMs stream at different rates (the last CTA of a purely static
+// split ended 25-35 % after the first; profiles/README.md).  The part of item i = b*L + l that unit u
+// covers writes its softmax partial to slot i + u (unique and consecutive per item: units grow along
+// the tile order), so item i's partials are slots i + sk_unit_of(S_i) .. i + sk_unit_of(S_i +
+// tiles_b - 1), S_i = item_start[b] + l * tiles_b; an item inside one unit is written to O directly.
+// Slots: at most B*L + G + nchunks <= B*L + grid * (1 + kSkMaxChunksPerCta).
 constexpr int kSkTile = 16;
+constexpr int kSkMaxChunksPerCta = 8;
 __host__ __device__ inline int sk_span(long T, int grid) { return T < grid ? (int)T : grid; }
 __host__ __device__ inline int sk_cta_of(long t, long T, int G) { return (int)(((t + 1) * (long)G - 1) / T); }
+struct SkPlan {
+  long T, Ts;      // tiles, static tiles
+  int G, C;        // static ranges, tiles per chunk
+  int nchunks;
+};
+__host__ __device__ inline SkPlan sk_plan(long T, int grid, int dyn_div, int chunk) {
+  SkPlan p;
+  p.T = T;
+  const long td = dyn_div > 0 ? T / dyn_div : 0;   // tiles handed out dynamically
+  long c = chunk > 0 ? chunk : 1;
+  const long cmin = (td + (long)kSkMaxChunksPerCta * grid - 1) / ((long)kSkMaxChunksPerCta * grid);
+  if (c < cmin) c = cmin;                          // bounded slot count
+  p.C = (int)c;
+  p.nchunks = (int)(td / p.C);
+  p.Ts = T - (long)p.nchunks * p.C;
+  p.G = sk_span(p.Ts, grid);
+  return p;
+}
+__host__ __device__ inline int sk_unit_of(const SkPlan& p, long t) {
+  return t < p.Ts ? sk_cta_of(t, p.Ts, p.G) : p.G + (int)((t - p.Ts) / p.C);
+}
 
 // One kernel launch described as data, so the same description serves a direct launch
 // (cudaLaunchKernel) and a CUDA-graph kernel node (cudaGraphAddKernelNode /

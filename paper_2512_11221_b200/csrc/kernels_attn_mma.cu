@@ -54,6 +54,7 @@ struct Geo {
     alignas(128) uint8_t q[2][kQBytes];    // q of the current / next work item
     float sc[kStagesRing][HK][kTM];       // per-warp head sums |S| of each token
     int start[kMaxB + 1];                 // work list: first item of each sequence
+    int4 unitq[16][2];                    // work units announced by the producer: cursor, stop, unit
     alignas(8) uint64_t full[kStagesRing];
     alignas(8) uint64_t empty[kStagesRing];
     alignas(8) uint64_t qfull[2];
@@ -237,8 +238,8 @@ __device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
 // With do_pre (batch 1, DevState::pre_in_attn) the CTA's extra warp runs its phase-A unit (entropy
 // split or append; the last unit of the sequence also runs phase B) beside the attention warps.
-template <int HK, typename TL>
-__device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q,
+template <int HK, typename TL, bool DYN>
+__device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bfloat16* __restrict__ q,
                                 const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
                                 typename Geo<HK>::Smem& sm, bool do_pre, const TL* pre_logits, float* entropy_out,
                                 units::UnitShm& u, float* __restrict__ o) {
@@ -261,11 +262,17 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       for (int b = 0; b <= s.B; ++b) s.item_start[b] = sm.start[b];
   }
   __syncthreads();
-  // this CTA's contiguous range of the stream-K tile order over sk_span(T, G) CTAs (gridDim.x == s.sk_grid)
-  const long T = sm.start[s.B];
-  const int Ge = sk_span(T, gridDim.x);
-  const int t_begin = blockIdx.x < Ge ? (int)((long)blockIdx.x * T / Ge) : 0;
-  const int t_end = blockIdx.x < Ge ? (int)((long)(blockIdx.x + 1) * T / Ge) : 0;
+  // units of work (asr_internal.h): this CTA's static stream-K range, then dynamic chunks; the
+  // producer announces each following unit in sm.unitq before the arrive of the current unit's last
+  // tile (a CTA without a static range: before a first arrive on stage 0)
+  // (DYN = false: the static stream-K split alone, compiled without the unit machinery — batch 1's
+  // producer is register-bound and the chunk overheads outweigh the balance there: DESIGN.md §6.1)
+  const SkPlan plan = sk_plan(sm.start[s.B], gridDim.x, DYN ? s.sk_dyn : 0, s.sk_chunk);   // gridDim.x == s.sk_grid
+  int t_begin = 0, t_end = 0;
+  if ((int)blockIdx.x < plan.G) {
+    t_begin = (int)((long)blockIdx.x * plan.Ts / plan.G);
+    t_end = (int)((long)(blockIdx.x + 1) * plan.Ts / plan.G);
+  }
 
   if (warp == kHK) {
     // ================================================================== producer warp
@@ -281,69 +288,188 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
         s.score_part[((long)it.b * s.L + it.l) * s.max_ctx + it.a0 + lane] = t;
       }
     };
-    const char* kvb = reinterpret_cast<const char*>(s.kv);
-    Cursor cur;
-    if (t_begin < t_end) cur.seek(s, alen, sm.start, t_begin);
-    else cur.t = t_end;
-    auto load_idx = [&](const Cursor& c) -> int {
-      if (c.t >= t_end || lane >= c.cnt()) return 0;
-      // device slot; through L2: recovery may recompact A_i while the kernel runs (redo pass)
-      return max(0, __ldcg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));
-    };
-    int j_cur = load_idx(cur);
-    int g = 0, it_local = -1;
-    // L2 policy of the KV stream: evict_first (ASR_KV_EVICT_FIRST=0: evict_normal, for comparison)
-    const uint64_t kv_policy = s.kv_evict_first ? policy_evict_first() : policy_evict_normal();
-    while (cur.t < t_end) {
-      Cursor nxt = cur;
-      nxt.next(s, alen);
-      const int j_next = load_idx(nxt);   // in flight while this tile waits for its stage
-      if (cur.t == t_begin || cur.ti == 0) {   // new piece: stage its q (Hq x 256 B) in the q ring
-        ++it_local;
-        const int qs = it_local & 1;
-        mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
-        if (lane == 0) {
-          mbar_expect_tx(&sm.qfull[qs], (uint32_t)qbytes);
-          bulk_g2s(&sm.q[qs][0], q + ((long)cur.b * s.L + cur.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
+    int g = 0;   // tiles issued (the drain below continues from it)
+    if constexpr (DYN) {
+      const char* kvb = reinterpret_cast<const char*>(s.kv);
+      // dynamic chunks: the ticket is drawn a few tiles before the current unit ends (its latency hidden
+      // behind them) and used when it does
+      int ticket = -1;   // lane 0
+      auto draw = [&]() {
+        if constexpr (DYN)
+          if (lane == 0 && ticket < 0) ticket = plan.nchunks > 0 ? atomicAdd(s.sk_ctr, 1) : plan.nchunks;
+      };
+      auto grab = [&](Cursor& c, int& stop, int& unit) -> bool {
+        if constexpr (!DYN) return false;
+        draw();
+        const int k = __shfl_sync(0xffffffffu, ticket, 0);
+        ticket = -1;
+        if (k >= plan.nchunks) return false;
+        const long t0 = plan.Ts + (long)k * plan.C;
+        stop = (int)min(plan.T, t0 + plan.C);
+        unit = plan.G + k;
+        c.seek(s, alen, sm.start, (int)t0);
+        return true;
+      };
+      auto announce = [&](int slot, bool have, const Cursor& c, int stop, int unit) {
+        if (DYN && lane == 0) {
+          sm.unitq[slot & 15][0] = have ? make_int4(c.t, c.b, c.l, c.ti) : make_int4(-1, 0, 0, 0);
+          sm.unitq[slot & 15][1] = make_int4(c.tiles, c.A, stop, unit);
         }
+      };
+      Cursor cur;
+      int t_stop = t_end, unit = blockIdx.x, u_local = 0;
+      bool have = t_begin < t_end;
+      if (have) {
+        cur.seek(s, alen, sm.start, t_begin);
+      } else if (DYN) {   // no static range: the first unit (or "none", with a bare arrive) for the consumers
+        have = grab(cur, t_stop, unit);
+        announce(0, have, cur, t_stop, unit);
+        if (lane == 0 && !have) mbar_arrive(&sm.full[0]);
       }
-      const int stage = g % kStagesRing;
-      const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
-      mbar_wait(&sm.empty[stage], ph ^ 1u);
-      __syncwarp();
-      epilogue(stage, pend[stage]);
-      const int cnt = cur.cnt();
-      ItemInfo tile{cur.b, cur.l, cur.ti * kTM, cnt};
-#pragma unroll
-      for (int i = 0; i < kStagesRing; ++i)
-        if (i == stage) pend[i] = tile;
-      if (cnt < kTM) {
-        // masked tail rows: their P is 0, but 0 * NaN would poison O, so their V slices get zeros
-        // (generic-proxy stores, ordered before later bulk copies into the same rows by the fence)
-        uint4* z = reinterpret_cast<uint4*>(&sm.kv[stage][0]);
-        const int per_row = kRowBytes / 16;
-        for (int t = cnt; t < kTM; ++t)
-          for (int k = lane; k < per_row; k += 32) z[(t * kTokPad + kRowBytes) / 16 + k] = make_uint4(0, 0, 0, 0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      }
-      if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
-      __syncwarp();
-      if (lane < cnt) {
-        if (cur.ti * kTM + lane == cur.A - 1) {
-          // the token this step appends (always last in A_i): read from the caller's k_new / v_new, so
-          // the attention does not wait for phase A's append
-          const long r = ((long)cur.b * s.L + cur.l) * (kRowBytes / 2);
-          bulk_g2s(&sm.kv[stage][lane * kTokPad], k_new + r, kRowBytes, &sm.full[stage]);
-          bulk_g2s(&sm.kv[stage][lane * kTokPad + kRowBytes], v_new + r, kRowBytes, &sm.full[stage]);
-        } else {
-          const long slot = j_cur;
-          bulk_g2s_hint(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
-                        &sm.full[stage], kv_policy);
+      auto load_idx = [&](const Cursor& c) -> int {
+        if (lane >= c.cnt()) return 0;
+        // device slot; through L2: recovery may recompact A_i while the kernel runs (redo pass)
+        return max(0, __ldcg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));
+      };
+      int j_cur = have ? load_idx(cur) : 0;
+      int it_local = -1;
+      bool unit_first = true;
+      // L2 policy of the KV stream: evict_first (ASR_KV_EVICT_FIRST=0: evict_normal, for comparison)
+      const uint64_t kv_policy = s.kv_evict_first ? policy_evict_first() : policy_evict_normal();
+      while (have) {
+        if (DYN && cur.t + 3 >= t_stop) draw();
+        Cursor nxt = cur;
+        nxt.next(s, alen);
+        int n_stop = t_stop, n_unit = unit;
+        bool n_have = true, n_first = false;
+        if (nxt.t >= t_stop) {   // this is the unit's last tile: announce the next unit (or none)
+          n_have = grab(nxt, n_stop, n_unit);
+          n_first = true;
+          if (DYN) announce(u_local + 1, n_have, nxt, n_stop, n_unit);
         }
+        const int j_next = n_have ? load_idx(nxt) : 0;   // in flight while this tile waits for its stage
+        if (unit_first || cur.ti == 0) {   // new piece: stage its q (Hq x 256 B) in the q ring
+          ++it_local;
+          const int qs = it_local & 1;
+          mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
+          if (lane == 0) {
+            mbar_expect_tx(&sm.qfull[qs], (uint32_t)qbytes);
+            bulk_g2s(&sm.q[qs][0], q + ((long)cur.b * s.L + cur.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
+          }
+        }
+        const int stage = g % kStagesRing;
+        const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
+        mbar_wait(&sm.empty[stage], ph ^ 1u);
+        __syncwarp();
+        epilogue(stage, pend[stage]);
+        const int cnt = cur.cnt();
+        ItemInfo tile{cur.b, cur.l, cur.ti * kTM, cnt};
+  #pragma unroll
+        for (int i = 0; i < kStagesRing; ++i)
+          if (i == stage) pend[i] = tile;
+        if (cnt < kTM) {
+          // masked tail rows: their P is 0, but 0 * NaN would poison O, so their V slices get zeros
+          // (generic-proxy stores, ordered before later bulk copies into the same rows by the fence)
+          uint4* z = reinterpret_cast<uint4*>(&sm.kv[stage][0]);
+          const int per_row = kRowBytes / 16;
+          for (int t = cnt; t < kTM; ++t)
+            for (int k = lane; k < per_row; k += 32) z[(t * kTokPad + kRowBytes) / 16 + k] = make_uint4(0, 0, 0, 0);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
+        __syncwarp();
+        if (lane < cnt) {
+          if (cur.ti * kTM + lane == cur.A - 1) {
+            // the token this step appends (always last in A_i): read from the caller's k_new / v_new, so
+            // the attention does not wait for phase A's append
+            const long r = ((long)cur.b * s.L + cur.l) * (kRowBytes / 2);
+            bulk_g2s(&sm.kv[stage][lane * kTokPad], k_new + r, kRowBytes, &sm.full[stage]);
+            bulk_g2s(&sm.kv[stage][lane * kTokPad + kRowBytes], v_new + r, kRowBytes, &sm.full[stage]);
+          } else {
+            const long slot = j_cur;
+            bulk_g2s_hint(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
+                          &sm.full[stage], kv_policy);
+          }
+        }
+        j_cur = j_next;
+        cur = nxt;
+        if (n_first) ++u_local;
+        t_stop = n_stop;
+        unit = n_unit;
+        unit_first = n_first;
+        have = n_have;
+        ++g;
       }
-      j_cur = j_next;
-      cur = nxt;
-      ++g;
+      // no more chunks for this CTA: the last CTA to get here resets the chunk ticket for the next launch
+      if (DYN && lane == 0 && plan.nchunks > 0 && atomicAdd(s.sk_ctr + 1, 1) == (int)gridDim.x - 1) {
+        s.sk_ctr[0] = 0;
+        s.sk_ctr[1] = 0;
+      }
+    } else {   // static stream-K range only (batch < 16): the round-1 producer, fewest registers
+      const char* kvb = reinterpret_cast<const char*>(s.kv);
+      Cursor cur;
+      if (t_begin < t_end) cur.seek(s, alen, sm.start, t_begin);
+      else cur.t = t_end;
+      auto load_idx = [&](const Cursor& c) -> int {
+        if (c.t >= t_end || lane >= c.cnt()) return 0;
+        // device slot; through L2: recovery may recompact A_i while the kernel runs (redo pass)
+        return max(0, __ldcg(aslot + (long)c.b * s.max_ctx + c.ti * kTM + lane));
+      };
+      int j_cur = load_idx(cur);
+      int it_local = -1;
+      // L2 policy of the KV stream: evict_first (ASR_KV_EVICT_FIRST=0: evict_normal, for comparison)
+      const uint64_t kv_policy = s.kv_evict_first ? policy_evict_first() : policy_evict_normal();
+      while (cur.t < t_end) {
+        Cursor nxt = cur;
+        nxt.next(s, alen);
+        const int j_next = load_idx(nxt);   // in flight while this tile waits for its stage
+        if (cur.t == t_begin || cur.ti == 0) {   // new piece: stage its q (Hq x 256 B) in the q ring
+          ++it_local;
+          const int qs = it_local & 1;
+          mbar_wait(&sm.qempty[qs], ((uint32_t)(it_local >> 1) & 1u) ^ 1u);
+          if (lane == 0) {
+            mbar_expect_tx(&sm.qfull[qs], (uint32_t)qbytes);
+            bulk_g2s(&sm.q[qs][0], q + ((long)cur.b * s.L + cur.l) * s.Hq * kD, (uint32_t)qbytes, &sm.qfull[qs]);
+          }
+        }
+        const int stage = g % kStagesRing;
+        const uint32_t ph = (uint32_t)(g / kStagesRing) & 1u;
+        mbar_wait(&sm.empty[stage], ph ^ 1u);
+        __syncwarp();
+        epilogue(stage, pend[stage]);
+        const int cnt = cur.cnt();
+        ItemInfo tile{cur.b, cur.l, cur.ti * kTM, cnt};
+  #pragma unroll
+        for (int i = 0; i < kStagesRing; ++i)
+          if (i == stage) pend[i] = tile;
+        if (cnt < kTM) {
+          // masked tail rows: their P is 0, but 0 * NaN would poison O, so their V slices get zeros
+          // (generic-proxy stores, ordered before later bulk copies into the same rows by the fence)
+          uint4* z = reinterpret_cast<uint4*>(&sm.kv[stage][0]);
+          const int per_row = kRowBytes / 16;
+          for (int t = cnt; t < kTM; ++t)
+            for (int k = lane; k < per_row; k += 32) z[(t * kTokPad + kRowBytes) / 16 + k] = make_uint4(0, 0, 0, 0);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        if (lane == 0) mbar_expect_tx(&sm.full[stage], (uint32_t)cnt * kTokBytes);
+        __syncwarp();
+        if (lane < cnt) {
+          if (cur.ti * kTM + lane == cur.A - 1) {
+            // the token this step appends (always last in A_i): read from the caller's k_new / v_new, so
+            // the attention does not wait for phase A's append
+            const long r = ((long)cur.b * s.L + cur.l) * (kRowBytes / 2);
+            bulk_g2s(&sm.kv[stage][lane * kTokPad], k_new + r, kRowBytes, &sm.full[stage]);
+            bulk_g2s(&sm.kv[stage][lane * kTokPad + kRowBytes], v_new + r, kRowBytes, &sm.full[stage]);
+          } else {
+            const long slot = j_cur;
+            bulk_g2s_hint(&sm.kv[stage][lane * kTokPad], kvb + (slot * s.L + cur.l) * (long)kTokBytes, kTokBytes,
+                          &sm.full[stage], kv_policy);
+          }
+        }
+        j_cur = j_next;
+        cur = nxt;
+        ++g;
+      }
     }
     // large batches: phase D is not latency-bound; fused tail: the aux warp prefetched at the start
     if (s.B <= 8 && !s.fuse_tail) prefetch_ledger(s, p, alen, step, lane);
@@ -392,10 +518,20 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
   const uint32_t v_lane = (uint32_t)((ri + (mi & 1) * 8) * kTokPad + kRowBytes + warp * kD * 2 + (mi >> 1) * 16);
   int g = 0, it_local = -1;
   Cursor cur;
-  if (t_begin < t_end) cur.seek(s, alen, sm.start, t_begin);
+  int t_stop = t_end, unit = blockIdx.x;
+  const bool has_static = t_begin < t_end;
+  if (has_static) cur.seek(s, alen, sm.start, t_begin);
+  else if (DYN) mbar_wait(&sm.full[0], 0u);   // unit 0 is announced before the first tile's (or a bare) arrive
   else cur.t = t_end;
-  while (cur.t < t_end) {   // one piece (the part of one (b, l) item in this CTA's range) per pass
-    const long piece = (long)cur.b * s.L + cur.l + blockIdx.x;
+  for (int u = 0; DYN || u == 0; ++u) {   // units; unit u + 1 is announced before the arrive of unit u's last tile
+    if (DYN && (u > 0 || !has_static)) {
+      const int4 u0 = sm.unitq[u & 15][0], u1 = sm.unitq[u & 15][1];
+      if (u0.x < 0) break;
+      cur.t = u0.x; cur.b = u0.y; cur.l = u0.z; cur.ti = u0.w;
+      cur.tiles = u1.x; cur.A = u1.y; t_stop = u1.z; unit = u1.w;
+    }
+  while (cur.t < t_stop) {   // one piece (the part of one (b, l) item in this unit) per pass
+    const long piece = (long)cur.b * s.L + cur.l + unit;
     const int pb = cur.b, pl = cur.l;
     const bool from_item_start = cur.ti == 0;
     bool to_item_end = false;
@@ -427,7 +563,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
       more = cur.ti + 1 < cur.tiles;   // the piece ends with its item's last tile or the range's end
       to_item_end = !more;
       cur.next(s, alen);
-      more = more && cur.t < t_end;
+      more = more && cur.t < t_stop;
       mbar_wait(&sm.full[stage], ph);
       const uint32_t ks_addr = kvbase + stage * kStageBytes + k_lane;
       const uint32_t vs_addr = kvbase + stage * kStageBytes + v_lane;
@@ -499,7 +635,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     if (r < G && o && from_item_start && to_item_end) {
-      // the whole item lies in this CTA's range: O directly (the combine skips single-piece items)
+      // the whole item lies in one unit: O directly (the combine skips single-piece items)
       const float inv = 1.0f / l_run;
       float* dst = o + (((long)pb * s.L + pl) * s.Hq + warp * G + r) * kD + 2 * qd;
 #pragma unroll
@@ -514,6 +650,7 @@ __device__ void attention_phase(const DevState& s, const __nv_bfloat16* __restri
 #pragma unroll
       for (int i = 0; i < 16; ++i) *reinterpret_cast<float2*>(dst + i * 8) = make_float2(acc[i][0], acc[i][1]);
     }
+  }
   }
 }
 
@@ -594,7 +731,7 @@ __device__ void fused_tail(const DevState& s, typename Geo<HK>::Smem& sm, int st
 // recompact A_i while the attention runs, every CTA then waits for phase B (*pre_done) and, only if
 // recovery fired (*redo, rare), all CTAs pass a grid barrier and redo the attention over the new A_i.
 // With fuse_tail the kernel then settles the step itself (fused_tail).
-template <int HK, typename TL>
+template <int HK, typename TL, bool DYN>
 __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
     attn_mma_kernel(const __grid_constant__ DevState s, const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k_new,
                     const __nv_bfloat16* __restrict__ v_new, const TL* logits, float* entropy_out, float* o) {
@@ -609,7 +746,7 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
   const int step = *s.step;
   {
     Stamp stamp(s.tl, 1);
-    attention_phase<HK, TL>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
+    attention_phase<HK, TL, DYN>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
     if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 7], gtimer());   // first CTA done
   }
   if (do_pre) {
@@ -633,7 +770,7 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
     if (redo) {
       grid_sync(s.gbar, s.err);    // every CTA is past its first pass
       attention_prologue<HK>(sm);  // fresh ring barriers
-      attention_phase<HK, TL>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
+      attention_phase<HK, TL, DYN>(s, q, k_new, v_new, sm, false, logits, entropy_out, u, o);
     }
   }
   if (s.pool_mode) {   // the attention's end, against which the prefetch copies are timed
@@ -660,36 +797,42 @@ bool attention_mma_supported(const DevState& s) {
   }
 }
 
-template <int HK>
+template <int HK, bool DYN>
 cudaError_t prep_one() {
-  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<HK, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(typename Geo<HK>::Smem));
+  cudaError_t e = cudaFuncSetAttribute(attn_mma_kernel<HK, __nv_bfloat16, DYN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(typename Geo<HK>::Smem));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(attn_mma_kernel<HK, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(attn_mma_kernel<HK, float, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(typename Geo<HK>::Smem));
 }
 
 cudaError_t attention_mma_prepare() {
   cudaError_t e;
-  if ((e = prep_one<8>()) != cudaSuccess || (e = prep_one<4>()) != cudaSuccess || (e = prep_one<2>()) != cudaSuccess ||
-      (e = prep_one<1>()) != cudaSuccess)
+  if ((e = prep_one<8, false>()) != cudaSuccess || (e = prep_one<8, true>()) != cudaSuccess ||
+      (e = prep_one<4, false>()) != cudaSuccess || (e = prep_one<2, false>()) != cudaSuccess ||
+      (e = prep_one<1, false>()) != cudaSuccess)
     return e;
   return cudaSuccess;
 }
 
-template <int HK>
+template <int HK, bool DYN>
 void shape_of(bool lf, const void** func, int* threads, unsigned* smem) {
-  *func = lf ? (const void*)attn_mma_kernel<HK, float> : (const void*)attn_mma_kernel<HK, __nv_bfloat16>;
+  *func = lf ? (const void*)attn_mma_kernel<HK, float, DYN> : (const void*)attn_mma_kernel<HK, __nv_bfloat16, DYN>;
   *threads = Geo<HK>::kThreads;
   *smem = sizeof(typename Geo<HK>::Smem);
 }
 
+// The dynamic work split (DevState::sk_dyn > 0) exists for 8 KV heads only (the host clears sk_dyn
+// otherwise).
 void attention_mma_launch_shape(const DevState& s, bool logits_f32, const void** func, int* threads, unsigned* smem) {
   switch (s.Hkv) {
-    case 8: shape_of<8>(logits_f32, func, threads, smem); break;
-    case 4: shape_of<4>(logits_f32, func, threads, smem); break;
-    case 2: shape_of<2>(logits_f32, func, threads, smem); break;
-    default: shape_of<1>(logits_f32, func, threads, smem); break;
+    case 8:
+      if (s.sk_dyn > 0) shape_of<8, true>(logits_f32, func, threads, smem);
+      else shape_of<8, false>(logits_f32, func, threads, smem);
+      break;
+    case 4: shape_of<4, false>(logits_f32, func, threads, smem); break;
+    case 2: shape_of<2, false>(logits_f32, func, threads, smem); break;
+    default: shape_of<1, false>(logits_f32, func, threads, smem); break;
   }
 }
 

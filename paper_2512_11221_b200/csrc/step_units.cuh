@@ -1090,9 +1090,9 @@ __device__ __noinline__ void combine_warp_tail(const DevState& s, int wid, float
   const int tiles = (is_b1 - is_b) / s.L;
   if (!tiles || T <= 0) return;
   const long S = is_b + (long)l * tiles;
-  const int G = sk_span(T, s.sk_grid);
-  const int cf = sk_cta_of(S, T, G);
-  int nch = sk_cta_of(S + tiles - 1, T, G) - cf + 1;
+  const SkPlan pl = sk_plan(T, s.sk_grid, s.sk_dyn, s.sk_chunk);
+  const int cf = sk_unit_of(pl, S);
+  int nch = sk_unit_of(pl, S + tiles - 1) - cf + 1;
   if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   if (!wr) nch = min(nch, 8);
   const long it0 = (long)b * s.L + l + cf;
@@ -1290,9 +1290,9 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   if (s.sk_grid) {   // stream-K pieces (asr_internal.h)
     const int tiles = per_seq;
     const long T = __ldcg(s.item_start + s.B), S = is_b + (long)l * tiles;
-    const int G = sk_span(T, s.sk_grid);
-    const int cf = tiles ? sk_cta_of(S, T, G) : 0;
-    nch = tiles ? sk_cta_of(S + tiles - 1, T, G) - cf + 1 : 0;
+    const SkPlan pl = sk_plan(T, s.sk_grid, s.sk_dyn, s.sk_chunk);
+    const int cf = tiles ? sk_unit_of(pl, S) : 0;
+    nch = tiles ? sk_unit_of(pl, S + tiles - 1) - cf + 1 : 0;
     it0 = (long)b * s.L + l + cf;
     if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   } else {
