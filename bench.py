@@ -356,6 +356,11 @@ def run_asr(a, rank: int, world: int, local_rank: int):
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     total_ms = sum(step_ms)
     stats = [ctx.stats(b) for b in range(B)]
+    rank_identical = None
+    if a.head_shard:   # every shard must have taken bitwise the same decisions: all-gathered digests
+        from paper_2512_11221_b200.dist import ledger_digest, ranks_agree
+        rank_identical = ranks_agree(ledger_digest(ctx, B))
+    allreduce_bytes_step = (stats[0]["allreduce_bytes"] - io0["allreduce_bytes"]) / K
     h2d_timed = stats[0]["bytes_h2d"] - io0["bytes_h2d"]    # context-wide counters
     d2h_timed = stats[0]["bytes_d2h"] - io0["bytes_d2h"]
     _, launches_timed = ctx.stage_times()   # library kernels launched in the timed region
@@ -557,7 +562,10 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                    "family": a.family, "state": state,
                    "l2": "flushed between timed steps (256 MiB write + 256 MiB read, outside the events)",
                    "parallelism": (f"head-sharded x{world} (NCCL all-reduce of per-token partial scores)" if a.head_shard
-                                   else f"sequence-sharded x{world} (no hot-path collective)")},
+                                   else f"sequence-sharded x{world} (no hot-path collective)"),
+                   "head_shard": {"rank_identical_decisions": rank_identical,
+                                  "allreduce_bytes_per_step": allreduce_bytes_step,
+                                  "attended_bytes_per_step": 4 * att_prof} if a.head_shard else None},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "attention+score (split-KV over A_i)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",

@@ -36,6 +36,7 @@ typedef enum {
   ASR_E_CUDA = 3,      /* CUDA runtime error */
   ASR_E_OOM = 4,       /* device or pinned-host allocation failed */
   ASR_E_CAPACITY = 5,  /* a sequence would exceed max_context */
+  ASR_E_NCCL = 6,      /* NCCL error (head-sharded mode), or libnccl.so.2 not loadable */
   ASR_E_STATE = 7      /* call order (e.g. use after destroy) */
 } asr_status;
 
@@ -145,6 +146,8 @@ typedef struct {
                                * (demand copies before compaction + prefetch copies outlasting the
                                * attention kernel), %globaltimer on the device (pressure mode) */
   int64_t free_slots;         /* pressure mode: free device slots after the last step (else 0) */
+  int64_t allreduce_bytes;    /* head-sharded mode, context-wide, cumulative: bytes of per-token partial
+                               * sums all-reduced by asr_step (4 per attended token of the batch) */
 } asr_stats_t;
 
 /* Host buffers for a full ledger snapshot of one sequence (any pointer may be NULL). */
@@ -180,13 +183,17 @@ asr_status asr_step(asr_ctx* ctx, const asr_step_io* io, void* cuda_stream);
  * same inputs except q / k_new / v_new, which hold its own heads; their ledgers stay identical. */
 asr_status asr_step_attend(asr_ctx* ctx, const asr_step_io* io, void* cuda_stream);
 asr_status asr_step_decide(asr_ctx* ctx, void* cuda_stream);
-/* Device buffer of per-token partial score sums: [batch][row] fp32, row >= max_context (entries past
- * |A_b| are unused); sum it element-wise across shards (e.g. an NCCL all-reduce). */
+/* Device buffer of the last asr_step_attend's per-token partial score sums, packed: sequence b's
+ * attended index a at (sum over b' < b of |A_b'|) + a, count = sum over b of |A_b| fp32 values; sum
+ * it element-wise across shards (e.g. an NCCL all-reduce) before asr_step_decide.  Synchronises the
+ * context's stream (the count is produced on the device). */
 asr_status asr_score_partials(asr_ctx* ctx, float** dev_ptr, int64_t* count);
 /* Head-sharded mode over NCCL (NVLink/NVSwitch): rank 0 creates an id (128 bytes), every rank
  * passes it to asr_attach_nccl (collective; one GPU per rank); from then on asr_step runs attend,
- * an in-place ncclAllReduce (sum) of the per-token partial sums on the step's stream, and decide.
- * Needs libnccl.so.2 in the process (loaded with dlopen). */
+ * an in-place ncclAllReduce (sum) of the packed per-token partial sums (4 bytes per attended token;
+ * the host reads the count from mapped memory after the attention, one host wait per step) on the
+ * step's stream, and decide.  Needs libnccl.so.2 in the process (loaded with dlopen); NCCL failures
+ * return ASR_E_NCCL. */
 asr_status asr_nccl_unique_id(void* out, int32_t n);
 asr_status asr_attach_nccl(asr_ctx* ctx, const void* unique_id, int32_t nranks, int32_t rank);
 

@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ASR_LIB_PATH") or os.path.join(_HERE, "libasr.so")   # override: A/B of two builds
 
-ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, ASR_E_STATE = 0, 1, 2, 3, 4, 5, 7
+ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, ASR_E_NCCL, ASR_E_STATE = 0, 1, 2, 3, 4, 5, 6, 7
 KV_BF16, KV_F32 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
 SR, WR, FR = 1, 2, 3
@@ -62,7 +62,7 @@ class asr_stats_t(ctypes.Structure):
                 ("bytes_h2d", ctypes.c_int64), ("bytes_d2h", ctypes.c_int64), ("device_error", ctypes.c_uint32),
                 ("resident", ctypes.c_int64), ("evicted_this_step", ctypes.c_int64),
                 ("prefetched_this_step", ctypes.c_int64), ("demand_restored_this_step", ctypes.c_int64),
-                ("h2d_stall_ns", ctypes.c_int64), ("free_slots", ctypes.c_int64)]
+                ("h2d_stall_ns", ctypes.c_int64), ("free_slots", ctypes.c_int64), ("allreduce_bytes", ctypes.c_int64)]
 
 
 class asr_ledger_view(ctypes.Structure):
@@ -286,7 +286,8 @@ def asr_step_decide(ctx, stream=None) -> None:
 
 
 def asr_score_partials(ctx):
-    """(device pointer, element count) of the per-token partial score sums of a head shard."""
+    """(device pointer, element count) of the packed per-token partial score sums of a head shard
+    (count = sum over sequences of |A_b|; synchronises)."""
     p, n = ctypes.c_void_p(), ctypes.c_int64()
     _check(lib().asr_score_partials(ctx, ctypes.byref(p), ctypes.byref(n)))
     return p.value, n.value

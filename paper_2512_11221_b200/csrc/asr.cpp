@@ -49,6 +49,9 @@ struct asr_ctx {
   bool uniform_prompt = true;
   int64_t step = 0;              // host mirror of the device step counter
   void* host_mirror = nullptr;   // pinned [B][max_ctx][L][2][Hkv][d]
+  int32_t* tok_count_host = nullptr;   // mapped pinned: the packed all-reduce count of the last attend
+  cudaEvent_t ev_attend = nullptr;
+  int64_t allreduce_bytes = 0;
   cudaStream_t side = nullptr;   // mirror copies
   cudaEvent_t ev_append = nullptr, ev_mirror = nullptr;
   cudaStream_t last_stream = nullptr;
@@ -105,6 +108,8 @@ struct asr_ctx {
     }
     for (void* p : allocs) cudaFree(p);
     if (host_mirror) cudaFreeHost(host_mirror);
+    if (tok_count_host) cudaFreeHost(tok_count_host);
+    if (ev_attend) cudaEventDestroy(ev_attend);
     if (side) cudaStreamDestroy(side);
     if (io_in) cudaStreamDestroy(io_in);
     if (io_out) cudaStreamDestroy(io_out);
@@ -317,11 +322,19 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     s.pool_reserve = cfg->pool_reserve;
     const size_t slots = s.pool_mode ? (size_t)cfg->pool_tokens : BT;
     CUDA_TRY(c->alloc(&s.kv, slots * c->tok_bytes));
+    s.kv_slots = (long)slots;
     CUDA_TRY(c->alloc(&s.act_slot, 2 * BT * 4));
     s.score_heads = cfg->score_heads > 0 ? cfg->score_heads : s.Hq;
     s.sharded = s.score_heads != s.Hq ? 1 : 0;
     CUDA_TRY(c->alloc(&s.tok_score, BT * 4));
     CUDA_TRY(cudaMemsetAsync(s.tok_score, 0, BT * 4, st));
+    {   // the packed all-reduce count, read by the host after the attention (head-sharded mode)
+      cudaError_t e = cudaHostAlloc((void**)&c->tok_count_host, 64, cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e != cudaSuccess) return fail(ASR_E_OOM, "pinned host allocation failed");
+      *c->tok_count_host = 0;
+      CUDA_TRY(cudaHostGetDevicePointer((void**)&s.tok_count, c->tok_count_host, 0));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_attend, cudaEventDisableTiming));
+    }
     std::vector<size_t> slot0(s.B, 0);   // first slot of each sequence's prompt
     for (int b = 0; b < s.B; ++b) slot0[b] = s.pool_mode ? (b ? slot0[b - 1] + prompt_len[b - 1] : 0) : (size_t)b * s.max_ctx;
     if (s.pool_mode) {
@@ -382,6 +395,7 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     if (max_items < sk_slots) max_items = sk_slots;
     CUDA_TRY(c->alloc(&s.sk_ctr, 8));
     CUDA_TRY(cudaMemsetAsync(s.sk_ctr, 0, 8, st));
+    s.max_items = (long)max_items;
     CUDA_TRY(c->alloc(&s.part_ml, max_items * s.Hq * 2 * 4));
     CUDA_TRY(c->alloc(&s.part_acc, max_items * s.Hq * s.d * 4));
     CUDA_TRY(c->alloc(&s.ent_part, (size_t)s.B * asr::kEntSplits * 3 * 4));
@@ -845,10 +859,15 @@ asr_status asr_step(asr_ctx* c, const asr_step_io* io, void* cuda_stream) {
   if (c->s.sharded) {
     r = step_launch(c, a, kPartAttend, st);
     if (r) return r;
-    // sum the shards' per-token partial scores in place (NCCL over NVLink / NVSwitch)
-    const int rc = c->nccl.all_reduce(c->s.tok_score, c->s.tok_score, (size_t)c->s.B * c->s.max_ctx, 7 /*ncclFloat32*/,
-                                      0 /*ncclSum*/, c->nccl_comm, st);
-    if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclAllReduce: ") + c->nccl.err(rc));
+    // sum the shards' per-token partial scores in place (NCCL over NVLink / NVSwitch): exactly the
+    // sum_b |A_b| packed entries, whose count the attention part produced on the device
+    CUDA_TRY(cudaEventRecord(c->ev_attend, st));
+    CUDA_TRY(cudaEventSynchronize(c->ev_attend));
+    const size_t count = (size_t)*(volatile int32_t*)c->tok_count_host;
+    const int rc = c->nccl.all_reduce(c->s.tok_score, c->s.tok_score, count, 7 /*ncclFloat32*/, 0 /*ncclSum*/,
+                                      c->nccl_comm, st);
+    if (rc != 0) return fail(ASR_E_NCCL, std::string("ncclAllReduce: ") + c->nccl.err(rc));
+    c->allreduce_bytes += (int64_t)count * 4;
     r = step_launch(c, a, kPartDecide, st);
   } else {
     r = step_launch(c, a, kPartFull, st);
@@ -886,17 +905,19 @@ asr_status asr_step_decide(asr_ctx* c, void* cuda_stream) {
 asr_status asr_score_partials(asr_ctx* c, float** dev_ptr, int64_t* count) {
   if (!c) return fail(ASR_E_STATE, "context is NULL");
   if (!dev_ptr || !count) return fail(ASR_E_INVALID, "NULL output");
+  CUDA_TRY(cudaSetDevice(c->cfg.device));
+  CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   *dev_ptr = c->s.tok_score;
-  *count = (int64_t)c->s.B * c->s.max_ctx;
+  *count = (int64_t)*(volatile int32_t*)c->tok_count_host;
   return ASR_OK;
 }
 
 asr_status asr_nccl_unique_id(void* out, int32_t n) {
   if (!out || n < 128) return fail(ASR_E_INVALID, "out must hold 128 bytes");
   asr::NcclApi& api = asr::nccl_api();
-  if (!api.ok) return fail(ASR_E_CUDA, "libnccl.so.2 not loadable");
+  if (!api.ok) return fail(ASR_E_NCCL, "libnccl.so.2 not loadable");
   const int rc = api.get_unique_id(out);
-  if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclGetUniqueId: ") + api.err(rc));
+  if (rc != 0) return fail(ASR_E_NCCL, std::string("ncclGetUniqueId: ") + api.err(rc));
   return ASR_OK;
 }
 
@@ -904,11 +925,11 @@ asr_status asr_attach_nccl(asr_ctx* c, const void* unique_id, int32_t nranks, in
   if (!c) return fail(ASR_E_STATE, "context is NULL");
   if (!unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(ASR_E_INVALID, "bad NCCL rank arguments");
   asr::NcclApi& api = asr::nccl_api();
-  if (!api.ok) return fail(ASR_E_CUDA, "libnccl.so.2 not loadable");
+  if (!api.ok) return fail(ASR_E_NCCL, "libnccl.so.2 not loadable");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   void* comm = nullptr;
   const int rc = api.comm_init_rank(&comm, nranks, unique_id, rank);
-  if (rc != 0) return fail(ASR_E_CUDA, std::string("ncclCommInitRank: ") + api.err(rc));
+  if (rc != 0) return fail(ASR_E_NCCL, std::string("ncclCommInitRank: ") + api.err(rc));
   c->nccl = api;
   c->nccl_comm = comm;
   // from now on every step runs attend -> all-reduce -> decide; cached graphs captured the
@@ -965,6 +986,7 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
   out->rewalk_requested = st.rewalk_requested;
   out->bytes_h2d = c->bytes_h2d;
   out->bytes_d2h = c->bytes_d2h;
+  out->allreduce_bytes = c->allreduce_bytes;
   out->device_error = err;
   out->resident = n;
   if (s.pool_mode) {

@@ -68,7 +68,23 @@ enum : uint32_t {
   kErrPoolEmpty = 8u,        // pressure mode: no free device slot (pool_tokens too small)
   kErrNotResident = 16u,     // pressure mode: an Active token without a device slot
   kErrStall = 32u,           // a wait inside the attention kernel timed out (phase B never finished)
+  kErrCheck = 64u,           // a bounds check of the -DASR_CHECKS build failed (index out of its array)
 };
+
+// Bounds checks of the diagnostic build (tools/build.py with ASR_CHECKS=1, -DASR_CHECKS): an index
+// outside its array latches kErrCheck (asr_stats reports ASR_E_INVARIANT) instead of corrupting
+// memory.  compute-sanitizer is closed on this GPU pool; these checks and the oracle comparisons of
+// tools/sanitize.py stand in for it.  Compiled out otherwise.
+#ifdef ASR_CHECKS
+#define ASR_CHECK(st, cond)                           \
+  do {                                                \
+    if (!(cond)) atomicOr((st).err, asr::kErrCheck);  \
+  } while (0)
+#else
+#define ASR_CHECK(st, cond) \
+  do {                      \
+  } while (0)
+#endif
 
 // Everything a kernel may need; passed by value (all pointers are device pointers).
 struct DevState {
@@ -105,6 +121,8 @@ struct DevState {
   int32_t* ev_ctrl;           // [4] Belady cut of this step: timer threshold T, quota at T, used, need
   unsigned long long* stall;  // [3] h2d stall ns (cumulative), attention end, prefetch-copy end (stamps)
   long tok_bytes;             // bytes of one token (all layers, K and V)
+  long kv_slots;              // device token slots of the KV pool (bounds checks)
+  long max_items;             // split-KV partial slots (bounds checks)
   int32_t* slot_of;           // [B][max_ctx] device slot of each position, -1 = evicted (pool mode)
   int32_t* spare;             // [B] slot reserved for the next appended token (pool mode)
   int32_t* free_stack;        // [pool] free slots
@@ -118,7 +136,9 @@ struct DevState {
   // head-sharded mode
   int sharded;                // 1: decide reads tok_score (summed across shards) instead of score_part
   int score_heads;            // H of Eq. 2 (all shards)
-  float* tok_score;           // [B][max_ctx] per-token score sums over this shard's heads, all layers
+  float* tok_score;           // packed [sum_b |A_b|]: entry prefix_b + a = the per-token score sum of
+                              // attended index a of sequence b over this shard's heads, all layers
+  int32_t* tok_count;         // mapped pinned host int: sum_b |A_b| of the step (the all-reduce count)
 
   void* kv;                   // pool [B*max_ctx][L][2][Hkv][d]
   uint8_t* res;               // [B][max_ctx] 1 Active / 0 Frozen

@@ -641,6 +641,7 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
 #pragma unroll
       for (int i = 0; i < 16; ++i) *reinterpret_cast<float2*>(dst + i * 8) = make_float2(acc[i][0] * inv, acc[i][1] * inv);
     } else if (r < G) {
+      ASR_CHECK(s, piece >= 0 && piece < s.max_items);
       const long pi = piece * s.Hq + warp * G + r;
       if (qd == 0) {
         s.part_ml[pi * 2] = m_run;

@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kUnitThreads) prepare_kernel(DevState s) {
 // Head-sharded mode: per-token partial score sums of this shard (grid decide_blocks x B).
 __global__ void __launch_bounds__(kUnitThreads) scoresum_kernel(DevState s) {
   pdl_wait();
-  units::unit_score_sum(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, *s.step);
+  __shared__ units::UnitShm u;
+  units::unit_score_sum(s, blockIdx.x / s.decide_blocks, blockIdx.x % s.decide_blocks, s.decide_blocks, *s.step, u);
 }
 
 // Explicit asr_restore at the boundary before step i (= *s.step); seq = -1 for all.  In pressure

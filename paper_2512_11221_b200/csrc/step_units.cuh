@@ -39,7 +39,16 @@ struct UnitShm {
   int total;
   int last;
   int lo, hi;   // decide: this block's position range
+  int pref;     // head-sharded mode: offset of this sequence in the packed per-token partial sums
 };
+
+// Head-sharded mode: offset of sequence b's entries in the packed per-token partial sums (the prefix
+// over |A_b'| of the step's lists), computed by one thread.
+__device__ __forceinline__ int packed_offset(const DevState& s, int b, int i) {
+  int acc = 0;
+  for (int x = 0; x < b; ++x) acc += s.act_len[(i & 1) * s.B + x];
+  return acc;
+}
 
 __device__ __forceinline__ float tof(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ float tof(float v) { return v; }
@@ -73,16 +82,21 @@ __device__ __forceinline__ int pool_pop(const DevState& s) {
     atomicOr(s.err, kErrPoolEmpty);
     return -1;
   }
-  return s.free_stack[idx];
+  ASR_CHECK(s, idx < s.kv_slots);
+  const int slot = s.free_stack[idx];
+  ASR_CHECK(s, slot >= 0 && slot < s.kv_slots);
+  return slot;
 }
 __device__ __forceinline__ void pool_push(const DevState& s, int slot) {
   const int idx = atomicAdd(s.free_top, 1);
+  ASR_CHECK(s, idx >= 0 && idx < s.kv_slots && slot >= 0 && slot < s.kv_slots);
   s.free_stack[idx] = slot;
 }
 // Block-cooperative copy of one token (all layers, K and V) from the pinned host mirror (mapped,
 // read over the host link) into its device slot.
 __device__ void copy_token_h2d(const DevState& s, int b, int pos, int slot) {
   if (slot < 0) return;
+  ASR_CHECK(s, slot < s.kv_slots && pos >= 0 && pos < s.cap);
   const uint4* src = reinterpret_cast<const uint4*>(s.host_kv + ((long)b * s.max_ctx + pos) * s.tok_bytes);
   uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s.kv) + (long)slot * s.tok_bytes);
   const int nv = (int)(s.tok_bytes / 16);
@@ -283,6 +297,7 @@ struct Compactor {
       int o = off + incl - c;
       while (m) {
         const int j = 4 * q + __ffs(m) - 1;
+        ASR_CHECK(s, o >= 0 && o < s.max_ctx && j < s.max_ctx);
         out[o] = j;
         out_slot[o] = s.pool_mode ? __ldcg(slot_of + j) : (int)(row + j);
         ++o;
@@ -331,6 +346,7 @@ __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __
   const long pos = s.prompt_len[b] + i;
   const long slot = s.pool_mode ? (long)s.spare[b] : (long)b * s.max_ctx + pos;
   if (slot < 0) return;   // pool exhausted (latched by the pop)
+  ASR_CHECK(s, slot < s.kv_slots && pos < s.cap);
   const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
   TK* dst = reinterpret_cast<TK*>(s.kv) + (slot * s.L + l) * 2 * row;
   // pressure mode: the write-once host mirror is written here too (mapped pinned memory), so a
@@ -582,13 +598,20 @@ __device__ __forceinline__ float layer_sum(const DevState& s, int b, int a) {
   return sum;
 }
 
-// Head-sharded mode: this shard's per-token sums (its heads, all layers) for a slice of A_b.
-__device__ void unit_score_sum(const DevState& s, int b, int x, int X, int i) {
+// Head-sharded mode: this shard's per-token sums (its heads, all layers) for a slice of A_b, packed
+// at prefix_b + a (the all-reduce then moves 4 bytes per attended token: 4 * sum_b |A_b|); unit 0 of
+// sequence 0 publishes the count for the host (mapped pinned memory).
+__device__ void unit_score_sum(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
   const int A = s.act_len[(i & 1) * s.B + b];
+  if (ASR_UNIT_TID() == 0) {
+    u.pref = packed_offset(s, b, i);
+    if (b == 0 && x == 0 && s.tok_count) *(volatile int32_t*)s.tok_count = packed_offset(s, s.B, i);
+  }
+  ASR_UNIT_SYNC();
   const int per_a = (A + X - 1) / X;
   const int a_end = min(A, (x + 1) * per_a);
   for (int a = x * per_a + ASR_UNIT_TID(); a < a_end; a += ASR_UNIT_THREADS())
-    s.tok_score[(long)b * s.max_ctx + a] = layer_sum(s, b, a);
+    s.tok_score[u.pref + a] = layer_sum(s, b, a);
 }
 
 // Alg. 1 lines 3-9 (+ the R0 tick of a token frozen now) for attended index a (position j) of
@@ -599,6 +622,7 @@ struct DecideCtx {
   uint8_t tag_now;
   float heads, sqrt_d;
   int n, pf_row;
+  int pref;   // head-sharded mode: offset of the sequence in the packed partial sums
 };
 __device__ __forceinline__ DecideCtx decide_ctx(const DevState& s, int b, int i) {
   DecideCtx c;
@@ -608,6 +632,7 @@ __device__ __forceinline__ DecideCtx decide_ctx(const DevState& s, int b, int i)
   c.sqrt_d = sqrtf((float)s.d);
   c.n = s.prompt_len[b] + i + 1;
   c.pf_row = (i & 1) * s.B + b;            // prefetch list written by this step (pressure mode)
+  c.pref = 0;
   return c;
 }
 
@@ -616,11 +641,12 @@ __device__ __forceinline__ DecideCtx decide_ctx(const DevState& s, int b, int i)
 __device__ __forceinline__ void decide_token(const DevState& s, const DecideCtx& c, int b, int a, int j, int i,
                                              int& frozen_now, int& restored, int& evicted, int* ev = nullptr) {
   const long base = c.base;
+  ASR_CHECK(s, j >= 0 && j < c.n && a >= 0 && a < s.max_ctx);
   float sj;
   if (s.ext_score) {
     sj = s.ext_score[(long)b * s.cap + j];   // policy replay: the caller's s_j, rows of max_context
   } else {
-    const float sum = s.sharded ? s.tok_score[base + a] : layer_sum(s, b, a);
+    const float sum = s.sharded ? s.tok_score[c.pref + a] : layer_sum(s, b, a);
     sj = sum / c.heads;               // mean over the L*Hq (layer, head) pairs (correctly rounded)
     if (s.score_scaled) sj = sj / c.sqrt_d;
   }
@@ -714,7 +740,12 @@ __device__ __forceinline__ void tick_position(const DevState& s, const DecideCtx
 // The two index sets are disjoint (A_i = the tokens Active at the step start) and tokens frozen in
 // this step carry the step-parity tag res_tag(i), so units need no ordering between them.
 __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitShm& u) {
-  const DecideCtx dc = decide_ctx(s, b, i);
+  DecideCtx dc = decide_ctx(s, b, i);
+  if (s.sharded) {
+    if (ASR_UNIT_TID() == 0) u.pref = packed_offset(s, b, i);
+    ASR_UNIT_SYNC();
+    dc.pref = u.pref;
+  }
   const int n = dc.n;
   const long base = dc.base;
   const int A = s.act_len[(i & 1) * s.B + b];
@@ -1096,6 +1127,7 @@ __device__ __noinline__ void combine_warp_tail(const DevState& s, int wid, float
   if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   if (!wr) nch = min(nch, 8);
   const long it0 = (long)b * s.L + l + cf;
+  ASR_CHECK(s, it0 >= 0 && it0 + nch <= s.max_items);
   float M = -INFINITY;
 #pragma unroll 1
   for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(s.part_ml + ((it0 + c) * s.Hq + h) * 2));

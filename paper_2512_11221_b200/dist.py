@@ -64,3 +64,26 @@ def share_nccl_id(make_id) -> bytes:
     obj = [make_id() if dist.get_rank() == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+def ledger_digest(ctx, batch: int) -> str:
+    """Hex digest of every sequence's ledger and attended list (head-sharded mode: every rank must take
+    bitwise the same decisions — the digests are all-gathered and compared)."""
+    import hashlib
+    h = hashlib.sha256()
+    for b in range(batch):
+        st = ctx.stats(b, detail=True)
+        for k in ("residency", "timer", "count", "freeze_step"):
+            h.update(st["ledger"][k].tobytes())
+        h.update(st["active_list"].tobytes())
+    return h.hexdigest()
+
+
+def ranks_agree(digest: str) -> bool:
+    """All-gather a per-rank digest over the process group; True iff every rank has the same one."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return True
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, digest)
+    return all(x == out[0] for x in out)

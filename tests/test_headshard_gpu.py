@@ -92,3 +92,33 @@ def test_nccl_single_rank_step():
     # a one-rank communicator: asr_step runs attend -> ncclAllReduce -> decide; parity with the oracle
     run(Case(L=2, Hq=8, Hkv=2, d=64, B=2, prompt=(30, 50), steps=30, window=8, hot_permille=300, seed=93,
              nccl_world1=True))
+
+
+def test_nccl_allreduce_moves_exactly_the_attended_partials():
+    # the head-sharded all-reduce is packed by a prefix over |A_b|: 4 bytes per attended token of the
+    # batch (not the [B][max_context] buffer); a one-rank communicator, LLaMA head layout
+    import torch
+    from paper_2512_11221_b200 import Config, Context, asr_nccl_unique_id
+    from paper_2512_11221_b200.dist import ledger_digest
+    B, P, L, Hq, Hkv, d = 3, 90, 2, 32, 8, 128
+    p = gen.GenParams(seed=95, L=L, Hq=Hq, Hkv=Hkv, d=d, hot_permille=300, a_hot=64)
+    cap = P + 40
+    KV = [gen.kv(p, b, 0, cap) for b in range(B)]
+    pk = np.stack([KV[b][0][:P] for b in range(B)])
+    pv = np.stack([KV[b][1][:P] for b in range(B)])
+    cfg = Config(n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, batch=B, max_context=cap, window=8, vocab=0)
+    ctx = Context(cfg, _t(pk), _t(pv), [P - 7 * b for b in range(B)])
+    ctx.attach_nccl(asr_nccl_unique_id(), 1, 0)
+    before = ctx.stats(0)["allreduce_bytes"]
+    for i in range(30):
+        q = np.stack([gen.q(p, b, i) for b in range(B)])
+        kn = np.stack([KV[b][0][P - 7 * b + i] for b in range(B)])
+        vn = np.stack([KV[b][1][P - 7 * b + i] for b in range(B)])
+        o = torch.zeros((B, L, Hq, d), dtype=torch.float32, device="cuda")
+        ctx.step(_t(q), _t(kn), _t(vn), o)
+        sts = [ctx.stats(b) for b in range(B)]
+        after = sts[0]["allreduce_bytes"]
+        assert after - before == 4 * sum(s["attended"] for s in sts), (i, after - before)
+        before = after
+    assert len(ledger_digest(ctx, B)) == 64
+    ctx.close()

@@ -101,14 +101,14 @@ def _nccl_include() -> str:
     return os.path.join(base, "include")
 
 
-def build_asr(force: bool = False) -> str:
+def build_asr(force: bool = False, out: str | None = None) -> str:
     with _locked():
-        return _build_asr(force)
+        return _build_asr(force, out)
 
 
-def _build_asr(force: bool) -> str:
+def _build_asr(force: bool, out_path: str | None = None) -> str:
     pkg = os.path.join(ROOT, "paper_2512_11221_b200")
-    out = os.path.join(pkg, "libasr.so")
+    out = out_path or os.path.join(pkg, "libasr.so")
     csrc = os.path.join(pkg, "csrc")
     cu = sorted(glob.glob(os.path.join(csrc, "*.cu")))
     cpp = sorted(glob.glob(os.path.join(csrc, "*.cpp")))
@@ -116,12 +116,14 @@ def _build_asr(force: bool) -> str:
                  + glob.glob(os.path.join(ROOT, "include", "*.h")))
     if not (force or _stale(out, cu + cpp + hdr)):
         return out
-    objdir = os.path.join(ROOT, "build", "asr")
+    objdir = os.path.join(ROOT, "build", "asr" if out_path is None else "asr_" + os.path.basename(out_path))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-I", os.path.join(ROOT, "include"), "-I", csrc]
     if os.environ.get("ASR_TAIL_TRACE") == "1":   # diagnostic build: per-warp stamps of the fused tail
         common.append("-DASR_TAIL_TRACE")
+    if os.environ.get("ASR_CHECKS") == "1":       # diagnostic build: device-side bounds checks (kErrCheck)
+        common.append("-DASR_CHECKS")
     for s in cu:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -146,5 +148,9 @@ def build_all(force: bool = False, cuda: bool = True) -> None:
 
 
 if __name__ == "__main__":
+    if "--checks" in sys.argv:   # the bounds-checked diagnostic library, beside the product one
+        os.environ["ASR_CHECKS"] = "1"
+        print(build_asr(force=True, out=os.path.join(ROOT, "build", "libasr_checks.so")))
+        sys.exit(0)
     build_all(force="--force" in sys.argv, cuda="--no-cuda" not in sys.argv)
     print("built")
