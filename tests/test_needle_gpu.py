@@ -106,3 +106,78 @@ def test_needle_restore_ladder_32k(pool):
     if pool:
         assert demand > 0   # SR / WR / FR copied evicted tokens back from the host mirror
     ctx.close()
+
+
+def test_needle_full_depth_32_layers():
+    """configs[3] at full depth: 32 layers of the LLaMA-3-8B shape, batch 2, the 32K prefill with the
+    needle, bench.py's launch (device-generated prompt and inputs).  Ledgers and attended lists of
+    every step bit-exact against the oracle's policy replay (LAT classes; the needle scores high on
+    its retrieval steps only); O of sampled (layer, head) rows at steps q, q+1 (SR restores the
+    needle's cohort: |A| jumps to the whole context) and q+2 against oracle.attend_head."""
+    import torch
+    from paper_2512_11221_b200 import Config, Context
+
+    L32 = 32
+    P = CTX - 256
+    q = find_q(P)
+    steps = q + 20
+    p = gen.GenParams(seed=4002, L=L32, Hq=HQ, Hkv=HKV, d=D, needle_pos=NEEDLE, query_first=q + 1, query_count=8,
+                      vocab=V, spike_first=q, spike_period=16, spike_count=2)
+    cap = P + steps + 1
+    cfg = Config(n_layers=L32, n_q_heads=HQ, n_kv_heads=HKV, head_dim=D, batch=B, max_context=cap, window=K, vocab=V,
+                 host_mirror=0)
+    bf = torch.bfloat16
+    pk = torch.empty((B, P, L32, HKV, D), dtype=bf, device="cuda")
+    pv = torch.empty_like(pk)
+    gen.dev_kv(p, B, 0, P, pk, pv)
+    torch.cuda.synchronize()
+    ctx = Context(cfg, pk, pv, [P] * B)
+    del pk, pv
+    torch.cuda.empty_cache()
+    qd = torch.empty((B, L32, HQ, D), dtype=bf, device="cuda")
+    kn = torch.empty((B, L32, HKV, D), dtype=bf, device="cuda")
+    vn = torch.empty_like(kn)
+    lg = torch.empty((B, V), dtype=bf, device="cuda")
+    o = torch.empty((B, L32, HQ, D), dtype=torch.float32, device="cuda")
+    pos = torch.full((B,), P, dtype=torch.int32, device="cuda")
+    ocfg = oracle.OrcCfg(L=L32, Hq=HQ, Hkv=HKV, d=D, window=K, vocab=V)
+    orc = [oracle.OracleSeq(ocfg, cap, P) for _ in range(B)]
+    checks = {q: None, q + 1: None, q + 2: None}
+    kv_host = {}
+    actions = []
+    rng = np.random.default_rng(7)
+    for i in range(steps):
+        gen.dev_q(p, B, i, qd)
+        gen.dev_kv(p, B, 0, 1, kn, vn, pos0_dev=pos + i)
+        gen.dev_logits(p, B, i - 1, lg)
+        ctx.step(qd, kn, vn, o, logits_prev=lg if i > 0 else None)
+        O = o.cpu().numpy() if i in checks else None
+        for b in range(B):
+            H = oracle.entropy(gen.logits(p, b, i - 1)) if i > 0 else None
+            below = np.ones(cap, np.uint8)
+            if gen.is_query_step(p, i):
+                below[NEEDLE] = 0
+            act, out = orc[b].step_policy(below, H)
+            g = ctx.stats(b, detail=True)
+            np.testing.assert_array_equal(g["active_list"], act, err_msg=f"step {i} seq {b}")
+            led = orc[b].ledger()
+            for key in ("residency", "timer", "count", "freeze_step"):
+                np.testing.assert_array_equal(g["ledger"][key], led[key], err_msg=f"step {i} seq {b} {key}")
+            assert g["recovery_action"] == out["recovery_action"] and g["device_error"] == 0
+            if b == 0 and out["recovery_action"]:
+                actions.append((i, out["recovery_action"]))
+            if O is not None:
+                qb = gen.q(p, b, i)
+                if b not in kv_host:   # every position's K/V rows, host build of the generator (4.3 GB)
+                    kv_host[b] = gen.kv(p, b, 0, cap)
+                Kb, Vb = kv_host[b][0][act], kv_host[b][1][act]
+                rows = {(0, 0), (L32 - 1, HQ - 1), *[(int(x), int(y)) for x, y in rng.integers(0, [L32, HQ], (14, 2))]}
+                for l, h in sorted(rows):
+                    kvh = h // (HQ // HKV)
+                    ref = oracle.attend_head(qb[l, h], Kb[:, l, kvh], Vb[:, l, kvh])
+                    err = float(np.max(np.abs(O[b, l, h] - ref)) / np.max(np.abs(ref)))
+                    assert err <= 2e-3, (i, b, l, h, err)
+                if b == 0 and i == q + 1:
+                    assert NEEDLE in act   # SR at the q/q+1 boundary restored the needle
+    assert actions == [(q + 1, 1), (q + 17, 2)]
+    ctx.close()
