@@ -629,7 +629,7 @@ def sample_point(local_rank: int) -> dict:
     import torch
 
     import gen
-    from paper_2512_11221_b200 import asr_sample
+    from paper_2512_11221_b200 import asr_sample, asr_sample_entropy
     dev = torch.device("cuda", local_rank)
     out = {}
     for B in (1, 64):
@@ -638,20 +638,27 @@ def sample_point(local_rank: int) -> dict:
         gen.dev_logits(g, B, 5, lg)
         u = torch.rand(B, device=dev)
         tok = torch.empty(B, dtype=torch.int32, device=dev)
+        ent = torch.empty(B, dtype=torch.float32, device=dev)
         res = {}
         for name, (T, k, P) in {"greedy": (0.0, 0, 1.0), "T0.8_k50_p0.9": (0.8, 50, 0.9), "T1_p0.95": (1.0, 0, 0.95)}.items():
-            for _ in range(3):
-                asr_sample(lg, u, tok, temperature=T, top_k=k, top_p=P)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(20):
-                asr_sample(lg, u, tok, temperature=T, top_k=k, top_p=P)
-            e1.record()
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1000 / 20
-            res[name] = {"us_per_call": round(us, 2), "rows_per_s": round(B / us * 1e6),
-                         "gbs_one_read": round(B * VOCAB * 2 / us / 1e3, 1)}
+            for fused in (False, True):   # fused: + the row's entropy for the next step (asr_sample_entropy)
+                def call():
+                    if fused:
+                        asr_sample_entropy(lg, u, tok, ent, temperature=T, top_k=k, top_p=P)
+                    else:
+                        asr_sample(lg, u, tok, temperature=T, top_k=k, top_p=P)
+                for _ in range(3):
+                    call()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(20):
+                    call()
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) * 1000 / 20
+                res[name + ("+entropy" if fused else "")] = {"us_per_call": round(us, 2), "rows_per_s": round(B / us * 1e6),
+                                                            "gbs_one_read": round(B * VOCAB * 2 / us / 1e3, 1)}
         out[f"batch{B}"] = res
     return out
 

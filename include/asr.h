@@ -41,6 +41,10 @@ typedef enum {
 } asr_status;
 
 typedef enum { ASR_KV_BF16 = 0, ASR_KV_F32 = 1 } asr_dtype;
+/* asr_step_io.logits_dtype = ASR_ENTROPY_GIVEN: logits_prev points to fp32 H[batch], the entropy of the
+ * previous step's logits rows already taken by asr_sample_entropy (one read of each row yields both the
+ * next token and H); the step skips its own pass over the rows. */
+enum { ASR_ENTROPY_GIVEN = 2 };
 typedef enum { ASR_TICK_LITERAL = 0 /* R0: Alg. 1 order, default */, ASR_TICK_SKIP_NEW = 1 /* R1 */ } asr_tick;
 typedef enum { ASR_SCORE_RAW = 0 /* Eq. 2 literal, default */, ASR_SCORE_SCALED = 1 /* x 1/sqrt(d) */ } asr_score_mode;
 typedef enum { ASR_SR = 1, ASR_WR = 2, ASR_FR = 3 } asr_level; /* P:80; RR = FR + rewalk flag */
@@ -113,8 +117,9 @@ typedef struct {
   const void* q;           /* [B][L][Hq][d]  kv_dtype: the current query Q_i (Eq. 1-2) */
   const void* k_new;       /* [B][L][Hkv][d] kv_dtype: K of the token appended this step */
   const void* v_new;       /* [B][L][Hkv][d] kv_dtype */
-  const void* logits_prev; /* [B][vocab] or NULL: the previous step's output logits (Sec 3.6) */
-  int32_t logits_dtype;    /* ASR_KV_BF16 or ASR_KV_F32 */
+  const void* logits_prev; /* [B][vocab] or NULL: the previous step's output logits (Sec 3.6); or fp32 [B]
+                            * entropies with ASR_ENTROPY_GIVEN */
+  int32_t logits_dtype;    /* ASR_KV_BF16, ASR_KV_F32 or ASR_ENTROPY_GIVEN */
   int32_t memory;          /* asr_memory of every pointer in this struct */
   float* o;                /* out [B][L][Hq][d] fp32 attention output over A_i */
   float* entropy;          /* out [B] fp32 H(logits_prev), or NULL */
@@ -267,6 +272,15 @@ asr_status asr_step_policy(asr_ctx* ctx, const float* scores, const void* logits
  * 1..2^24-1, or a non-finite temperature / top_p; launch failures as ASR_E_CUDA. */
 asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab, float temperature,
                       int32_t top_k, float top_p, const float* uniforms, int32_t* token_out, void* cuda_stream);
+
+/* NEXT-1 fused with the entropy stage (a6): the draw of asr_sample and, from the same read of each row
+ * (the row slice is kept in shared memory), entropy_out[b] = H(softmax(logits[b] / entropy_temperature))
+ * in nats (R-ent; Sec 3.6) — the value the next asr_step's detector needs, passed there with
+ * logits_dtype = ASR_ENTROPY_GIVEN instead of the logits rows.  entropy_out: device fp32 [batch].
+ * Errors as asr_sample, plus ASR_E_INVALID for a NULL entropy_out or entropy_temperature <= 0. */
+asr_status asr_sample_entropy(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab,
+                              float temperature, int32_t top_k, float top_p, const float* uniforms, int32_t* token_out,
+                              float entropy_temperature, float* entropy_out, void* cuda_stream);
 
 /* NEXT-4 (§Future Work, "hybrid compression combining ASR-KF-EGR with
  * quantization methods"): the frozen tier stored quantised so a restore moves fewer bytes over the host

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("ASR_LIB_PATH") or os.path.join(_HERE, "libasr.so")   
 
 ASR_OK, ASR_E_INVALID, ASR_E_INVARIANT, ASR_E_CUDA, ASR_E_OOM, ASR_E_CAPACITY, ASR_E_NCCL, ASR_E_STATE = 0, 1, 2, 3, 4, 5, 6, 7
 KV_BF16, KV_F32 = 0, 1
+ENTROPY_GIVEN = 2   # asr_step_io.logits_dtype: logits_prev holds fp32 H[batch] (asr_sample_entropy)
 MEM_DEVICE, MEM_HOST = 0, 1
 SR, WR, FR = 1, 2, 3
 EVICT_BELADY, EVICT_AT_FREEZE = 0, 1
@@ -74,7 +75,8 @@ class asr_ledger_view(ctypes.Structure):
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
            "asr_stage_times", "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_last_error",
            "asr_step_attend", "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-           "asr_time_attention", "asr_sample", "asr_step_policy", "asr_kv_quantize", "asr_kv_dequantize")
+           "asr_time_attention", "asr_sample", "asr_sample_entropy", "asr_step_policy", "asr_kv_quantize",
+           "asr_kv_dequantize")
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -112,13 +114,15 @@ def lib() -> ctypes.CDLL:
         L.asr_attach_nccl.argtypes = [vp, vp, i32, i32]
         L.asr_time_attention.argtypes = [vp, i32, vp]
         L.asr_sample.argtypes = [vp, i32, i32, i32, ctypes.c_float, i32, ctypes.c_float, vp, vp, vp]
+        L.asr_sample_entropy.argtypes = [vp, i32, i32, i32, ctypes.c_float, i32, ctypes.c_float, vp, vp,
+                                         ctypes.c_float, vp, vp]
         L.asr_step_policy.argtypes = [vp, vp, vp, i32, vp, vp]
         L.asr_kv_quantize.argtypes = [vp, ctypes.c_int64, i32, i32, vp, vp, vp]
         L.asr_kv_dequantize.argtypes = [vp, vp, ctypes.c_int64, i32, i32, vp, vp]
         for f in ("asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv", "asr_stage_times",
                   "asr_set_profile", "asr_timeline", "asr_flush", "asr_destroy", "asr_step_attend",
                   "asr_step_decide", "asr_score_partials", "asr_nccl_unique_id", "asr_attach_nccl",
-                  "asr_time_attention", "asr_sample", "asr_step_policy", "asr_kv_quantize",
+                  "asr_time_attention", "asr_sample", "asr_sample_entropy", "asr_step_policy", "asr_kv_quantize",
                   "asr_kv_dequantize"):
             getattr(L, f).restype = ctypes.c_int
         L.asr_last_error.argtypes = []
@@ -251,7 +255,7 @@ def asr_create(cfg: Config, prompt_k, prompt_v, prompt_len, stream=None) -> ctyp
 _CFGS: dict = {}   # ctx handle value -> Config (for argument validation)
 
 
-def _io(ctx, q, k_new, v_new, o, logits_prev, entropy):
+def _io(ctx, q, k_new, v_new, o, logits_prev, entropy, entropy_given=False):
     cfg = _CFGS.get(ctx.value if isinstance(ctx, ctypes.c_void_p) else ctx)
     host = _is_host(q)
     if cfg is not None:
@@ -262,17 +266,20 @@ def _io(ctx, q, k_new, v_new, o, logits_prev, entropy):
         _arg("k_new", k_new, kv, (B, L, Hkv, d), host, dev)
         _arg("v_new", v_new, kv, (B, L, Hkv, d), host, dev)
         _arg("o", o, ["f32"], (B, L, Hq, d), host, dev)
-        if logits_prev is not None:
+        if logits_prev is not None and entropy_given:
+            _arg("entropy (given)", logits_prev, ["f32"], (B,), host, dev)
+        elif logits_prev is not None:
             _arg("logits_prev", logits_prev, ["bf16", "f32"], (B, cfg.vocab), host, dev)
         if entropy is not None:
             _arg("entropy", entropy, ["f32"], (B,), host, dev)
-    return asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev),
-                       _dtype_code(logits_prev) if logits_prev is not None else 0,
+    code = ENTROPY_GIVEN if entropy_given else (_dtype_code(logits_prev) if logits_prev is not None else 0)
+    return asr_step_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(logits_prev), code,
                        MEM_HOST if host else MEM_DEVICE, _ptr(o), _ptr(entropy))
 
 
-def asr_step(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None) -> None:
-    io = _io(ctx, q, k_new, v_new, o, logits_prev, entropy)
+def asr_step(ctx, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None, entropy_given=False) -> None:
+    """entropy_given: logits_prev is fp32 H[batch] from asr_sample_entropy instead of the logits rows."""
+    io = _io(ctx, q, k_new, v_new, o, logits_prev, entropy, entropy_given)
     _check(lib().asr_step(ctx, ctypes.byref(io), _stream(stream)))
 
 
@@ -388,6 +395,22 @@ def asr_sample(logits, uniforms, token_out, temperature: float = 1.0, top_k: int
                             _stream(stream)))
 
 
+def asr_sample_entropy(logits, uniforms, token_out, entropy_out, temperature: float = 1.0, top_k: int = 0,
+                       top_p: float = 1.0, entropy_temperature: float = 1.0, stream=None) -> None:
+    """NEXT-1 + (a6) in one pass over each row (include/asr.h asr_sample_entropy): the draw of asr_sample
+    and entropy_out[b] = H(softmax(logits[b] / entropy_temperature)) — pass entropy_out to the next
+    asr_step as logits_prev with entropy_given=True."""
+    import torch
+    _arg("logits", logits, ["bf16", "f32"], (None, None), False)
+    B, V = logits.shape
+    _arg("uniforms", uniforms, ["f32"], (B,), False, logits.device.index)
+    _arg("token_out", token_out, ["i32"], (B,), False, logits.device.index)
+    _arg("entropy_out", entropy_out, ["f32"], (B,), False, logits.device.index)
+    dt = KV_BF16 if logits.dtype == torch.bfloat16 else KV_F32
+    _check(lib().asr_sample_entropy(_vp(logits), dt, B, V, float(temperature), int(top_k), float(top_p), _vp(uniforms),
+                                    _vp(token_out), float(entropy_temperature), _vp(entropy_out), _stream(stream)))
+
+
 def asr_kv_quantize(kv, codes, scales, bits: int = 8, stream=None) -> None:
     """NEXT-4 frozen-tier quantisation (include/asr.h asr_kv_quantize): kv [..., n] bf16 (rows = all
     leading dims), codes [rows][n] int8 (bits 8) or [rows][n/2] uint8 (bits 4), scales [rows] fp32 —
@@ -430,8 +453,8 @@ class Context:
         self.cfg = cfg
         self._h = asr_create(cfg, prompt_k, prompt_v, prompt_len, stream)
 
-    def step(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None):
-        asr_step(self._h, q, k_new, v_new, o, logits_prev, entropy, stream)
+    def step(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None, entropy_given=False):
+        asr_step(self._h, q, k_new, v_new, o, logits_prev, entropy, stream, entropy_given)
 
     def attend(self, q, k_new, v_new, o, logits_prev=None, entropy=None, stream=None):
         asr_step_attend(self._h, q, k_new, v_new, o, logits_prev, entropy, stream)

@@ -82,7 +82,7 @@ struct asr_ctx {
     std::vector<asr::KNode> last;
     std::vector<cudaGraphNode_t> evnodes;
   };
-  StepGraph graphs[18];  // [has_logits][device io | host io set 0 | 1][full | attend | decide]
+  StepGraph graphs[36];  // [entropy given][has_logits][device io | host io set 0 | 1][full | attend | decide]
   bool attend_pending = false;
   std::unique_ptr<struct StepArgsBox> pending;
   asr::NcclApi nccl;
@@ -558,7 +558,7 @@ static cudaError_t prof_mark(asr_ctx* c, std::array<cudaEvent_t, asr::kStages + 
 enum Part { kPartFull = 0, kPartAttend = 1, kPartDecide = 2 };
 
 struct StepArgs {
-  bool has_logits = false, host_io = false;
+  bool has_logits = false, host_io = false, ent_given = false;
   int logits_dtype = 0;
   const void *q = nullptr, *kn = nullptr, *vn = nullptr, *lg = nullptr;
   float *o = nullptr, *ent = nullptr;           // device outputs (staging in host-io mode)
@@ -577,7 +577,8 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
   if (!io || !io->q || !io->k_new || !io->v_new || !io->o) return fail(ASR_E_INVALID, "io has NULL q/k_new/v_new/o");
   if (io->memory != ASR_MEM_DEVICE && io->memory != ASR_MEM_HOST) return fail(ASR_E_INVALID, "io->memory");
   const DevState& s = c->s;
-  a.has_logits = io->logits_prev != nullptr && s.vocab > 0;
+  a.ent_given = io->logits_prev != nullptr && io->logits_dtype == ASR_ENTROPY_GIVEN;
+  a.has_logits = io->logits_prev != nullptr && s.vocab > 0 && !a.ent_given;
   a.logits_dtype = io->logits_dtype;
   if (a.has_logits && io->logits_dtype != ASR_KV_BF16 && io->logits_dtype != ASR_KV_F32)
     return fail(ASR_E_INVALID, "logits_dtype");
@@ -594,7 +595,7 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
   a.host_io = io->memory == ASR_MEM_HOST;
   asr_ctx::Staging& S = c->stg[c->step & 1];
   if (a.host_io) {
-    asr_status r = ensure_staging(c, S, a.has_logits, io->logits_dtype);
+    asr_status r = ensure_staging(c, S, a.has_logits || a.ent_given, a.ent_given ? ASR_KV_F32 : io->logits_dtype);
     if (r) return r;
     // inputs: copied on io_in as soon as the step is issued (overlapping the previous step's kernels),
     // once the graph that last read this staging set is done
@@ -605,8 +606,8 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
     CUDA_TRY(cudaMemcpyAsync(S.k, a.kn, kb, cudaMemcpyHostToDevice, c->io_in));
     CUDA_TRY(cudaMemcpyAsync(S.v, a.vn, kb, cudaMemcpyHostToDevice, c->io_in));
     c->bytes_h2d += (int64_t)(qb + 2 * kb);
-    if (a.has_logits) {
-      const size_t lb = (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
+    if (a.has_logits || a.ent_given) {
+      const size_t lb = a.ent_given ? (size_t)s.B * 4 : (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
       CUDA_TRY(cudaMemcpyAsync(S.logits, a.lg, lb, cudaMemcpyHostToDevice, c->io_in));
       c->bytes_h2d += (int64_t)lb;
       a.lg = S.logits;
@@ -632,6 +633,7 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
     a.ev = &c->prof_pending.back();
   }
   a.sd = s;   // the step's view: timeline stamps when profiling the fused kernel or on request
+  if (a.ent_given) a.sd.ent_given = static_cast<const float*>(a.lg);   // H per sequence, no logits pass
   if (c->timeline_on) a.sd.tl = c->tl_buf;
   if (a.sd.tl) {   // timeline of this step: start stamps = +inf, end stamps = 0 (+ phase D detail)
     unsigned long long init[asr::kTimelineSlots];
@@ -662,7 +664,7 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
   int stage_of[8];   // 0 ledger pre, 1 attention, 2 decide/combine (profiling events)
   int nk = 0;
   const void* lgp = a.has_logits ? a.lg : nullptr;
-  float* entp = a.has_logits ? a.ent : nullptr;
+  float* entp = (a.has_logits || a.ent_given) ? a.ent : nullptr;
   int kT = -1;
   if (part != kPartDecide) {
     if (s.pre_in_attn) {
@@ -719,7 +721,8 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
     if (last_part)
       for (int e = 0; e <= asr::kStages; ++e) CUDA_TRY(record(e));
   } else {
-    const int variant = (a.has_logits ? 9 : 0) + (a.host_io ? 3 * (1 + (int)(c->step & 1)) : 0) + part;
+    const int variant = (a.has_logits ? 9 : 0) + (a.ent_given ? 18 : 0) + (a.host_io ? 3 * (1 + (int)(c->step & 1)) : 0) +
+                        part;
     asr_ctx::StepGraph& G = c->graphs[variant];
     if (G.x && G.profiled != prof) {
       cudaGraphExecDestroy(G.x);
@@ -790,9 +793,11 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
       CUDA_TRY(cudaGraphInstantiate(&G.x, G.g, 0));
     } else {
       for (int k = 0; k < nk; ++k) {
-        if (memcmp(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra)) != 0) {
+        if (memcmp(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra)) != 0 ||
+            memcmp(&G.last[k].s, &kn_list[k].s, sizeof(DevState)) != 0) {   // a pointer of the step changed
           CUDA_TRY(cudaGraphExecKernelNodeSetParams(G.x, G.knodes[k], &kn_list[k].p));
           memcpy(G.last[k].extra, kn_list[k].extra, sizeof(kn_list[k].extra));
+          G.last[k].s = kn_list[k].s;
         }
       }
       for (size_t e = 0; e < evs.size(); ++e)
@@ -834,7 +839,7 @@ static asr_status step_finish(asr_ctx* c, StepArgs& a, cudaStream_t st) {
     const size_t ob = (size_t)s.B * s.L * s.Hq * s.d * 4;
     CUDA_TRY(cudaMemcpyAsync(a.o_user, a.o, ob, cudaMemcpyDeviceToHost, c->io_out));
     c->bytes_d2h += (int64_t)ob;
-    if (a.ent_user && a.has_logits) {
+    if (a.ent_user && (a.has_logits || a.ent_given)) {
       CUDA_TRY(cudaMemcpyAsync(a.ent_user, a.ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, c->io_out));
       c->bytes_d2h += (int64_t)s.B * 4;
     }
@@ -1188,7 +1193,24 @@ asr_status asr_sample(const void* logits, int32_t logits_dtype, int32_t batch, i
     return fail(ASR_E_INVALID, "asr_sample: batch / vocab out of range");
   if (!isfinite(temperature) || !isfinite(top_p)) return fail(ASR_E_INVALID, "asr_sample: temperature / top_p");
   CUDA_TRY(asr::launch_sample(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out,
-                              (cudaStream_t)cuda_stream));
+                              1.f, nullptr, (cudaStream_t)cuda_stream));
+  return ASR_OK;
+}
+
+asr_status asr_sample_entropy(const void* logits, int32_t logits_dtype, int32_t batch, int32_t vocab,
+                              float temperature, int32_t top_k, float top_p, const float* uniforms, int32_t* token_out,
+                              float entropy_temperature, float* entropy_out, void* cuda_stream) {
+  if (!entropy_out) return fail(ASR_E_INVALID, "asr_sample_entropy: entropy_out is NULL");
+  if (!(entropy_temperature > 0.f) || !isfinite(entropy_temperature))
+    return fail(ASR_E_INVALID, "asr_sample_entropy: entropy_temperature must be > 0");
+  if (!logits || !uniforms || !token_out) return fail(ASR_E_INVALID, "asr_sample_entropy: NULL pointer");
+  if (logits_dtype != ASR_KV_BF16 && logits_dtype != ASR_KV_F32)
+    return fail(ASR_E_INVALID, "asr_sample_entropy: logits_dtype");
+  if (batch < 1 || batch > 65535 || vocab < 1 || vocab >= (1 << 24))
+    return fail(ASR_E_INVALID, "asr_sample_entropy: batch / vocab out of range");
+  if (!isfinite(temperature) || !isfinite(top_p)) return fail(ASR_E_INVALID, "asr_sample_entropy: temperature / top_p");
+  CUDA_TRY(asr::launch_sample(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out,
+                              entropy_temperature, entropy_out, (cudaStream_t)cuda_stream));
   return ASR_OK;
 }
 

@@ -106,6 +106,7 @@ struct DevState {
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
   int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
   const float* ext_score;     // policy replay (NEXT-2): s_j given per position [B][max_ctx]; NULL = Eq. 2
+  const float* ent_given;     // [B] H(logits_prev) computed by the caller (asr_sample_entropy); NULL = from logits
   unsigned long long* hmask;  // [B][max_ctx][2] finite W: bit t = detection at step hstep - t
   int32_t* hstep;             // [B][max_ctx]    finite W: step of bit 0 (never: a large negative)
   int combine_in_decide;      // 1: the combine runs as extra blocks of the phase-D kernel (small batch)
@@ -347,7 +348,8 @@ void node_evict(KNode& n, const DevState& s, int grid);  // pressure mode: Belad
 void node_scoresum(KNode& n, const DevState& s);          // head-sharded mode: layer sums -> tok_score
 int attention_grid(const DevState& s, int num_sms);
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
-                          float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st);   // NEXT-1
+                          float top_p, const float* uniforms, int32_t* token_out, float ent_temp, float* entropy_out,
+                          cudaStream_t st);   // NEXT-1 (+ the row's entropy in the same pass)
 cudaError_t launch_kv_quantize(const void* kv, long rows, int n, int bits, int8_t* codes, float* scales,
                                cudaStream_t st);   // NEXT-4
 cudaError_t launch_kv_dequantize(const int8_t* codes, const float* scales, long rows, int n, int bits, void* kv,

@@ -55,6 +55,7 @@ struct SampleShm {
   unsigned long long res[2 * kWays];       // cluster totals of the last reduction
   float fout;
   int iout;
+  float zout, sout;   // this CTA's entropy partials (Z, S) about the row max, read by the cluster's rank 0
 };
 
 // Visit elements j = first, first + stride, ... < end: kU loads are issued before any is used (the
@@ -201,10 +202,14 @@ __device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned
 }
 
 // CS CTAs (one cluster) per row
+// With entropy_out, the same read of the row also yields H = ln Z - S / Z of p = softmax(x / ent_temp)
+// (Z = sum e^{(x-m)/T}, S = sum e^{(x-m)/T} (x-m)/T about the row max m; R-ent) for the step's recovery
+// detector (asr_step with ASR_ENTROPY_GIVEN): fp32 per thread, CTA partials summed in warp / rank order.
 template <typename TL, int CS>
 __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logits, int V, float temperature, int top_k,
                                                      float top_p, const float* __restrict__ uniforms,
-                                                     int32_t* __restrict__ token_out, int cache) {
+                                                     int32_t* __restrict__ token_out, int cache, float ent_temp,
+                                                     float* __restrict__ entropy_out) {
   __shared__ SampleShm sh;
   extern __shared__ __align__(16) uint8_t slice_smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -265,7 +270,39 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
   }
   cl.sync();
   const float m = mx;
+  if (entropy_out) {   // the entropy of the row, from the same (cached) slice
+    const float invTe = 1.0f / ent_temp;
+    float z = 0.f, sx = 0.f;
+    visit8(x, s0, s1, aligned, [&](float v, int) {
+      const float d = (v - m) * invTe;
+      const float e = __expf(d);
+      z += e;
+      sx += e > 0.f ? e * d : 0.f;
+    });
+    z = warp_sum(z);
+    sx = warp_sum(sx);
+    if (lane == 0) { sh.wq[w][0] = __float_as_uint(z); sh.wq[w][1] = __float_as_uint(sx); }
+    __syncthreads();
+    if (tid == 0) {
+      float zc = 0.f, sc = 0.f;
+      for (int q = 0; q < kSW; ++q) { zc += __uint_as_float((uint32_t)sh.wq[q][0]); sc += __uint_as_float((uint32_t)sh.wq[q][1]); }
+      sh.zout = zc;
+      sh.sout = sc;
+    }
+    cl.sync();
+    if (rank == 0 && tid == 0) {
+      float zt = 0.f, st = 0.f;
+      for (int r = 0; r < CS; ++r) {
+        const SampleShm* o = cl.map_shared_rank(&sh, r);
+        zt += o->zout;
+        st += o->sout;
+      }
+      entropy_out[row] = logf(zt) - st / zt;
+    }
+    __syncthreads();   // sh.wq is reused by the passes below
+  }
   if (!(temperature > 0.f) || top_k == 1 || V == 1) {
+    if (entropy_out) cl.sync();   // rank 0 reads every CTA's partials before any CTA leaves
     if (rank == 0 && tid == 0) token_out[row] = mi;
     return;
   }
@@ -496,7 +533,8 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
 
 template <int CS>
 cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
-                      float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
+                      float top_p, const float* uniforms, int32_t* token_out, float ent_temp, float* entropy_out,
+                      cudaStream_t st) {
   const size_t esz = logits_dtype == 1 ? 4 : 2;
   const size_t slice = (size_t)(((vocab + CS - 1) / CS + 31) & ~31) * esz;
   int cache = slice <= 96 * 1024 ? 1 : 0;   // the slice in shared memory (two CTAs per SM still fit)
@@ -524,13 +562,13 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
     cudaError_t e = cudaFuncSetAttribute(sample_kernel<float, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024 + kCand * 8);
     if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, sample_kernel<float, CS>, (const float*)logits, vocab, temperature, top_k, top_p,
-                              uniforms, token_out, cache);
+                              uniforms, token_out, cache, ent_temp, entropy_out);
   }
   cudaError_t e = cudaFuncSetAttribute(sample_kernel<__nv_bfloat16, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        96 * 1024 + kCand * 8);
   if (e != cudaSuccess) return e;
   return cudaLaunchKernelEx(&cfg, sample_kernel<__nv_bfloat16, CS>, (const __nv_bfloat16*)logits, vocab, temperature,
-                            top_k, top_p, uniforms, token_out, cache);
+                            top_k, top_p, uniforms, token_out, cache, ent_temp, entropy_out);
 }
 
 }  // namespace
@@ -539,13 +577,17 @@ cudaError_t launch_cs(const void* logits, int logits_dtype, int batch, int vocab
 // otherwise; each CTA keeps its slice of the row in shared memory when it fits (all passes then read
 // shared memory).
 cudaError_t launch_sample(const void* logits, int logits_dtype, int batch, int vocab, float temperature, int top_k,
-                          float top_p, const float* uniforms, int32_t* token_out, cudaStream_t st) {
+                          float top_p, const float* uniforms, int32_t* token_out, float ent_temp, float* entropy_out,
+                          cudaStream_t st) {
   const bool greedy = !(temperature > 0.f) || top_k == 1;   // one pass: the larger cluster's launch costs more
   if (batch <= 4 && !greedy)   // few rows: 16-CTA clusters (non-portable size; one per GPC) halve every pass
-    return launch_cs<16>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
+    return launch_cs<16>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, ent_temp,
+                         entropy_out, st);
   if (batch >= 8 && logits_dtype != 1)
-    return launch_cs<4>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
-  return launch_cs<8>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, st);
+    return launch_cs<4>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, ent_temp,
+                        entropy_out, st);
+  return launch_cs<8>(logits, logits_dtype, batch, vocab, temperature, top_k, top_p, uniforms, token_out, ent_temp,
+                      entropy_out, st);
 }
 
 }  // namespace asr

@@ -463,20 +463,25 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
   if (w == 0) {
     int level = 0;
     if (has_logits) {
-      // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
-      const float* ep = s.ent_part + (long)b * kEntSplits * 3;   // written by other blocks: via L2
-      float M = -INFINITY, Zl = 0.f, Sl = 0.f;
-      float pv[kEntSplits / 32][3];   // all loads first, then the merges
+      float H;
+      if (s.ent_given) {   // the caller's H (asr_sample_entropy took it in its pass over the row)
+        H = __ldcg(s.ent_given + b);
+      } else {
+        // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
+        const float* ep = s.ent_part + (long)b * kEntSplits * 3;   // written by other blocks: via L2
+        float M = -INFINITY, Zl = 0.f, Sl = 0.f;
+        float pv[kEntSplits / 32][3];   // all loads first, then the merges
 #pragma unroll
-      for (int k = 0; k < kEntSplits / 32; ++k)
+        for (int k = 0; k < kEntSplits / 32; ++k)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pv[k][c] = __ldcg(ep + (k * 32 + lane) * 3 + c);
+          for (int c = 0; c < 3; ++c) pv[k][c] = __ldcg(ep + (k * 32 + lane) * 3 + c);
 #pragma unroll
-      for (int k = 0; k < kEntSplits / 32; ++k) tri_merge(M, Zl, Sl, pv[k][0], pv[k][1], pv[k][2]);
-      for (int o = 16; o > 0; o >>= 1)
-        tri_merge(M, Zl, Sl, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Zl, o),
-                  __shfl_xor_sync(0xffffffffu, Sl, o));
-      const float H = logf(Zl) - Sl / Zl;
+        for (int k = 0; k < kEntSplits / 32; ++k) tri_merge(M, Zl, Sl, pv[k][0], pv[k][1], pv[k][2]);
+        for (int o = 16; o > 0; o >>= 1)
+          tri_merge(M, Zl, Sl, __shfl_xor_sync(0xffffffffu, M, o), __shfl_xor_sync(0xffffffffu, Zl, o),
+                    __shfl_xor_sync(0xffffffffu, Sl, o));
+        H = logf(Zl) - Sl / Zl;
+      }
       DetState& ds = s.det[b];
       double* hist = s.hist + (long)b * s.det_baseline;
       const int hl = ds.hist_len;
@@ -1435,7 +1440,7 @@ __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logit
   ASR_UNIT_SYNC();
   if (u.last) {
     if (s.tl && ASR_UNIT_TID() == 0) atomicMax(&s.tl[2 * kStages + 5], gtimer());
-    unit_finish(s, b, i, has_logits, entropy_out, u);
+    unit_finish(s, b, i, has_logits || s.ent_given != nullptr, entropy_out, u);
     if (s.tl && ASR_UNIT_TID() == 0) atomicMax(&s.tl[2 * kStages + 6], gtimer());
     ASR_UNIT_SYNC();
     if (ASR_UNIT_TID() == 0)

@@ -61,6 +61,7 @@ class Case:
     history_window: int = 0        # W (NEXT-3): 0 = lifetime counts
     time_attention_at: tuple = ()  # steps before which asr_time_attention runs (must leave no trace)
     fr_clear_counts: int = 0       # FR also clears the detection counts (SPEC S:391 reading)
+    entropy_given: bool = False    # H taken by asr_sample_entropy (with a draw) and passed to the step
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -147,6 +148,16 @@ def run(c: Case, check_o: bool = True) -> dict:
             o = np.zeros((c.B, c.L, c.Hq, c.d), np.float32)
             ent = np.zeros(c.B, np.float32)
             ctx.step(q, kn, vn, o, logits_prev=lg, entropy=ent)
+        elif c.entropy_given and lg is not None:
+            # NEXT-1 fused with (a6): one read of each logits row yields the next token and H
+            from paper_2512_11221_b200 import asr_sample_entropy
+            o_t = torch.zeros((c.B, c.L, c.Hq, c.d), dtype=torch.float32, device="cuda")
+            e_t = torch.zeros(c.B, dtype=torch.float32, device="cuda")
+            h_t = torch.empty(c.B, dtype=torch.float32, device="cuda")
+            tok = torch.empty(c.B, dtype=torch.int32, device="cuda")
+            asr_sample_entropy(to_t(lg), torch.full((c.B,), 0.5, device="cuda"), tok, h_t, temperature=0.8, top_k=50,
+                               top_p=0.9)
+            ctx.step(to_t(q), to_t(kn), to_t(vn), o_t, logits_prev=h_t, entropy=e_t, entropy_given=True)
         else:
             o_t = torch.zeros((c.B, c.L, c.Hq, c.d), dtype=torch.float32, device="cuda")
             e_t = torch.zeros(c.B, dtype=torch.float32, device="cuda")

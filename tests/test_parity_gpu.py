@@ -208,3 +208,14 @@ def test_pressure_belady_llama_batch_with_recovery():
              spike_first=60, spike_period=16, spike_count=1, pool_tokens=390, pool_reserve=24)
     s = run(c)
     assert s["evicted"] > 0 and s["prefetched"] > 0
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_entropy_given_by_the_sampler(B):
+    # NEXT-1 fused with the entropy stage: asr_sample_entropy draws the next token and takes H in the
+    # same read of each row; the step consumes H (ASR_ENTROPY_GIVEN) instead of re-reading the row.
+    # Planted spikes drive the ladder; ledgers, lists and H bitwise / within 1e-4 of the oracle.
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=B, prompt=(60, 41)[:B], steps=120, window=8, vocab=128256, seed=97,
+             spike_first=50, spike_period=16, spike_count=3, entropy_given=True)
+    s = run(c)
+    assert s["recoveries"] >= 3 * B

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import gen
+import oracle
 from oracle.sample import interval, kept_set, sample
 
 pytestmark = pytest.mark.gpu
@@ -154,3 +155,29 @@ def test_sample_uncached_slice():
         asr_sample(xt, torch.tensor([0.5 * (lo + hi)], dtype=torch.float32, device="cuda"), out,
                    temperature=T, top_k=k, top_p=P)
         assert int(out.item()) == tok, (T, k, P, int(out.item()), tok)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("B", [1, 5, 9])
+def test_sample_entropy_one_pass(dtype, B):
+    # asr_sample_entropy: the same token as asr_sample, and H of softmax(x / T_ent) within 1e-4 nats of the
+    # oracle (fp32 accumulation over 128256 terms), for greedy and filtered draws, T_ent 1 and 0.7
+    import torch
+    from paper_2512_11221_b200 import asr_sample, asr_sample_entropy
+    V = 128256
+    g = gen.GenParams(seed=31, vocab=V, spike_first=2, spike_period=3, spike_count=9)
+    rows = np.stack([gen.logits(g, b, b % 4, "bf16" if dtype == "bf16" else "f32") for b in range(B)])
+    xt = torch.from_numpy(rows.view(np.int16) if dtype == "bf16" else rows).cuda()
+    xt = xt.view(torch.bfloat16) if dtype == "bf16" else xt
+    u = torch.rand(B, device="cuda")
+    for (T, k, P) in ((0.0, 0, 1.0), (0.8, 50, 0.9), (1.0, 0, 0.95)):
+        for te in (1.0, 0.7):
+            t1 = torch.empty(B, dtype=torch.int32, device="cuda")
+            t2 = torch.empty(B, dtype=torch.int32, device="cuda")
+            h = torch.empty(B, dtype=torch.float32, device="cuda")
+            asr_sample(xt, u, t1, temperature=T, top_k=k, top_p=P)
+            asr_sample_entropy(xt, u, t2, h, temperature=T, top_k=k, top_p=P, entropy_temperature=te)
+            assert torch.equal(t1, t2)
+            for b in range(B):
+                want = oracle.entropy(rows[b], te)
+                assert abs(float(h[b]) - want) <= 1e-4, (T, k, P, te, b, float(h[b]), want)
