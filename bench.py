@@ -772,6 +772,26 @@ def spawn_ranks(a) -> int:
     return subprocess.call(cmd)
 
 
+def sweep_point(local_rank: int) -> dict:
+    """NEXT-2: the (tau, K, k, W) sensitivity sweep (SPEC run_sweep) of the policy on a uniform
+    relevance trace, 4 sequences grown from a 1024-token prompt by 512 steps, 32 cells replayed on the GPU
+    (paper_2512_11221_b200/sweep.py); cell-steps per second over the whole sweep (host stats included)."""
+    import torch
+
+    import gen
+    from paper_2512_11221_b200.sweep import run_sweep
+    B, prompt, steps = 4, 1024, 512
+    sc = torch.from_numpy(gen.score_trace("uniform", B, prompt + steps + 1, seed=3)).cuda(local_rank)
+    grid = {"tau": [0.2, 0.4, 0.6, 0.8], "window": [32, 512], "softness": [1.0, 2.0], "history_window": [0, 64]}
+    t0 = time.perf_counter()
+    rows = run_sweep(grid, sc, steps, prompt, device=local_rank)
+    dt = time.perf_counter() - t0
+    table = [{k: r[k] for k in ("tau", "window", "softness", "history_window", "mean_compression", "max_absence",
+                                "recoveries", "final_active", "final_total")} for r in rows]
+    return {"workload": f"uniform trace, batch {B}, prompt {prompt} + {steps} steps, {len(rows)} cells",
+            "seconds": dt, "cell_steps_per_s": len(rows) * steps / dt, "table": table}
+
+
 def main():
     a = parse()
     if "WORLD_SIZE" not in os.environ and a.gpus > 1:
@@ -801,7 +821,7 @@ def main():
         sys.exit(0)
     points = {}
     wanted = [x for x in a.points.split(",") if x]
-    for name in [x for x in wanted if x not in ("sample", "replay", "quant")]:
+    for name in [x for x in wanted if x not in ("sample", "replay", "quant", "sweep")]:
         b = argparse.Namespace(**vars(a))
         for k, v in POINTS[name].items():
             setattr(b, k, v)
@@ -829,6 +849,8 @@ def main():
         line["detail"]["policy_replay"] = replay_point(local_rank)
     if line is not None and world == 1 and "quant" in wanted:
         line["detail"]["frozen_tier_quant"] = quant_point(local_rank)
+    if line is not None and world == 1 and "sweep" in wanted:
+        line["detail"]["sensitivity_sweep"] = sweep_point(local_rank)
     if line is not None:
         if points:
             line["points"] = points
@@ -841,7 +863,7 @@ def main():
 
 
 def parse_default_points() -> str:
-    return "c2,ctx32k,c3,w1,full,pool,sample,replay,quant"
+    return "c2,ctx32k,c3,w1,full,pool,sample,replay,quant,sweep"
 
 
 if __name__ == "__main__":

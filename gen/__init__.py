@@ -209,3 +209,37 @@ def dev_logits(p: GenParams, B: int, step: int, out) -> None:
     rc = dev_lib().asrgen_dev_logits(ctypes.byref(pc), B, step, out.data_ptr(), _code(out), _stream())
     if rc:
         raise RuntimeError(f"asrgen_dev_logits failed: {rc}")
+
+
+# ---------------------------------------------------------------- policy-replay score traces (NEXT-2)
+
+def _splitmix64(x: np.ndarray) -> np.ndarray:
+    x = x + np.uint64(0x9E3779B97F4A7C15)
+    z = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def score_trace(kind: str, batch: int, n: int, seed: int = 1, p: GenParams | None = None) -> np.ndarray:
+    """Per-position relevance scores s_j, constant over the steps, fp32 [batch][n] — the input of a
+    policy replay (asr_step_policy / OracleSeq.step_policy).  kind: "w0" every token 0.25 (all-cold
+    under tau in (0.25, 1.5]); "w1" 1.5 for the LAT hot set of `p` (30 % with hot_permille=300), else
+    0.25; "uniform" u_j in [0, 1) from a counter hash of (seed, b, j) with 2^-24 resolution (so
+    `s < tau` is decided identically in fp32 and fp64 for tau on that lattice)."""
+    if kind == "w0":
+        return np.full((batch, n), 0.25, np.float32)
+    if kind == "w1":
+        assert p is not None
+        out = np.full((batch, n), 0.25, np.float32)
+        for b in range(batch):
+            for j in range(n):
+                if is_hot(p, b, j):
+                    out[b, j] = 1.5
+        return out
+    if kind == "uniform":
+        with np.errstate(over="ignore"):
+            idx = (np.uint64(seed) << np.uint64(40)) + (np.arange(batch, dtype=np.uint64)[:, None] << np.uint64(24)) \
+                + np.arange(n, dtype=np.uint64)[None, :]
+            h = _splitmix64(idx)
+        return ((h >> np.uint64(40)).astype(np.float64) * 2.0 ** -24).astype(np.float32)
+    raise ValueError(kind)
