@@ -60,6 +60,7 @@ def parse():
                     help="pressure mode: device slots = pool_frac * batch * context (0 = full residency)")
     ap.add_argument("--evict-min", type=int, default=2, help="pressure mode: never evict tokens returning sooner")
     ap.add_argument("--evict-policy", type=int, default=0, help="pressure mode: 0 Belady under pressure, 1 at freeze")
+    ap.add_argument("--mirror-bits", type=int, default=0, help="pressure mode: 0 bf16 host mirror, 8 INT8 frozen tier")
     ap.add_argument("--points", default=parse_default_points(),
                     help="comma list of extra workloads (POINTS, or 'sample': the next-token draw) or '' for none")
     ap.add_argument("--workload", default="c1", choices=["c1", "c3", "c4"],
@@ -257,6 +258,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
                  kv_dtype=KV_BF16, window=a.window, tau=a.tau, softness=2.0, vocab=VOCAB, profile_stages=0,
                  device=local_rank, pool_tokens=pool, evict_min_absence=a.evict_min, history_window=a.history_window,
                  evict_policy=a.evict_policy, host_mirror=0 if (a.no_mirror and a.pool_frac == 0) else 1,
+                 mirror_bits=a.mirror_bits if pool else 0,
                  score_heads=HQ if a.head_shard else 0)
     need = B * max_ctx * TOKEN_KV_BYTES * (2 if a.workload == "c3" else 1) * 1.03 + (2 << 30)
     free_b, _ = torch.cuda.mem_get_info(dev)
@@ -548,7 +550,7 @@ def run_asr(a, rank: int, world: int, local_rank: int):
         state = "grown from a 512-token prompt"
     else:
         wl = (f"llama3-8b-shape ctx{a.context} batch{B} window{a.window} {a.family}"
-              + (f" pool{a.pool_frac:g}" if pool else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else "")
+              + (f" pool{a.pool_frac:g}" if pool else "") + (" int8-tier" if pool and a.mirror_bits == 8 else "") + (f" tau{a.tau:g}" if a.tau != 0.5 else "")
               + (f" W{a.history_window}" if a.history_window else ""))
         state = "grown from a 512-token prompt"
     line = {
@@ -618,6 +620,7 @@ POINTS = {   # extra workloads measured after the headline
     "w1": dict(family="w1"),                                        # 30 % hot tokens (SURVEY W1 family)
     "full": dict(tau=0.0),                                          # full-KV baseline: nothing freezes
     "pool": dict(pool_frac=0.5, steps=16, warmup=4),                # pressure mode: 50 % device pool, Belady
+    "pool8": dict(pool_frac=0.5, steps=16, warmup=4, mirror_bits=8),   # + the INT8 frozen tier on the link
     "w128": dict(history_window=128),                               # NEXT-3: finite history window W
     "c4share": dict(workload="c4", context=32768, batch=32, steps=8, warmup=3, no_mirror=True),  # opt-in
 }
@@ -863,7 +866,7 @@ def main():
 
 
 def parse_default_points() -> str:
-    return "c2,ctx32k,c3,w1,full,pool,sample,replay,quant,sweep"
+    return "c2,ctx32k,c3,w1,full,pool,pool8,sample,replay,quant,sweep"
 
 
 if __name__ == "__main__":

@@ -98,6 +98,12 @@ typedef struct {
                            * slots cover the next step's appends + prefetches + pool_reserve.
                            * ASR_EVICT_AT_FREEZE: every token frozen for >= evict_min_absence steps
                            * is evicted when it freezes (round-1 policy, kept for comparison). */
+  int32_t mirror_bits;    /* pressure mode, bf16 KV, head_dim a multiple of 32: 0 = the host mirror holds
+                           * bf16 rows; 8 = the quantised frozen tier (NEXT-4, R-quant): every row
+                           * (token, layer, K|V, KV head) stored as INT8 codes + one fp32 scale, written
+                           * at append, dequantised into the device slot on prefetch / demand restore
+                           * (1.94x fewer host-link bytes at d = 128; lossy by R-quant's bound) */
+  int32_t reserved2;
 } asr_config;
 typedef enum { ASR_EVICT_BELADY = 0, ASR_EVICT_AT_FREEZE = 1 } asr_evict_policy;
 
@@ -165,6 +171,8 @@ typedef struct {
   int32_t* active_len;    /* [1] |A_i| */
   float* scores;          /* [capacity] s_j per attended index of the last step */
   int32_t capacity;       /* length of the arrays above (>= total) */
+  uint8_t* dequantized;   /* [capacity] INT8 tier (mirror_bits = 8): 1 = the token's device slot holds its
+                           * dequantised rows (it was copied back from the quantised mirror) */
 } asr_ledger_view;
 
 /* Create a context: allocates the device KV pool [B][max_context][L][2][Hkv][d], the ledger and

@@ -45,7 +45,8 @@ class asr_config(ctypes.Structure):
                 ("det_z", ctypes.c_float), ("det_sigma_floor", ctypes.c_float), ("fr_clear_counts", ctypes.c_int32),
                 ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("evict_min_absence", ctypes.c_int32), ("pool_reserve", ctypes.c_int32), ("pool_tokens", ctypes.c_int64),
-                ("score_heads", ctypes.c_int32), ("evict_policy", ctypes.c_int32)]
+                ("score_heads", ctypes.c_int32), ("evict_policy", ctypes.c_int32), ("mirror_bits", ctypes.c_int32),
+                ("reserved2", ctypes.c_int32)]
 
 
 class asr_step_io(ctypes.Structure):
@@ -69,7 +70,8 @@ class asr_stats_t(ctypes.Structure):
 class asr_ledger_view(ctypes.Structure):
     _fields_ = [("residency", ctypes.c_void_p), ("timer", ctypes.c_void_p), ("count", ctypes.c_void_p),
                 ("freeze_step", ctypes.c_void_p), ("active_list", ctypes.c_void_p),
-                ("active_len", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("capacity", ctypes.c_int32)]
+                ("active_len", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("capacity", ctypes.c_int32),
+                ("dequantized", ctypes.c_void_p)]
 
 
 EXPORTS = ("asr_config_defaults", "asr_create", "asr_step", "asr_restore", "asr_stats", "asr_read_kv",
@@ -170,6 +172,8 @@ class Config:
     pool_tokens: int = 0             # 0 = full residency; > 0 = pressure mode (device slot pool)
     score_heads: int = 0             # head-sharded mode: H of Eq. 2 over all shards (0 = n_q_heads)
     evict_policy: int = 0            # pressure mode: EVICT_BELADY (capacity-driven) or EVICT_AT_FREEZE
+    mirror_bits: int = 0             # pressure mode: 0 bf16 host mirror, 8 the INT8 frozen tier (R-quant)
+    reserved2: int = 0
 
     def c(self) -> asr_config:
         v = dataclasses.asdict(self)
@@ -323,15 +327,16 @@ def asr_stats(ctx, seq: int, capacity: int = 0, detail: bool = False) -> dict:
         arrays = {"residency": np.zeros(capacity, np.uint8), "timer": np.zeros(capacity, np.int32),
                   "count": np.zeros(capacity, np.uint32), "freeze_step": np.zeros(capacity, np.int32),
                   "active_list": np.zeros(capacity, np.int32), "active_len": np.zeros(1, np.int32),
-                  "scores": np.zeros(capacity, np.float32)}
+                  "scores": np.zeros(capacity, np.float32), "dequantized": np.zeros(capacity, np.uint8)}
         view = asr_ledger_view(*(arrays[k].ctypes.data for k in ("residency", "timer", "count", "freeze_step",
                                                                  "active_list", "active_len", "scores")),
-                               capacity)
+                               capacity, arrays["dequantized"].ctypes.data)
     _check(lib().asr_stats(ctx, seq, ctypes.byref(st), ctypes.byref(view) if view is not None else None))
     out = {f[0]: getattr(st, f[0]) for f in asr_stats_t._fields_}
     if detail:
         n, A = int(st.total), int(arrays["active_len"][0])
         out["ledger"] = {k: arrays[k][:n] for k in ("residency", "timer", "count", "freeze_step")}
+        out["dequantized"] = arrays["dequantized"][:n]
         out["active_list"] = arrays["active_list"][:A]
         out["scores"] = arrays["scores"][:A]
     return out

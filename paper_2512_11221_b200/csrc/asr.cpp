@@ -49,6 +49,9 @@ struct asr_ctx {
   bool uniform_prompt = true;
   int64_t step = 0;              // host mirror of the device step counter
   void* host_mirror = nullptr;   // pinned [B][max_ctx][L][2][Hkv][d]
+  int8_t* host_codes = nullptr;  // INT8 tier (mirror_bits = 8): pinned mapped codes and scales
+  float* host_scales = nullptr;
+  size_t mirror_tok_bytes = 0;   // host-mirror bytes of one token
   int32_t* tok_count_host = nullptr;   // mapped pinned: the packed all-reduce count of the last attend
   cudaEvent_t ev_attend = nullptr;
   int64_t allreduce_bytes = 0;
@@ -108,6 +111,8 @@ struct asr_ctx {
     }
     for (void* p : allocs) cudaFree(p);
     if (host_mirror) cudaFreeHost(host_mirror);
+    if (host_codes) cudaFreeHost(host_codes);
+    if (host_scales) cudaFreeHost(host_scales);
     if (tok_count_host) cudaFreeHost(tok_count_host);
     if (ev_attend) cudaEventDestroy(ev_attend);
     if (side) cudaStreamDestroy(side);
@@ -196,6 +201,8 @@ void asr_config_defaults(asr_config* c) {
   c->pool_tokens = 0;
   c->score_heads = 0;
   c->evict_policy = ASR_EVICT_BELADY;
+  c->mirror_bits = 0;
+  c->reserved2 = 0;
 }
 
 static asr_status validate(const asr_config* c) {
@@ -230,6 +237,9 @@ static asr_status validate(const asr_config* c) {
   if (c->evict_policy != ASR_EVICT_BELADY && c->evict_policy != ASR_EVICT_AT_FREEZE)
     return fail(ASR_E_INVALID, "evict_policy");
   if (c->pool_reserve < 0) return fail(ASR_E_INVALID, "pool_reserve < 0");
+  if (c->mirror_bits != 0 && c->mirror_bits != 8) return fail(ASR_E_INVALID, "mirror_bits must be 0 or 8");
+  if (c->mirror_bits == 8 && (c->pool_tokens <= 0 || c->kv_dtype != ASR_KV_BF16 || c->head_dim % 32))
+    return fail(ASR_E_INVALID, "mirror_bits = 8 needs pressure mode (pool_tokens > 0), bf16 KV and head_dim >= 32");
   if (c->score_heads != 0 && c->score_heads < c->n_q_heads)
     return fail(ASR_E_INVALID, "score_heads must be 0 or >= n_q_heads (the heads of all shards)");
   return ASR_OK;
@@ -424,11 +434,24 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     CUDA_TRY(cudaMemcpyAsync(s.prompt_len, prompt_len, (size_t)s.B * 4, cudaMemcpyHostToDevice, st));
     for (int b = 0; b < s.B; ++b)
       if (prompt_len[b] > 0) CUDA_TRY(cudaMemsetAsync(s.res + (size_t)b * s.max_ctx, 1, prompt_len[b], st));
-    if (cfg->host_mirror) {
+    s.mirror_bits = cfg->mirror_bits;
+    if (cfg->host_mirror && s.mirror_bits == 8) {   // the INT8 frozen tier: codes + scales, mapped
+      const size_t R = (size_t)s.L * 2 * s.Hkv;
+      cudaError_t e = cudaHostAlloc(&c->host_codes, BT * R * s.d, cudaHostAllocPortable | cudaHostAllocMapped);
+      if (e == cudaSuccess)
+        e = cudaHostAlloc(&c->host_scales, BT * R * 4, cudaHostAllocPortable | cudaHostAllocMapped);
+      if (e != cudaSuccess) return fail(ASR_E_OOM, "pinned host mirror allocation failed");
+      CUDA_TRY(cudaHostGetDevicePointer((void**)&s.host_codes, c->host_codes, 0));
+      CUDA_TRY(cudaHostGetDevicePointer((void**)&s.host_scales, c->host_scales, 0));
+      CUDA_TRY(c->alloc(&s.deq, BT));
+      CUDA_TRY(cudaMemsetAsync(s.deq, 0, BT, st));
+      c->mirror_tok_bytes = R * (s.d + 4);
+    } else if (cfg->host_mirror) {
       cudaError_t e = cudaHostAlloc(&c->host_mirror, BT * c->tok_bytes,
                                     cudaHostAllocPortable | (s.pool_mode ? cudaHostAllocMapped : 0));
       if (e != cudaSuccess) return fail(ASR_E_OOM, "pinned host mirror allocation failed");
       if (s.pool_mode) CUDA_TRY(cudaHostGetDevicePointer((void**)&s.host_kv, c->host_mirror, 0));
+      c->mirror_tok_bytes = c->tok_bytes;
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_append, cudaEventDisableTiming));
@@ -447,6 +470,12 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
         char* hdst = (char*)c->host_mirror + (size_t)b * s.max_ctx * c->tok_bytes;
         CUDA_TRY(cudaMemcpyAsync(hdst, dst, (size_t)prompt_len[b] * c->tok_bytes, cudaMemcpyDeviceToHost, st));
         c->bytes_d2h += (int64_t)prompt_len[b] * c->tok_bytes;
+      } else if (c->host_codes) {   // the prompt's rows quantised straight into the mapped INT8 tier
+        const size_t R = (size_t)s.L * 2 * s.Hkv;
+        CUDA_TRY(asr::launch_kv_quantize(dst, (long)(prompt_len[b] * R), s.d, 8,
+                                         s.host_codes + (size_t)b * s.max_ctx * R * s.d,
+                                         s.host_scales + (size_t)b * s.max_ctx * R, st));
+        c->bytes_d2h += (int64_t)prompt_len[b] * c->mirror_tok_bytes;
       }
     }
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -813,8 +842,8 @@ static asr_status step_launch(asr_ctx* c, StepArgs& a, int part, cudaStream_t st
 static asr_status step_finish(asr_ctx* c, StepArgs& a, cudaStream_t st) {
   const DevState& s = c->s;
   // (a5) write-once host mirror of the appended token (side stream, overlapped with compute)
-  if (c->host_mirror && s.pool_mode) {
-    c->bytes_d2h += (int64_t)s.B * c->tok_bytes;   // written by the append units (mapped mirror)
+  if ((c->host_mirror || c->host_codes) && s.pool_mode) {
+    c->bytes_d2h += (int64_t)s.B * c->mirror_tok_bytes;   // written by the append units (mapped mirror)
   } else if (c->host_mirror) {
     CUDA_TRY(cudaEventRecord(c->ev_append, st));
     CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_append, 0));
@@ -1051,6 +1080,10 @@ asr_status asr_stats(asr_ctx* c, int32_t seq, asr_stats_t* out, asr_ledger_view*
       CUDA_TRY(cudaMemcpy(detail->active_list, s.act_pos + asr::act_off(s, p) + base, (size_t)A * 4,
                           cudaMemcpyDeviceToHost));
     if (detail->scores && A) CUDA_TRY(cudaMemcpy(detail->scores, s.score + base, (size_t)A * 4, cudaMemcpyDeviceToHost));
+    if (detail->dequantized) {
+      if (s.deq) CUDA_TRY(cudaMemcpy(detail->dequantized, s.deq + base, n, cudaMemcpyDeviceToHost));
+      else memset(detail->dequantized, 0, n);
+    }
   }
   if (err) return fail(ASR_E_INVARIANT, "device invariant violation, flags=" + std::to_string(err));
   return ASR_OK;
@@ -1061,13 +1094,23 @@ asr_status asr_read_kv(asr_ctx* c, int32_t seq, int32_t pos, int32_t from_mirror
   const DevState& s = c->s;
   if (seq < 0 || seq >= s.B) return fail(ASR_E_INVALID, "seq out of range");
   if (pos < 0 || pos >= c->prompt_len[seq] + c->step) return fail(ASR_E_INVALID, "pos not stored");
-  if (from_mirror && !c->host_mirror) return fail(ASR_E_INVALID, "no host mirror");
+  if (from_mirror && !c->host_mirror && !c->host_codes) return fail(ASR_E_INVALID, "no host mirror");
   CUDA_TRY(cudaSetDevice(c->cfg.device));
   CUDA_TRY(cudaStreamSynchronize(c->last_stream));
   CUDA_TRY(cudaStreamSynchronize(c->side));
   std::vector<char> tok(c->tok_bytes);
   const size_t off = ((size_t)seq * s.max_ctx + pos) * c->tok_bytes;
-  if (from_mirror) {
+  if (from_mirror && c->host_codes) {   // INT8 tier: the dequantised rows, bf16_rn(code * scale)
+    const size_t R = (size_t)s.L * 2 * s.Hkv, r0 = ((size_t)seq * s.max_ctx + pos) * R;
+    uint16_t* o = reinterpret_cast<uint16_t*>(tok.data());
+    for (size_t r = 0; r < R; ++r)
+      for (int e = 0; e < s.d; ++e) {
+        const float x = (float)c->host_codes[(r0 + r) * s.d + e] * c->host_scales[r0 + r];
+        uint32_t u;
+        memcpy(&u, &x, 4);
+        o[r * s.d + e] = (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);   // round to nearest even
+      }
+  } else if (from_mirror) {
     memcpy(tok.data(), (const char*)c->host_mirror + off, c->tok_bytes);
   } else {
     size_t doff = off;

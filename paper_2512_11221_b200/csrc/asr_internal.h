@@ -129,6 +129,10 @@ struct DevState {
   int32_t* free_stack;        // [pool] free slots
   int32_t* free_top;          // [1] number of free slots
   char* host_kv;              // device-mapped pointer of the pinned host mirror (pool mode)
+  int mirror_bits;            // 0: bf16 mirror; 8: R-quant INT8 tier (codes + one fp32 scale per row)
+  int8_t* host_codes;         // INT8 tier: mapped [B][max_ctx][L][2][Hkv][d] codes
+  float* host_scales;         // INT8 tier: mapped [B][max_ctx][L][2][Hkv] scales
+  uint8_t* deq;               // INT8 tier: [B][max_ctx] 1 = the device slot holds the dequantised row values
   int32_t* pf_list;           // [2][B][max_ctx] positions to prefetch (timer reached 1), by step parity
   int32_t* pf_count;          // [2][B]
   int32_t* cp_list;           // [B][max_ctx] positions whose slot the copy kernel fills this step

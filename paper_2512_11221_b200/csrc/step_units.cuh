@@ -92,11 +92,82 @@ __device__ __forceinline__ void pool_push(const DevState& s, int slot) {
   ASR_CHECK(s, idx >= 0 && idx < s.kv_slots && slot >= 0 && slot < s.kv_slots);
   s.free_stack[idx] = slot;
 }
+// ---------------------------------------------------------------------------------- (a5) INT8 tier
+// NEXT-4 wired into the host link: with mirror_bits = 8 the write-once host mirror holds every row
+// (token, layer, K|V, KV head; d values) as R-quant INT8 codes + one fp32 scale (DESIGN.md §2,
+// oracle/quant.py): scale = RN(amax / 127), code = clamp(rint(RN(x / scale)), +-127) (IEEE fp32
+// divisions, half-to-even), x' = bf16_rn(code * scale).  A restore moves d + 4 bytes per row instead of
+// 2d (1.94x fewer at d = 128) and writes the dequantised row into the device slot.
+// One warp quantises one row (d a multiple of 32, <= 256): lane e holds values e*(d/32) ...
+__device__ __forceinline__ void quant_row8_warp(const __nv_bfloat16* __restrict__ x, int d, int8_t* codes,
+                                                float* scale_out) {
+  const int lane = threadIdx.x & 31;
+  const int per = d >> 5;   // values per lane (1 .. 8)
+  float v[8];
+  float amax = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    v[e] = e < per ? __bfloat162float(x[lane * per + e]) : 0.f;
+    amax = fmaxf(amax, fabsf(v[e]));
+  }
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float scale = __fdiv_rn(amax, 127.f);
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (e < per) {
+      int c = 0;
+      if (scale != 0.f) c = max(-127, min(127, __float2int_rn(__fdiv_rn(v[e], scale))));
+      codes[lane * per + e] = (int8_t)c;
+    }
+  if (lane == 0) *scale_out = scale;
+}
+
 // Block-cooperative copy of one token (all layers, K and V) from the pinned host mirror (mapped,
-// read over the host link) into its device slot.
+// read over the host link) into its device slot (INT8 tier: dequantised on the way).
 __device__ void copy_token_h2d(const DevState& s, int b, int pos, int slot) {
   if (slot < 0) return;
   ASR_CHECK(s, slot < s.kv_slots && pos >= 0 && pos < s.cap);
+  if (s.mirror_bits == 8) {
+    const int R = s.L * 2 * s.Hkv;                 // rows of the token
+    const long r0 = ((long)b * s.max_ctx + pos) * R;
+    const int per_row = s.d / 16;                  // 16 codes per item
+    const int items = R * per_row;
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(s.kv) + (long)slot * s.tok_bytes);
+    for (int t0 = (int)ASR_UNIT_TID(); t0 < items; t0 += 4 * (int)ASR_UNIT_THREADS()) {
+      uint4 cw[4];
+      float sc[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {   // the items' codes and scales in flight over the host link
+        const int t = min(t0 + k * (int)ASR_UNIT_THREADS(), items - 1);
+        const int r = t / per_row, c = t % per_row;
+        cw[k] = *reinterpret_cast<const uint4*>(s.host_codes + (r0 + r) * s.d + c * 16);
+        sc[k] = s.host_scales[r0 + r];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = t0 + k * (int)ASR_UNIT_THREADS();
+        if (t >= items) break;
+        const int r = t / per_row, c = t % per_row;
+        const uint32_t w[4] = {cw[k].x, cw[k].y, cw[k].z, cw[k].w};
+        uint32_t o[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c0 = (int)(int8_t)(w[q >> 1] >> (16 * (q & 1)));
+          const int c1 = (int)(int8_t)(w[q >> 1] >> (16 * (q & 1) + 8));
+          const __nv_bfloat162 h = __floats2bfloat162_rn((float)c0 * sc[k], (float)c1 * sc[k]);
+          o[q] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst + (long)r * s.d + c * 16);
+        d4[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        d4[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    if (ASR_UNIT_TID() == 0) {
+      atomicAdd(s.h2d, (unsigned long long)R * (s.d + 4));
+      s.deq[(long)b * s.max_ctx + pos] = 1;
+    }
+    return;
+  }
   const uint4* src = reinterpret_cast<const uint4*>(s.host_kv + ((long)b * s.max_ctx + pos) * s.tok_bytes);
   uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<char*>(s.kv) + (long)slot * s.tok_bytes);
   const int nv = (int)(s.tok_bytes / 16);
@@ -350,10 +421,23 @@ __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __
   const int row = s.Hkv * s.d;  // elements of K (or V) per token-layer
   TK* dst = reinterpret_cast<TK*>(s.kv) + (slot * s.L + l) * 2 * row;
   // pressure mode: the write-once host mirror is written here too (mapped pinned memory), so a
-  // token's bytes are off-GPU before it can ever be evicted
-  TK* mir = s.pool_mode ? reinterpret_cast<TK*>(s.host_kv) + (((long)b * s.max_ctx + pos) * s.L + l) * 2 * row : nullptr;
+  // token's bytes are off-GPU before it can ever be evicted (INT8 tier: quantised rows, below)
+  TK* mir = s.pool_mode && s.mirror_bits == 0
+                ? reinterpret_cast<TK*>(s.host_kv) + (((long)b * s.max_ctx + pos) * s.L + l) * 2 * row
+                : nullptr;
   const TK* ks = k_new + ((long)b * s.L + l) * row;
   const TK* vs = v_new + ((long)b * s.L + l) * row;
+  if constexpr (sizeof(TK) == 2) {
+    if (s.pool_mode && s.mirror_bits == 8) {   // one warp per row: 2 * Hkv rows of d for this (b, l)
+      const long r0 = (((long)b * s.max_ctx + pos) * s.L + l) * 2 * s.Hkv;
+      const int nw = (int)ASR_UNIT_THREADS() >> 5, w = (int)ASR_UNIT_TID() >> 5;
+      for (int r = w; r < 2 * s.Hkv; r += nw) {
+        const TK* x = (r < s.Hkv ? ks : vs) + (long)(r % s.Hkv) * s.d;
+        quant_row8_warp(reinterpret_cast<const __nv_bfloat16*>(x), s.d, s.host_codes + (r0 + r) * s.d,
+                        s.host_scales + r0 + r);
+      }
+    }
+  }
   const int vec = (int)(16 / sizeof(TK));
   if (row % vec == 0) {
     const int nv = row / vec;

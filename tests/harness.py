@@ -62,6 +62,7 @@ class Case:
     time_attention_at: tuple = ()  # steps before which asr_time_attention runs (must leave no trace)
     fr_clear_counts: int = 0       # FR also clears the detection counts (SPEC S:391 reading)
     entropy_given: bool = False    # H taken by asr_sample_entropy (with a draw) and passed to the step
+    mirror_bits: int = 0           # 8: the INT8 frozen tier (restored tokens come back dequantised)
 
     def gen_params(self) -> gen.GenParams:
         return gen.GenParams(seed=self.seed, family=self.family, L=self.L, Hq=self.Hq, Hkv=self.Hkv, d=self.d,
@@ -88,7 +89,8 @@ def asr_cfg(c: Case):
                   window=c.window, tau=c.tau, softness=c.softness, pinned_prefix=c.pinned_prefix,
                   score_mode=c.score_mode, tick_order=c.tick_order, vocab=c.vocab, wr_window=c.wr_window,
                   pool_tokens=c.pool_tokens, evict_min_absence=c.evict_min, history_window=c.history_window,
-                  fr_clear_counts=c.fr_clear_counts, evict_policy=c.evict_policy, pool_reserve=c.pool_reserve)
+                  fr_clear_counts=c.fr_clear_counts, evict_policy=c.evict_policy, pool_reserve=c.pool_reserve,
+                  mirror_bits=c.mirror_bits)
 
 
 def o_rel_err(o: np.ndarray, o_ref: np.ndarray) -> float:
@@ -124,6 +126,19 @@ def run(c: Case, check_o: bool = True) -> dict:
         return t if c.host_io else t.cuda()
 
     ctx = Context(asr_cfg(c), to_t(pk), to_t(pv), P)
+    # INT8 tier: a token copied back from the quantised mirror is attended with its R-quant
+    # dequantised rows (oracle/quant.py); the oracle is given exactly those values for the tokens the
+    # device flags (asr_ledger_view.dequantized), the appended values for all others
+    KVq, KVo = None, KV
+    if c.mirror_bits == 8:
+        from oracle import quant
+
+        def deq(a):   # [n][L][Hkv][d] bf16 bits -> the same, every row through R-quant INT8
+            rows = a.reshape(-1, c.d)
+            codes, scales = quant.quantize(rows, 8)
+            return quant.dequantize(codes, scales).reshape(a.shape)
+        KVq = [(deq(KV[b][0]), deq(KV[b][1])) for b in range(c.B)]
+        KVo = [(KV[b][0].copy(), KV[b][1].copy()) for b in range(c.B)]
     if c.nccl_world1:
         from paper_2512_11221_b200 import asr_nccl_unique_id
         ctx.attach_nccl(asr_nccl_unique_id(), 1, 0)
@@ -168,7 +183,10 @@ def run(c: Case, check_o: bool = True) -> dict:
             o = o_t.cpu().numpy()
             ent = e_t.cpu().numpy()
         for b in range(c.B):
-            Ob, act, scores, out = orc[b].step(q[b], KV[b][0], KV[b][1], None if lg is None else lg[b])
+            if KVq is not None:   # the tokens the device now holds dequantised
+                fl = np.flatnonzero(stats[b]["dequantized"])
+                KVo[b][0][fl], KVo[b][1][fl] = KVq[b][0][fl], KVq[b][1][fl]
+            Ob, act, scores, out = orc[b].step(q[b], KVo[b][0], KVo[b][1], None if lg is None else lg[b])
             g = stats[b]
             where = f"step {i} seq {b}"
             np.testing.assert_array_equal(g["active_list"], act, err_msg=where)
@@ -213,17 +231,18 @@ def run(c: Case, check_o: bool = True) -> dict:
     for b in range(c.B):
         n = P[b] + c.steps
         led = ctx.stats(b, detail=True)["ledger"]
+        mir = KVq[b] if KVq is not None else KV[b]   # INT8 tier: the mirror holds R-quant rows exactly
         for j in range(n):
             km, vm = ctx.read_kv(b, j, from_mirror=True)
-            np.testing.assert_array_equal(km, KV[b][0][j], err_msg=f"mirror K seq {b} pos {j}")
-            np.testing.assert_array_equal(vm, KV[b][1][j], err_msg=f"mirror V seq {b} pos {j}")
+            np.testing.assert_array_equal(km, mir[0][j], err_msg=f"mirror K seq {b} pos {j}")
+            np.testing.assert_array_equal(vm, mir[1][j], err_msg=f"mirror V seq {b} pos {j}")
             try:
                 kd, vd = ctx.read_kv(b, j)
             except Exception:
                 assert c.pool_tokens and led["residency"][j] == 0, (b, j)   # only frozen tokens may be evicted
                 continue
-            np.testing.assert_array_equal(kd, KV[b][0][j], err_msg=f"device K seq {b} pos {j}")
-            np.testing.assert_array_equal(vd, KV[b][1][j], err_msg=f"device V seq {b} pos {j}")
+            np.testing.assert_array_equal(kd, KVo[b][0][j], err_msg=f"device K seq {b} pos {j}")
+            np.testing.assert_array_equal(vd, KVo[b][1][j], err_msg=f"device V seq {b} pos {j}")
     summary = {"worst_o": worst_o, "worst_h": worst_h, "frozen": frozen_total, "restored": restored_total,
                "recoveries": recoveries,
                "evicted": evicted_total, "prefetched": prefetched_total, "demand": demand_total,

@@ -219,3 +219,16 @@ def test_entropy_given_by_the_sampler(B):
              spike_first=50, spike_period=16, spike_count=3, entropy_given=True)
     s = run(c)
     assert s["recoveries"] >= 3 * B
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_pressure_int8_frozen_tier(policy):
+    # NEXT-4 wired into the host link: the mirror holds R-quant INT8 rows; restored tokens come back
+    # dequantised.  Decisions, lists and scores bitwise, O within the bf16 bar, against the oracle fed
+    # the dequantised rows for exactly the tokens the device holds dequantised; the mirror's bytes equal
+    # oracle/quant.py's codes and scales, the device slots the appended or dequantised rows.
+    c = Case(L=2, Hq=32, Hkv=8, d=128, B=2, prompt=(70, 40), steps=120, window=8, vocab=4096, seed=99,
+             hot_permille=300, a_hot=64, spike_first=60, spike_period=16, spike_count=1, mirror_bits=8,
+             evict_policy=policy, evict_min=1 if policy else 2, pool_tokens=340 if policy else 330, pool_reserve=48)
+    s = run(c)
+    assert s["evicted"] > 0 and s["prefetched"] > 0
