@@ -103,7 +103,15 @@ typedef struct {
                            * (token, layer, K|V, KV head) stored as INT8 codes + one fp32 scale, written
                            * at append, dequantised into the device slot on prefetch / demand restore
                            * (1.94x fewer host-link bytes at d = 128; lossy by R-quant's bound) */
-  int32_t reserved2;
+  int32_t per_layer_ledgers; /* NEXT-3 ("per-token granularity" made per (token, layer)): 0 = one
+                           * ledger per sequence, s_j the mean over all layers' heads (R-layer, default);
+                           * 1 = one ledger per (sequence, layer): layer l freezes token j on its own
+                           * score s_j^(l) = (1/Hq) sum_h |q_l,h . k_l,j,h| and attends its own active
+                           * list.  The context then holds batch * n_layers virtual sequences of one
+                           * layer each: every per-sequence call (asr_stats, asr_restore, asr_read_kv,
+                           * asr_step_policy's score rows) indexes seq = b * n_layers + l; the step's
+                           * q / k_new / v_new / o keep their [batch][n_layers] shapes; logits_prev /
+                           * entropy stay [batch] (ASR_ENTROPY_GIVEN avoids n_layers passes per row). */
 } asr_config;
 typedef enum { ASR_EVICT_BELADY = 0, ASR_EVICT_AT_FREEZE = 1 } asr_evict_policy;
 

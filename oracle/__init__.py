@@ -179,6 +179,7 @@ class OracleSeq:
         c = self.cfg
         assert K.shape[0] >= self.capacity and K.shape[1:] == (c.L, c.Hkv, c.d), K.shape
         q = np.ascontiguousarray(q)
+        K, V = np.ascontiguousarray(K), np.ascontiguousarray(V)   # the C side reads dense rows
         O = np.empty((c.L, c.Hq, c.d), np.float64)
         out = _Out()
         lp = None if logits_prev is None else np.ascontiguousarray(logits_prev)

@@ -46,7 +46,7 @@ class asr_config(ctypes.Structure):
                 ("host_mirror", ctypes.c_int32), ("profile_stages", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("evict_min_absence", ctypes.c_int32), ("pool_reserve", ctypes.c_int32), ("pool_tokens", ctypes.c_int64),
                 ("score_heads", ctypes.c_int32), ("evict_policy", ctypes.c_int32), ("mirror_bits", ctypes.c_int32),
-                ("reserved2", ctypes.c_int32)]
+                ("per_layer_ledgers", ctypes.c_int32)]
 
 
 class asr_step_io(ctypes.Structure):
@@ -173,7 +173,8 @@ class Config:
     score_heads: int = 0             # head-sharded mode: H of Eq. 2 over all shards (0 = n_q_heads)
     evict_policy: int = 0            # pressure mode: EVICT_BELADY (capacity-driven) or EVICT_AT_FREEZE
     mirror_bits: int = 0             # pressure mode: 0 bf16 host mirror, 8 the INT8 frozen tier (R-quant)
-    reserved2: int = 0
+    per_layer_ledgers: int = 0       # NEXT-3: one ledger per (sequence, layer); per-sequence calls take
+                                     # seq = b * n_layers + l
 
     def c(self) -> asr_config:
         v = dataclasses.asdict(self)
@@ -344,7 +345,7 @@ def asr_stats(ctx, seq: int, capacity: int = 0, detail: bool = False) -> dict:
 
 def asr_read_kv(ctx, cfg: Config, seq: int, pos: int, from_mirror: bool = False):
     dt = np.uint16 if cfg.kv_dtype == KV_BF16 else np.float32
-    k = np.zeros((cfg.n_layers, cfg.n_kv_heads, cfg.head_dim), dt)
+    k = np.zeros((1 if cfg.per_layer_ledgers else cfg.n_layers, cfg.n_kv_heads, cfg.head_dim), dt)
     v = np.zeros_like(k)
     _check(lib().asr_read_kv(ctx, seq, pos, int(from_mirror), k.ctypes.data, v.ctypes.data))
     return k, v
@@ -476,6 +477,11 @@ class Context:
     def restore(self, seq: int, level: int, stream=None):
         asr_restore(self._h, seq, level, stream)
 
+    @property
+    def n_seq(self) -> int:
+        """Sequences of the context's per-sequence calls (batch, or batch * n_layers with per-layer ledgers)."""
+        return self.cfg.batch * (self.cfg.n_layers if self.cfg.per_layer_ledgers else 1)
+
     def stats(self, seq: int, detail: bool = False) -> dict:
         return asr_stats(self._h, seq, self.cfg.max_context, detail)
 
@@ -498,7 +504,7 @@ class Context:
         """NEXT-2 policy replay step: scores [B][max_context] fp32 (CUDA tensor) instead of attention."""
         import torch
         c = self.cfg
-        _arg("scores", scores, ["f32"], (c.batch, c.max_context), False, c.device)
+        _arg("scores", scores, ["f32"], (self.n_seq, c.max_context), False, c.device)
         lg = None if logits_prev is None else _arg("logits_prev", logits_prev, ["bf16", "f32"],
                                                    (c.batch, c.vocab), False, c.device)
         if entropy is not None:

@@ -47,6 +47,7 @@ struct asr_ctx {
   size_t tok_bytes = 0;          // one token, all layers, K and V
   std::vector<int32_t> prompt_len;
   bool uniform_prompt = true;
+  int user_batch = 0;            // batch of the caller's logits / entropy rows (batch / n_layers with per-layer ledgers)
   int64_t step = 0;              // host mirror of the device step counter
   void* host_mirror = nullptr;   // pinned [B][max_ctx][L][2][Hkv][d]
   int8_t* host_codes = nullptr;  // INT8 tier (mirror_bits = 8): pinned mapped codes and scales
@@ -202,7 +203,7 @@ void asr_config_defaults(asr_config* c) {
   c->score_heads = 0;
   c->evict_policy = ASR_EVICT_BELADY;
   c->mirror_bits = 0;
-  c->reserved2 = 0;
+  c->per_layer_ledgers = 0;
 }
 
 static asr_status validate(const asr_config* c) {
@@ -245,9 +246,73 @@ static asr_status validate(const asr_config* c) {
   return ASR_OK;
 }
 
+static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const void* prompt_v,
+                              const int32_t* prompt_len, int32_t prompt_stride, int32_t memory, void* cuda_stream,
+                              asr_ctx** out, int ent_div);
+
+// NEXT-3 per-layer ledgers: the context is built over batch * n_layers virtual sequences of one layer
+// each (ledger, lists, pool slots of a token-layer); the prompt is rearranged from [B][stride][L]
+// [Hkv][d] to [B*L][stride][1][Hkv][d] on the device first.  Everything else is the per-sequence
+// engine unchanged; ent_div = L maps a virtual sequence to its logits row / entropy slot.
 asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* prompt_v,
                       const int32_t* prompt_len, int32_t prompt_stride, int32_t memory, void* cuda_stream,
                       asr_ctx** out) {
+  if (!cfg || !cfg->per_layer_ledgers) return create_impl(cfg, prompt_k, prompt_v, prompt_len, prompt_stride, memory,
+                                                          cuda_stream, out, 1);
+  if (!out) return fail(ASR_E_INVALID, "out is NULL");
+  *out = nullptr;
+  if (cfg->per_layer_ledgers != 1) return fail(ASR_E_INVALID, "per_layer_ledgers must be 0 or 1");
+  asr_status v = validate(cfg);
+  if (v) return v;
+  if (!prompt_len) return fail(ASR_E_INVALID, "prompt_len is NULL");
+  const int B = cfg->batch, L = cfg->n_layers;
+  if ((int64_t)B * L > 4096) return fail(ASR_E_INVALID, "per-layer ledgers: batch * n_layers must be <= 4096");
+  asr_config vc = *cfg;
+  vc.batch = B * L;
+  vc.n_layers = 1;
+  vc.per_layer_ledgers = 0;
+  if (vc.pool_tokens > 0) vc.pool_tokens *= L;   // token-layer slots
+  std::vector<int32_t> vlen((size_t)B * L);
+  int32_t pmax = 0;
+  for (int b = 0; b < B; ++b) {
+    if (prompt_len[b] < 0 || prompt_len[b] > prompt_stride)
+      return fail(ASR_E_INVALID, "prompt_len[b] must be in [0, prompt_stride]");
+    for (int l = 0; l < L; ++l) vlen[(size_t)b * L + l] = prompt_len[b];
+    pmax = prompt_len[b] > pmax ? prompt_len[b] : pmax;
+  }
+  if (pmax == 0 || !prompt_k || !prompt_v)
+    return create_impl(&vc, nullptr, nullptr, vlen.data(), 0, ASR_MEM_DEVICE, cuda_stream, out, L);
+  CUDA_TRY(cudaSetDevice(cfg->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const size_t row = (size_t)cfg->n_kv_heads * cfg->head_dim * (cfg->kv_dtype == ASR_KV_BF16 ? 2 : 4);
+  const size_t bytes = (size_t)B * L * pmax * row;
+  void *vk = nullptr, *vv = nullptr;
+  CUDA_TRY(cudaMalloc(&vk, bytes));
+  cudaError_t e = cudaMalloc(&vv, bytes);
+  if (e != cudaSuccess) {
+    cudaFree(vk);
+    return fail(ASR_E_OOM, "per-layer ledgers: prompt staging");
+  }
+  const cudaMemcpyKind kind = memory == ASR_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  for (int b = 0; b < B && e == cudaSuccess; ++b)
+    for (int l = 0; l < L && e == cudaSuccess; ++l) {
+      if (!prompt_len[b]) continue;
+      const size_t src = ((size_t)b * prompt_stride * L + l) * row, dst = ((size_t)b * L + l) * pmax * row;
+      e = cudaMemcpy2DAsync((char*)vk + dst, row, (const char*)prompt_k + src, L * row, row, prompt_len[b], kind, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync((char*)vv + dst, row, (const char*)prompt_v + src, L * row, row, prompt_len[b], kind, st);
+    }
+  asr_status r = e == cudaSuccess ? create_impl(&vc, vk, vv, vlen.data(), pmax, ASR_MEM_DEVICE, cuda_stream, out, L)
+                                  : fail(ASR_E_CUDA, std::string("per-layer prompt copy: ") + cudaGetErrorString(e));
+  cudaStreamSynchronize(st);
+  cudaFree(vk);
+  cudaFree(vv);
+  return r;
+}
+
+static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const void* prompt_v,
+                              const int32_t* prompt_len, int32_t prompt_stride, int32_t memory, void* cuda_stream,
+                              asr_ctx** out, int ent_div) {
   if (!out) return fail(ASR_E_INVALID, "out is NULL");
   *out = nullptr;
   asr_status v = validate(cfg);
@@ -276,6 +341,8 @@ asr_status asr_create(const asr_config* cfg, const void* prompt_k, const void* p
     DevState& s = c->s;
     s.B = cfg->batch;
     s.L = cfg->n_layers;
+    s.ent_div = ent_div;
+    c->user_batch = cfg->batch / ent_div;
     s.Hq = cfg->n_q_heads;
     s.Hkv = cfg->n_kv_heads;
     s.d = cfg->head_dim;
@@ -557,7 +624,7 @@ static asr_status ensure_staging(asr_ctx* c, asr_ctx::Staging& S, bool logits, i
     CUDA_TRY(c->alloc(&S.k, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
     CUDA_TRY(c->alloc(&S.v, (size_t)s.B * s.L * s.Hkv * s.d * c->kv_elem));
     CUDA_TRY(c->alloc(&S.o, (size_t)s.B * s.L * s.Hq * s.d * 4));
-    CUDA_TRY(c->alloc(&S.ent, (size_t)s.B * 4));
+    CUDA_TRY(c->alloc(&S.ent, (size_t)c->user_batch * 4));
     CUDA_TRY(cudaEventCreateWithFlags(&S.in_done, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&S.graph_done, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&S.out_done, cudaEventDisableTiming));
@@ -567,7 +634,8 @@ static asr_status ensure_staging(asr_ctx* c, asr_ctx::Staging& S, bool logits, i
     CUDA_TRY(cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking));
   }
   if (logits) {
-    size_t need = (size_t)s.B * s.vocab * (logits_dtype == ASR_KV_BF16 ? 2 : 4);
+    size_t need = (size_t)c->user_batch * (logits_dtype == ASR_ENTROPY_GIVEN ? 1 : s.vocab) *
+                  (logits_dtype == ASR_KV_BF16 ? 2 : 4);
     if (need > S.logits_bytes) {
       CUDA_TRY(c->alloc(&S.logits, need));
       S.logits_bytes = need;
@@ -624,7 +692,7 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
   a.host_io = io->memory == ASR_MEM_HOST;
   asr_ctx::Staging& S = c->stg[c->step & 1];
   if (a.host_io) {
-    asr_status r = ensure_staging(c, S, a.has_logits || a.ent_given, a.ent_given ? ASR_KV_F32 : io->logits_dtype);
+    asr_status r = ensure_staging(c, S, a.has_logits || a.ent_given, a.ent_given ? ASR_ENTROPY_GIVEN : io->logits_dtype);
     if (r) return r;
     // inputs: copied on io_in as soon as the step is issued (overlapping the previous step's kernels),
     // once the graph that last read this staging set is done
@@ -636,7 +704,8 @@ static asr_status step_prepare(asr_ctx* c, const asr_step_io* io, cudaStream_t s
     CUDA_TRY(cudaMemcpyAsync(S.v, a.vn, kb, cudaMemcpyHostToDevice, c->io_in));
     c->bytes_h2d += (int64_t)(qb + 2 * kb);
     if (a.has_logits || a.ent_given) {
-      const size_t lb = a.ent_given ? (size_t)s.B * 4 : (size_t)s.B * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
+      const size_t lb = a.ent_given ? (size_t)c->user_batch * 4
+                                    : (size_t)c->user_batch * s.vocab * (io->logits_dtype == ASR_KV_BF16 ? 2 : 4);
       CUDA_TRY(cudaMemcpyAsync(S.logits, a.lg, lb, cudaMemcpyHostToDevice, c->io_in));
       c->bytes_h2d += (int64_t)lb;
       a.lg = S.logits;
@@ -869,8 +938,8 @@ static asr_status step_finish(asr_ctx* c, StepArgs& a, cudaStream_t st) {
     CUDA_TRY(cudaMemcpyAsync(a.o_user, a.o, ob, cudaMemcpyDeviceToHost, c->io_out));
     c->bytes_d2h += (int64_t)ob;
     if (a.ent_user && (a.has_logits || a.ent_given)) {
-      CUDA_TRY(cudaMemcpyAsync(a.ent_user, a.ent, (size_t)s.B * 4, cudaMemcpyDeviceToHost, c->io_out));
-      c->bytes_d2h += (int64_t)s.B * 4;
+      CUDA_TRY(cudaMemcpyAsync(a.ent_user, a.ent, (size_t)c->user_batch * 4, cudaMemcpyDeviceToHost, c->io_out));
+      c->bytes_d2h += (int64_t)c->user_batch * 4;
     }
     CUDA_TRY(cudaEventRecord(S.out_done, c->io_out));
     c->last_out = S.out_done;

@@ -107,6 +107,7 @@ struct DevState {
   int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
   const float* ext_score;     // policy replay (NEXT-2): s_j given per position [B][max_ctx]; NULL = Eq. 2
   const float* ent_given;     // [B] H(logits_prev) computed by the caller (asr_sample_entropy); NULL = from logits
+  int ent_div;                // sequences per logits row: 1, or n_layers with per-layer ledgers (NEXT-3)
   unsigned long long* hmask;  // [B][max_ctx][2] finite W: bit t = detection at step hstep - t
   int32_t* hstep;             // [B][max_ctx]    finite W: step of bit 0 (never: a large negative)
   int combine_in_decide;      // 1: the combine runs as extra blocks of the phase-D kernel (small batch)

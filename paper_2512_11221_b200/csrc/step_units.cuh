@@ -204,7 +204,7 @@ __device__ void warp_entropy_split(const DevState& s, const TL* __restrict__ log
   const int V = s.vocab;
   const int seg = (((V + kEntSplits - 1) / kEntSplits) + 7) & ~7;   // multiple of 8 elements
   const int e0 = min(V, split * seg), e1 = min(V, e0 + seg);
-  const TL* row = logits + (long)b * V;
+  const TL* row = logits + (long)(b / s.ent_div) * V;   // per-layer ledgers: the sequence's row
   const bool vecok = (reinterpret_cast<uintptr_t>(row) & 31) == 0;
   const float invT = 1.0f / s.ent_temp;
   float m = -INFINITY, z = 0.f, sx = 0.f;
@@ -549,7 +549,7 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
     if (has_logits) {
       float H;
       if (s.ent_given) {   // the caller's H (asr_sample_entropy took it in its pass over the row)
-        H = __ldcg(s.ent_given + b);
+        H = __ldcg(s.ent_given + b / s.ent_div);
       } else {
         // merge the kEntSplits partials in fp32 (lane k holds splits k and k + 32; fixed-order tree)
         const float* ep = s.ent_part + (long)b * kEntSplits * 3;   // written by other blocks: via L2
@@ -603,7 +603,7 @@ __device__ void unit_finish(const DevState& s, int b, int i, bool has_logits, fl
             ds.has_last = 1;
           }
         }
-        if (entropy_out) entropy_out[b] = H;
+        if (entropy_out && b % s.ent_div == 0) entropy_out[b / s.ent_div] = H;
         s.stats[b].entropy = H;
       }
     }

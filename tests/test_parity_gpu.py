@@ -232,3 +232,64 @@ def test_pressure_int8_frozen_tier(policy):
              evict_policy=policy, evict_min=1 if policy else 2, pool_tokens=340 if policy else 330, pool_reserve=48)
     s = run(c)
     assert s["evicted"] > 0 and s["prefetched"] > 0
+
+
+@pytest.mark.parametrize("shape", [(3, 8, 2, 64), (2, 32, 8, 128)])
+def test_per_layer_ledgers(shape):
+    # NEXT-3: one ledger per (sequence, layer) — layer l freezes on s_j^(l) = (1/Hq) sum_h |q.k| of its
+    # own heads and attends its own list.  Oracle: one single-layer OracleSeq per (b, l) fed that
+    # layer's q / K / V and the sequence's logits; ledgers, lists, scores bitwise, O within 2e-3, every
+    # step, generic (d = 64) and tensor-core (LLaMA layout) attention; planted spikes drive recovery
+    import torch
+    from harness import o_rel_err
+    from paper_2512_11221_b200 import Config, Context
+    import oracle
+    L, Hq, Hkv, d = shape
+    B, P, steps, K, V = 2, (50, 31), 90, 8, 4096
+    p = gen.GenParams(seed=321 + d, L=L, Hq=Hq, Hkv=Hkv, d=d, hot_permille=300, a_hot=64, vocab=V,
+                      spike_first=40, spike_period=16, spike_count=2)
+    cap = max(P) + steps + 1
+    # tau between the LAT cold scores: per-layer scores are multiples of u = 2^-8 / Hq (exact in fp32), so
+    # tau at a half-lattice point decides identically in fp32 and fp64, and cold tokens score above or
+    # below it depending on the layer's q — the layers' ledgers diverge
+    u = 2.0 ** -8 / Hq
+    tau = (np.floor(0.055 / u) + 0.5) * u   # near the median cold per-layer score
+    KV = [gen.kv(p, b, 0, cap) for b in range(B)]
+    pk = np.zeros((B, max(P), L, Hkv, d), np.uint16)
+    pv = np.zeros_like(pk)
+    for b in range(B):
+        pk[b, :P[b]], pv[b, :P[b]] = KV[b][0][:P[b]], KV[b][1][:P[b]]
+    to_t = lambda a: torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).cuda()
+    cfg = Config(n_layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, batch=B, max_context=cap, window=K, vocab=V,
+                 tau=float(tau), per_layer_ledgers=1)
+    ctx = Context(cfg, to_t(pk), to_t(pv), list(P))
+    assert ctx.n_seq == B * L
+    ocfg = oracle.OrcCfg(L=1, Hq=Hq, Hkv=Hkv, d=d, window=K, vocab=V, tau=float(tau))
+    orc = [[oracle.OracleSeq(ocfg, cap, P[b]) for _ in range(L)] for b in range(B)]
+    differ = False
+    for i in range(steps):
+        q = np.stack([gen.q(p, b, i) for b in range(B)])
+        kn = np.stack([KV[b][0][P[b] + i] for b in range(B)])
+        vn = np.stack([KV[b][1][P[b] + i] for b in range(B)])
+        lg = np.stack([gen.logits(p, b, i - 1) for b in range(B)]) if i > 0 else None
+        o = torch.zeros((B, L, Hq, d), dtype=torch.float32, device="cuda")
+        ctx.step(to_t(q), to_t(kn), to_t(vn), o, logits_prev=None if lg is None else to_t(lg))
+        O = o.cpu().numpy()
+        for b in range(B):
+            acts = []
+            for l in range(L):
+                Ob, act, scores, out = orc[b][l].step(q[b][l:l + 1], KV[b][0][:, l:l + 1], KV[b][1][:, l:l + 1],
+                                                       None if lg is None else lg[b])
+                g = ctx.stats(b * L + l, detail=True)
+                where = f"step {i} seq {b} layer {l}"
+                np.testing.assert_array_equal(g["active_list"], act, err_msg=where)
+                assert np.array_equal(g["scores"], scores.astype(np.float32)), where
+                led = orc[b][l].ledger()
+                for key in ("residency", "timer", "count", "freeze_step"):
+                    np.testing.assert_array_equal(g["ledger"][key], led[key], err_msg=f"{where} {key}")
+                assert g["recovery_action"] == out["recovery_action"] and g["device_error"] == 0, where
+                assert o_rel_err(O[b, l:l + 1], Ob) <= 2e-3, where
+                acts.append(tuple(act))
+            differ |= len(set(acts)) > 1
+    assert differ   # the layers' ledgers do diverge (per-layer scores differ)
+    ctx.close()
