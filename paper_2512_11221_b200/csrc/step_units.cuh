@@ -302,7 +302,10 @@ __device__ __forceinline__ uint32_t active_bits4(const uint32_t* res4, int q, in
 }
 
 struct Compactor {
-  static constexpr int kKeep = 8;   // masks of a warp's first kKeep groups stay in registers
+#ifndef ASR_KKEEP
+#define ASR_KKEEP 1   // measured: 8 -> 1 saves ~2 us of the batch-1 phase D (code size), batch 64 unchanged
+#endif
+  static constexpr int kKeep = ASR_KKEEP;   // masks of a warp's first kKeep groups stay in registers
   const uint32_t* res4;
   int lo, hi, g0, g1, lo_al;
   uint32_t keep[kKeep];
@@ -674,15 +677,15 @@ __device__ __forceinline__ int duration(uint32_t c, float k, int kint) {
 // Eq. 2 numerator of attended index a: sum over layers in order l = 0..L-1 of the per-layer head sums
 // (the loads of up to 32 layers are issued before the first add, so their latencies overlap).
 __device__ __forceinline__ float layer_sum(const DevState& s, int b, int a) {
+  // unconditional loads from clamped (always valid) addresses: straight-line code, no branch per load
   const float* sp = s.score_part + (long)b * s.L * s.max_ctx + a;
   float sum = 0.f;
   for (int l0 = 0; l0 < s.L; l0 += 32) {
     float v[32];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = l0 + q < s.L ? __ldcg(sp + (long)(l0 + q) * s.max_ctx) : 0.f;
+    for (int q = 0; q < 32; ++q) v[q] = __ldcg(sp + (long)min(l0 + q, s.L - 1) * s.max_ctx);
 #pragma unroll
-    for (int q = 0; q < 32; ++q)
-      if (l0 + q < s.L) sum += v[q];
+    for (int q = 0; q < 32; ++q) sum += l0 + q < s.L ? v[q] : 0.f;
   }
   return sum;
 }
@@ -843,7 +846,10 @@ __device__ void unit_decide(const DevState& s, int b, int x, int X, int i, UnitS
   const int32_t* timer = s.timer + base;
   // prefetch the tick's ledger entries of this unit's position slice (independent of the freeze
   // loop: tokens of A_i read Active here and are skipped by the tick below)
-  constexpr int kPF = 8;
+#ifndef ASR_KPF
+#define ASR_KPF 4
+#endif
+  constexpr int kPF = ASR_KPF;
   // this block: A-slice [a0, a_end) (x-th of X equal parts) and the positions [pos(a0), pos(a_end))
   // with pos(0) = 0, pos(A) = n — exactly its A-tokens and the frozen tokens between them, so the
   // block alone settles the final residency of its positions (unit_next_list compacts them)

@@ -124,6 +124,7 @@ def _build_asr(force: bool, out_path: str | None = None) -> str:
         common.append("-DASR_TAIL_TRACE")
     if os.environ.get("ASR_CHECKS") == "1":       # diagnostic build: device-side bounds checks (kErrCheck)
         common.append("-DASR_CHECKS")
+    common += os.environ.get("ASR_NVCC_DEFS", "").split()   # A/B experiments (e.g. -DASR_KPF=2)
     for s in cu:
         o = os.path.join(objdir, os.path.basename(s) + ".o")
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -151,6 +152,10 @@ if __name__ == "__main__":
     if "--checks" in sys.argv:   # the bounds-checked diagnostic library, beside the product one
         os.environ["ASR_CHECKS"] = "1"
         print(build_asr(force=True, out=os.path.join(ROOT, "build", "libasr_checks.so")))
+        sys.exit(0)
+    if "--variant" in sys.argv:   # an experiment library: --variant NAME (flags from ASR_NVCC_DEFS)
+        name = sys.argv[sys.argv.index("--variant") + 1]
+        print(build_asr(force=True, out=os.path.join(ROOT, "build", "ab", f"libasr_{name}.so")))
         sys.exit(0)
     build_all(force="--force" in sys.argv, cuda="--no-cuda" not in sys.argv)
     print("built")
