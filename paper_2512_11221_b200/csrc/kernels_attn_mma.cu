@@ -472,7 +472,7 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
       }
     }
     // large batches: phase D is not latency-bound; fused tail: the aux warp prefetched at the start
-    if (s.B <= 8 && !s.fuse_tail) prefetch_ledger(s, p, alen, step, lane);
+    // (the ledger rows phase D reads are prefetched into L2 by the aux warp, off the producer's exit)
     // drain: the last (up to) kStagesRing tiles still owe their score epilogue
     for (int k = 0; k < kStagesRing; ++k) {
       const int gg = g + k;  // waiting for the release of tile gg - kStagesRing
@@ -491,7 +491,10 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
       units::phaseA_block<TL, __nv_bfloat16>(s, blockIdx.x, step, pre_logits, k_new, v_new, entropy_out, u);
       if (s.tl && lane == 0) atomicMax(&s.tl[1], gtimer());
     }
-    if (s.fuse_tail && s.B <= 8) prefetch_ledger(s, step & 1, s.act_len + (step & 1) * s.B, step, lane);
+    // small batches: the ledger rows phase D (or the fused tail) reads, into L2 while the attention
+    // streams (KV loads are evict_first, these stay) — not at the producer's exit, where it delayed
+    // the CTA's end by ~2 us
+    if (s.B <= 8) prefetch_ledger(s, step & 1, s.act_len + (step & 1) * s.B, step, lane);
     if (s.fuse_tail && !(s.tail_exp & 2)) {
       // instruction prefetch: a dry run (loads and arithmetic only, no stores, no waits) of the fused
       // tail's two functions while the attention streams, so their code is on chip when the tail runs
