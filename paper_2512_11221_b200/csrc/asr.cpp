@@ -379,10 +379,11 @@ static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const
     s.max_splits = (int)(want < 1 ? 1 : want > cap ? cap : want);
     if (s.max_splits > 64 && s.dtype == ASR_KV_BF16) s.max_splits = 64;
     {
-      // decide blocks per sequence: ~1K positions each (measured best at 8K); X > 1 only if all B*X blocks are co-resident
+      // decide blocks per sequence: ~256 positions each, at most 32 (round 2: 256 / 512 / 1024 -> 49.8 / 49.9 / 50.5 us
+      // per 8K batch-1 step); X > 1 only if all B*X blocks are co-resident
       // (one per SM), since a block waits for its predecessors' counts to place its part of A_{i+1}
       const char* dbe = getenv("ASR_DECIDE_POSITIONS");   // positions per decide block (tuning)
-      const int per_block = dbe ? atoi(dbe) : 1024;
+      const int per_block = dbe ? atoi(dbe) : 256;
       int db = (s.max_ctx + per_block - 1) / (per_block > 0 ? per_block : 2048);
       db = db < 1 ? 1 : db > 32 ? 32 : db;
       if ((long)s.B * db > c->num_sms) db = 1;
