@@ -602,6 +602,20 @@ static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const
       s.sk_dyn = sd ? atoi(sd) : (s.B >= 16 ? 8 : 0);
       s.sk_chunk = sc ? atoi(sc) : 2;
       if (s.Hkv != 8) s.sk_dyn = 0;   // the dynamic variant is compiled for 8 KV heads only
+      // rate-balanced static split (asr_internal.h, sk_weighted), batch 1 by default (ASR_SK_BALANCE=1:
+      // any static-split batch, 0: off).  Measured (profiles/r2/balance_ab.txt): batch 1 8K 51.1 ->
+      // 49.5 us, 32K 79.3 -> 77.2 us; batch 4 / 8 / 64 the attention alone gains 2-5 % but the step
+      // loses 3-55 us — there the rates move with the cut (the first-to-last CTA spread grew from
+      // 226 to 384 us at batch 64), so the feedback chases its own effect
+      const char* sb = getenv("ASR_SK_BALANCE");
+      const bool bal = sb ? sb[0] == '1' : s.B == 1;
+      s.sk_bal = bal && s.sk_grid > 0 && s.sk_grid < asr::kSkBalMax && s.sk_dyn == 0 && !s.fuse_tail;
+      CUDA_TRY(c->alloc(&s.sk_w, sizeof(float) * 4 * asr::kSkBalMax));
+      CUDA_TRY(cudaMemsetAsync(s.sk_w, 0, sizeof(float) * 4 * asr::kSkBalMax, st));
+      CUDA_TRY(c->alloc(&s.sk_f, sizeof(float) * 4 * asr::kSkBalMax));
+      CUDA_TRY(cudaMemsetAsync(s.sk_f, 0xff, sizeof(float) * 4 * asr::kSkBalMax, st));   // NaN: not computed yet
+      CUDA_TRY(c->alloc(&s.sk_bound, sizeof(int) * asr::kSkBalMax));
+      CUDA_TRY(cudaMemsetAsync(s.sk_bound, 0, sizeof(int) * asr::kSkBalMax, st));
     }
     const char* ke = getenv("ASR_KV_EVICT_FIRST");
     s.kv_evict_first = !(ke && ke[0] == '0');

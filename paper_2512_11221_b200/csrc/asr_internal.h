@@ -103,6 +103,10 @@ struct DevState {
   int sk_grid;                // > 0: stream-K split of the tensor-core attention over sk_grid CTAs (sk_* below)
   int sk_dyn, sk_chunk;       // 1/sk_dyn of the tiles go out as dynamic chunks of sk_chunk tiles (0: none)
   int32_t* sk_ctr;            // [2] next dynamic chunk, CTAs done with chunks (the last one resets both)
+  int sk_bal;                 // 1: rate-balanced static split (sk_weighted below; sk_dyn == 0 only)
+  float* sk_w;                // [4][kSkBalMax] per-CTA streaming rates (EWMA), by step parity, double-buffered
+  float* sk_f;                // [4][kSkBalMax] cut fractions f_0..f_G (NaN: not computed yet), same buffering
+  int* sk_bound;              // [kSkBalMax] this step's static range starts (+ Ts), written by CTA 0
   int pre_in_attn;            // 1: phase A (+B) runs inside the tensor-core attention kernel (batch 1)
   int hist_w;                 // W of Eq. 3's count: 0 = lifetime count, 1..128 = detections in (i-W, i]
   const float* ext_score;     // policy replay (NEXT-2): s_j given per position [B][max_ctx]; NULL = Eq. 2
@@ -291,6 +295,26 @@ __host__ __device__ inline SkPlan sk_plan(long T, int grid, int dyn_div, int chu
 }
 __host__ __device__ inline int sk_unit_of(const SkPlan& p, long t) {
   return t < p.Ts ? sk_cta_of(t, p.Ts, p.G) : p.G + (int)((t - p.Ts) / p.C);
+}
+// Rate-balanced static split (DevState::sk_bal, static split only): SMs stream at different but
+// stable rates (profiles/README.md: per-CTA durations correlate 0.99 between the halves of a run,
+// with a step-parity component), so the static ranges are cut in proportion to each CTA's measured
+// rate: range c = [floor(T f_c), floor(T f_{c+1})), f_c = P_c / P_G, P the prefix sums of the rates
+// normalised by their mean and clamped to [0.5, 2] — with T >= 8G every range holds >= 2 tiles and
+// the slot scheme above is unchanged.  Each CTA measures its rate (tiles per clock) over its first
+// pass and folds it (EWMA 1/2) into the other buffer of its step parity; one warp computes the
+// fractions for step i + 2 from the rates of step i - 2 beside step i's attention (so no launch
+// reads what it writes, and nothing of it sits on the critical path); each CTA then needs f_c and
+// f_{c+1} only, and stores its range start in sk_bound for the combine.  Only the order of the
+// partial sums in the softmax combine depends on the split (O within fp32 rounding; scores and
+// decisions do not).
+constexpr int kSkBalMax = 256;      // grid <= 255 (the + 1 boundary fits)
+constexpr int kSkBalPer = kSkBalMax / 32;
+__host__ __device__ inline bool sk_weighted(int sk_bal, const SkPlan& p) {
+  return sk_bal && p.nchunks == 0 && p.Ts >= 8L * p.G;
+}
+__host__ __device__ inline int sk_wbuf(int step, bool write) {
+  return (step & 1) * 2 + (((step >> 1) & 1) ^ (write ? 1 : 0));
 }
 
 // One kernel launch described as data, so the same description serves a direct launch

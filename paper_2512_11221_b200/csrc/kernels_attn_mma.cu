@@ -54,6 +54,7 @@ struct Geo {
     alignas(128) uint8_t q[2][kQBytes];    // q of the current / next work item
     float sc[kStagesRing][HK][kTM];       // per-warp head sums |S| of each token
     int start[kMaxB + 1];                 // work list: first item of each sequence
+    int range[2];                         // this CTA's static tile range (rate-balanced split)
     int4 unitq[16][2];                    // work units announced by the producer: cursor, stop, unit
     alignas(8) uint64_t full[kStagesRing];
     alignas(8) uint64_t empty[kStagesRing];
@@ -235,6 +236,60 @@ __device__ void attention_prologue(typename Geo<HK>::Smem& sm) {
   }
 }
 
+// Cut fractions of the rate-balanced split (asr_internal.h, sk_weighted) for step + 2 (same
+// parity), from the rates the CTAs measured in step - 2 (complete: that kernel has finished), run by
+// one warp beside the attention (the last CTA's phase-A warp), off the critical path: f_c = P_c / P_G,
+// P the prefix sums of the rates normalised by their mean and clamped to [0.5, 2]; CTA c = 8 lane + i.
+__device__ __noinline__ void sk_fractions(const DevState& s, int step) {
+  const int lane = threadIdx.x & 31;
+  const int Gg = gridDim.x;
+  const float* wr = s.sk_w + sk_wbuf(step, false) * kSkBalMax;
+  float* fw = s.sk_f + sk_wbuf(step, true) * kSkBalMax;
+  float w[kSkBalPer];
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kSkBalPer; ++i) {
+    const int cc = lane * kSkBalPer + i;
+    w[i] = cc < Gg ? __ldcg(wr + cc) : 0.f;
+    tot += w[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (!(tot > 0.f)) return;   // no rates yet: step + 2 keeps the uniform split
+  const float inv_mean = (float)Gg / tot;
+  float run = 0.f;
+#pragma unroll
+  for (int i = 0; i < kSkBalPer; ++i) {
+    const int cc = lane * kSkBalPer + i;
+    const float x = cc < Gg ? fminf(fmaxf(w[i] * inv_mean, 0.5f), 2.f) : 0.f;
+    w[i] = run;   // exclusive prefix within the lane
+    run += x;
+  }
+  float incl = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.f;
+  const float inv_p = 1.f / __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+  for (int i = 0; i < kSkBalPer; ++i) {
+    const int cc = lane * kSkBalPer + i;
+    if (cc <= Gg) __stcg(fw + cc, cc == 0 ? 0.f : cc == Gg ? 1.f : (excl + w[i]) * inv_p);
+  }
+}
+
+// Folds this CTA's streaming rate over its first pass (tiles per clock since c0) into the rate
+// buffer the next step of the same parity reads (sk_weighted).
+__device__ __forceinline__ void sk_rate_update(const DevState& s, int step, const int* range, long long c0) {
+  const int tiles = range[1] - range[0];
+  const long long dc = clock64() - c0;
+  if (tiles <= 0 || dc <= 0) return;
+  const float rate = (float)tiles * 1e6f / (float)dc;   // tiles per 10^6 clocks
+  const float old = __ldcg(s.sk_w + sk_wbuf(step, false) * kSkBalMax + blockIdx.x);
+  s.sk_w[sk_wbuf(step, true) * kSkBalMax + blockIdx.x] = old > 0.f ? 0.5f * (old + rate) : rate;
+}
+
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
 // With do_pre (batch 1, DevState::pre_in_attn) the CTA's extra warp runs its phase-A unit (entropy
 // split or append; the last unit of the sequence also runs phase B) beside the attention warps.
@@ -252,6 +307,15 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
   const int qbytes = s.Hq * kD * 2;         // q of one (b, l)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    // rate-balanced split: this CTA's cut fractions (a step of this parity computed them); loaded
+    // before the list lengths so the two latencies overlap
+    const int c = blockIdx.x, Gg = gridDim.x;
+    float f0 = 0.f, f1 = 0.f;
+    if (!DYN && s.sk_bal) {
+      const float* fr = s.sk_f + sk_wbuf(step, false) * kSkBalMax;
+      f0 = __ldcg(fr + c);
+      f1 = __ldcg(fr + c + 1);
+    }
     int acc = 0;
     for (int b = 0; b < s.B; ++b) {
       sm.start[b] = acc;
@@ -260,6 +324,24 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
     sm.start[s.B] = acc;
     if (blockIdx.x == 0)
       for (int b = 0; b <= s.B; ++b) s.item_start[b] = sm.start[b];
+    if (!DYN && s.sk_bal) {
+      // sk_weighted: T >= 8 G (G = grid); fractions NaN: none computed yet -> uniform cut
+      int r0, r1;
+      if (acc < 8 * Gg) {
+        const int G = min(acc, Gg);
+        r0 = c < G ? c * acc / G : 0;
+        r1 = c < G ? (c + 1) * acc / G : 0;
+      } else if (!(f0 >= 0.f) || !(f1 >= 0.f)) {
+        r0 = (int)((long)c * acc / Gg);
+        r1 = (int)((long)(c + 1) * acc / Gg);
+      } else {
+        r0 = c == 0 ? 0 : (int)((float)acc * f0);
+        r1 = c + 1 == Gg ? acc : (int)((float)acc * f1);
+      }
+      sm.range[0] = r0;
+      sm.range[1] = r1;
+      s.sk_bound[c] = r0;   // the combine's piece lookup (step_units.cuh combine_warp)
+    }
   }
   __syncthreads();
   // units of work (asr_internal.h): this CTA's static stream-K range, then dynamic chunks; the
@@ -269,7 +351,10 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
   // producer is register-bound and the chunk overheads outweigh the balance there: DESIGN.md §6.1)
   const SkPlan plan = sk_plan(sm.start[s.B], gridDim.x, DYN ? s.sk_dyn : 0, s.sk_chunk);   // gridDim.x == s.sk_grid
   int t_begin = 0, t_end = 0;
-  if ((int)blockIdx.x < plan.G) {
+  if (!DYN && s.sk_bal) {
+    t_begin = sm.range[0];
+    t_end = sm.range[1];
+  } else if ((int)blockIdx.x < plan.G) {
     t_begin = (int)((long)blockIdx.x * plan.Ts / plan.G);
     t_end = (int)((long)(blockIdx.x + 1) * plan.Ts / plan.G);
   }
@@ -495,6 +580,7 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
     // streams (KV loads are evict_first, these stay) — not at the producer's exit, where it delayed
     // the CTA's end by ~2 us
     if (s.B <= 8) prefetch_ledger(s, step & 1, s.act_len + (step & 1) * s.B, step, lane);
+    if (!DYN && s.sk_bal && blockIdx.x == gridDim.x - 1) sk_fractions(s, step);
     if (s.fuse_tail && !(s.tail_exp & 2)) {
       // instruction prefetch: a dry run (loads and arithmetic only, no stores, no waits) of the fused
       // tail's two functions while the attention streams, so their code is on chip when the tail runs
@@ -748,14 +834,20 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
   pdl_trigger();
   const bool do_pre = s.pre_in_attn;
   const int step = *s.step;
+  const long long c0 = clock64();
   {
     Stamp stamp(s.tl, 1);
     attention_phase<HK, TL, DYN>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
     if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 7], gtimer());   // first CTA done
   }
+  if (!DYN && s.sk_bal && !do_pre) {
+    __syncthreads();
+    if (threadIdx.x == 0) sk_rate_update(s, step, sm.range, c0);
+  }
   if (do_pre) {
     __syncthreads();
     if (threadIdx.x == 0) {
+      if (!DYN && s.sk_bal) sk_rate_update(s, step, sm.range, c0);
       if (s.tl) atomicMax(&s.tl[kTlTail + 8], gtimer());   // every warp of the CTA is past the attention
       const unsigned long long t0 = gtimer();
       bool ok = true;

@@ -1412,14 +1412,32 @@ __device__ void combine_warp(const DevState& s, int wid, float* __restrict__ o) 
   int nch;
   long it0;
   // (read through L2: in the fused tail these were written by other CTAs of the same kernel)
+  int bnd[kSkBalPer] = {};   // range starts of a rate-balanced split (loaded beside item_start; phase D
+                             // runs after the attention kernel, so the non-coherent path is safe)
+  if (s.sk_bal) {
+#pragma unroll
+    for (int i = 0; i < kSkBalPer; ++i) bnd[i] = i * 32 + lane < s.sk_grid ? __ldg(s.sk_bound + i * 32 + lane) : 0x7fffffff;
+  }
   const int is_b = __ldcg(s.item_start + b), is_b1 = __ldcg(s.item_start + b + 1);
   const int per_seq = (is_b1 - is_b) / s.L;   // tiles (or chunks) per layer
   if (s.sk_grid) {   // stream-K pieces (asr_internal.h)
     const int tiles = per_seq;
     const long T = __ldcg(s.item_start + s.B), S = is_b + (long)l * tiles;
     const SkPlan pl = sk_plan(T, s.sk_grid, s.sk_dyn, s.sk_chunk);
-    const int cf = tiles ? sk_unit_of(pl, S) : 0;
-    nch = tiles ? sk_unit_of(pl, S + tiles - 1) - cf + 1 : 0;
+    int cf, cl;
+    if (sk_weighted(s.sk_bal, pl)) {   // unit of t: the number of range starts <= t, minus one
+      cf = cl = -1;
+#pragma unroll
+      for (int i = 0; i < kSkBalPer; ++i) {
+        cf += __popc(__ballot_sync(0xffffffffu, bnd[i] <= S));
+        cl += __popc(__ballot_sync(0xffffffffu, bnd[i] <= S + tiles - 1));
+      }
+    } else {
+      cf = tiles ? sk_unit_of(pl, S) : 0;
+      cl = tiles ? sk_unit_of(pl, S + tiles - 1) : -1;
+    }
+    if (!tiles) cf = cl + 1;
+    nch = cl - cf + 1;
     it0 = (long)b * s.L + l + cf;
     if (nch == 1) return;   // one CTA held the whole item and wrote O itself
   } else {

@@ -146,6 +146,7 @@ def run(c: Case, check_o: bool = True) -> dict:
     worst_o, worst_h, frozen_total, restored_total = 0.0, 0.0, 0, 0
     evicted_total = prefetched_total = demand_total = 0
     recoveries = 0
+    tiles = []
     for i in range(c.steps):
         if i in c.time_attention_at:
             ctx.time_attention(2)
@@ -179,6 +180,7 @@ def run(c: Case, check_o: bool = True) -> dict:
             ctx.step(to_t(q), to_t(kn), to_t(vn), o_t, logits_prev=None if lg is None else to_t(lg),
                      entropy=e_t)
         stats = [ctx.stats(b, detail=True) for b in range(c.B)]
+        tiles.append(sum(c.L * ((g["attended"] + 15) // 16) for g in stats))   # the attention's work items
         if not c.host_io:
             o = o_t.cpu().numpy()
             ent = e_t.cpu().numpy()
@@ -244,7 +246,7 @@ def run(c: Case, check_o: bool = True) -> dict:
             np.testing.assert_array_equal(kd, KVo[b][0][j], err_msg=f"device K seq {b} pos {j}")
             np.testing.assert_array_equal(vd, KVo[b][1][j], err_msg=f"device V seq {b} pos {j}")
     summary = {"worst_o": worst_o, "worst_h": worst_h, "frozen": frozen_total, "restored": restored_total,
-               "recoveries": recoveries,
+               "recoveries": recoveries, "tiles": tiles,
                "evicted": evicted_total, "prefetched": prefetched_total, "demand": demand_total,
                "final": [ctx.stats(b) for b in range(c.B)]}
     ctx.close()

@@ -173,6 +173,23 @@ def test_fr_clear_counts(B):
 
 
 @pytest.fixture
+def sk_balance(monkeypatch):
+    monkeypatch.setenv("ASR_SK_BALANCE", "1")   # read at asr_create (default: batch 1 only)
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_rate_balanced_split(sk_balance, B):
+    # the rate-balanced cut of the attention's static split (asr_internal.h, sk_weighted) engages at
+    # T >= 8 x grid tiles once step i - 4's rates exist: 32 layers over ~1000 attended tokens, 14
+    # steps; ledgers bitwise, O within the bf16 bar at every step (only the combine's order moves)
+    import torch
+    s = run(Case(L=32, Hq=32, Hkv=8, d=128, B=B, prompt=(2000, 1900)[:B], steps=14, window=16, hot_permille=500,
+                 a_hot=64, vocab=4096, seed=720 + B))
+    grid = torch.cuda.get_device_properties(0).multi_processor_count   # the attention's persistent grid
+    assert min(s["tiles"][4:]) >= 8 * grid, s["tiles"]
+
+
+@pytest.fixture
 def fused_tail(monkeypatch):
     monkeypatch.setenv("ASR_FUSE_TAIL", "1")   # read at asr_create
 
