@@ -628,7 +628,9 @@ POINTS = {   # extra workloads measured after the headline
 
 def sample_point(local_rank: int) -> dict:
     """NEXT-1: the next-token draw (asr_sample) at the LLaMA-3 vocabulary, batch 1 and 64, timed with
-    CUDA events over 20 calls (logits resident in HBM; algorithmic bytes = one read of each row)."""
+    CUDA events over 20 calls (logits resident in HBM; algorithmic bytes = one read of each row):
+    us_per_call back to back from Python (the host launch path included), us_per_call_device the same
+    calls replayed from a CUDA graph (rows_per_s and GB/s from the device time)."""
     import torch
 
     import gen
@@ -660,8 +662,24 @@ def sample_point(local_rank: int) -> dict:
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1000 / 20
-                res[name + ("+entropy" if fused else "")] = {"us_per_call": round(us, 2), "rows_per_s": round(B / us * 1e6),
-                                                            "gbs_one_read": round(B * VOCAB * 2 / us / 1e3, 1)}
+                # device time: the same 20 calls replayed from a CUDA graph (no Python launch path)
+                s = torch.cuda.Stream(device=dev)
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(gr, stream=s):
+                        for _ in range(20):
+                            call()
+                torch.cuda.synchronize()
+                gr.replay()
+                torch.cuda.synchronize()
+                e0.record()
+                gr.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                ud = e0.elapsed_time(e1) * 1000 / 20
+                res[name + ("+entropy" if fused else "")] = {"us_per_call": round(us, 2), "us_per_call_device": round(ud, 2),
+                                                            "rows_per_s": round(B / ud * 1e6),
+                                                            "gbs_one_read": round(B * VOCAB * 2 / ud / 1e3, 1)}
         out[f"batch{B}"] = res
     return out
 

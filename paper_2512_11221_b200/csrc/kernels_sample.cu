@@ -21,10 +21,18 @@
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "asr_internal.h"
 
 namespace cg = cooperative_groups;
+
+// -DASR_SAMPLE_PROF (diagnostic builds only): rank 0 / thread 0 of row 0 prints the phase times
+#ifdef ASR_SAMPLE_PROF
+#define SPROF(k) do { if (tid == 0 && rank == 0 && row == 0) { unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); sp_t[k] = t_; } } while (0)
+#else
+#define SPROF(k) do { } while (0)
+#endif
 
 namespace asr {
 namespace {
@@ -34,6 +42,8 @@ constexpr int kSW = kST / 32;        // warps per CTA
 constexpr int kWays = 8;             // split points per search pass: kWays - 1
 constexpr float kFix = 68719476736.0f;   // 2^36
 constexpr int kCand = 1024;          // top-k candidates kept per CTA in shared memory (value + index)
+constexpr int kFastK = 256;          // top-k fast path: k <= kFastK, at most kSlot(CS) candidates per CTA
+constexpr int kCS16Slots = 2048;     // candidate slots of the fast path at rank 0 (kSlot = kCS16Slots / CS)
 
 __device__ __forceinline__ float lg(const __nv_bfloat16* p, int j) { return __bfloat162float(p[j]); }
 __device__ __forceinline__ float lg(const float* p, int j) { return p[j]; }
@@ -56,7 +66,30 @@ struct SampleShm {
   float fout;
   int iout;
   float zout, sout;   // this CTA's entropy partials (Z, S) about the row max, read by the cluster's rank 0
+  // top-k fast path
+  uint32_t tkout;                    // this CTA's bound T_c, read by the cluster
+  int cnt[16];                       // candidates of every CTA of the cluster (each CTA writes its own into all)
+  unsigned long long ck[kCS16Slots]; // rank 0: candidate keys (key << 32 | ~index), kSlot slots per CTA
+  unsigned long long cd[kCand];      // rank 0: the candidates, dense, in index order
+  unsigned long long kk2[kFastK];    // rank 0: the top-k keys, in index order
+  unsigned long long kw[kFastK];     // rank 0: their masses
+  unsigned long long wsum[kSW];      // per-warp partials
+  unsigned long long bkey;           // rank 0: the top-p boundary key
+  int tok;                           // rank 0: the drawn index
 };
+
+// Largest t with #{threads whose key >= t} >= k (k >= 1) over one key per thread of the CTA, built
+// bit by bit from the top over the bits in `vary` (bits outside it are those of `fixed`): one
+// __syncthreads_count per bit; every thread calls it.
+__device__ __forceinline__ uint32_t block_kth_u32(uint32_t key, bool valid, int k, uint32_t vary, uint32_t fixed) {
+  uint32_t t = fixed & ~vary;
+  for (int bit = 31; bit >= 0; --bit) {
+    if (!((vary >> bit) & 1u)) continue;
+    const uint32_t c = t | (1u << bit);
+    if (__syncthreads_count(valid && key >= c) >= k) t = c;
+  }
+  return t;
+}
 
 // Visit elements j = first, first + stride, ... < end: kU loads are issued before any is used (the
 // loops are latency-bound otherwise: one L2 round trip per element), then f(value, j) runs on each.
@@ -206,7 +239,7 @@ __device__ void cluster_sum(cg::cluster_group& cl, SampleShm& sh, const unsigned
 // (Z = sum e^{(x-m)/T}, S = sum e^{(x-m)/T} (x-m)/T about the row max m; R-ent) for the step's recovery
 // detector (asr_step with ASR_ENTROPY_GIVEN): fp32 per thread, CTA partials summed in warp / rank order.
 template <typename TL, int CS>
-__global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logits, int V, float temperature, int top_k,
+__global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ logits, int V, float temperature, int top_k,
                                                      float top_p, const float* __restrict__ uniforms,
                                                      int32_t* __restrict__ token_out, int cache, float ent_temp,
                                                      float* __restrict__ entropy_out) {
@@ -219,6 +252,10 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int S = ((V + CS - 1) / CS + 31) & ~31;   // slice of this CTA: [s0, s1)
   int par = 0;                                     // cluster_sum slot parity
+#ifdef ASR_SAMPLE_PROF
+  unsigned long long sp_t[12] = {};
+#endif
+  SPROF(0);
   const int s0 = min(V, rank * S), s1 = min(V, s0 + S);
   const bool galigned = (reinterpret_cast<uintptr_t>(xg) & 15) == 0;   // s0 is a multiple of 32
   // the slice is read by every pass: with `cache`, once from global into shared memory
@@ -238,6 +275,7 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
     x = c - s0;   // x[j] for j in [s0, s1) now reads shared memory
   }
   const bool aligned = cache || galigned;
+  SPROF(1);
 
   // ---- max and its first index (greedy)
   float mx = -INFINITY;
@@ -245,6 +283,10 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
   visit8(x, s0, s1, aligned, [&](float v, int j) {
     if (v > mx) { mx = v; mi = j; }
   });
+  // top-k fast path (k <= kFastK): T_c = the CTA's k-th largest thread maximum — k of its elements are
+  // >= T_c, so the row's k-th largest value g_k >= T* = max_c T_c and every top-k element is >= T*
+  const bool fast = temperature > 0.f && top_k > 1 && top_k <= kFastK && top_k < V;
+  const uint32_t tkey = mx == -INFINITY ? 0u : fkey(mx);
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
     const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
@@ -252,6 +294,13 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
   }
   if (lane == 0) { sh.wq[w][0] = __float_as_uint(mx); sh.wq[w][1] = (unsigned)mi; }
   __syncthreads();
+  SPROF(2);
+  if (fast) {
+    // T_c: the k-th largest thread-maximum key (bf16 keys: the low 16 bits are zero)
+    const uint32_t tc = block_kth_u32(tkey, true, top_k, sizeof(TL) == 2 ? 0xffff0000u : 0xffffffffu, 0u);
+    if (tid == 0) sh.tkout = tc;
+  }
+  SPROF(3);
   if (tid == 0) {
     for (int q = 0; q < kSW; ++q) {
       const float om = __uint_as_float((uint32_t)sh.wq[q][0]);
@@ -262,13 +311,34 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
     sh.iout = mi;
   }
   cl.sync();
-  for (int r = 0; r < CS; ++r) {
-    const SampleShm* o = cl.map_shared_rank(&sh, r);
-    const float om = o->fout;
-    const int oi = o->iout;
-    if (om > mx || (om == mx && oi < mi)) { mx = om; mi = oi; }
+  // lane r of warp 0 reads CTA r's values (one DSMEM round trip), reduced by shuffles, then broadcast
+  if (w == 0) {
+    float om = -INFINITY;
+    int oi = 0x7fffffff;
+    uint32_t ot = 0;
+    if (lane < CS) {
+      const SampleShm* o = cl.map_shared_rank(&sh, lane);
+      om = o->fout;
+      oi = o->iout;
+      ot = o->tkout;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const float pm = __shfl_xor_sync(0xffffffffu, om, off);
+      const int pi = __shfl_xor_sync(0xffffffffu, oi, off);
+      const uint32_t pt = __shfl_xor_sync(0xffffffffu, ot, off);
+      if (pm > om || (pm == om && pi < oi)) { om = pm; oi = pi; }
+      ot = max(ot, pt);
+    }
+    if (lane == 0) { sh.wq[0][8] = __float_as_uint(om); sh.wq[0][9] = (unsigned)oi; sh.wq[0][10] = ot; }
   }
-  cl.sync();
+  __syncthreads();
+  mx = __uint_as_float((uint32_t)sh.wq[0][8]);
+  mi = (int)sh.wq[0][9];
+  const uint32_t tstar = fast ? (uint32_t)sh.wq[0][10] : 0u;
+  __syncthreads();   // sh.wq is reused below
+  // (no second barrier: fout / tkout are never rewritten, and every path syncs the cluster again
+  // before a CTA leaves)
+  SPROF(4);
   const float m = mx;
   if (entropy_out) {   // the entropy of the row, from the same (cached) slice
     const float invTe = 1.0f / ent_temp;
@@ -302,7 +372,7 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
     __syncthreads();   // sh.wq is reused by the passes below
   }
   if (!(temperature > 0.f) || top_k == 1 || V == 1) {
-    if (entropy_out) cl.sync();   // rank 0 reads every CTA's partials before any CTA leaves
+    cl.sync();   // no CTA leaves while another reads its max (or, with entropy_out, its partials)
     if (rank == 0 && tid == 0) token_out[row] = mi;
     return;
   }
@@ -471,6 +541,182 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
     }
   };
 
+  float* cv = reinterpret_cast<float*>(slice_smem + (cache ? (S * (int)sizeof(TL) + 15) / 16 * 16 : 0));
+  int* ci = reinterpret_cast<int*>(cv + kCand);
+  if (fast) {
+    // ---- top-k fast path: every CTA sends its elements >= T* (in index order) to kSlot slots of its
+    //      own at rank 0 and its count to every CTA; after one cluster barrier all know whether every
+    //      count fit (else all take the general path below); rank 0 then finishes alone
+    const int kSlot = kCS16Slots / CS;
+    const int per = ((s1 - s0 + kSW - 1) / kSW + 31) & ~31;
+    const int c0 = s0 + min(s1 - s0, w * per), c1 = min(s1, c0 + per);
+    const int cend = c0 + ((c1 - c0 + 31) & ~31);   // whole groups of 32: every lane reaches the ballots
+    unsigned cnt = 0;
+    for (int j = c0 + lane; j < cend; j += 32) {
+      const bool in = j < c1 && fkey(lg(x, j < c1 ? j : c0)) >= tstar;
+      cnt += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    if (lane == 0) sh.wq[w][2] = cnt;
+    __syncthreads();
+    unsigned wbase = 0, ccount = 0;
+    for (int q = 0; q < kSW; ++q) {
+      if (q < w) wbase += (unsigned)sh.wq[q][2];
+      ccount += (unsigned)sh.wq[q][2];
+    }
+    if (tid < CS) cl.map_shared_rank(sh.cnt, tid)[rank] = (int)ccount;
+    if (ccount <= (unsigned)kSlot) {
+      unsigned long long* gk = cl.map_shared_rank(sh.ck, 0) + rank * kSlot;
+      unsigned p0 = wbase;
+      for (int j = c0 + lane; j < cend; j += 32) {
+        const uint32_t kk = j < c1 ? fkey(lg(x, j < c1 ? j : c0)) : 0u;
+        const bool in = j < c1 && kk >= tstar;
+        const unsigned msk = __ballot_sync(0xffffffffu, in);
+        if (in) gk[p0 + __popc(msk & ((1u << lane) - 1u))] = ((unsigned long long)kk << 32) | (0xffffffffu - (uint32_t)j);
+        p0 += __popc(msk);
+      }
+    }
+    cl.sync();   // counts and candidates have landed; no CTA reads another's memory after this
+    SPROF(5);
+    bool fit = true;
+    int ntot = 0;
+    for (int r = 0; r < CS; ++r) {
+      fit = fit && sh.cnt[r] <= kSlot;
+      ntot += sh.cnt[r];
+    }
+    fit = fit && ntot <= kCand;
+    if (fit) {
+      if (rank != 0) return;
+      // rank 0: the candidates, dense and in index order (slot r holds CTA r's, CTAs in index order)
+      for (int i = tid; i < CS * kSlot; i += kST) {
+        const int r = i / kSlot, e = i - r * kSlot;
+        if (e < sh.cnt[r]) {
+          int off = 0;
+          for (int q = 0; q < r; ++q) off += sh.cnt[q];
+          sh.cd[off + e] = sh.ck[i];
+        }
+      }
+      __syncthreads();
+      // the k-th largest key (key desc, index asc: composite keys are unique); two candidates per thread
+      const unsigned long long a0 = tid < ntot ? sh.cd[tid] : 0ull;
+      const unsigned long long a1 = tid + kST < ntot ? sh.cd[tid + kST] : 0ull;
+      // the k-th largest value key kv over the candidates, bit by bit over the bits that vary (OR / AND
+      // over the block; the others are fixed); then the top-k = keys above kv plus the first `need`
+      // candidates at kv in index order (array order)
+      const int K = top_k;
+      const bool v0 = tid < ntot, v1 = tid + kST < ntot;
+      const uint32_t k0 = (uint32_t)(a0 >> 32), k1 = (uint32_t)(a1 >> 32);
+      uint32_t vo = (v0 ? k0 : 0u) | (v1 ? k1 : 0u);
+      uint32_t va = (v0 ? k0 : ~0u) & (v1 ? k1 : ~0u);
+      for (int o = 16; o > 0; o >>= 1) {
+        vo |= __shfl_xor_sync(0xffffffffu, vo, o);
+        va &= __shfl_xor_sync(0xffffffffu, va, o);
+      }
+      if (lane == 0) { sh.wq[w][3] = vo; sh.wq[w][4] = va; }
+      __syncthreads();
+      vo = 0u;
+      va = ~0u;
+      for (int q = 0; q < kSW; ++q) { vo |= (uint32_t)sh.wq[q][3]; va &= (uint32_t)sh.wq[q][4]; }
+      const uint32_t vary = vo ^ va;
+      uint32_t kv = va & ~vary;
+      for (int bit = 31; bit >= 0; --bit) {
+        if (!((vary >> bit) & 1u)) continue;
+        const uint32_t c = kv | (1u << bit);
+        int n = __syncthreads_count(v0 && k0 >= c);
+        if (ntot > kST) n += __syncthreads_count(v1 && k1 >= c);   // (CTA-uniform)
+        if (n >= K) kv = c;
+      }
+      SPROF(6);
+      // ties at kv: their rank in index order (halves: every first-half candidate precedes the second)
+      const bool t0 = v0 && k0 == kv, t1 = v1 && k1 == kv;
+      const bool g0 = v0 && k0 > kv, g1 = v1 && k1 > kv;
+      const unsigned lt = (1u << lane) - 1u;
+      {
+        const unsigned mt0 = __ballot_sync(0xffffffffu, t0), mt1 = __ballot_sync(0xffffffffu, t1);
+        const unsigned mg0 = __ballot_sync(0xffffffffu, g0), mg1 = __ballot_sync(0xffffffffu, g1);
+        if (lane == 0) {
+          sh.wq[w][5] = __popc(mt0);
+          sh.wq[w][6] = __popc(mt1);
+          sh.wq[w][7] = __popc(mg0) + __popc(mg1);
+        }
+        __syncthreads();
+        int tb0 = 0, tb1 = 0, ng = 0;
+        for (int q = 0; q < kSW; ++q) {
+          if (q < w) { tb0 += (int)sh.wq[q][5]; tb1 += (int)sh.wq[q][6]; }
+          tb1 += (int)sh.wq[q][5];
+          ng += (int)sh.wq[q][7];
+        }
+        const int need = K - ng;   // >= 1
+        const bool i0 = g0 || (t0 && tb0 + __popc(mt0 & lt) < need);
+        const bool i1 = g1 || (t1 && tb1 + __popc(mt1 & lt) < need);
+        __syncthreads();   // wq[.][5..7] reused
+        // the top-k into kk2, in index order
+        const unsigned m0 = __ballot_sync(0xffffffffu, i0), m1 = __ballot_sync(0xffffffffu, i1);
+        if (lane == 0) { sh.wq[w][5] = __popc(m0); sh.wq[w][6] = __popc(m1); }
+        __syncthreads();
+        int b0 = 0, b1 = 0;
+        for (int q = 0; q < kSW; ++q) {
+          if (q < w) { b0 += (int)sh.wq[q][5]; b1 += (int)sh.wq[q][6]; }
+          b1 += (int)sh.wq[q][5];
+        }
+        if (i0) sh.kk2[b0 + __popc(m0 & lt)] = a0;
+        if (i1) sh.kk2[b1 + __popc(m1 & lt)] = a1;
+      }
+      __syncthreads();
+      SPROF(7);
+      // per kept element e (one per thread): mass, and the mass ranked above it (key desc, index asc) —
+      // exact fixed-point sums
+      unsigned long long we = 0, above = 0;
+      const unsigned long long ke = tid < K ? sh.kk2[tid] : 0ull;
+      if (tid < K) {
+        we = wfix(unkey((uint32_t)(ke >> 32)), m, invT);
+        sh.kw[tid] = we;
+      }
+      __syncthreads();
+      if (tid < K)
+        for (int q = 0; q < K; ++q)
+          if (sh.kk2[q] > ke) above += sh.kw[q];
+      unsigned long long ws = warp_sum(we);
+      if (lane == 0) sh.wsum[w] = ws;
+      __syncthreads();
+      unsigned long long kmass = 0;
+      for (int q = 0; q < kSW; ++q) kmass += sh.wsum[q];
+      // top-p: keep the elements ranked at or above the first whose running mass reaches
+      // ceil(P * kept mass) (the general path's boundary: ties carry equal masses, ordered by index)
+      unsigned long long cut = 0ull;   // keep keys >= cut
+      if (use_p) {
+        const unsigned long long target = (unsigned long long)ceil((double)top_p * (double)kmass);
+        if (tid < K && above < target && above + we >= target) sh.bkey = ke;   // exactly one (masses > 0)
+        __syncthreads();
+        cut = sh.bkey;
+      }
+      // the kept mass and, in index order, the draw: the smallest kept index whose running mass exceeds
+      // u * kept mass (zero masses are never drawn)
+      const bool kept = tid < K && ke >= cut;
+      unsigned long long kw = kept ? we : 0ull;
+      unsigned long long upk = 0;
+      if (kept)
+        for (int q = 0; q <= tid; ++q)
+          if (sh.kk2[q] >= cut) upk += sh.kw[q];
+      ws = warp_sum(kw);
+      if (lane == 0) sh.wq[w][7] = ws;
+      if (tid == 0) sh.tok = 0x7fffffff;
+      __syncthreads();
+      unsigned long long total = 0;
+      for (int q = 0; q < kSW; ++q) total += sh.wq[q][7];
+      const unsigned long long target = (unsigned long long)((double)uniforms[row] * (double)total);
+      if (kept && we > 0 && upk > target) atomicMin(&sh.tok, (int)(0xffffffffu - (uint32_t)(ke & 0xffffffffull)));
+      __syncthreads();
+      if (tid == 0) token_out[row] = sh.tok;
+      SPROF(8);
+#ifdef ASR_SAMPLE_PROF
+      if (tid == 0 && row == 0)
+        printf("sprof ntot %d | load %llu max %llu bound %llu xchg %llu gather %llu search %llu topk %llu finish %llu ns\n",
+               ntot, sp_t[1] - sp_t[0], sp_t[2] - sp_t[1], sp_t[3] - sp_t[2], sp_t[4] - sp_t[3], sp_t[5] - sp_t[4],
+               sp_t[6] - sp_t[5], sp_t[7] - sp_t[6], sp_t[8] - sp_t[7]);
+#endif
+      return;
+    }
+  }
   const SliceSrc<TL> slice{x, s0, s1 - s0, aligned};
   if (!use_k) {
     unsigned long long v = 0, tot;
@@ -498,8 +744,6 @@ __global__ void __launch_bounds__(kST) sample_kernel(const TL* __restrict__ logi
       if (q < w) base += sh.wq[q][2];
       ncand += sh.wq[q][2];
     }
-    float* cv = reinterpret_cast<float*>(slice_smem + (cache ? (S * (int)sizeof(TL) + 15) / 16 * 16 : 0));
-    int* ci = reinterpret_cast<int*>(cv + kCand);
     const bool compact = ncand <= (unsigned long long)kCand;   // CTA-uniform
     if (compact) {
       for (int j = c0 + lane; j < cend; j += 32) {
