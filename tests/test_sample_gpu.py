@@ -52,6 +52,9 @@ def test_sample_matches_oracle(kind, V, dtype):
     rng = np.random.default_rng(V)
     settings = [(0.0, 0, 1.0), (1.0, 1, 1.0), (1.0, 0, 1.0), (0.7, 50, 1.0), (1.0, 0, None), (0.8, 100, None),
                 (1.3, 7, None),
+                # k = 256, the top-k fast path's limit (on the 3000-value tie rows every element passes
+                # the thread-maxima bound: more candidates than rank 0 holds -> the general path)
+                (0.9, 256, None),
                 # large k: the kept candidates overflow a CTA's shared-memory list (kCand) on some or all
                 # CTAs, which then keep reading their slice
                 (0.9, 2000, 1.0), (1.0, 20000, None)]
