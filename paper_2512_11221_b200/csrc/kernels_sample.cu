@@ -44,6 +44,7 @@ constexpr float kFix = 68719476736.0f;   // 2^36
 constexpr int kCand = 1024;          // top-k candidates kept per CTA in shared memory (value + index)
 constexpr int kFastK = 256;          // top-k fast path: k <= kFastK, at most kSlot(CS) candidates per CTA
 constexpr int kCS16Slots = 2048;     // candidate slots of the fast path at rank 0 (kSlot = kCS16Slots / CS)
+constexpr int kFastPB = 64;          // pure top-p fast path: candidates >= the 64-th largest thread maximum
 
 __device__ __forceinline__ float lg(const __nv_bfloat16* p, int j) { return __bfloat162float(p[j]); }
 __device__ __forceinline__ float lg(const float* p, int j) { return p[j]; }
@@ -69,6 +70,7 @@ struct SampleShm {
   // top-k fast path
   uint32_t tkout;                    // this CTA's bound T_c, read by the cluster
   int cnt[16];                       // candidates of every CTA of the cluster (each CTA writes its own into all)
+  unsigned long long cms[16], sms[16];   // pure top-p: every CTA's candidate mass and slice mass
   unsigned long long ck[kCS16Slots]; // rank 0: candidate keys (key << 32 | ~index), kSlot slots per CTA
   unsigned long long cd[kCand];      // rank 0: the candidates, dense, in index order
   unsigned long long kk2[kFastK];    // rank 0: the top-k keys, in index order
@@ -285,7 +287,12 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
   });
   // top-k fast path (k <= kFastK): T_c = the CTA's k-th largest thread maximum — k of its elements are
   // >= T_c, so the row's k-th largest value g_k >= T* = max_c T_c and every top-k element is >= T*
-  const bool fast = temperature > 0.f && top_k > 1 && top_k <= kFastK && top_k < V;
+  // (pure top-p — no top-k — takes the same path with the bound of the kFastPB largest thread maxima
+  // when the candidates hold the nucleus: their mass reaches P of the row's, checked by every CTA)
+  const bool fastk = temperature > 0.f && top_k > 1 && top_k <= kFastK && top_k < V;
+  const bool fastp = temperature > 0.f && !(top_k > 0 && top_k < V) && top_k != 1 && top_p > 0.f && top_p < 1.f && V > 1;
+  const bool fast = fastk || fastp;
+  const int kb = fastk ? top_k : min(kFastPB, V);
   const uint32_t tkey = mx == -INFINITY ? 0u : fkey(mx);
   for (int o = 16; o > 0; o >>= 1) {
     const float om = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
   SPROF(2);
   if (fast) {
     // T_c: the k-th largest thread-maximum key (bf16 keys: the low 16 bits are zero)
-    const uint32_t tc = block_kth_u32(tkey, true, top_k, sizeof(TL) == 2 ? 0xffff0000u : 0xffffffffu, 0u);
+    const uint32_t tc = block_kth_u32(tkey, true, kb, sizeof(TL) == 2 ? 0xffff0000u : 0xffffffffu, 0u);
     if (tid == 0) sh.tkout = tc;
   }
   SPROF(3);
@@ -552,9 +559,26 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
     const int c0 = s0 + min(s1 - s0, w * per), c1 = min(s1, c0 + per);
     const int cend = c0 + ((c1 - c0 + 31) & ~31);   // whole groups of 32: every lane reaches the ballots
     unsigned cnt = 0;
-    for (int j = c0 + lane; j < cend; j += 32) {
-      const bool in = j < c1 && fkey(lg(x, j < c1 ? j : c0)) >= tstar;
-      cnt += __popc(__ballot_sync(0xffffffffu, in));
+    unsigned long long cms = 0, sms = 0;   // pure top-p: masses of the candidates / of the whole slice
+    if (fastp) {
+      for (int j = c0 + lane; j < cend; j += 32) {
+        const float v = lg(x, j < c1 ? j : c0);
+        const bool in = j < c1 && fkey(v) >= tstar;
+        cnt += __popc(__ballot_sync(0xffffffffu, in));
+        const unsigned long long wv = j < c1 ? wfix(v, m, invT) : 0ull;
+        sms += wv;
+        if (in) cms += wv;
+      }
+    } else {
+      for (int j = c0 + lane; j < cend; j += 32) {
+        const bool in = j < c1 && fkey(lg(x, j < c1 ? j : c0)) >= tstar;
+        cnt += __popc(__ballot_sync(0xffffffffu, in));
+      }
+    }
+    if (fastp) {
+      cms = warp_sum(cms);
+      sms = warp_sum(sms);
+      if (lane == 0) { sh.wq[w][11] = cms; sh.wq[w][12] = sms; }
     }
     if (lane == 0) sh.wq[w][2] = cnt;
     __syncthreads();
@@ -563,7 +587,16 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
       if (q < w) wbase += (unsigned)sh.wq[q][2];
       ccount += (unsigned)sh.wq[q][2];
     }
-    if (tid < CS) cl.map_shared_rank(sh.cnt, tid)[rank] = (int)ccount;
+    if (tid < CS) {
+      SampleShm* o = cl.map_shared_rank(&sh, tid);
+      o->cnt[rank] = (int)ccount;
+      if (fastp) {
+        unsigned long long cc = 0, ss = 0;
+        for (int q = 0; q < kSW; ++q) { cc += sh.wq[q][11]; ss += sh.wq[q][12]; }
+        o->cms[rank] = cc;
+        o->sms[rank] = ss;
+      }
+    }
     if (ccount <= (unsigned)kSlot) {
       unsigned long long* gk = cl.map_shared_rank(sh.ck, 0) + rank * kSlot;
       unsigned p0 = wbase;
@@ -584,6 +617,13 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
       ntot += sh.cnt[r];
     }
     fit = fit && ntot <= kCand;
+    unsigned long long ptarget = 0;   // pure top-p: ceil(P * the row's mass), as the general path
+    if (fastp) {
+      unsigned long long ca = 0, mall = 0;
+      for (int r = 0; r < CS; ++r) { ca += sh.cms[r]; mall += sh.sms[r]; }
+      ptarget = (unsigned long long)ceil((double)top_p * (double)mall);
+      fit = fit && ca >= ptarget;   // the candidates (a prefix of the sorted row) hold the nucleus
+    }
     if (fit) {
       if (rank != 0) return;
       // rank 0: the candidates, dense and in index order (slot r holds CTA r's, CTAs in index order)
@@ -599,6 +639,81 @@ __global__ void __launch_bounds__(kST, 2) sample_kernel(const TL* __restrict__ l
       // the k-th largest key (key desc, index asc: composite keys are unique); two candidates per thread
       const unsigned long long a0 = tid < ntot ? sh.cd[tid] : 0ull;
       const unsigned long long a1 = tid + kST < ntot ? sh.cd[tid + kST] : 0ull;
+      if (fastp) {
+        // ---- pure top-p over the candidates: the boundary key t = the largest key with mass(key >= t)
+        //      >= ceil(P * M) (bit by bit over the key bits that vary), then the fewest ties at t in
+        //      index order that reach it, then the draw — the general path's rules and arithmetic
+        const bool v0 = tid < ntot, v1 = tid + kST < ntot;
+        const uint32_t k0 = (uint32_t)(a0 >> 32), k1 = (uint32_t)(a1 >> 32);
+        const unsigned long long w0 = v0 ? wfix(unkey(k0), m, invT) : 0ull, w1 = v1 ? wfix(unkey(k1), m, invT) : 0ull;
+        auto bsum = [&](unsigned long long v) -> unsigned long long {
+          v = warp_sum(v);
+          if (lane == 0) sh.wsum[w] = v;
+          __syncthreads();
+          unsigned long long s2 = 0;
+          for (int q = 0; q < kSW; ++q) s2 += sh.wsum[q];
+          __syncthreads();
+          return s2;
+        };
+        uint32_t vo = (v0 ? k0 : 0u) | (v1 ? k1 : 0u);
+        uint32_t va = (v0 ? k0 : ~0u) & (v1 ? k1 : ~0u);
+        for (int o = 16; o > 0; o >>= 1) {
+          vo |= __shfl_xor_sync(0xffffffffu, vo, o);
+          va &= __shfl_xor_sync(0xffffffffu, va, o);
+        }
+        if (lane == 0) { sh.wq[w][3] = vo; sh.wq[w][4] = va; }
+        __syncthreads();
+        vo = 0u;
+        va = ~0u;
+        for (int q = 0; q < kSW; ++q) { vo |= (uint32_t)sh.wq[q][3]; va &= (uint32_t)sh.wq[q][4]; }
+        const uint32_t vary = vo ^ va;
+        uint32_t tb = va & ~vary;
+        for (int bit = 31; bit >= 0; --bit) {
+          if (!((vary >> bit) & 1u)) continue;
+          const uint32_t c = tb | (1u << bit);
+          if (bsum((v0 && k0 >= c ? w0 : 0ull) + (v1 && k1 >= c ? w1 : 0ull)) >= ptarget) tb = c;
+        }
+        const unsigned long long ma = bsum((v0 && k0 > tb ? w0 : 0ull) + (v1 && k1 > tb ? w1 : 0ull));
+        const unsigned long long wb = wfix(unkey(tb), m, invT);
+        const unsigned long long need = wb ? (ptarget - ma + wb - 1) / wb : 1;
+        // ties at tb in index order (every first-half candidate precedes the second half)
+        const bool t0 = v0 && k0 == tb, t1 = v1 && k1 == tb;
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned mt0 = __ballot_sync(0xffffffffu, t0), mt1 = __ballot_sync(0xffffffffu, t1);
+        if (lane == 0) { sh.wq[w][5] = __popc(mt0); sh.wq[w][6] = __popc(mt1); }
+        __syncthreads();
+        unsigned long long tb0 = 0, tb1 = 0;
+        for (int q = 0; q < kSW; ++q) {
+          if (q < w) { tb0 += sh.wq[q][5]; tb1 += sh.wq[q][6]; }
+          tb1 += sh.wq[q][5];
+        }
+        const bool i0 = v0 && (k0 > tb || (t0 && tb0 + __popc(mt0 & lt) < need));
+        const bool i1 = v1 && (k1 > tb || (t1 && tb1 + __popc(mt1 & lt) < need));
+        // the draw: inclusive kept mass in index order (first half, then second), first > u * total
+        const unsigned long long x0 = i0 ? w0 : 0ull, x1 = i1 ? w1 : 0ull;
+        unsigned long long s0i = x0, s1i = x1;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned long long y0 = __shfl_up_sync(0xffffffffu, s0i, o), y1 = __shfl_up_sync(0xffffffffu, s1i, o);
+          if (lane >= o) { s0i += y0; s1i += y1; }
+        }
+        __syncthreads();   // wq[.][5..6] read by every thread
+        if (lane == 31) { sh.wq[w][5] = s0i; sh.wq[w][6] = s1i; }
+        if (tid == 0) sh.tok = 0x7fffffff;
+        __syncthreads();
+        unsigned long long off0 = 0, off1 = 0, tot0 = 0, tot1 = 0;
+        for (int q = 0; q < kSW; ++q) {
+          if (q < w) { off0 += sh.wq[q][5]; off1 += sh.wq[q][6]; }
+          tot0 += sh.wq[q][5];
+          tot1 += sh.wq[q][6];
+        }
+        const unsigned long long total = tot0 + tot1;
+        const unsigned long long target = (unsigned long long)((double)uniforms[row] * (double)total);
+        if (i0 && w0 > 0 && off0 + s0i > target) atomicMin(&sh.tok, (int)(0xffffffffu - (uint32_t)(a0 & 0xffffffffull)));
+        if (i1 && w1 > 0 && tot0 + off1 + s1i > target) atomicMin(&sh.tok, (int)(0xffffffffu - (uint32_t)(a1 & 0xffffffffull)));
+        __syncthreads();
+        if (tid == 0) token_out[row] = sh.tok;
+        return;
+      }
       // the k-th largest value key kv over the candidates, bit by bit over the bits that vary (OR / AND
       // over the block; the others are fixed); then the top-k = keys above kv plus the first `need`
       // candidates at kv in index order (array order)
