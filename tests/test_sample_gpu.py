@@ -184,3 +184,49 @@ def test_sample_entropy_one_pass(dtype, B):
             for b in range(B):
                 want = oracle.entropy(rows[b], te)
                 assert abs(float(h[b]) - want) <= 1e-4, (T, k, P, te, b, float(h[b]), want)
+
+
+@pytest.mark.parametrize("B", [1, 3, 16])
+def test_sample_fast_paths_tied_peaks(B):
+    """The top-k / pure top-p fast paths (candidates above the thread-maxima bound, finished by one
+    CTA) where the decisions hinge on ties: a low bulk (N(0,1) - 6) under two tied peak groups (7
+    tokens at 6.0, 9 at 5.5, bf16-exact), top-p between two consecutive cumulative masses inside a
+    tie group (the boundary takes the lowest indices first), top-k cutting a tie group; u mid-interval
+    of an oracle-drawn token (exact), then random u (validity).  Clusters of 16 / 8 / 4 CTAs."""
+    import torch
+    from paper_2512_11221_b200 import asr_sample
+    V = 128256
+    rng = np.random.default_rng(900 + B)
+    X = np.empty((B, V), np.uint16)
+    for b in range(B):
+        x = (rng.normal(size=V) - 6.0).astype(np.float32)
+        idx = rng.choice(V, 16, replace=False)
+        x[idx[:7]] = 6.0
+        x[idx[7:]] = 5.5
+        X[b] = (x.view(np.uint32) >> 16).astype(np.uint16)   # bf16 bits (6.0 and 5.5 are exact)
+    xt = torch.from_numpy(X.view(np.int16)).view(torch.bfloat16).cuda()
+    for T, k in [(1.0, 0), (1.0, 10), (0.9, 12), (1.0, 200)]:
+        for b in range(B):
+            P = _p_between(X[b], T, k)
+            tok = lo = hi = None
+            for _ in range(50):
+                tok = sample(X[b], T, k, P, float(rng.random()))
+                lo, hi = interval(X[b], T, k, P, tok)
+                if hi - lo >= 1e-4:
+                    break
+            if hi - lo < 1e-4:
+                continue
+            u = torch.tensor([0.5 * (lo + hi)], dtype=torch.float32, device="cuda")
+            out = torch.empty(1, dtype=torch.int32, device="cuda")
+            asr_sample(xt[b:b + 1], u, out, temperature=T, top_k=k, top_p=P)
+            assert int(out.item()) == tok, (B, T, k, P, b, int(out.item()), tok)
+        # the whole batch in one call, random u: the drawn token is kept and its interval holds u
+        P = 0.6
+        u = rng.random(B).astype(np.float32)
+        out = torch.empty(B, dtype=torch.int32, device="cuda")
+        asr_sample(xt, torch.from_numpy(u).cuda(), out, temperature=T, top_k=k, top_p=P)
+        got = out.cpu().numpy()
+        for b in range(B):
+            lo, hi = interval(X[b], T, k, P, int(got[b]))
+            assert lo == lo, (B, T, k, b, int(got[b]), "not in the kept set")
+            assert lo - 2e-6 <= float(u[b]) <= hi + 2e-6, (B, T, k, b, lo, float(u[b]), hi)
