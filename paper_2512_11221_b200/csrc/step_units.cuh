@@ -470,6 +470,41 @@ __device__ void unit_append(const DevState& s, int b, int l, int i, const TK* __
   }
 }
 
+// Layers [l0, l1) of sequence b's new token at once (full residency, no mirror write here, 16-byte
+// rows): one flat loop over every 16-byte vector of those layers, 8 loads in flight per thread — a
+// unit of several layers is then one or two memory round trips instead of one per layer (batch 64:
+// 16 layers per unit; the per-layer loop left phase A's appends ending ~11 us after its entropy units).
+template <typename TK>
+__device__ void unit_append_layers(const DevState& s, int b, int l0, int l1, int i, const TK* __restrict__ k_new,
+                                   const TK* __restrict__ v_new) {
+  const long pos = s.prompt_len[b] + i;
+  const long slot = (long)b * s.max_ctx + pos;
+  ASR_CHECK(s, slot < s.kv_slots && pos < s.cap);
+  const int row = s.Hkv * s.d;
+  const int nv = row * (int)sizeof(TK) / 16;   // 16-byte vectors per K (or V) row of a layer
+  const int per_l = 2 * nv;
+  const int total = (l1 - l0) * per_l;
+  const int T = (int)ASR_UNIT_THREADS();
+  uint4* dst0 = reinterpret_cast<uint4*>(reinterpret_cast<TK*>(s.kv) + (slot * s.L + l0) * 2 * row);   // layers contiguous
+  for (int t0 = ASR_UNIT_TID(); t0 < total; t0 += 8 * T) {
+    uint4 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = t0 + k * T;
+      if (t < total) {
+        const int l = l0 + t / per_l, r = t % per_l;
+        const TK* src = (r < nv ? k_new : v_new) + ((long)b * s.L + l) * row;
+        x[k] = __ldg(reinterpret_cast<const uint4*>(src) + (r < nv ? r : r - nv));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = t0 + k * T;
+      if (t < total) dst0[t] = x[k];
+    }
+  }
+}
+
 // Recovery levels on one sequence's ledger over positions [0, n): returns this thread's
 // restored count.  SR: frozen with d > 1; WR: frozen at step >= i - N; FR: every frozen token.
 __device__ int apply_level(const DevState& s, int b, int n, int level, int i) {
@@ -1525,7 +1560,11 @@ __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* lo
   } else if (k_new) {   // (policy replay appends no K/V)
     const int a = unit - ne;
     const int b = a / au, k = a % au;
-    for (int l = k * s.layers_per_unit; l < min(s.L, (k + 1) * s.layers_per_unit); ++l) unit_append<TK>(s, b, l, i, k_new, v_new);
+    const int l0 = k * s.layers_per_unit, l1 = min(s.L, (k + 1) * s.layers_per_unit);
+    if (!s.pool_mode && (s.Hkv * s.d * (int)sizeof(TK)) % 16 == 0)
+      unit_append_layers<TK>(s, b, l0, l1, i, k_new, v_new);
+    else
+      for (int l = l0; l < l1; ++l) unit_append<TK>(s, b, l, i, k_new, v_new);
   }
 }
 
