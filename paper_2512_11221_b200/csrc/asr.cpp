@@ -557,7 +557,9 @@ static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const
       // phase-A unit grouping: one unit per warp-sized piece inside the attention kernel; otherwise
       // one entropy split per warp (8 per 256-thread unit) and appends grouped to ~one unit per SM
       auto pow2ceil = [](long v) { int p = 1; while (p < v) p <<= 1; return p; };
-      s.ent_per_unit = s.pre_in_attn ? 1 : 8;
+      const char* epu = getenv("ASR_ENT_PER_UNIT");   // tuning: entropy splits per phase-A unit (divides 64)
+      s.ent_per_unit = s.pre_in_attn ? 1 : epu ? atoi(epu) : 8;
+      if (asr::kEntSplits % s.ent_per_unit) s.ent_per_unit = 8;
       const int l = s.pre_in_attn ? 1 : pow2ceil(((long)s.L * s.B + c->num_sms - 1) / c->num_sms);
       s.layers_per_unit = l > s.L ? s.L : l;
       // small batch: the combine rides in the phase-D kernel (one launch fewer on the critical path)
