@@ -11,6 +11,13 @@ namespace asr {
 namespace {
 
 constexpr int kUnitThreads = 512;
+#ifndef ASR_PHASED_THREADS
+#define ASR_PHASED_THREADS 512
+#endif
+#ifndef ASR_PHASED_MINB
+#define ASR_PHASED_MINB 1
+#endif
+constexpr int kPhaseDThreads = ASR_PHASED_THREADS;   // phase-D block size (128 / 256 measured slower: profiles/r2/phaseD_block_ab.txt)
 constexpr int kPhaseAThreads = 256;   // 16K registers: a phase-A block fits beside an attention CTA
 
 // One phase-A unit per block (+ phase B of its sequence if it finishes last).
@@ -33,7 +40,7 @@ __global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, cons
 // the other parity (unit_next_list); the last decide block overall advances the step counter and
 // clears the redo flag.  With combine_in_decide (small batch) further blocks combine O (one warp
 // per (b, l, h)), saving the separate combine launch.
-__global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float* __restrict__ o) {
+__global__ void __launch_bounds__(kPhaseDThreads, ASR_PHASED_MINB) phaseD_kernel(DevState s, float* __restrict__ o) {
   Stamp stamp(s.tl, 2);
   pdl_wait();      // every input comes from the attention kernel(s) and phase A
   if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 8], gtimer());
@@ -41,7 +48,7 @@ __global__ void __launch_bounds__(kUnitThreads) phaseD_kernel(DevState s, float*
   const int nd = s.decide_blocks * s.B;
   if ((int)blockIdx.x >= nd) {   // combine_in_decide: blocks after the decide blocks combine O
     if (!o) return;                // policy replay: no attention, nothing to combine
-    const int wid = ((int)blockIdx.x - nd) * (kUnitThreads / 32) + (threadIdx.x >> 5);
+    const int wid = ((int)blockIdx.x - nd) * (kPhaseDThreads / 32) + (threadIdx.x >> 5);
     if (wid < s.B * s.L * s.Hq) units::combine_warp(s, wid, o);
     if (s.tl) {
       __syncthreads();
@@ -151,9 +158,9 @@ void node_phaseD(KNode& n, const DevState& s, float* o) {
   n.s = s;
   n.set(0, o);
   const int warps = s.B * s.L * s.Hq;
-  const int wpb = kUnitThreads / 32;
+  const int wpb = kPhaseDThreads / 32;
   const int nc = s.combine_in_decide ? (warps + wpb - 1) / wpb : 0;
-  n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + nc), dim3(kUnitThreads), 0);
+  n.finalize((const void*)phaseD_kernel, dim3(s.decide_blocks * s.B + nc), dim3(kPhaseDThreads), 0);
 }
 
 void node_combine(KNode& n, const DevState& s, float* o) {

@@ -118,6 +118,7 @@ def _build_asr(force: bool, out_path: str | None = None) -> str:
         return out
     objdir = os.path.join(ROOT, "build", "asr" if out_path is None else "asr_" + os.path.basename(out_path))
     os.makedirs(objdir, exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     objs = []
     common = ["-I", os.path.join(ROOT, "include"), "-I", csrc]
     if os.environ.get("ASR_TAIL_TRACE") == "1":   # diagnostic build: per-warp stamps of the fused tail
