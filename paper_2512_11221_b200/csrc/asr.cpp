@@ -612,6 +612,7 @@ static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const
       const char* sb = getenv("ASR_SK_BALANCE");
       const bool bal = sb ? sb[0] == '1' : s.B == 1;
       s.sk_bal = bal && s.sk_grid > 0 && s.sk_grid < asr::kSkBalMax && s.sk_dyn == 0 && !s.fuse_tail;
+      s.sk_learn = 1;
       CUDA_TRY(c->alloc(&s.sk_w, sizeof(float) * 4 * asr::kSkBalMax));
       CUDA_TRY(cudaMemsetAsync(s.sk_w, 0, sizeof(float) * 4 * asr::kSkBalMax, st));
       CUDA_TRY(c->alloc(&s.sk_f, sizeof(float) * 4 * asr::kSkBalMax));
@@ -1275,6 +1276,7 @@ asr_status asr_time_attention(asr_ctx* c, int32_t reps, void* cuda_stream) {
   sd.pre_in_attn = 0;   // the attention alone
   sd.fuse_tail = 0;
   sd.tl = nullptr;
+  sd.sk_learn = 0;      // uses the step's cut, leaves the rate / cut state as it was
   asr::KNode n;
   asr::node_attention(n, sd, c->scratch_q, c->scratch_k, c->scratch_v, c->attn_grid, nullptr, 0, nullptr,
                       c->scratch_o);

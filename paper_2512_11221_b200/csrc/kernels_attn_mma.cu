@@ -580,7 +580,7 @@ __device__ __forceinline__ void attention_phase(const DevState& s, const __nv_bf
     // streams (KV loads are evict_first, these stay) — not at the producer's exit, where it delayed
     // the CTA's end by ~2 us
     if (s.B <= 8) prefetch_ledger(s, step & 1, s.act_len + (step & 1) * s.B, step, lane);
-    if (!DYN && s.sk_bal && blockIdx.x == gridDim.x - 1) sk_fractions(s, step);
+    if (!DYN && s.sk_bal && s.sk_learn && blockIdx.x == gridDim.x - 1) sk_fractions(s, step);
     if (s.fuse_tail && !(s.tail_exp & 2)) {
       // instruction prefetch: a dry run (loads and arithmetic only, no stores, no waits) of the fused
       // tail's two functions while the attention streams, so their code is on chip when the tail runs
@@ -840,14 +840,14 @@ __global__ void __launch_bounds__(Geo<HK>::kThreads, 1)
     attention_phase<HK, TL, DYN>(s, q, k_new, v_new, sm, do_pre, logits, entropy_out, u, o);
     if (s.tl && threadIdx.x == 0) atomicMin(&s.tl[2 * kStages + 7], gtimer());   // first CTA done
   }
-  if (!DYN && s.sk_bal && !do_pre) {
+  if (!DYN && s.sk_bal && s.sk_learn && !do_pre) {
     __syncthreads();
     if (threadIdx.x == 0) sk_rate_update(s, step, sm.range, c0);
   }
   if (do_pre) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (!DYN && s.sk_bal) sk_rate_update(s, step, sm.range, c0);
+      if (!DYN && s.sk_bal && s.sk_learn) sk_rate_update(s, step, sm.range, c0);
       if (s.tl) atomicMax(&s.tl[kTlTail + 8], gtimer());   // every warp of the CTA is past the attention
       const unsigned long long t0 = gtimer();
       bool ok = true;
