@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kPhaseAThreads) phaseA_kernel(DevState s, cons
     if (ae && ce > ae) s.stall[0] += ce - ae;
     s.stall[1] = s.stall[2] = 0;
   }
-  units::phaseA_block<TL, TK>(s, blockIdx.x, *s.step, logits, k_new, v_new, entropy_out, u);
+  units::phaseA_block<TL, TK, true>(s, blockIdx.x, *s.step, logits, k_new, v_new, entropy_out, u);
 }
 
 // decide_blocks blocks per sequence: decide + tick (unit x of sequence b), then together A_{i+1} into

@@ -1547,7 +1547,7 @@ __host__ __device__ inline int phaseA_seq(const DevState& s, bool has_logits, in
 __host__ __device__ inline int phaseA_units_per_seq(const DevState& s, bool has_logits) {
   return (has_logits ? ent_units_per_seq(s) : 0) + app_units_per_seq(s);
 }
-template <typename TL, typename TK>
+template <typename TL, typename TK, bool kFlatAppend>
 __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* logits, const TK* k_new,
                                 const TK* v_new, UnitShm& u) {
   const int eu = ent_units_per_seq(s), au = app_units_per_seq(s);
@@ -1561,7 +1561,9 @@ __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* lo
     const int a = unit - ne;
     const int b = a / au, k = a % au;
     const int l0 = k * s.layers_per_unit, l1 = min(s.L, (k + 1) * s.layers_per_unit);
-    if (!s.pool_mode && (s.Hkv * s.d * (int)sizeof(TK)) % 16 == 0)
+    // (the flat loop only in the phase-A kernel: compiled into the attention kernel, whose phase-A
+    // warp appends one layer per unit anyway, it slowed the batch-64 attention by 3 %: code layout)
+    if (kFlatAppend && !s.pool_mode && (s.Hkv * s.d * (int)sizeof(TK)) % 16 == 0)
       unit_append_layers<TK>(s, b, l0, l1, i, k_new, v_new);
     else
       for (int l = l0; l < l1; ++l) unit_append<TK>(s, b, l, i, k_new, v_new);
@@ -1570,11 +1572,11 @@ __device__ void run_phaseA_unit(const DevState& s, int unit, int i, const TL* lo
 
 // Phase A unit `unit` of step i and, when it is the last unit of its sequence to finish (per-sequence
 // ticket, threadfence pattern), phase B of that sequence (unit_finish) — no dependent launch between.
-template <typename TL, typename TK>
+template <typename TL, typename TK, bool kFlatAppend = false>
 __device__ void phaseA_block(const DevState& s, int unit, int i, const TL* logits, const TK* k_new, const TK* v_new,
                              float* entropy_out, UnitShm& u) {
   const bool has_logits = logits != nullptr;
-  run_phaseA_unit<TL, TK>(s, unit, i, logits, k_new, v_new, u);
+  run_phaseA_unit<TL, TK, kFlatAppend>(s, unit, i, logits, k_new, v_new, u);
   if (s.tl && ASR_UNIT_TID() == 0)
     atomicMax(&s.tl[2 * kStages + 3 + ((has_logits && unit < s.B * ent_units_per_seq(s)) ? 0 : 1)], gtimer());
   const int b = phaseA_seq(s, has_logits, unit);
