@@ -613,6 +613,9 @@ static asr_status create_impl(const asr_config* cfg, const void* prompt_k, const
       const bool bal = sb ? sb[0] == '1' : s.B == 1;
       s.sk_bal = bal && s.sk_grid > 0 && s.sk_grid < asr::kSkBalMax && s.sk_dyn == 0 && !s.fuse_tail;
       s.sk_learn = 1;
+      const char* se = getenv("ASR_SK_EWMA");
+      s.sk_ewma = se ? (float)atof(se) : 0.5f;
+      if (!(s.sk_ewma > 0.f && s.sk_ewma <= 1.f)) s.sk_ewma = 0.5f;
       CUDA_TRY(c->alloc(&s.sk_w, sizeof(float) * 4 * asr::kSkBalMax));
       CUDA_TRY(cudaMemsetAsync(s.sk_w, 0, sizeof(float) * 4 * asr::kSkBalMax, st));
       CUDA_TRY(c->alloc(&s.sk_f, sizeof(float) * 4 * asr::kSkBalMax));

@@ -105,6 +105,7 @@ struct DevState {
   int32_t* sk_ctr;            // [2] next dynamic chunk, CTAs done with chunks (the last one resets both)
   int sk_bal;                 // 1: rate-balanced static split (sk_weighted below; sk_dyn == 0 only)
   int sk_learn;               // 1: the launch measures its rates / computes later cuts (steps; 0: asr_time_attention)
+  float sk_ewma;              // weight of a new rate measurement in the per-CTA rate average (0.5)
   float* sk_w;                // [4][kSkBalMax] per-CTA streaming rates (EWMA), by step parity, double-buffered
   float* sk_f;                // [4][kSkBalMax] cut fractions f_0..f_G (NaN: not computed yet), same buffering
   int* sk_bound;              // [kSkBalMax] this step's static range starts (+ Ts), written by CTA 0

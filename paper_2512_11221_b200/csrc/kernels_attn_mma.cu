@@ -287,7 +287,7 @@ __device__ __forceinline__ void sk_rate_update(const DevState& s, int step, cons
   if (tiles <= 0 || dc <= 0) return;
   const float rate = (float)tiles * 1e6f / (float)dc;   // tiles per 10^6 clocks
   const float old = __ldcg(s.sk_w + sk_wbuf(step, false) * kSkBalMax + blockIdx.x);
-  s.sk_w[sk_wbuf(step, true) * kSkBalMax + blockIdx.x] = old > 0.f ? 0.5f * (old + rate) : rate;
+  s.sk_w[sk_wbuf(step, true) * kSkBalMax + blockIdx.x] = old > 0.f ? old + s.sk_ewma * (rate - old) : rate;
 }
 
 // The attention + score phase of one step (needs A_i, |A_i|, q and the appended K/V in memory).
